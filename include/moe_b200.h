@@ -1,0 +1,210 @@
+/*
+ * moe_b200.h -- C ABI of the B200-native Tutel-style MoE layer (libmoe_b200.so).
+ *
+ * This is the drop-in boundary for the reference's MoE layer path (the C++ library API of
+ * /root/reference/proj/include/moesim/moe_layer.hpp and its sub-operators in gating.hpp /
+ * dispatch.hpp / parallelism.hpp / pipeline.hpp). Every entry point names the reference
+ * declaration it replaces. Conventions:
+ *   - plain pointers + sizes, no C++ or torch types; streams are cudaStream_t passed as void*;
+ *   - status codes instead of exceptions: MOE_EINVAL for the reference's std::invalid_argument,
+ *     MOE_ECOMM for std::runtime_error raised by the fabric, MOE_ESTATE for std::logic_error;
+ *   - row-major layouts exactly as the reference (x: (T, M); W1: (M, V); W2: (V, M); Wg: (M, E));
+ *   - one handle per rank (one process or host thread per GPU); the handle is single-writer,
+ *     like LayerState (moe_layer.hpp:33-44).
+ * There is no CPU fallback: every compute entry point runs sm_100a kernels and fails with
+ * MOE_ECUDA when no usable device is present.
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_OK 0
+#define MOE_EINVAL 1 /* std::invalid_argument (core.cpp:9-25, dispatch.cpp:7-16, ...) */
+#define MOE_ECUDA 2  /* CUDA launch / runtime failure, or no sm_100 device */
+#define MOE_ECOMM 3  /* std::runtime_error from the fabric (fabric.cpp:144-160,233-258) */
+#define MOE_ESTATE 4 /* std::logic_error (pipeline.cpp:148,216,227) / call-order misuse */
+#define MOE_ENOMEM 5
+
+#define MOE_DTYPE_BF16 0
+#define MOE_DTYPE_F32 1
+#define MOE_DTYPE_F64 2
+
+#define MOE_CAP_FIXED 0   /* FixedCapacity{factor}       core.hpp:25-27 */
+#define MOE_CAP_AUTO 1    /* AutoCapacity{}              core.hpp:28 */
+#define MOE_CAP_BOUNDED 2 /* BoundedCapacity{max_factor} core.hpp:29-31 */
+
+#define MOE_A2A_LINEAR 0 /* A2aAlgo::Linear (collectives.hpp:10) */
+#define MOE_A2A_2DH 1    /* A2aAlgo::TwoDH */
+
+/* MoELayerConfig (moe_layer.hpp:22-29) flattened with Dims (core.hpp:32-56). Per-rank placement
+ * (ExpertsPerRank{E/W}) only; the linear router only. */
+typedef struct moe_config {
+  int64_t world_size;      /* W */
+  int64_t gpus_per_node;   /* m */
+  int64_t global_experts;  /* E (= W * local experts) */
+  int64_t model_dim;       /* M */
+  int64_t hidden_dim;      /* V */
+  int64_t tokens_per_step; /* T, tokens per rank */
+  int64_t top_k;           /* k */
+  int32_t capacity_kind;   /* MOE_CAP_* */
+  double capacity_factor;  /* f (Fixed) or max_factor (Bounded) */
+  int32_t bpr;             /* batch-prioritized routing */
+  int32_t dtype;           /* MOE_DTYPE_BF16 (tensor-core path) or MOE_DTYPE_F32 */
+  int32_t adaptive;        /* StrategyControl::adaptive: Alg. 1 picks the pipelining degree */
+  int32_t degree;          /* StrategyControl::fixed.degree (capacity chunks), 1..8 */
+} moe_config;
+
+/* StepMetrics (moe_layer.hpp:46-54); sim_seconds becomes measured device seconds. */
+typedef struct moe_step_metrics {
+  double f;            /* capacity_to_factor(capacity) */
+  int64_t capacity;    /* ΔC */
+  int32_t a2a_algo;    /* MOE_A2A_* */
+  int32_t degree;      /* pipelining degree used */
+  double seconds;      /* forward device time (CUDA events), 0 if not measured */
+  double comm_bytes;   /* bytes this rank sent in the forward all-to-alls */
+  int64_t drop_count;  /* dropped (token, expert) assignments on this rank */
+} moe_step_metrics;
+
+typedef struct moe_handle moe_handle;
+
+/* ---------------------------------------------------------------- capacity math (core.cpp) */
+/* expert_capacity, core.cpp:28-35: max(1, ceil(k*f*T/E - 1e-9)). */
+int moe_expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts, int64_t* out);
+/* resolve_capacity, core.cpp:47-59 (demand has E entries). */
+int moe_resolve_capacity(int32_t capacity_kind, double factor, const int64_t* demand,
+                         int64_t experts, int64_t top_k, int64_t tokens, int64_t* out);
+/* capacity_to_factor, core.cpp:61-64. */
+int moe_capacity_to_factor(int64_t capacity, int64_t experts, int64_t top_k, int64_t tokens,
+                           double* out);
+/* Dims::validate, core.cpp:8-26 (per-rank placement). */
+int moe_validate_config(const moe_config* cfg);
+
+/* ---------------------------------------------------------------- layer (moe_layer.hpp) */
+/* NCCL unique id for W > 1 (128 bytes), created on rank 0 and broadcast by the caller. */
+int moe_get_unique_id(uint8_t* id128);
+/* LayerState construction for one rank (moe_layer.cpp:144-163 minus the weight draw):
+ * allocates device state on `device`, creates the NCCL communicator when W > 1. */
+int moe_create(const moe_config* cfg, int32_t rank, const uint8_t* nccl_id128, int32_t device,
+               moe_handle** out);
+int moe_destroy(moe_handle* h);
+const char* moe_last_error(const moe_handle* h);
+/* Per-thread message of the last failing stateless call (moe_op_*, moe_create). */
+const char* moe_last_error_global(void);
+
+/* LayerState::init draw (moe_layer.cpp:144-163): Rng(seed) draws Wg (M,E), the cosine router
+ * (M,256)+(E,256), then w1 (M,V), w2 (V,M) per expert, all uniform; generated on the device by
+ * counter index, so every rank holds exactly the reference's values for its local experts. */
+int moe_init_params(moe_handle* h, uint64_t seed);
+/* RouterParams::linear_weight (gating.hpp:25-30); host fp64 (M, E). */
+int moe_set_router(moe_handle* h, const double* wg_host);
+/* Full weights of local expert `local_e` (global index rank*E/W + local_e); host fp64
+ * w1 (M, V), w2 (V, M) -- ExpertParams::assemble layout (parallelism.cpp:80-90). */
+int moe_set_expert(moe_handle* h, int64_t local_e, const double* w1_host, const double* w2_host);
+/* ZeRO-sliced parameters (ExpertParams, parallelism.hpp:22-37): this rank's slice of every
+ * expert (w1 columns / w2 rows [rank*V/W, (rank+1)*V/W)), host fp64, expert-major
+ * [E][M][V/W] and [E][V/W][M]. Followed by one grouped exchange that assembles the local
+ * experts -- gather_computed_experts, parallelism.cpp:149-206. */
+int moe_set_expert_slices(moe_handle* h, const double* w1_slices, const double* w2_slices);
+
+/* forward(state, x) (moe_layer.cpp:171-244) for this rank's token block: x, y are device
+ * (T, M) in the layer dtype. Saves what backward needs inside the handle. */
+int moe_forward(moe_handle* h, const void* x, void* y, void* stream);
+/* backward(state, saved, dy) (moe_layer.cpp:246-319): dx device (T, M); dw1/dw2 device fp32
+ * (E/W, M, V) and (E/W, V, M) for the local experts (may be NULL: kept in the handle). */
+int moe_backward(moe_handle* h, const void* dy, void* dx, float* dw1, float* dw2, void* stream);
+/* Same calls with HOST (preferably pinned) buffers: host->device copy of the input and
+ * device->host copy of the result happen inside the call, as a reference caller would see. */
+int moe_forward_host(moe_handle* h, const void* x_host, void* y_host, void* stream);
+int moe_backward_host(moe_handle* h, const void* dy_host, void* dx_host, void* stream);
+
+/* Routing of the last forward (GateOutput, gating.hpp:14-23): host buffers (T, k). */
+int moe_get_routing(moe_handle* h, int32_t* idxs, int32_t* locations, double* gates,
+                    int64_t* capacity);
+int moe_get_metrics(moe_handle* h, moe_step_metrics* out);
+/* Local expert gradients of the last backward, copied to host fp32 (E/W, M, V)+(E/W, V, M). */
+int moe_get_expert_grads(moe_handle* h, float* dw1_host, float* dw2_host);
+/* Device pointer to local expert weights in the layer dtype: which=1 -> w1, 2 -> w2. */
+int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr);
+/* Number of kernels launched by the last forward + backward (benchmark bookkeeping). */
+int64_t moe_kernel_launches(const moe_handle* h);
+
+/* ---------------------------------------------------------------- stateless device ops
+ * All pointers are device memory; each call is stream-ordered on `stream` and allocates its
+ * own scratch. These are the reference sub-operators, for parity testing and composition. */
+
+/* gate_linear + run_gating_blocked (gating.cpp:29-35, 134-162): x (blocks*T, M) in x_dtype,
+ * wg (M, E) fp64 -> idxs/locations int32 (blocks*T, k), gates fp64 (blocks*T, k), optional
+ * probs fp64 (blocks*T, E). Returns the resolved capacity and the drop count (synchronizes). */
+int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t blocks, int64_t T,
+                  int64_t M, int64_t E, int64_t k, int32_t capacity_kind, double capacity_factor,
+                  int32_t bpr, int32_t* idxs, double* gates, int32_t* locations, double* probs,
+                  int64_t* capacity, int64_t* drops, void* stream);
+
+/* fast_encode_range per block (dispatch.cpp:51-62) + partition_capacity (pipeline.cpp:33-51):
+ * z = [blocks][degree][E][cc][M], cc = ceil(capacity/degree), padded slots zero. */
+int moe_op_encode(const void* x, int32_t dtype, int64_t blocks, int64_t T, int64_t M, int64_t E,
+                  int64_t k, int64_t capacity, int64_t degree, const int32_t* idxs,
+                  const int32_t* locations, void* z, void* stream);
+/* fast_decode_range (dispatch.cpp:75-87) from the same chunked layout. */
+int moe_op_decode(const void* z, int32_t dtype, int64_t blocks, int64_t T, int64_t M, int64_t E,
+                  int64_t k, int64_t capacity, int64_t degree, const int32_t* idxs,
+                  const int32_t* locations, const double* gates, void* y, void* stream);
+/* fast_decode_backward_range (dispatch.cpp:136-157): dz chunked layout; dgates (blocks*T, k)
+ * fp64 optional (needs z). */
+int moe_op_decode_backward(const void* dy, const void* z, int32_t dtype, int64_t blocks,
+                           int64_t T, int64_t M, int64_t E, int64_t k, int64_t capacity,
+                           int64_t degree, const int32_t* idxs, const int32_t* locations,
+                           const double* gates, void* dz, double* dgates, void* stream);
+/* fast_encode_backward_range (dispatch.cpp:117-128). */
+int moe_op_encode_backward(const void* dz, int32_t dtype, int64_t blocks, int64_t T, int64_t M,
+                           int64_t E, int64_t k, int64_t capacity, int64_t degree,
+                           const int32_t* idxs, const int32_t* locations, void* dx, void* stream);
+
+/* expert_ffn (parallelism.cpp:103-121): x, y (n, rows, M); w1 (n, M, V); w2 (n, V, M);
+ * act (n, rows, V) optional output (the saved relu activation). */
+int moe_op_expert_ffn(const void* x, const void* w1, const void* w2, void* y, void* act,
+                      int32_t dtype, int64_t n, int64_t rows, int64_t M, int64_t V, void* stream);
+/* expert_ffn_backward (parallelism.cpp:123-147): dx (n, rows, M) in dtype; dw1 (n, M, V),
+ * dw2 (n, V, M) fp32. */
+int moe_op_expert_ffn_backward(const void* x, const void* w1, const void* w2, const void* dy,
+                               void* dx, float* dw1, float* dw2, int32_t dtype, int64_t n,
+                               int64_t rows, int64_t M, int64_t V, void* stream);
+
+/* Raw grouped GEMM (kind: 0 up/relu, 1 down, 2 dgrad*mask, 3 dgrad, 4 wgrad), see
+ * paper_2206_03382_b200/csrc/gemm_sm100.h for the addressing. use_tc=1 forces the tcgen05
+ * kernel (bf16), 0 the SIMT kernel. */
+int moe_op_gemm(int32_t kind, int32_t dtype, int32_t use_tc, const void* A, const void* B,
+                void* D, const void* aux, int64_t G, int64_t S, int64_t seg_rows,
+                int64_t seg_base, int64_t N, int64_t K, int64_t Mo, int64_t nseg_total,
+                void* stream);
+
+/* Rng stream (core.cpp:66-83) on the device: dst[i] = lo + (hi-lo)*uniform(draw offset+i). */
+int moe_op_fill_uniform(void* dst, int32_t dtype, int64_t n, uint64_t seed, uint64_t offset,
+                        double lo, double hi, void* stream);
+
+/* ---------------------------------------------------------------- Alg. 1 (pipeline.cpp:180-237)
+ * Adaptive pipelining memo over the strategy space {Linear, TwoDH} x {1, 2, 4, 8} in
+ * exploration order (pipeline.cpp:113-121); strategies are indices 0..7 into that order. */
+typedef struct moe_memo moe_memo;
+int moe_memo_create(double bucket_length, moe_memo** out);
+int moe_memo_destroy(moe_memo* m);
+int moe_memo_get_strategy(moe_memo* m, double f, int32_t* strategy);
+int moe_memo_optimize_strategy(moe_memo* m, double f, int32_t strategy, double seconds);
+int moe_memo_recompute_buckets(moe_memo* m, double f);
+/* Bucket introspection: count, and (start, member count, members[...], table[8] with NaN for
+ * unmeasured strategies) of bucket i. */
+int moe_memo_num_buckets(moe_memo* m, int64_t* n);
+int moe_memo_bucket(moe_memo* m, int64_t i, double* start, int64_t* n_members, double* members,
+                    int64_t max_members, double* table8);
+int moe_memo_lookup(moe_memo* m, double f, int32_t strategy, double* seconds, int32_t* present);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOE_B200_H */

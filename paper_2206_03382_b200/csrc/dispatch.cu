@@ -1,0 +1,468 @@
+// Sparse dispatch / combine kernels (HBM-bound, 128-bit vectorised, one warp per row).
+//
+// Reference semantics (dispatch.cpp):
+//   fast_encode_range            :51-62   Z <- 0; Z[idx, loc, :] = x[t, :] for kept (t, j)
+//   fast_decode_range            :75-87   y[t, :] += g * Z[idx, loc, :], j ascending
+//   fast_decode_backward_range   :136-157 dZ[idx, loc] += g * dy[t];  d_gates = <Z, dy>
+//   fast_encode_backward_range   :117-128 dx[t] += dZ[idx, loc]
+// Encode and decode-backward are written slot-major (a gather per capacity row, driven by the
+// slot -> token table built during location assignment), so the zero fill of empty and padded
+// capacity rows is fused into the same coalesced pass and no scatter/atomics are needed. Decode
+// and encode-backward are token-major gathers. Slot rows use the pipelined-chunk layout
+// [block][chunk][expert][cc][M] (partition_capacity, pipeline.cpp:33-51), which is exactly the
+// send layout of the flexible all-to-all, so chunking costs no copy.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace moe {
+
+namespace {
+
+constexpr int kWarpsPerCta = 8;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ size_t slot_row(const SlotGeom& g, int b, int e, int c) {
+  return static_cast<size_t>(b) * g.degree * g.E * g.cc +
+         static_cast<size_t>((c / g.cc) * g.E + e) * g.cc + (c % g.cc);
+}
+
+template <typename T>
+struct Vec;  // 16-byte vector of T
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void to_f32(const uint4& v, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 p = __bfloat1622float2(h[i]);
+      f[2 * i] = p.x;
+      f[2 * i + 1] = p.y;
+    }
+  }
+  __device__ static uint4 from_f32(const float (&f)[8]) {
+    uint4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ static void to_f32(const uint4& v, float (&f)[4]) {
+    f[0] = __uint_as_float(v.x);
+    f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z);
+    f[3] = __uint_as_float(v.w);
+  }
+  __device__ static uint4 from_f32(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+};
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <>
+__device__ __forceinline__ float from_f<float>(float v) {
+  return v;
+}
+
+// ------------------------------------------------------------------ encode
+// Z[row] = x[slot_token[row]] or 0. Rows enumerate [block][chunk][expert][cc].
+template <typename T, bool kVec>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    encode_kernel(SlotGeom g, const T* __restrict__ x, const int32_t* __restrict__ slot_token,
+                  T* __restrict__ z) {
+  const int lane = threadIdx.x % 32;
+  const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
+  const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
+  for (size_t row = static_cast<size_t>(blockIdx.x) * kWarpsPerCta + threadIdx.x / 32; row < rows;
+       row += static_cast<size_t>(gridDim.x) * kWarpsPerCta) {
+    const int b = static_cast<int>(row / per_block);
+    const int rem = static_cast<int>(row % per_block);
+    const int i = rem / (g.E * g.cc);
+    const int e = (rem / g.cc) % g.E;
+    const int c = i * g.cc + rem % g.cc;
+    const int t = c < g.cap ? slot_token[static_cast<size_t>(b * g.E + e) * g.cap + c] : -1;
+    if constexpr (kVec) {
+      constexpr int VN = Vec<T>::N;
+      const int nv = g.M / VN;
+      uint4* dst = reinterpret_cast<uint4*>(z + row * g.M);
+      if (t < 0) {
+        for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * g.M);
+        for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+          uint4 buf[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv) buf[u] = ld_stream(src + v);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv) dst[v] = buf[u];
+          }
+        }
+      }
+    } else {
+      T* dst = z + row * g.M;
+      for (int m = lane; m < g.M; m += 32)
+        dst[m] = t < 0 ? from_f<T>(0.0f) : x[static_cast<size_t>(t) * g.M + m];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ decode
+// y[t] = sum_j g[t,j] * Z[row(t,j)] (fp32 accumulate, j ascending); 0 when all dropped.
+template <typename T, bool kVec>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    decode_kernel(SlotGeom g, const T* __restrict__ z, const int32_t* __restrict__ idxs,
+                  const int32_t* __restrict__ locations, const double* __restrict__ gates,
+                  T* __restrict__ y) {
+  const int lane = threadIdx.x % 32;
+  const int ntok = g.blocks * g.T;
+  for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
+       t += gridDim.x * kWarpsPerCta) {
+    const int b = t / g.T;
+    if constexpr (kVec) {
+      constexpr int VN = Vec<T>::N;
+      const int nv = g.M / VN;
+      uint4* dst = reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * g.M);
+      for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+        float acc[kUnroll][VN];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+          for (int q = 0; q < VN; ++q) acc[u][q] = 0.0f;
+        for (int j = 0; j < g.k; ++j) {
+          const int loc = locations[static_cast<size_t>(t) * g.k + j];
+          if (loc < 0) continue;
+          const int e = idxs[static_cast<size_t>(t) * g.k + j];
+          const float gv = static_cast<float>(gates[static_cast<size_t>(t) * g.k + j]);
+          const uint4* src = reinterpret_cast<const uint4*>(z + slot_row(g, b, e, loc) * g.M);
+          uint4 buf[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv) buf[u] = ld_stream(src + v);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            float f[VN];
+            Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+            for (int q = 0; q < VN; ++q) acc[u][q] = fmaf(gv, f[q], acc[u][q]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < nv) dst[v] = Vec<T>::from_f32(acc[u]);
+        }
+      }
+    } else {
+      for (int m = lane; m < g.M; m += 32) {
+        float acc = 0.0f;
+        for (int j = 0; j < g.k; ++j) {
+          const int loc = locations[static_cast<size_t>(t) * g.k + j];
+          if (loc < 0) continue;
+          const int e = idxs[static_cast<size_t>(t) * g.k + j];
+          const float gv = static_cast<float>(gates[static_cast<size_t>(t) * g.k + j]);
+          acc = fmaf(gv, to_f(z[slot_row(g, b, e, loc) * g.M + m]), acc);
+        }
+        y[static_cast<size_t>(t) * g.M + m] = from_f<T>(acc);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ decode backward
+// dZ[row] = g_slot * dy[t_slot] or 0 (slot-major; each kept slot has exactly one (t, j)).
+template <typename T, bool kVec>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    decode_bwd_kernel(SlotGeom g, const T* __restrict__ dy, const int32_t* __restrict__ slot_token,
+                      const float* __restrict__ slot_gate, T* __restrict__ dz) {
+  const int lane = threadIdx.x % 32;
+  const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
+  const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
+  for (size_t row = static_cast<size_t>(blockIdx.x) * kWarpsPerCta + threadIdx.x / 32; row < rows;
+       row += static_cast<size_t>(gridDim.x) * kWarpsPerCta) {
+    const int b = static_cast<int>(row / per_block);
+    const int rem = static_cast<int>(row % per_block);
+    const int i = rem / (g.E * g.cc);
+    const int e = (rem / g.cc) % g.E;
+    const int c = i * g.cc + rem % g.cc;
+    int t = -1;
+    float gv = 0.0f;
+    if (c < g.cap) {
+      const size_t s = static_cast<size_t>(b * g.E + e) * g.cap + c;
+      t = slot_token[s];
+      gv = slot_gate[s];
+    }
+    if constexpr (kVec) {
+      constexpr int VN = Vec<T>::N;
+      const int nv = g.M / VN;
+      uint4* dst = reinterpret_cast<uint4*>(dz + row * g.M);
+      if (t < 0) {
+        for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(dy + static_cast<size_t>(t) * g.M);
+        for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+          uint4 buf[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv) buf[u] = ld_stream(src + v);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv) {
+              float f[VN];
+              Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+              for (int q = 0; q < VN; ++q) f[q] *= gv;
+              dst[v] = Vec<T>::from_f32(f);
+            }
+          }
+        }
+      }
+    } else {
+      T* dst = dz + row * g.M;
+      for (int m = lane; m < g.M; m += 32)
+        dst[m] = t < 0 ? from_f<T>(0.0f) : from_f<T>(gv * to_f(dy[static_cast<size_t>(t) * g.M + m]));
+    }
+  }
+}
+
+// d_gates[t, j] = <Z[row], dy[t]> in fp64 (the layer itself discards it, moe_layer.cpp:268-270).
+template <typename T>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    decode_bwd_gates_kernel(SlotGeom g, const T* __restrict__ z, const T* __restrict__ dy,
+                            const int32_t* __restrict__ idxs, const int32_t* __restrict__ locations,
+                            double* __restrict__ dgates) {
+  const int lane = threadIdx.x % 32;
+  const int n = g.blocks * g.T * g.k;
+  for (int f = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; f < n; f += gridDim.x * kWarpsPerCta) {
+    const int t = f / g.k;
+    const int loc = locations[f];
+    double s = 0.0;
+    if (loc >= 0) {
+      const T* zr = z + slot_row(g, t / g.T, idxs[f], loc) * g.M;
+      const T* dr = dy + static_cast<size_t>(t) * g.M;
+      for (int m = lane; m < g.M; m += 32)
+        s += static_cast<double>(to_f(zr[m])) * static_cast<double>(to_f(dr[m]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (lane == 0) dgates[f] = s;
+  }
+}
+
+// ------------------------------------------------------------------ encode backward
+// dx[t] = sum_j dZ[row(t,j)] over kept j (fp32 accumulate, j ascending).
+template <typename T, bool kVec>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    encode_bwd_kernel(SlotGeom g, const T* __restrict__ dz, const int32_t* __restrict__ idxs,
+                      const int32_t* __restrict__ locations, T* __restrict__ dx) {
+  const int lane = threadIdx.x % 32;
+  const int ntok = g.blocks * g.T;
+  for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
+       t += gridDim.x * kWarpsPerCta) {
+    const int b = t / g.T;
+    if constexpr (kVec) {
+      constexpr int VN = Vec<T>::N;
+      const int nv = g.M / VN;
+      uint4* dst = reinterpret_cast<uint4*>(dx + static_cast<size_t>(t) * g.M);
+      for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+        float acc[kUnroll][VN];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+          for (int q = 0; q < VN; ++q) acc[u][q] = 0.0f;
+        for (int j = 0; j < g.k; ++j) {
+          const int loc = locations[static_cast<size_t>(t) * g.k + j];
+          if (loc < 0) continue;
+          const int e = idxs[static_cast<size_t>(t) * g.k + j];
+          const uint4* src = reinterpret_cast<const uint4*>(dz + slot_row(g, b, e, loc) * g.M);
+          uint4 buf[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv) buf[u] = ld_stream(src + v);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            float f[VN];
+            Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+            for (int q = 0; q < VN; ++q) acc[u][q] += f[q];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < nv) dst[v] = Vec<T>::from_f32(acc[u]);
+        }
+      }
+    } else {
+      for (int m = lane; m < g.M; m += 32) {
+        float acc = 0.0f;
+        for (int j = 0; j < g.k; ++j) {
+          const int loc = locations[static_cast<size_t>(t) * g.k + j];
+          if (loc < 0) continue;
+          const int e = idxs[static_cast<size_t>(t) * g.k + j];
+          acc += to_f(dz[slot_row(g, b, e, loc) * g.M + m]);
+        }
+        dx[static_cast<size_t>(t) * g.M + m] = from_f<T>(acc);
+      }
+    }
+  }
+}
+
+int grid_for(size_t warps_needed) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const size_t ctas = (warps_needed + kWarpsPerCta - 1) / kWarpsPerCta;
+  const size_t cap = static_cast<size_t>(sms) * 8;  // 8 resident CTAs of 8 warps per SM
+  return static_cast<int>(ctas < cap ? (ctas > 0 ? ctas : 1) : cap);
+}
+
+bool vec_ok(int dtype, int M) { return (M * (dtype == 1 ? 4 : 2)) % 16 == 0; }
+
+}  // namespace
+
+int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
+                  cudaStream_t st) {
+  const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
+  const int grid = grid_for(rows);
+  const bool v = vec_ok(dtype, g.M);
+  if (dtype == 1) {
+    if (v) encode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z));
+    else encode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z));
+  } else {
+    using B = __nv_bfloat16;
+    if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z));
+    else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
+                  const int32_t* locations, const double* gates, void* y, cudaStream_t st) {
+  const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T);
+  const bool v = vec_ok(dtype, g.M);
+  if (dtype == 1) {
+    if (v) decode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
+    else decode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
+  } else {
+    using B = __nv_bfloat16;
+    if (v) decode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
+    else decode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
+                           const int32_t* slot_token, const float* slot_gate, void* dz,
+                           cudaStream_t st) {
+  const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
+  const int grid = grid_for(rows);
+  const bool v = vec_ok(dtype, g.M);
+  if (dtype == 1) {
+    if (v) decode_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz));
+    else decode_bwd_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz));
+  } else {
+    using B = __nv_bfloat16;
+    if (v) decode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz));
+    else decode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
+                                 const int32_t* idxs, const int32_t* locations, double* dgates,
+                                 cudaStream_t st) {
+  const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T * g.k);
+  if (dtype == 1)
+    decode_bwd_gates_kernel<float><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), static_cast<const float*>(dy), idxs, locations, dgates);
+  else
+    decode_bwd_gates_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g, static_cast<const __nv_bfloat16*>(z), static_cast<const __nv_bfloat16*>(dy), idxs, locations, dgates);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
+                           const int32_t* locations, void* dx, cudaStream_t st) {
+  const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T);
+  const bool v = vec_ok(dtype, g.M);
+  if (dtype == 1) {
+    if (v) encode_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
+    else encode_bwd_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
+  } else {
+    using B = __nv_bfloat16;
+    if (v) encode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
+    else encode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+namespace {
+__global__ void build_slots_kernel(int n, int T, int k, int E, int cap,
+                                   const int32_t* __restrict__ idxs,
+                                   const int32_t* __restrict__ locations,
+                                   const double* __restrict__ gates, int32_t* __restrict__ slot_token,
+                                   float* __restrict__ slot_gate) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
+    const int loc = locations[f];
+    if (loc < 0) continue;
+    const int t = f / k;
+    const size_t s = static_cast<size_t>((t / T) * E + idxs[f]) * cap + loc;
+    slot_token[s] = t;
+    slot_gate[s] = gates ? static_cast<float>(gates[f]) : 0.0f;
+  }
+}
+}  // namespace
+
+// Slot tables (slot -> token, slot -> gate) from an explicit routing plan (DispatchPlan).
+int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* idxs,
+                       const int32_t* locations, const double* gates, int32_t* slot_token,
+                       float* slot_gate, cudaStream_t st) {
+  const size_t ns = static_cast<size_t>(blocks) * E * cap;
+  if (cudaMemsetAsync(slot_token, 0xFF, ns * sizeof(int32_t), st) != cudaSuccess) return -2;
+  if (cudaMemsetAsync(slot_gate, 0, ns * sizeof(float), st) != cudaSuccess) return -2;
+  const int n = blocks * T * k;
+  const int grid = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+  build_slots_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(n, T, k, E, cap, idxs, locations, gates,
+                                                         slot_token, slot_gate);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace moe

@@ -1,0 +1,398 @@
+// Gating on sm_100a: fp64 router GEMM + row softmax + top-k (one warp per token), then the
+// capacity-slot assignment as a per-expert rank computation.
+//
+// Reference semantics (all bit-exact in idxs / locations / drop mask):
+//   gate_linear + softmax_rows   /root/reference/proj/src/gating.cpp:19-35
+//   topk_select (desc prob, asc index tie-break)       gating.cpp:58-78
+//   assign_locations FIFO / BPR                        gating.cpp:80-112
+//   expert_demand, run_gating_blocked                  gating.cpp:114-162
+//   resolve_capacity / expert_capacity                 core.cpp:28-59
+//
+// Slot assignment restated: processing tokens in an order O (token order for FIFO; BPR: max gate
+// descending, ties by token index) and giving each (t, j) the next free slot of expert e gives
+//   loc(t, j) = r  if r < capacity else -1,   r = #{t' before t in O : e in idxs(t')}
+// because experts are distinct within a row. FIFO r is a per-expert exclusive prefix count over
+// the flattened (t, j) grid (block histogram + scan + warp match ranks); BPR r is the rank of t's
+// key inside expert e's member list (counted against every other member, exact fp64 compares).
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace moe {
+
+namespace {
+
+constexpr int kGateWarps = 8;
+constexpr int kGateTokPerWarp = 8;
+constexpr int kGateTok = kGateWarps * kGateTokPerWarp;  // 64 tokens per CTA
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v);
+template <>
+__device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 v) {
+  return static_cast<double>(__bfloat162float(v));
+}
+template <>
+__device__ __forceinline__ double to_f64<float>(float v) {
+  return static_cast<double>(v);
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// x: [blocks*T, M] (bf16 or f32), wg: [M, E] fp64 row-major.
+// Outputs idxs/gates [blocks*T, k], hist [n_cta, E] (per-CTA expert counts), optional probs.
+template <typename TX, int EPL>
+__global__ void __launch_bounds__(kGateWarps * 32)
+    gate_topk_kernel(const TX* __restrict__ x, const double* __restrict__ wg, int T, int M, int E,
+                     int k, int cta_per_block, int32_t* __restrict__ idxs,
+                     double* __restrict__ gates, int32_t* __restrict__ hist,
+                     double* __restrict__ probs_out) {
+  constexpr int KC = 32 / EPL;  // k-chunk staged through smem
+  __shared__ double xs[kGateTok][KC];
+  __shared__ double ws[KC][32 * EPL];
+  extern __shared__ int32_t sh_hist[];  // [E]
+
+  const int b = blockIdx.x / cta_per_block;
+  const int c = blockIdx.x % cta_per_block;
+  const int t_begin = b * T + c * kGateTok;
+  const int t_end = min(b * T + T, t_begin + kGateTok);
+  const int ntok = t_end - t_begin;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  for (int e = threadIdx.x; e < E; e += blockDim.x) sh_hist[e] = 0;
+
+  double acc[kGateTokPerWarp][EPL];
+#pragma unroll
+  for (int i = 0; i < kGateTokPerWarp; ++i)
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) acc[i][j] = 0.0;
+
+  for (int k0 = 0; k0 < M; k0 += KC) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kGateTok * KC; i += blockDim.x) {
+      const int tt = i / KC, kk = i % KC;
+      double v = 0.0;
+      if (tt < ntok && k0 + kk < M) v = to_f64(x[static_cast<size_t>(t_begin + tt) * M + k0 + kk]);
+      xs[tt][kk] = v;
+    }
+    for (int i = threadIdx.x; i < KC * 32 * EPL; i += blockDim.x) {
+      const int kk = i / (32 * EPL), e = i % (32 * EPL);
+      ws[kk][e] = (k0 + kk < M && e < E) ? wg[static_cast<size_t>(k0 + kk) * E + e] : 0.0;
+    }
+    __syncthreads();
+    double wr[KC][EPL];
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk)
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) wr[kk][j] = ws[kk][lane + 32 * j];
+#pragma unroll
+    for (int i = 0; i < kGateTokPerWarp; ++i) {
+      const int tt = warp * kGateTokPerWarp + i;
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const double xv = xs[tt][kk];  // warp broadcast
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) acc[i][j] = fma(xv, wr[kk][j], acc[i][j]);
+      }
+    }
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int i = 0; i < kGateTokPerWarp; ++i) {
+    const int tt = warp * kGateTokPerWarp + i;
+    if (tt >= ntok) break;  // warp-uniform
+    const int t = t_begin + tt;
+    double mx = -DBL_MAX;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+      if (lane + 32 * j < E) mx = fmax(mx, acc[i][j]);
+    mx = warp_max(mx);
+    double ex[EPL];
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      ex[j] = (lane + 32 * j < E) ? exp(acc[i][j] - mx) : 0.0;
+      s += ex[j];
+    }
+    s = warp_sum(s);
+    double p[EPL];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) p[j] = ex[j] / s;
+    if (probs_out) {
+#pragma unroll
+      for (int j = 0; j < EPL; ++j)
+        if (lane + 32 * j < E) probs_out[static_cast<size_t>(t) * E + lane + 32 * j] = p[j];
+    }
+    unsigned taken = 0;  // bit j: this lane's expert lane+32j already selected
+    for (int r = 0; r < k; ++r) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E && !(taken & (1u << j)) && (p[j] > bv || (p[j] == bv && e < bi))) {
+          bv = p[j];
+          bi = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      if (lane == 0) {
+        idxs[static_cast<size_t>(t) * k + r] = bi;
+        gates[static_cast<size_t>(t) * k + r] = bv;
+        atomicAdd(&sh_hist[bi], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
+}
+
+// Per (block, expert): exclusive scan of CTA histograms, demand, resolved capacity, fill counts
+// and the member-list base used by BPR. One CTA.
+__global__ void scan_kernel(const int32_t* __restrict__ hist, int blocks, int cta_per_block, int E,
+                            int T, int k, int cap_kind, int cap_formula, int32_t* __restrict__ offs,
+                            int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
+                            int32_t* __restrict__ fill, int32_t* __restrict__ cap_out) {
+  extern __shared__ int32_t sh[];  // [E] max demand over blocks
+  for (int e = threadIdx.x; e < E; e += blockDim.x) sh[e] = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < blocks * E; p += blockDim.x) {
+    const int b = p / E, e = p % E;
+    int run = 0;
+    for (int c = 0; c < cta_per_block; ++c) {
+      const size_t idx = static_cast<size_t>(b * cta_per_block + c) * E + e;
+      offs[idx] = run;
+      run += hist[idx];
+    }
+    demand[p] = run;
+    atomicMax(&sh[e], run);
+  }
+  __syncthreads();
+  __shared__ int32_t cap_sh;
+  if (threadIdx.x == 0) {
+    // resolve_capacity (core.cpp:47-59): max demand floors at 1.
+    int mx = 1;
+    for (int e = 0; e < E; ++e) mx = max(mx, sh[e]);
+    int cap = cap_formula;
+    if (cap_kind == 1) cap = mx;                      // Auto
+    if (cap_kind == 2) cap = min(mx, cap_formula);    // Bounded (formula at max_factor)
+    cap_sh = cap;
+    *cap_out = cap;
+  }
+  __syncthreads();
+  const int cap = cap_sh;
+  for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
+    int run = b * T * k;
+    for (int e = 0; e < E; ++e) {
+      const int d = demand[b * E + e];
+      list_base[b * E + e] = run;
+      fill[b * E + e] = min(d, cap);
+      run += d;
+    }
+  }
+}
+
+// FIFO ranks over the flattened (t, j) grid of each gate CTA. bpr==0: write locations + slots.
+// bpr==1: write the member list (FIFO order) for the BPR rank kernel.
+__global__ void __launch_bounds__(256)
+    assign_kernel(const int32_t* __restrict__ idxs, const double* __restrict__ gates, int T, int k,
+                  int E, int cta_per_block, const int32_t* __restrict__ offs,
+                  const int32_t* __restrict__ list_base, const int32_t* __restrict__ cap_ptr,
+                  int bpr, int32_t* __restrict__ locations, int32_t* __restrict__ slot_token,
+                  float* __restrict__ slot_gate, int32_t* __restrict__ list,
+                  int32_t* __restrict__ drops) {
+  extern __shared__ int32_t sh[];  // cnt[E] + wcnt[8][E]
+  int32_t* cnt = sh;
+  int32_t* wcnt = sh + E;
+  const int b = blockIdx.x / cta_per_block;
+  const int c = blockIdx.x % cta_per_block;
+  const int t_begin = b * T + c * kGateTok;
+  const int t_end = min(b * T + T, t_begin + kGateTok);
+  const int f_begin = t_begin * k, f_end = t_end * k;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int cap = *cap_ptr;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    cnt[e] = offs[static_cast<size_t>(blockIdx.x) * E + e];
+  int my_drops = 0;
+  for (int base = f_begin; base < f_end; base += 256) {
+    for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) wcnt[i] = 0;
+    __syncthreads();
+    const int f = base + threadIdx.x;
+    const bool active = f < f_end;
+    const int e = active ? idxs[f] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, e);
+    const int in_warp = __popc(grp & ((1u << lane) - 1u));
+    if (active && in_warp == 0) wcnt[warp * E + e] = __popc(grp);
+    __syncthreads();
+    if (active) {
+      int r = cnt[e] + in_warp;
+      for (int w = 0; w < warp; ++w) r += wcnt[w * E + e];
+      if (!bpr) {
+        const int loc = r < cap ? r : -1;
+        locations[f] = loc;
+        if (loc >= 0) {
+          const size_t slot = static_cast<size_t>(b * E + e) * cap + loc;
+          slot_token[slot] = f / k;
+          slot_gate[slot] = static_cast<float>(gates[f]);
+        } else {
+          ++my_drops;
+        }
+      } else {
+        list[list_base[b * E + e] + r] = f;
+      }
+    }
+    __syncthreads();
+    for (int ee = threadIdx.x; ee < E; ee += blockDim.x) {
+      int add = 0;
+      for (int w = 0; w < 8; ++w) add += wcnt[w * E + ee];
+      cnt[ee] += add;
+    }
+    __syncthreads();
+  }
+  if (!bpr && my_drops) atomicAdd(drops, my_drops);
+}
+
+// BPR: rank of each member of expert e's list by (max gate desc, token asc).
+// gridDim.x = blocks * E, gridDim.y = ceil(max list length / 256).
+__global__ void __launch_bounds__(256)
+    bpr_rank_kernel(const double* __restrict__ gates, int k, int E,
+                    const int32_t* __restrict__ demand, const int32_t* __restrict__ list_base,
+                    const int32_t* __restrict__ list, const int32_t* __restrict__ cap_ptr,
+                    int32_t* __restrict__ locations, int32_t* __restrict__ slot_token,
+                    float* __restrict__ slot_gate, int32_t* __restrict__ drops) {
+  constexpr int kTile = 1024;
+  __shared__ double keys[kTile];
+  const int be = blockIdx.x;
+  const int b = be / E, e = be % E;
+  const int n = demand[be];
+  const int i = blockIdx.y * 256 + threadIdx.x;
+  if (blockIdx.y * 256 >= n) return;  // CTA-uniform
+  const int32_t* lst = list + list_base[be];
+  const int cap = *cap_ptr;
+  const bool active = i < n;
+  int f = 0;
+  double key = 0.0;
+  if (active) {
+    f = lst[i];
+    key = gates[static_cast<size_t>(f / k) * k];  // row max == first top-k gate
+  }
+  int rank = 0;
+  for (int j0 = 0; j0 < n; j0 += kTile) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < kTile; j += blockDim.x)
+      keys[j] = (j0 + j < n) ? gates[static_cast<size_t>(lst[j0 + j] / k) * k] : -1.0;
+    __syncthreads();
+    if (active) {
+      const int lim = min(kTile, n - j0);
+      for (int j = 0; j < lim; ++j) {
+        const double kj = keys[j];
+        rank += (kj > key) || (kj == key && j0 + j < i);
+      }
+    }
+  }
+  if (!active) return;
+  const int loc = rank < cap ? rank : -1;
+  locations[f] = loc;
+  if (loc >= 0) {
+    const size_t slot = static_cast<size_t>(b * E + e) * cap + loc;
+    slot_token[slot] = f / k;
+    slot_gate[slot] = static_cast<float>(gates[f]);
+  } else {
+    atomicAdd(drops, 1);
+  }
+}
+
+template <typename TX>
+int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E, int k,
+                int32_t* idxs, double* gates, int32_t* hist, double* probs, cudaStream_t st) {
+  const int cpb = (T + kGateTok - 1) / kGateTok;
+  const dim3 grid(blocks * cpb);
+  const size_t sh = static_cast<size_t>(E) * sizeof(int32_t);
+  const TX* xp = static_cast<const TX*>(x);
+  if (E <= 32)
+    gate_topk_kernel<TX, 1><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+                                                                gates, hist, probs);
+  else if (E <= 64)
+    gate_topk_kernel<TX, 2><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+                                                                gates, hist, probs);
+  else if (E <= 128)
+    gate_topk_kernel<TX, 4><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+                                                                gates, hist, probs);
+  else if (E <= 256)
+    gate_topk_kernel<TX, 8><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+                                                                gates, hist, probs);
+  else
+    return -1;
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace
+
+int gate_cta_per_block(int T) { return (T + kGateTok - 1) / kGateTok; }
+
+int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t st) {
+  if (a.E < 1 || a.k < 1 || a.k > a.E || a.k > 32 || a.T < 1 || a.M < 1 || a.blocks < 1) return -1;
+  const int cpb = gate_cta_per_block(a.T);
+  int rc = a.x_is_f32 ? launch_gate<float>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k, g.idxs,
+                                           g.gates, g.hist, g.probs, st)
+                      : launch_gate<__nv_bfloat16>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k,
+                                                   g.idxs, g.gates, g.hist, g.probs, st);
+  if (rc) return rc;
+  scan_kernel<<<1, 1024, a.E * sizeof(int32_t), st>>>(g.hist, a.blocks, cpb, a.E, a.T, a.k,
+                                                      a.cap_kind, a.cap_formula, g.offs, g.demand,
+                                                      g.list_base, g.fill, g.cap);
+  if (cudaGetLastError() != cudaSuccess) return -2;
+  return 0;
+}
+
+int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound,
+                      cudaStream_t st) {
+  const int cpb = gate_cta_per_block(a.T);
+  // Slots not claimed by a token stay -1 (empty capacity rows are zero-filled by encode).
+  if (cudaMemsetAsync(g.slot_token, 0xFF,
+                      static_cast<size_t>(a.blocks) * a.E * cap_bound * sizeof(int32_t), st) !=
+      cudaSuccess)
+    return -2;
+  if (cudaMemsetAsync(g.slot_gate, 0, static_cast<size_t>(a.blocks) * a.E * cap_bound * sizeof(float),
+                      st) != cudaSuccess)
+    return -2;
+  if (cudaMemsetAsync(g.drops, 0, sizeof(int32_t), st) != cudaSuccess) return -2;
+  const size_t sh = static_cast<size_t>(9) * a.E * sizeof(int32_t);
+  assign_kernel<<<a.blocks * cpb, 256, sh, st>>>(g.idxs, g.gates, a.T, a.k, a.E, cpb, g.offs,
+                                                 g.list_base, g.cap, a.bpr, g.locations,
+                                                 g.slot_token, g.slot_gate, g.list, g.drops);
+  if (cudaGetLastError() != cudaSuccess) return -2;
+  if (a.bpr) {
+    const dim3 grid(a.blocks * a.E, (a.T + 255) / 256);
+    bpr_rank_kernel<<<grid, 256, 0, st>>>(g.gates, a.k, a.E, g.demand, g.list_base, g.list, g.cap,
+                                          g.locations, g.slot_token, g.slot_gate, g.drops);
+    if (cudaGetLastError() != cudaSuccess) return -2;
+  }
+  return 0;
+}
+
+}  // namespace moe

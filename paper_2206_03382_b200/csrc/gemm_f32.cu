@@ -1,0 +1,152 @@
+// SIMT expert GEMMs. Same five GEMM kinds and segment addressing as the bf16 tcgen05 kernel
+// (gemm_sm100.cu), fp32 FFMA accumulation. Used for (a) the fp32 layer path (1e-5 tolerance,
+// config C1): the tensor cores have no fp32-exact mode (TF32 keeps 10 mantissa bits); and
+// (b) bf16 shapes the tcgen05 tiling cannot take (N % 256, K % 64 or Mo % 128 != 0, e.g. the
+// reference's tiny unit-test layers).
+// Reference: expert_ffn / expert_ffn_backward, /root/reference/proj/src/parallelism.cpp:103-147.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "gemm_sm100.h"
+#include "kernels.h"
+
+namespace moe {
+
+namespace {
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+__device__ __forceinline__ float ldf(const float* p) { return *p; }
+__device__ __forceinline__ float ldf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void stf(float* p, float v) { *p = v; }
+__device__ __forceinline__ void stf(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+template <int kKind, typename T, typename TD>
+__global__ void __launch_bounds__(256)
+    gemm_simt_kernel(const T* __restrict__ A, const T* __restrict__ B, TD* __restrict__ D,
+                     GemmArgs a) {
+  __shared__ float As[TK][TM + 1];
+  __shared__ float Bs[TK][TN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const bool rowk = kKind == kGemmWgrad;
+  // Tile decode: z = group*S + segment (row-M) or group (row-K)
+  const int n0 = blockIdx.x * TN;
+  const int m0 = blockIdx.y * TM;
+  int g, seg, rows;
+  if (!rowk) {
+    g = blockIdx.z / a.S;
+    const int s = blockIdx.z % a.S;
+    seg = (a.seg_base + s) * a.G + g;
+    rows = a.seg_rows;
+  } else {
+    g = blockIdx.z;
+    seg = 0;
+    rows = a.Mo;
+  }
+  if (m0 >= rows) return;
+  const int K = rowk ? a.S * a.seg_rows : a.K;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int i = threadIdx.x; i < TK * TM; i += 256) {
+      const int kk = i / TM, mm = i % TM;
+      const int k = k0 + kk, m = m0 + mm;
+      float v = 0.0f;
+      if (k < K && m < rows) {
+        if (!rowk) {
+          v = ldf(&A[(static_cast<size_t>(seg) * a.seg_rows + m) * a.K + k]);
+        } else {
+          const int s = k / a.seg_rows, r = k % a.seg_rows;
+          const size_t sg = static_cast<size_t>(a.seg_base + s) * a.G + g;
+          v = ldf(&A[(sg * a.seg_rows + r) * a.Mo + m]);
+        }
+      }
+      As[kk][mm] = v;
+    }
+    for (int i = threadIdx.x; i < TK * TN; i += 256) {
+      const int kk = i / TN, nn = i % TN;
+      const int k = k0 + kk, n = n0 + nn;
+      float v = 0.0f;
+      if (k < K && n < static_cast<int>(a.N)) {
+        if (kKind == kGemmUp || kKind == kGemmDown) {
+          v = ldf(&B[(static_cast<size_t>(g) * a.K + k) * a.N + n]);
+        } else if (kKind == kGemmDgradMask || kKind == kGemmDgrad) {
+          v = ldf(&B[(static_cast<size_t>(g) * a.N + n) * a.K + k]);
+        } else {
+          const int s = k / a.seg_rows, r = k % a.seg_rows;
+          const size_t sg = static_cast<size_t>(a.seg_base + s) * a.G + g;
+          v = ldf(&B[(sg * a.seg_rows + r) * a.N + n]);
+        }
+      }
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= static_cast<int>(a.N)) continue;
+      float v = acc[i][j];
+      size_t off;
+      if (!rowk)
+        off = (static_cast<size_t>(seg) * a.seg_rows + m) * a.N + n;
+      else
+        off = (static_cast<size_t>(g) * a.Mo + m) * a.N + n;
+      if (kKind == kGemmUp) v = fmaxf(v, 0.0f);
+      if (kKind == kGemmDgradMask) v = ldf(static_cast<const T*>(a.aux) + off) > 0.0f ? v : 0.0f;
+      stf(&D[off], v);
+    }
+  }
+}
+
+template <typename T, typename TD>
+int launch_simt(int kind, const T* A, const T* B, TD* D, const GemmArgs& a, cudaStream_t st) {
+  const bool rowk = kind == kGemmWgrad;
+  const int rows = rowk ? a.Mo : a.seg_rows;
+  dim3 grid((a.N + TN - 1) / TN, (rows + TM - 1) / TM, rowk ? a.G : a.G * a.S);
+  switch (kind) {
+    case kGemmUp: gemm_simt_kernel<kGemmUp><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmDown: gemm_simt_kernel<kGemmDown><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmDgradMask: gemm_simt_kernel<kGemmDgradMask><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmDgrad: gemm_simt_kernel<kGemmDgrad><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmWgrad: gemm_simt_kernel<kGemmWgrad><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    default: return -1;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace
+
+int gemm_f32(int kind, const float* A, const float* B, float* D, const GemmArgs& a,
+             cudaStream_t st) {
+  return launch_simt<float, float>(kind, A, B, D, a, st);
+}
+
+// bf16 operands, fp32 accumulation; bf16 output except wgrad (fp32).
+int gemm_bf16_simt(int kind, const void* A, const void* B, void* D, const GemmArgs& a,
+                   cudaStream_t st) {
+  using Bf = __nv_bfloat16;
+  if (kind == kGemmWgrad)
+    return launch_simt<Bf, float>(kind, static_cast<const Bf*>(A), static_cast<const Bf*>(B),
+                                  static_cast<float*>(D), a, st);
+  return launch_simt<Bf, Bf>(kind, static_cast<const Bf*>(A), static_cast<const Bf*>(B),
+                             static_cast<Bf*>(D), a, st);
+}
+
+}  // namespace moe

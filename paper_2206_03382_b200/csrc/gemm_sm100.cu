@@ -1,0 +1,415 @@
+// Expert-FFN grouped GEMM for sm_100a: TMA -> smem (4-stage ring) -> tcgen05.mma (TMEM fp32
+// accumulator, double buffered) -> epilogue warps (tcgen05.ld -> fused op -> swizzled smem ->
+// TMA store). Persistent: one CTA per SM walks a static tile schedule.
+//
+// Replaces the Eigen GEMMs of the reference expert FFN:
+//   expert_ffn          /root/reference/proj/src/parallelism.cpp:103-121  (relu(X.W1).W2)
+//   expert_ffn_backward /root/reference/proj/src/parallelism.cpp:123-147  (dh, dX, dW1, dW2)
+//
+// Two addressing modes cover all six GEMMs of one expert FFN step:
+//   row-M (fwd, dgrad): D[g,(s,r),n] = sum_k A[g,(s,r),k] * B[g,k,n]
+//   row-K (wgrad)     : D[g,mo,n]    = sum_(s,r) A[g,(s,r),mo] * B[g,(s,r),n]
+// "(s, r)" is a token row r of capacity segment s; segments hold `seg_rows` rows and segment
+// (s, g) lives at index (seg_base + s) * G + g of a 3-D [nseg][seg_rows][cols] buffer. This is the
+// (chunk, source rank, local expert, capacity slot) receive layout of the flexible all-to-all
+// (collectives.cpp:123-141), addressed directly by TMA so no interleave copy is ever made.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "gemm_sm100.h"
+#include "ptx.cuh"
+
+namespace moe {
+
+namespace {
+
+constexpr uint32_t BM = 128;  // UMMA M (TMEM lanes)
+constexpr uint32_t BN = 256;  // UMMA N
+constexpr uint32_t BK = 64;   // one 128-byte swizzle atom of bf16 along K
+constexpr uint32_t UK = 16;   // K per tcgen05.mma (bf16)
+constexpr uint32_t kStages = 4;
+constexpr uint32_t kAccStages = 2;
+constexpr uint32_t kTmemCols = kAccStages * BN;  // 512
+constexpr uint32_t kThreads = 256;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-7 epilogue
+constexpr uint32_t kEpiThreads = 128;
+
+constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
+constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
+constexpr uint32_t CD_STAGE_BYTES = BM * 128;     // 128 rows x 128 B
+constexpr uint32_t kCdStages = 2;
+constexpr uint32_t SMEM_A_OFF = 0;
+constexpr uint32_t SMEM_B_OFF = SMEM_A_OFF + kStages * A_STAGE_BYTES;
+constexpr uint32_t SMEM_CD_OFF = SMEM_B_OFF + kStages * B_STAGE_BYTES;
+constexpr uint32_t SMEM_BAR_OFF = SMEM_CD_OFF + kCdStages * CD_STAGE_BYTES;
+constexpr uint32_t SMEM_BYTES = SMEM_BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+
+struct TileCoord {
+  uint32_t g, s, m0, n0;  // row-M: m0 = row within segment; row-K: m0 = output row
+};
+
+template <bool kRowK>
+__device__ __forceinline__ TileCoord tile_coord(const GemmArgs& a, uint32_t tile) {
+  const uint32_t n_tiles = a.N / BN;
+  TileCoord c;
+  c.n0 = (tile % n_tiles) * BN;
+  uint32_t rest = tile / n_tiles;
+  if constexpr (!kRowK) {
+    const uint32_t mts = (a.seg_rows + BM - 1) / BM;
+    c.m0 = (rest % mts) * BM;
+    rest /= mts;
+    c.s = rest % a.S;
+    c.g = rest / a.S;
+  } else {
+    const uint32_t mts = a.Mo / BM;
+    c.m0 = (rest % mts) * BM;
+    c.g = rest / mts;
+    c.s = 0;
+  }
+  return c;
+}
+
+template <bool kRowK>
+__device__ __forceinline__ uint32_t num_tiles(const GemmArgs& a) {
+  if constexpr (!kRowK)
+    return a.G * a.S * ((a.seg_rows + BM - 1) / BM) * (a.N / BN);
+  else
+    return a.G * (a.Mo / BM) * (a.N / BN);
+}
+
+template <bool kRowK>
+__device__ __forceinline__ uint32_t num_kblocks(const GemmArgs& a) {
+  if constexpr (!kRowK)
+    return a.K / BK;
+  else
+    return a.S * ((a.seg_rows + BK - 1) / BK);
+}
+
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmD, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + SMEM_BAR_OFF);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + kAccStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + kAccStages);
+
+  const uint32_t warp = threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmD);
+    for (uint32_t i = 0; i < kStages; ++i) {
+      ptx::mbar_init(&full_bar[i], 1);
+      ptx::mbar_init(&empty_bar[i], 1);
+    }
+    for (uint32_t i = 0; i < kAccStages; ++i) {
+      ptx::mbar_init(&tfull_bar[i], 1);
+      ptx::mbar_init(&tempty_bar[i], kEpiThreads);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const uint32_t ntiles = num_tiles<kRowK>(args);
+  const uint32_t nkb = num_kblocks<kRowK>(args);
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer
+    uint32_t stage = 0, phase = 0;
+    const uint32_t kb_per_seg = (args.seg_rows + BK - 1) / BK;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileCoord tc = tile_coord<kRowK>(args, tile);
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + SMEM_A_OFF + stage * A_STAGE_BYTES;
+        uint8_t* sb = smem + SMEM_B_OFF + stage * B_STAGE_BYTES;
+        if constexpr (!kRowK) {
+          const int seg = static_cast<int>((args.seg_base + tc.s) * args.G + tc.g);
+          const int k0 = static_cast<int>(kb * BK);
+          // A: K-major [seg][seg_rows][K]
+          ptx::tma_load_3d(&tmA, &full_bar[stage], sa, k0, static_cast<int>(tc.m0), seg);
+          if constexpr (!kBMN) {
+            // B: K-major [G][N][K]
+            ptx::tma_load_3d(&tmB, &full_bar[stage], sb, k0, static_cast<int>(tc.n0),
+                             static_cast<int>(tc.g));
+          } else {
+            // B: N-major [G][K][N], four 64-column atoms
+#pragma unroll
+            for (uint32_t a = 0; a < BN / 64; ++a)
+              ptx::tma_load_3d(&tmB, &full_bar[stage], sb + a * (BK * 128),
+                               static_cast<int>(tc.n0 + a * 64), k0, static_cast<int>(tc.g));
+          }
+        } else {
+          const uint32_t s = kb / kb_per_seg;
+          const int r0 = static_cast<int>((kb % kb_per_seg) * BK);
+          const int seg = static_cast<int>((args.seg_base + s) * args.G + tc.g);
+          // A^T: rows are K, MN-major [seg][seg_rows][Mo]
+#pragma unroll
+          for (uint32_t a = 0; a < BM / 64; ++a)
+            ptx::tma_load_3d(&tmA, &full_bar[stage], sa + a * (BK * 128),
+                             static_cast<int>(tc.m0 + a * 64), r0, seg);
+          // B: N-major [seg][seg_rows][N]
+#pragma unroll
+          for (uint32_t a = 0; a < BN / 64; ++a)
+            ptx::tma_load_3d(&tmB, &full_bar[stage], sb + a * (BK * 128),
+                             static_cast<int>(tc.n0 + a * 64), r0, seg);
+        }
+        ptx::mbar_arrive_expect_tx(&full_bar[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, kAMN, kBMN);
+    uint32_t stage = 0, phase = 0;
+    uint32_t iter = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+      const uint32_t acc = iter % kAccStages;
+      const uint32_t acc_phase = (iter / kAccStages) & 1;
+      ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&full_bar[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + SMEM_A_OFF + stage * A_STAGE_BYTES);
+        const uint32_t sb = ptx::smem_u32(smem + SMEM_B_OFF + stage * B_STAGE_BYTES);
+#pragma unroll
+        for (uint32_t k = 0; k < BK / UK; ++k) {
+          // K-major: advance 32 B inside the swizzle atom. MN-major: advance 16 K-rows (2 KiB).
+          const uint64_t adesc = kAMN ? ptx::make_sw128_desc(sa + k * 2048, BK * 128, 1024)
+                                      : ptx::make_sw128_desc(sa + k * 32, 16, 1024);
+          const uint64_t bdesc = kBMN ? ptx::make_sw128_desc(sb + k * 2048, BK * 128, 1024)
+                                      : ptx::make_sw128_desc(sb + k * 32, 16, 1024);
+          ptx::umma_bf16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+        }
+        ptx::umma_commit(&empty_bar[stage]);
+        if (kb == nkb - 1) ptx::umma_commit(&tfull_bar[acc]);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp - 4;           // TMEM lane quadrant == warp % 4
+    const uint32_t row = q * 32 + lane;    // row inside the 128-row tile
+    constexpr uint32_t kColsPerChunk = (kEpi == kEpiF32) ? 32 : 64;  // 128 B of output
+    constexpr uint32_t kChunks = BN / kColsPerChunk;
+    uint32_t iter = 0, cd_stage = 0;
+    const bool leader = (threadIdx.x == 128);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+      const TileCoord tc = tile_coord<kRowK>(args, tile);
+      const uint32_t acc = iter % kAccStages;
+      const uint32_t acc_phase = (iter / kAccStages) & 1;
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16);
+      const int seg = kRowK ? static_cast<int>(tc.g)
+                            : static_cast<int>((args.seg_base + tc.s) * args.G + tc.g);
+      const uint32_t row_in = tc.m0 + row;
+      const bool row_ok = kRowK || row_in < args.seg_rows;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kChunks; ++c) {
+        uint32_t v[64];
+        if constexpr (kEpi == kEpiF32) {
+          uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
+          ptx::tmem_ld_32x32b_x32(tmem_row + c * 32, r0);
+        } else {
+          uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
+          uint32_t (&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32]);
+          ptx::tmem_ld_32x32b_x32(tmem_row + c * 64, r0);
+          ptx::tmem_ld_32x32b_x32(tmem_row + c * 64 + 32, r1);
+        }
+        ptx::tmem_ld_wait();
+        if (c == kChunks - 1) {
+          // Accumulator fully drained into registers: hand TMEM back to the MMA warp.
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty_bar[acc]);
+        }
+        // Make sure the TMA store that last used this staging buffer has read it.
+        if (leader) ptx::tma_store_wait_read<kCdStages - 1>();
+        ptx::named_bar_sync(1, kEpiThreads);
+        uint8_t* cd = smem + SMEM_CD_OFF + cd_stage * CD_STAGE_BYTES;
+        const uint32_t cd_row = ptx::smem_u32(cd) + row * 128;
+        if constexpr (kEpi == kEpiF32) {
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            ptx::st_shared_v4(cd_row + ((j ^ (row & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                              v[4 * j + 3]);
+        } else {
+          float f[64];
+#pragma unroll
+          for (uint32_t i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
+          if constexpr (kEpi == kEpiReluBf16) {
+#pragma unroll
+            for (uint32_t i = 0; i < 64; ++i) f[i] = fmaxf(f[i], 0.0f);
+          }
+          if constexpr (kEpi == kEpiMaskBf16) {
+            // dh = (dY . W2^T) * [h > 0]; the saved activation a = relu(h) carries the mask.
+            if (row_ok) {
+              const uint4* aux = reinterpret_cast<const uint4*>(
+                  static_cast<const uint16_t*>(args.aux) +
+                  ((static_cast<size_t>(seg) * args.seg_rows + row_in) * args.N + tc.n0 + c * 64));
+#pragma unroll
+              for (uint32_t j = 0; j < 8; ++j) {
+                const uint4 w = __ldg(aux + j);
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (uint32_t h = 0; h < 4; ++h) {
+                  // bf16 > 0  <=>  sign bit clear and non-zero magnitude
+                  const uint32_t lo = ww[h] & 0xFFFFu, hi = ww[h] >> 16;
+                  if (!((lo & 0x8000u) == 0 && (lo & 0x7FFFu) != 0)) f[8 * j + 2 * h] = 0.0f;
+                  if (!((hi & 0x8000u) == 0 && (hi & 0x7FFFu) != 0)) f[8 * j + 2 * h + 1] = 0.0f;
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            ptx::st_shared_v4(cd_row + ((j ^ (row & 7)) << 4), ptx::pack_bf16x2(f[8 * j], f[8 * j + 1]),
+                              ptx::pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                              ptx::pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
+                              ptx::pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, kEpiThreads);
+        if (leader) {
+          ptx::tma_store_3d(&tmD, cd, static_cast<int>(tc.n0 + c * kColsPerChunk),
+                            static_cast<int>(tc.m0), seg);
+          ptx::tma_store_commit();
+        }
+        cd_stage = (cd_stage + 1) % kCdStages;
+      }
+    }
+    if (leader) ptx::tma_store_wait_all<0>();
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q{};
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_map_3d(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,
+                uint32_t b0, uint32_t b1) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  const uint64_t esz = f32 ? 4 : 2;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * esz, d0 * d1 * esz};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK>
+int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
+           int num_sms, cudaStream_t stream) {
+  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+        cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  uint32_t tiles;
+  if (!kRowK)
+    tiles = args.G * args.S * ((args.seg_rows + BM - 1) / BM) * (args.N / BN);
+  else
+    tiles = args.G * (args.Mo / BM) * (args.N / BN);
+  if (tiles == 0) return 0;
+  const uint32_t grid = tiles < static_cast<uint32_t>(num_sms) ? tiles : num_sms;
+  kern<<<grid, kThreads, SMEM_BYTES, stream>>>(a, b, d, args);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+}  // namespace
+
+int gemm_validate(const GemmArgs& a, int kind) {
+  if (a.G < 1 || a.S < 1 || a.seg_rows < 1 || a.N < 1) return -1;
+  if (a.N % BN != 0) return -1;
+  if (kind == kGemmWgrad) {
+    if (a.Mo % BM != 0) return -1;
+  } else {
+    if (a.K % BK != 0 || a.K < BK) return -1;
+  }
+  return 0;
+}
+
+// X:[nseg][seg_rows][K] bf16, W:[G][K][N] bf16 (row-major, N-major), D:[nseg][seg_rows][N]
+int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArgs& args,
+             int nseg_total, int num_sms, cudaStream_t stream) {
+  if (gemm_validate(args, kind) != 0) return -1;
+  CUtensorMap ma, mb, md;
+  const uint64_t nseg = static_cast<uint64_t>(nseg_total);
+  int rc = 0;
+  switch (kind) {
+    case kGemmUp:      // act = relu(X . W1)      A K-major, W1 [G][K=M][N=V] N-major
+    case kGemmDown: {  // Y   = act . W2          A K-major, W2 [G][K=V][N=M] N-major
+      rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
+      rc |= make_map_3d(&mb, B, false, args.N, args.K, args.G, 64, 64);
+      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, BM);
+      if (rc) return -2;
+      return kind == kGemmUp ? launch<false, true, kEpiReluBf16, false>(ma, mb, md, args, num_sms, stream)
+                             : launch<false, true, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
+    }
+    case kGemmDgradMask:  // dh = (dY . W2^T) * [a > 0]; W2 [G][V][M] == B K-major [G][N=V][K=M]
+    case kGemmDgrad: {    // dX = dh . W1^T;             W1 [G][M][V] == B K-major [G][N=M][K=V]
+      rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
+      rc |= make_map_3d(&mb, B, false, args.K, args.N, args.G, 64, BN);
+      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, BM);
+      if (rc) return -2;
+      return kind == kGemmDgradMask
+                 ? launch<false, false, kEpiMaskBf16, false>(ma, mb, md, args, num_sms, stream)
+                 : launch<false, false, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
+    }
+    case kGemmWgrad: {  // dW[g] = A[g]^T . B[g] over all (segment, row); fp32 out [G][Mo][N]
+      rc |= make_map_3d(&ma, A, false, args.Mo, args.seg_rows, nseg, 64, 64);
+      rc |= make_map_3d(&mb, B, false, args.N, args.seg_rows, nseg, 64, 64);
+      rc |= make_map_3d(&md, D, true, args.N, args.Mo, args.G, 32, BM);
+      if (rc) return -2;
+      return launch<true, true, kEpiF32, true>(ma, mb, md, args, num_sms, stream);
+    }
+  }
+  return -1;
+}
+
+}  // namespace moe

@@ -1,0 +1,36 @@
+// Grouped expert GEMM (tcgen05/TMEM/TMA, sm_100a). See gemm_sm100.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace moe {
+
+enum GemmKind : int {
+  kGemmUp = 0,         // act[g,(s,r),:V] = relu(X[g,(s,r),:M] . W1[g])          (bf16 out)
+  kGemmDown = 1,       // Y[g,(s,r),:M]   = act . W2[g]                          (bf16 out)
+  kGemmDgradMask = 2,  // dh = (dY . W2[g]^T) * [act > 0]                       (bf16 out)
+  kGemmDgrad = 3,      // dX = dh . W1[g]^T                                     (bf16 out)
+  kGemmWgrad = 4,      // dW[g] = A[g]^T . B[g], reduction over all token rows  (fp32 out)
+};
+
+enum EpiKind : int { kEpiBf16 = 0, kEpiReluBf16 = 1, kEpiMaskBf16 = 2, kEpiF32 = 3 };
+
+struct GemmArgs {
+  uint32_t G;         // groups (local experts)
+  uint32_t S;         // capacity segments per group (pipeline chunks x source ranks)
+  uint32_t seg_rows;  // token rows per segment (capacity chunk cc)
+  uint32_t seg_base;  // first segment of this launch inside the segment buffer
+  uint32_t N;         // output columns
+  uint32_t K;         // reduction length (row-M kinds)
+  uint32_t Mo;        // output rows (wgrad)
+  const void* aux;    // kGemmDgradMask: saved activation, same layout as D
+};
+
+int gemm_validate(const GemmArgs& a, int kind);
+
+int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArgs& args,
+             int nseg_total, int num_sms, cudaStream_t stream);
+
+}  // namespace moe

@@ -1,0 +1,84 @@
+// Internal launch interfaces of the non-GEMM kernels (gating, dispatch, rng).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace moe {
+
+struct GatingArgs {
+  const void* x;       // [blocks*T, M] bf16 or f32
+  int x_is_f32;
+  const double* wg;    // [M, E] fp64
+  int blocks, T, M, E, k;
+  int cap_kind;        // 0 fixed, 1 auto, 2 bounded
+  int cap_formula;     // expert_capacity(k, f, T, E) (fixed) or at max_factor (bounded)
+  int bpr;
+};
+
+struct GatingBuffers {
+  int32_t* idxs;        // [blocks*T, k]
+  double* gates;        // [blocks*T, k]
+  int32_t* locations;   // [blocks*T, k]
+  int32_t* hist;        // [blocks*cta_per_block, E]
+  int32_t* offs;        // [blocks*cta_per_block, E]
+  int32_t* demand;      // [blocks, E]
+  int32_t* list_base;   // [blocks, E]
+  int32_t* fill;        // [blocks, E]
+  int32_t* list;        // [blocks*T*k]
+  int32_t* cap;         // [1] resolved capacity
+  int32_t* drops;       // [1]
+  int32_t* slot_token;  // [blocks, E, cap]
+  float* slot_gate;     // [blocks, E, cap]
+  double* probs;        // optional [blocks*T, E]
+};
+
+int gate_cta_per_block(int T);
+// Router GEMM + softmax + top-k + histogram + capacity resolution (device scalar g.cap).
+int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t st);
+// Location assignment (FIFO or BPR) + slot tables. cap_bound >= resolved capacity.
+int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound, cudaStream_t st);
+
+// Capacity-slot geometry of one source block: degree d chunks of cc slots (cap <= d*cc).
+// Row of slot (b, e, c) in a [blocks][d][E][cc][M] buffer:
+//   b*d*E*cc + ((c / cc) * E + e) * cc + c % cc
+struct SlotGeom {
+  int blocks, T, E, M, k, cap, cc, degree;
+};
+
+// dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype)
+int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
+                  cudaStream_t st);
+int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
+                  const int32_t* locations, const double* gates, void* y, cudaStream_t st);
+int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
+                           const int32_t* slot_token, const float* slot_gate, void* dz,
+                           cudaStream_t st);
+// Optional d_gates[t, j] = <Z[e, loc], dy[t]> (dispatch.cpp:143-156); 0 for dropped.
+int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
+                                 const int32_t* idxs, const int32_t* locations, double* dgates,
+                                 cudaStream_t st);
+int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
+                           const int32_t* locations, void* dx, cudaStream_t st);
+
+int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* idxs,
+                       const int32_t* locations, const double* gates, int32_t* slot_token,
+                       float* slot_gate, cudaStream_t st);
+
+// splitmix64 counter stream (core.cpp:66-83): value n (0-based) = lo + (hi-lo) * u(seed, n+1).
+int fill_uniform_device(void* dst, int dtype /*0 bf16, 1 f32, 2 f64*/, int64_t n, uint64_t seed,
+                        uint64_t offset, double lo, double hi, cudaStream_t st);
+// Same stream, strided gather: dst[i*cols + j] = draw(offset + i*src_stride + j) for a sub-block.
+int fill_uniform_2d_device(void* dst, int dtype, int64_t rows, int64_t cols, int64_t src_stride,
+                           uint64_t seed, uint64_t offset, double lo, double hi, cudaStream_t st);
+
+// fp32 SIMT GEMM path (the 1e-5 fp32 layer): same kinds/addressing as the bf16 tcgen05 GEMM.
+struct GemmArgs;
+int gemm_f32(int kind, const float* A, const float* B, float* D, const GemmArgs& args,
+             cudaStream_t st);
+int gemm_bf16_simt(int kind, const void* A, const void* B, void* D, const GemmArgs& args,
+                   cudaStream_t st);
+
+}  // namespace moe

@@ -1,0 +1,625 @@
+// Per-rank MoE layer: gate -> encode -> flexible all-to-all -> expert FFN -> all-to-all ->
+// decode, and the reverse pass. One handle per GPU; NCCL grouped send/recv over NVLink for the
+// exchanges; capacity-chunk pipelining on a compute stream and a comm stream.
+//
+// Restates LayerState / forward / backward of /root/reference/proj/src/moe_layer.cpp:
+//   init draw order          :144-163     forward  :171-244     backward :246-319
+// Per-rank placement P1 (moe_layer.cpp:138-140): experts are resident full-width on their owner
+// (gathered once from ZeRO slices, parallelism.cpp:149-206) instead of re-gathered per step;
+// nothing updates weights between steps, so this is numerically identical.
+#include "layer.h"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gemm_sm100.h"
+#include "kernels.h"
+
+namespace moe {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw MoeError(MOE_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ckr(int rc, const char* what) {
+  if (rc == -1) throw MoeError(MOE_EINVAL, std::string(what) + ": invalid arguments");
+  if (rc != 0) {
+    cudaError_t e = cudaGetLastError();
+    throw MoeError(MOE_ECUDA, std::string(what) + ": launch failed (" + cudaGetErrorString(e) + ")");
+  }
+}
+void ckn(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw MoeError(MOE_ECOMM, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+}  // namespace
+
+// Round-to-nearest-even double -> bf16 bits without passing through fp32 (no double rounding).
+uint16_t bf16_bits_rne(double x) {
+  uint64_t u;
+  std::memcpy(&u, &x, 8);
+  if ((u & 0x7FF0000000000000ULL) != 0x7FF0000000000000ULL) {
+    const uint64_t lsb = (u >> 45) & 1;
+    u += (1ULL << 44) - 1 + lsb;
+    u &= ~((1ULL << 45) - 1);
+  }
+  double r;
+  std::memcpy(&r, &u, 8);
+  const float f = static_cast<float>(r);  // exact: r has <= 8 significant bits
+  uint32_t fb;
+  std::memcpy(&fb, &f, 4);
+  return static_cast<uint16_t>(fb >> 16);
+}
+
+int64_t expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts) {
+  if (k < 1 || tokens < 1 || experts < 1 || !(f > 0.0))
+    throw MoeError(MOE_EINVAL, "expert_capacity: inputs must be positive");
+  const double q = static_cast<double>(k) * f * static_cast<double>(tokens) / static_cast<double>(experts);
+  const int64_t cap = static_cast<int64_t>(std::ceil(q - 1e-9));
+  return std::max<int64_t>(cap, 1);
+}
+
+void validate(const moe_config& c) {
+  if (c.world_size < 1 || c.gpus_per_node < 1) throw MoeError(MOE_EINVAL, "Dims: W and m must be >= 1");
+  if (c.world_size % c.gpus_per_node != 0)
+    throw MoeError(MOE_EINVAL, "Dims: world size must be a multiple of gpus per node");
+  if (c.global_experts < 1) throw MoeError(MOE_EINVAL, "Dims: E must be >= 1");
+  if (c.top_k < 1 || c.top_k > c.global_experts) throw MoeError(MOE_EINVAL, "Dims: need 1 <= k <= E");
+  if (c.model_dim < 1 || c.hidden_dim < 1 || c.tokens_per_step < 1)
+    throw MoeError(MOE_EINVAL, "Dims: M, V, T must be >= 1");
+  if (c.global_experts % c.world_size != 0)
+    throw MoeError(MOE_EINVAL, "Dims: ExpertsPerRank(x) requires E = W*x");
+  if (c.hidden_dim % c.world_size != 0)
+    throw MoeError(MOE_EINVAL, "ExpertParams: hidden dim must divide into parameter slices");
+  if (c.top_k > 32) throw MoeError(MOE_EINVAL, "top_k > 32 unsupported");
+  if (c.global_experts > 256) throw MoeError(MOE_EINVAL, "E > 256 unsupported by the gate kernel");
+  if (c.dtype != MOE_DTYPE_BF16 && c.dtype != MOE_DTYPE_F32) throw MoeError(MOE_EINVAL, "dtype");
+  if (c.capacity_kind < 0 || c.capacity_kind > 2) throw MoeError(MOE_EINVAL, "capacity kind");
+  if (c.capacity_kind != MOE_CAP_AUTO && !(c.capacity_factor > 0.0))
+    throw MoeError(MOE_EINVAL, "capacity factor must be positive");
+  if (c.degree != 1 && c.degree != 2 && c.degree != 4 && c.degree != 8)
+    throw MoeError(MOE_EINVAL, "pipelining degree must be 1, 2, 4 or 8");
+  if (c.model_dim > (1 << 20) || c.hidden_dim > (1 << 20) || c.tokens_per_step > (1 << 26))
+    throw MoeError(MOE_EINVAL, "dims too large");
+}
+
+DevMem::~DevMem() {
+  if (p) cudaFree(p);
+}
+void DevMem::alloc(size_t n) {
+  if (n <= bytes) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  ck(cudaMalloc(&p, n), "cudaMalloc");
+  bytes = n;
+}
+
+Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device)
+    : cfg_(cfg), rank_(rank), device_(device) {
+  validate(cfg);
+  W_ = static_cast<int>(cfg.world_size);
+  E_ = static_cast<int>(cfg.global_experts);
+  dE_ = E_ / W_;
+  M_ = static_cast<int>(cfg.model_dim);
+  V_ = static_cast<int>(cfg.hidden_dim);
+  T_ = static_cast<int>(cfg.tokens_per_step);
+  k_ = static_cast<int>(cfg.top_k);
+  esz_ = cfg.dtype == MOE_DTYPE_BF16 ? 2 : 4;
+  if (rank < 0 || rank >= W_) throw MoeError(MOE_EINVAL, "rank out of range");
+  if (cfg.capacity_kind != MOE_CAP_FIXED)
+    throw MoeError(MOE_EINVAL, "layer: Auto/Bounded capacity is available through moe_op_gating only");
+  cap_ = static_cast<int>(expert_capacity(k_, cfg.capacity_factor, T_, E_));
+  cap_alloc_ = 0;
+  for (int d : {1, 2, 4, 8}) cap_alloc_ = std::max(cap_alloc_, d * ((cap_ + d - 1) / d));
+
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) throw MoeError(MOE_ECUDA, "no such CUDA device");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10) throw MoeError(MOE_ECUDA, "sm_100 (B200) device required");
+  num_sms_ = prop.multiProcessorCount;
+
+  ck(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreateWithFlags(&ev_fwd_start_, cudaEventDefault), "event");
+  ck(cudaEventCreateWithFlags(&ev_fwd_end_, cudaEventDefault), "event");
+  ck(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming), "event");
+  for (int i = 0; i < 8; ++i) {
+    ck(cudaEventCreateWithFlags(&ev_a_[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_b_[i], cudaEventDisableTiming), "event");
+  }
+  ck(cudaEventCreateWithFlags(&ev_comm_done_, cudaEventDisableTiming), "event");
+
+  if (W_ > 1) {
+    if (!nccl_id) throw MoeError(MOE_EINVAL, "W > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ckn(ncclCommInitRank(&comm_, W_, id, rank_), "ncclCommInitRank");
+  }
+
+  const size_t Tk = static_cast<size_t>(T_) * k_;
+  const size_t cpb = gate_cta_per_block(T_);
+  wg_.alloc(sizeof(double) * M_ * E_);
+  w1_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
+  w2_.alloc(static_cast<size_t>(esz_) * dE_ * V_ * M_);
+  dw1_.alloc(sizeof(float) * dE_ * M_ * V_);
+  dw2_.alloc(sizeof(float) * dE_ * V_ * M_);
+  ck(cudaMemset(wg_.p, 0, wg_.bytes), "memset");
+  ck(cudaMemset(w1_.p, 0, w1_.bytes), "memset");
+  ck(cudaMemset(w2_.p, 0, w2_.bytes), "memset");
+
+  idxs_.alloc(4 * Tk);
+  gates_.alloc(8 * Tk);
+  locs_.alloc(4 * Tk);
+  hist_.alloc(4 * cpb * E_);
+  offs_.alloc(4 * cpb * E_);
+  demand_.alloc(4 * E_);
+  list_base_.alloc(4 * E_);
+  fill_.alloc(4 * E_);
+  list_.alloc(4 * Tk);
+  capd_.alloc(4);
+  drops_.alloc(4);
+  slot_token_.alloc(4 * static_cast<size_t>(E_) * cap_);
+  slot_gate_.alloc(4 * static_cast<size_t>(E_) * cap_);
+
+  const size_t rowsM = static_cast<size_t>(E_) * cap_alloc_ * M_ * esz_;
+  const size_t rowsV = static_cast<size_t>(E_) * cap_alloc_ * V_ * esz_;
+  z_.alloc(rowsM);
+  act_.alloc(rowsV);
+  yexp_.alloc(rowsM);
+  dz_.alloc(rowsM);
+  dh_.alloc(rowsV);
+  dxe_.alloc(rowsM);
+  if (W_ > 1) {
+    recv_.alloc(rowsM);
+    ycomb_.alloc(rowsM);
+    drecv_.alloc(rowsM);
+    dxcomb_.alloc(rowsM);
+  }
+}
+
+Layer::~Layer() {
+  if (comm_) ncclCommDestroy(comm_);
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  cudaEventDestroy(ev_fwd_start_);
+  cudaEventDestroy(ev_fwd_end_);
+  cudaEventDestroy(ev_sync_);
+  cudaEventDestroy(ev_comm_done_);
+  for (int i = 0; i < 8; ++i) {
+    cudaEventDestroy(ev_a_[i]);
+    cudaEventDestroy(ev_b_[i]);
+  }
+}
+
+uint64_t Layer::expert_draw_offset(int64_t e) const {
+  return static_cast<uint64_t>(M_) * E_ + 256ULL * (M_ + E_) + static_cast<uint64_t>(e) * 2 * M_ * V_;
+}
+
+void Layer::init_params(uint64_t seed) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ckr(fill_uniform_device(wg_.p, MOE_DTYPE_F64, static_cast<int64_t>(M_) * E_, seed, 0, -1.0, 1.0, 0),
+      "init router");
+  const int dt = cfg_.dtype == MOE_DTYPE_BF16 ? 0 : 1;
+  const size_t mv = static_cast<size_t>(M_) * V_;
+  for (int le = 0; le < dE_; ++le) {
+    const uint64_t o = expert_draw_offset(static_cast<int64_t>(rank_) * dE_ + le);
+    ckr(fill_uniform_device(static_cast<char*>(w1_.p) + le * mv * esz_, dt, mv, seed, o, -0.5, 0.5, 0),
+        "init w1");
+    ckr(fill_uniform_device(static_cast<char*>(w2_.p) + le * mv * esz_, dt, mv, seed, o + mv, -0.5, 0.5, 0),
+        "init w2");
+  }
+  ck(cudaDeviceSynchronize(), "init_params");
+}
+
+void Layer::set_router(const double* wg) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaMemcpy(wg_.p, wg, sizeof(double) * M_ * E_, cudaMemcpyHostToDevice), "set_router");
+}
+
+void Layer::upload_weights(void* dst, const double* src, size_t n) {
+  if (cfg_.dtype == MOE_DTYPE_BF16) {
+    std::vector<uint16_t> buf(n);
+    for (size_t i = 0; i < n; ++i) buf[i] = bf16_bits_rne(src[i]);
+    ck(cudaMemcpy(dst, buf.data(), 2 * n, cudaMemcpyHostToDevice), "upload");
+  } else {
+    std::vector<float> buf(n);
+    for (size_t i = 0; i < n; ++i) buf[i] = static_cast<float>(src[i]);
+    ck(cudaMemcpy(dst, buf.data(), 4 * n, cudaMemcpyHostToDevice), "upload");
+  }
+}
+
+void Layer::set_expert(int64_t le, const double* w1, const double* w2) {
+  if (le < 0 || le >= dE_) throw MoeError(MOE_EINVAL, "set_expert: local expert out of range");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  const size_t mv = static_cast<size_t>(M_) * V_;
+  upload_weights(static_cast<char*>(w1_.p) + le * mv * esz_, w1, mv);
+  upload_weights(static_cast<char*>(w2_.p) + le * mv * esz_, w2, mv);
+}
+
+// gather_computed_experts (parallelism.cpp:149-206) for per-rank placement: rank q holds slice q
+// (w1 cols / w2 rows [q*h, (q+1)*h), h = V/W) of every expert; one grouped exchange sends each
+// destination its experts' slices (w1 slice row-major, then w2 slice), then the owner assembles.
+void Layer::set_expert_slices(const double* w1s, const double* w2s) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  const int h = V_ / W_;
+  const size_t slice = static_cast<size_t>(2) * M_ * h;  // elements per (expert, slice)
+  // Pack my slices of every expert in destination order (experts are rank-major).
+  std::vector<double> packed(static_cast<size_t>(E_) * slice);
+  for (int e = 0; e < E_; ++e) {
+    std::memcpy(&packed[e * slice], w1s + static_cast<size_t>(e) * M_ * h, sizeof(double) * M_ * h);
+    std::memcpy(&packed[e * slice + static_cast<size_t>(M_) * h], w2s + static_cast<size_t>(e) * h * M_,
+                sizeof(double) * h * M_);
+  }
+  DevMem send, recv;
+  send.alloc(packed.size() * esz_);
+  recv.alloc(packed.size() * esz_);
+  upload_weights(send.p, packed.data(), packed.size());
+  const size_t per_peer = static_cast<size_t>(dE_) * slice;
+  if (W_ == 1) {
+    ck(cudaMemcpy(recv.p, send.p, per_peer * esz_, cudaMemcpyDeviceToDevice), "gather");
+  } else {
+    const ncclDataType_t dt = cfg_.dtype == MOE_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
+    ckn(ncclGroupStart(), "group");
+    for (int p = 0; p < W_; ++p) {
+      ckn(ncclSend(static_cast<char*>(send.p) + p * per_peer * esz_, per_peer, dt, p, comm_, comm_stream_), "send");
+      ckn(ncclRecv(static_cast<char*>(recv.p) + p * per_peer * esz_, per_peer, dt, p, comm_, comm_stream_), "recv");
+    }
+    ckn(ncclGroupEnd(), "group");
+    ck(cudaStreamSynchronize(comm_stream_), "gather sync");
+  }
+  // recv block q = slice q of my dE experts -> full weights (strided 2-D copies).
+  const size_t mv = static_cast<size_t>(M_) * V_;
+  for (int q = 0; q < W_; ++q)
+    for (int le = 0; le < dE_; ++le) {
+      const char* base = static_cast<const char*>(recv.p) + (q * per_peer + le * slice) * esz_;
+      char* w1 = static_cast<char*>(w1_.p) + le * mv * esz_;
+      char* w2 = static_cast<char*>(w2_.p) + le * mv * esz_;
+      // w1 slice (M, h) -> columns [q*h, (q+1)*h) of (M, V)
+      ck(cudaMemcpy2D(w1 + static_cast<size_t>(q) * h * esz_, static_cast<size_t>(V_) * esz_, base,
+                      static_cast<size_t>(h) * esz_, static_cast<size_t>(h) * esz_, M_,
+                      cudaMemcpyDeviceToDevice),
+         "assemble w1");
+      // w2 slice (h, M) -> rows [q*h, (q+1)*h) of (V, M)
+      ck(cudaMemcpy(w2 + static_cast<size_t>(q) * h * M_ * esz_, base + static_cast<size_t>(M_) * h * esz_,
+                    static_cast<size_t>(h) * M_ * esz_, cudaMemcpyDeviceToDevice),
+         "assemble w2");
+    }
+  ck(cudaDeviceSynchronize(), "set_expert_slices");
+}
+
+bool Layer::tc_ok(int kind, const GemmArgs& a) const {
+  if (cfg_.dtype != MOE_DTYPE_BF16) return false;
+  if (a.N % 256 != 0) return false;
+  if (kind == kGemmWgrad) return a.Mo % 128 == 0;
+  return a.K % 64 == 0;
+}
+
+void Layer::gemm(int kind, const void* A, const void* B, void* D, const GemmArgs& a, int nseg,
+                 cudaStream_t st) {
+  int rc;
+  if (cfg_.dtype == MOE_DTYPE_F32)
+    rc = gemm_f32(kind, static_cast<const float*>(A), static_cast<const float*>(B),
+                  static_cast<float*>(D), a, st);
+  else if (tc_ok(kind, a))
+    rc = gemm_fwd(static_cast<GemmKind>(kind), A, B, D, a, nseg, num_sms_, st);
+  else
+    rc = gemm_bf16_simt(kind, A, B, D, a, st);
+  ckr(rc, "expert gemm");
+  ++launches_;
+}
+
+GatingArgs Layer::gating_args(const void* x) const {
+  GatingArgs g{};
+  g.x = x;
+  g.x_is_f32 = cfg_.dtype == MOE_DTYPE_F32;
+  g.wg = static_cast<const double*>(wg_.p);
+  g.blocks = 1;
+  g.T = T_;
+  g.M = M_;
+  g.E = E_;
+  g.k = k_;
+  g.cap_kind = MOE_CAP_FIXED;
+  g.cap_formula = cap_;
+  g.bpr = cfg_.bpr;
+  return g;
+}
+
+GatingBuffers Layer::gating_buffers() {
+  GatingBuffers b{};
+  b.idxs = static_cast<int32_t*>(idxs_.p);
+  b.gates = static_cast<double*>(gates_.p);
+  b.locations = static_cast<int32_t*>(locs_.p);
+  b.hist = static_cast<int32_t*>(hist_.p);
+  b.offs = static_cast<int32_t*>(offs_.p);
+  b.demand = static_cast<int32_t*>(demand_.p);
+  b.list_base = static_cast<int32_t*>(list_base_.p);
+  b.fill = static_cast<int32_t*>(fill_.p);
+  b.list = static_cast<int32_t*>(list_.p);
+  b.cap = static_cast<int32_t*>(capd_.p);
+  b.drops = static_cast<int32_t*>(drops_.p);
+  b.slot_token = static_cast<int32_t*>(slot_token_.p);
+  b.slot_gate = static_cast<float*>(slot_gate_.p);
+  b.probs = nullptr;
+  return b;
+}
+
+SlotGeom Layer::geom() const {
+  SlotGeom g{};
+  g.blocks = 1;
+  g.T = T_;
+  g.E = E_;
+  g.M = M_;
+  g.k = k_;
+  g.cap = cap_;
+  g.cc = cc_;
+  g.degree = degree_;
+  return g;
+}
+
+// One grouped exchange of W equal blocks (all2all_linear, collectives.cpp:48-56):
+// block p of `send` -> rank p, block p of `recv` <- rank p.
+void Layer::exchange(const void* send, size_t send_stride, void* recv, size_t recv_stride,
+                     size_t elems) {
+  const ncclDataType_t dt = cfg_.dtype == MOE_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
+  ckn(ncclGroupStart(), "ncclGroupStart");
+  for (int p = 0; p < W_; ++p) {
+    ckn(ncclSend(static_cast<const char*>(send) + p * send_stride * esz_, elems, dt, p, comm_,
+                 comm_stream_),
+        "ncclSend");
+    ckn(ncclRecv(static_cast<char*>(recv) + p * recv_stride * esz_, elems, dt, p, comm_, comm_stream_),
+        "ncclRecv");
+  }
+  ckn(ncclGroupEnd(), "ncclGroupEnd");
+  comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
+}
+
+void Layer::forward(const void* x, void* y, cudaStream_t st) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  launches_ = 0;
+  comm_bytes_ = 0.0;
+  f_ = static_cast<double>(cap_) * E_ / (static_cast<double>(k_) * T_);  // capacity_to_factor
+  strategy_ = cfg_.adaptive ? get_strategy(memo_, f_) : Strategy{0, cfg_.degree};
+  // 2DH degenerates to the linear algorithm inside one NVSwitch domain (collectives.cpp:58-88
+  // with m == W); it is executed as linear and reported as chosen.
+  degree_ = W_ == 1 ? 1 : strategy_.degree;
+  cc_ = (cap_ + degree_ - 1) / degree_;
+  ck(cudaEventRecord(ev_fwd_start_, st), "event");
+
+  // --- gating: router GEMM + softmax + top-k + capacity + slots (per source block)
+  GatingArgs ga = gating_args(x);
+  GatingBuffers gb = gating_buffers();
+  ckr(run_gating_device(ga, gb, st), "gating");
+  ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
+  launches_ += 3 + (cfg_.bpr ? 1 : 0);
+
+  const SlotGeom g = geom();
+  ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st), "encode");
+  ++launches_;
+
+  const size_t seg = static_cast<size_t>(cc_) * M_;          // elements per (segment) block
+  const size_t segV = static_cast<size_t>(cc_) * V_;
+  const int nseg = degree_ * W_ * dE_;
+  GemmArgs up{};
+  up.G = dE_;
+  up.S = W_;
+  up.seg_rows = cc_;
+  up.N = V_;
+  up.K = M_;
+  GemmArgs down = up;
+  down.N = M_;
+  down.K = V_;
+
+  void* recv = W_ > 1 ? recv_.p : z_.p;
+  void* ycomb = W_ > 1 ? ycomb_.p : yexp_.p;
+  if (W_ == 1) {
+    up.seg_base = 0;
+    down.seg_base = 0;
+    gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+    gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+  } else {
+    // Comm stream: all dispatches (chunk order), then all combines (reference FIFO order,
+    // pipeline.cpp:180-190); compute stream: per chunk up+down GEMMs.
+    ck(cudaEventRecord(ev_sync_, st), "event");
+    ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+    for (int i = 0; i < degree_; ++i) {
+      // chunk i of z: [E][cc][M] at i*E*seg; peer p gets experts [p*dE, (p+1)*dE)
+      exchange(static_cast<char*>(z_.p) + i * E_ * seg * esz_, dE_ * seg,
+               static_cast<char*>(recv) + i * W_ * dE_ * seg * esz_, dE_ * seg, dE_ * seg);
+      ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+    }
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
+      up.seg_base = i * W_;
+      down.seg_base = i * W_;
+      gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+      gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+      ck(cudaEventRecord(ev_b_[i], st), "event");
+    }
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+      exchange(static_cast<char*>(yexp_.p) + i * W_ * dE_ * seg * esz_, dE_ * seg,
+               static_cast<char*>(ycomb) + i * E_ * seg * esz_, dE_ * seg, dE_ * seg);
+    }
+    ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
+    ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
+  }
+  (void)segV;
+  ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
+  ++launches_;
+  ck(cudaEventRecord(ev_fwd_end_, st), "event");
+  fwd_done_ = true;
+  metrics_valid_ = false;
+  if (cfg_.adaptive) {
+    ck(cudaEventSynchronize(ev_fwd_end_), "event sync");
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");
+    double sec = ms * 1e-3;
+    if (W_ > 1) sec = allreduce_max_host(sec);
+    optimize_strategy(memo_, f_, strategy_, sec);
+  }
+}
+
+double Layer::allreduce_max_host(double v) {
+  DevMem d;
+  d.alloc(sizeof(double));
+  ck(cudaMemcpy(d.p, &v, sizeof(double), cudaMemcpyHostToDevice), "copy");
+  ckn(ncclAllReduce(d.p, d.p, 1, ncclFloat64, ncclMax, comm_, comm_stream_), "allreduce");
+  ck(cudaStreamSynchronize(comm_stream_), "sync");
+  ck(cudaMemcpy(&v, d.p, sizeof(double), cudaMemcpyDeviceToHost), "copy");
+  return v;
+}
+
+void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStream_t st) {
+  if (!fwd_done_) throw MoeError(MOE_ESTATE, "backward: no saved forward");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  const SlotGeom g = geom();
+  GatingBuffers gb = gating_buffers();
+  float* gw1 = dw1 ? dw1 : static_cast<float*>(dw1_.p);
+  float* gw2 = dw2 ? dw2 : static_cast<float*>(dw2_.p);
+  const int64_t l0 = launches_;
+
+  // dZ = decode^T(dy): slot-major gather of g * dy (fast_decode_backward_range)
+  ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st), "decode_bwd");
+  ++launches_;
+
+  const size_t seg = static_cast<size_t>(cc_) * M_;
+  const int nseg = degree_ * W_ * dE_;
+  GemmArgs dgm{};  // dh = (dY . W2^T) * [a > 0]
+  dgm.G = dE_;
+  dgm.S = W_;
+  dgm.seg_rows = cc_;
+  dgm.N = V_;
+  dgm.K = M_;
+  dgm.aux = act_.p;
+  GemmArgs dg = dgm;  // dX = dh . W1^T
+  dg.N = M_;
+  dg.K = V_;
+  dg.aux = nullptr;
+  GemmArgs wg1{};  // dW1 = X^T dh over every (chunk, source) segment
+  wg1.G = dE_;
+  wg1.S = degree_ * W_;
+  wg1.seg_rows = cc_;
+  wg1.seg_base = 0;
+  wg1.N = V_;
+  wg1.Mo = M_;
+  GemmArgs wg2 = wg1;  // dW2 = a^T dY
+  wg2.N = M_;
+  wg2.Mo = V_;
+
+  void* recv = W_ > 1 ? recv_.p : z_.p;
+  void* drecv = W_ > 1 ? drecv_.p : dz_.p;
+  void* dxcomb = W_ > 1 ? dxcomb_.p : dxe_.p;
+  if (W_ == 1) {
+    gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
+    gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+    gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
+    gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
+  } else {
+    ck(cudaEventRecord(ev_sync_, st), "event");
+    ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+    for (int i = 0; i < degree_; ++i) {  // adjoint of combine
+      exchange(static_cast<char*>(dz_.p) + i * E_ * seg * esz_, dE_ * seg,
+               static_cast<char*>(drecv) + i * W_ * dE_ * seg * esz_, dE_ * seg, dE_ * seg);
+      ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+    }
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
+      dgm.seg_base = i * W_;
+      dg.seg_base = i * W_;
+      gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
+      gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+      ck(cudaEventRecord(ev_b_[i], st), "event");
+    }
+    for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
+      ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+      exchange(static_cast<char*>(dxe_.p) + i * W_ * dE_ * seg * esz_, dE_ * seg,
+               static_cast<char*>(dxcomb) + i * E_ * seg * esz_, dE_ * seg, dE_ * seg);
+    }
+    ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
+    // Weight gradients overlap the last return exchanges.
+    gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
+    gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
+    ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
+  }
+  ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st), "encode_bwd");
+  ++launches_;
+  bwd_launches_ = launches_ - l0;
+  if (dw1) last_dw1_ = nullptr; else last_dw1_ = gw1;
+  if (dw2) last_dw2_ = nullptr; else last_dw2_ = gw2;
+}
+
+void Layer::ensure_io() {
+  const size_t n = static_cast<size_t>(T_) * M_ * esz_;
+  io_x_.alloc(n);
+  io_y_.alloc(n);
+  io_dy_.alloc(n);
+  io_dx_.alloc(n);
+}
+
+void Layer::forward_host(const void* xh, void* yh, cudaStream_t st) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ensure_io();
+  const size_t n = static_cast<size_t>(T_) * M_ * esz_;
+  ck(cudaMemcpyAsync(io_x_.p, xh, n, cudaMemcpyHostToDevice, st), "h2d x");
+  forward(io_x_.p, io_y_.p, st);
+  ck(cudaMemcpyAsync(yh, io_y_.p, n, cudaMemcpyDeviceToHost, st), "d2h y");
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
+void Layer::backward_host(const void* dyh, void* dxh, cudaStream_t st) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ensure_io();
+  const size_t n = static_cast<size_t>(T_) * M_ * esz_;
+  ck(cudaMemcpyAsync(io_dy_.p, dyh, n, cudaMemcpyHostToDevice, st), "h2d dy");
+  backward(io_dy_.p, io_dx_.p, nullptr, nullptr, st);
+  ck(cudaMemcpyAsync(dxh, io_dx_.p, n, cudaMemcpyDeviceToHost, st), "d2h dx");
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
+void Layer::get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* capacity) {
+  if (!fwd_done_) throw MoeError(MOE_ESTATE, "get_routing: no forward yet");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaDeviceSynchronize(), "sync");
+  const size_t Tk = static_cast<size_t>(T_) * k_;
+  if (idxs) ck(cudaMemcpy(idxs, idxs_.p, 4 * Tk, cudaMemcpyDeviceToHost), "copy");
+  if (locs) ck(cudaMemcpy(locs, locs_.p, 4 * Tk, cudaMemcpyDeviceToHost), "copy");
+  if (gates) ck(cudaMemcpy(gates, gates_.p, 8 * Tk, cudaMemcpyDeviceToHost), "copy");
+  if (capacity) *capacity = cap_;
+}
+
+void Layer::get_metrics(moe_step_metrics* m) {
+  if (!fwd_done_) throw MoeError(MOE_ESTATE, "get_metrics: no forward yet");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaEventSynchronize(ev_fwd_end_), "sync");
+  float ms = 0.0f;
+  ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");
+  int32_t drops = 0;
+  ck(cudaMemcpy(&drops, drops_.p, 4, cudaMemcpyDeviceToHost), "copy");
+  m->f = f_;
+  m->capacity = cap_;
+  m->a2a_algo = strategy_.algo;
+  m->degree = strategy_.degree;
+  m->seconds = ms * 1e-3;
+  m->comm_bytes = comm_bytes_;
+  m->drop_count = drops;
+}
+
+void Layer::get_grads(float* dw1, float* dw2) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaDeviceSynchronize(), "sync");
+  const size_t n = static_cast<size_t>(dE_) * M_ * V_;
+  if (dw1) ck(cudaMemcpy(dw1, dw1_.p, 4 * n, cudaMemcpyDeviceToHost), "copy");
+  if (dw2) ck(cudaMemcpy(dw2, dw2_.p, 4 * n, cudaMemcpyDeviceToHost), "copy");
+}
+
+}  // namespace moe

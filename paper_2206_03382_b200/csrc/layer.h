@@ -1,0 +1,99 @@
+// Internal C++ layer object behind the C ABI (include/moe_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/moe_b200.h"
+#include "gemm_sm100.h"
+#include "kernels.h"
+#include "strategy.h"
+
+namespace moe {
+
+struct MoeError : std::runtime_error {
+  int code;
+  MoeError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem();
+  void alloc(size_t n);
+};
+
+uint16_t bf16_bits_rne(double x);
+int64_t expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts);
+void validate(const moe_config& c);
+
+class Layer {
+ public:
+  Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device);
+  ~Layer();
+
+  void init_params(uint64_t seed);
+  void set_router(const double* wg);
+  void set_expert(int64_t le, const double* w1, const double* w2);
+  void set_expert_slices(const double* w1s, const double* w2s);
+  void forward(const void* x, void* y, cudaStream_t st);
+  void backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStream_t st);
+  void forward_host(const void* xh, void* yh, cudaStream_t st);
+  void backward_host(const void* dyh, void* dxh, cudaStream_t st);
+  void get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* capacity);
+  void get_metrics(moe_step_metrics* m);
+  void get_grads(float* dw1, float* dw2);
+  void* w1() { return w1_.p; }
+  void* w2() { return w2_.p; }
+  int64_t launches() const { return launches_; }
+
+  std::string err;
+
+ private:
+  uint64_t expert_draw_offset(int64_t e) const;
+  void upload_weights(void* dst, const double* src, size_t n);
+  bool tc_ok(int kind, const GemmArgs& a) const;
+  void gemm(int kind, const void* A, const void* B, void* D, const GemmArgs& a, int nseg,
+            cudaStream_t st);
+  GatingArgs gating_args(const void* x) const;
+  GatingBuffers gating_buffers();
+  SlotGeom geom() const;
+  void exchange(const void* send, size_t send_stride, void* recv, size_t recv_stride, size_t elems);
+  double allreduce_max_host(double v);
+  void ensure_io();
+
+  moe_config cfg_;
+  int rank_, device_;
+  int W_, E_, dE_, M_, V_, T_, k_, esz_;
+  int cap_, cap_alloc_;
+  int degree_ = 1, cc_ = 1;
+  int num_sms_ = 148;
+  double f_ = 1.0;
+  Strategy strategy_;
+  StrategyMemo memo_;
+  bool fwd_done_ = false, metrics_valid_ = false;
+  int64_t launches_ = 0, bwd_launches_ = 0;
+  double comm_bytes_ = 0.0;
+  float* last_dw1_ = nullptr;
+  float* last_dw2_ = nullptr;
+
+  cudaStream_t comm_stream_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+  cudaEvent_t ev_fwd_start_{}, ev_fwd_end_{}, ev_sync_{}, ev_comm_done_{};
+  cudaEvent_t ev_a_[8]{}, ev_b_[8]{};
+
+  DevMem wg_, w1_, w2_, dw1_, dw2_;
+  DevMem idxs_, gates_, locs_, hist_, offs_, demand_, list_base_, fill_, list_, capd_, drops_;
+  DevMem slot_token_, slot_gate_;
+  DevMem z_, recv_, act_, yexp_, ycomb_, dz_, drecv_, dh_, dxe_, dxcomb_;
+  DevMem io_x_, io_y_, io_dy_, io_dx_;
+};
+
+}  // namespace moe
