@@ -1,11 +1,15 @@
 // SIMT expert GEMMs. Same five GEMM kinds and segment addressing as the bf16 tcgen05 kernel
-// (gemm_sm100.cu), fp32 FFMA accumulation. Used for (a) the fp32 layer path (1e-5 tolerance,
+// (gemm_sm100.cu). The fp32 layer accumulates in fp64 (DFMA; fp32 x fp32 products are exact in
+// fp64), so the ReLU mask [h > 0] agrees with the fp64 reference except for |h| < ~1e-13 and the
+// 1e-5 bound holds for gradients too; the bf16 SIMT fallback accumulates in fp32. Used for (a) the fp32 layer path (1e-5 tolerance,
 // config C1): the tensor cores have no fp32-exact mode (TF32 keeps 10 mantissa bits); and
 // (b) bf16 shapes the tcgen05 tiling cannot take (N % 256, K % 64 or Mo % 128 != 0, e.g. the
 // reference's tiny unit-test layers).
 // Reference: expert_ffn / expert_ffn_backward, /root/reference/proj/src/parallelism.cpp:103-147.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "gemm_sm100.h"
 #include "kernels.h"
@@ -45,7 +49,8 @@ __global__ void __launch_bounds__(256)
   }
   if (m0 >= rows) return;
   const int K = rowk ? a.S * a.seg_rows : a.K;
-  float acc[4][4] = {};
+  using Acc = typename std::conditional<std::is_same<T, float>::value, double, float>::type;
+  Acc acc[4][4] = {};
   for (int k0 = 0; k0 < K; k0 += TK) {
     for (int i = threadIdx.x; i < TK * TM; i += 256) {
       const int kk = i / TM, mm = i % TM;
@@ -82,7 +87,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
-      float av[4], bv[4];
+      Acc av[4], bv[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
 #pragma unroll
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -102,7 +107,7 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
       if (n >= static_cast<int>(a.N)) continue;
-      float v = acc[i][j];
+      float v = static_cast<float>(acc[i][j]);
       size_t off;
       if (!rowk)
         off = (static_cast<size_t>(seg) * a.seg_rows + m) * a.N + n;

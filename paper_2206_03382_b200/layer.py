@@ -1,0 +1,259 @@
+"""Python mirror of the reference layer API (moe_layer.hpp) over the C ABI.
+
+    state = LayerState.init(MoELayerConfig(...), seed=402)     # LayerState::init
+    res = forward(state, x)                                    # forward(state, x)
+    grads = backward(state, res.saved, dy)                     # backward(state, saved, dy)
+
+x / dy are this rank's (T, M) token block as torch CUDA tensors in the layer dtype. All work
+runs in libmoe_b200.so (sm_100a kernels + NCCL); there is no Python or CPU compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import MoeConfig, StepMetrics, check, lib
+
+_DT = {"bf16": _lib.DTYPE_BF16, "f32": _lib.DTYPE_F32}
+_TORCH_DT = {"bf16": torch.bfloat16, "f32": torch.float32}
+_CAP = {"fixed": _lib.CAP_FIXED, "auto": _lib.CAP_AUTO, "bounded": _lib.CAP_BOUNDED}
+
+
+@dataclass
+class MoELayerConfig:
+    """MoELayerConfig + Dims (moe_layer.hpp:22-29, core.hpp:32-56), per-rank placement."""
+    world_size: int = 1
+    gpus_per_node: int = 1
+    global_experts: int = 1
+    model_dim: int = 1
+    hidden_dim: int = 1
+    tokens_per_step: int = 1
+    top_k: int = 1
+    capacity: str = "fixed"
+    capacity_factor: float = 1.0
+    bpr: bool = False
+    dtype: str = "bf16"
+    adaptive: bool = False
+    degree: int = 1
+
+    def to_c(self) -> MoeConfig:
+        return MoeConfig(self.world_size, self.gpus_per_node, self.global_experts, self.model_dim,
+                         self.hidden_dim, self.tokens_per_step, self.top_k, _CAP[self.capacity],
+                         float(self.capacity_factor), int(self.bpr), _DT[self.dtype],
+                         int(self.adaptive), int(self.degree))
+
+    @property
+    def local_experts(self) -> int:
+        return self.global_experts // self.world_size
+
+    @property
+    def torch_dtype(self) -> torch.dtype:
+        return _TORCH_DT[self.dtype]
+
+    def validate(self) -> None:
+        c = self.to_c()
+        check(lib().moe_validate_config(C.byref(c)))
+
+
+@dataclass
+class StepMetricsPy:
+    f: float
+    capacity: int
+    a2a_algo: str
+    degree: int
+    seconds: float
+    comm_bytes: float
+    drop_count: int
+
+
+@dataclass
+class SavedForward:
+    """Handle-owned saved tensors of the last forward (SavedForward, moe_layer.hpp:56-66)."""
+    step: int
+
+
+@dataclass
+class ForwardResult:
+    y: torch.Tensor
+    saved: SavedForward
+    state: "LayerState" = field(repr=False, default=None)
+
+    @property
+    def metrics(self) -> StepMetricsPy:
+        return self.state.metrics()
+
+
+@dataclass
+class LayerGrads:
+    dx: torch.Tensor
+    dw1: torch.Tensor  # (E/W, M, V) fp32, local experts
+    dw2: torch.Tensor  # (E/W, V, M) fp32
+
+
+def _ptr(t: torch.Tensor | None):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(device) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class LayerState:
+    """One rank's layer (LayerState, moe_layer.hpp:33-44) backed by a moe_handle."""
+
+    def __init__(self, config: MoELayerConfig, rank: int = 0, device: int = 0,
+                 nccl_id: bytes | None = None):
+        self.config = config
+        self.rank = rank
+        self.device = torch.device("cuda", device)
+        self._h = C.c_void_p()
+        c = config.to_c()
+        check(lib().moe_create(C.byref(c), rank, nccl_id, device, C.byref(self._h)))
+        self._step = 0
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().moe_get_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def init(cls, config: MoELayerConfig, seed: int, rank: int = 0, device: int = 0,
+             nccl_id: bytes | None = None) -> "LayerState":
+        """LayerState::init (moe_layer.cpp:144-163) with the Rng(seed) draw order."""
+        s = cls(config, rank, device, nccl_id)
+        check(lib().moe_init_params(s._h, C.c_uint64(seed)), s._h)
+        return s
+
+    def close(self) -> None:
+        if self._h:
+            lib().moe_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- parameters
+    def set_router(self, wg) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(wg, np.float64)
+        check(lib().moe_set_router(self._h, a.ctypes.data_as(C.c_void_p)), self._h)
+
+    def set_expert(self, local_e: int, w1, w2) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(w1, np.float64)
+        b = np.ascontiguousarray(w2, np.float64)
+        check(lib().moe_set_expert(self._h, local_e, a.ctypes.data_as(C.c_void_p),
+                                   b.ctypes.data_as(C.c_void_p)), self._h)
+
+    def set_expert_slices(self, w1_slices, w2_slices) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(w1_slices, np.float64)
+        b = np.ascontiguousarray(w2_slices, np.float64)
+        check(lib().moe_set_expert_slices(self._h, a.ctypes.data_as(C.c_void_p),
+                                          b.ctypes.data_as(C.c_void_p)), self._h)
+
+    def weights(self):
+        """Device views (E/W, M, V) / (E/W, V, M) of the resident local expert weights."""
+        cfg = self.config
+        out = []
+        for which, shape in ((1, (cfg.local_experts, cfg.model_dim, cfg.hidden_dim)),
+                             (2, (cfg.local_experts, cfg.hidden_dim, cfg.model_dim))):
+            p = C.c_void_p()
+            check(lib().moe_get_weights_device(self._h, which, C.byref(p)), self._h)
+            n = shape[0] * shape[1] * shape[2]
+            esz = 2 if cfg.dtype == "bf16" else 4
+            out.append(_from_ptr(p.value, n * esz, cfg.torch_dtype, shape, self.device))
+        return out
+
+    # -- results
+    def routing(self):
+        import numpy as np
+        cfg = self.config
+        n = cfg.tokens_per_step * cfg.top_k
+        idxs = np.empty(n, np.int32)
+        loc = np.empty(n, np.int32)
+        gates = np.empty(n, np.float64)
+        cap = C.c_int64()
+        check(lib().moe_get_routing(self._h, idxs.ctypes.data_as(C.c_void_p),
+                                    loc.ctypes.data_as(C.c_void_p),
+                                    gates.ctypes.data_as(C.c_void_p), C.byref(cap)), self._h)
+        k = cfg.top_k
+        return idxs.reshape(-1, k), loc.reshape(-1, k), gates.reshape(-1, k), cap.value
+
+    def metrics(self) -> StepMetricsPy:
+        m = StepMetrics()
+        check(lib().moe_get_metrics(self._h, C.byref(m)), self._h)
+        return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
+                             m.seconds, m.comm_bytes, m.drop_count)
+
+    def kernel_launches(self) -> int:
+        return int(lib().moe_kernel_launches(self._h))
+
+    @property
+    def handle(self):
+        return self._h
+
+
+def _from_ptr(ptr: int, nbytes: int, dtype, shape, device):
+    """Zero-copy torch view of handle-owned device memory (lifetime bound to the handle)."""
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+        }
+    raw = torch.as_tensor(_Holder(), device=device)
+    return raw.view(dtype).view(*shape)
+
+
+def forward(state: LayerState, x: torch.Tensor, y: torch.Tensor | None = None) -> ForwardResult:
+    """forward(state, x) (moe_layer.cpp:171-244) for this rank's (T, M) block."""
+    cfg = state.config
+    if x.shape != (cfg.tokens_per_step, cfg.model_dim) or x.dtype != cfg.torch_dtype:
+        raise _lib.MoeError(_lib.MOE_EINVAL, "forward: expected (T, M) input in the layer dtype")
+    if not x.is_cuda or not x.is_contiguous():
+        raise _lib.MoeError(_lib.MOE_EINVAL, "forward: x must be a contiguous CUDA tensor")
+    if y is None:
+        y = torch.empty_like(x)
+    check(lib().moe_forward(state.handle, _ptr(x), _ptr(y), _stream(x.device)), state.handle)
+    state._step += 1
+    return ForwardResult(y=y, saved=SavedForward(step=state._step), state=state)
+
+
+def backward(state: LayerState, saved: SavedForward, dy: torch.Tensor,
+             dx: torch.Tensor | None = None, dw1: torch.Tensor | None = None,
+             dw2: torch.Tensor | None = None) -> LayerGrads:
+    """backward(state, saved, dy) (moe_layer.cpp:246-319): routing/gates frozen to the plan."""
+    cfg = state.config
+    if saved.step != state._step:
+        raise _lib.MoeError(_lib.MOE_ESTATE, "backward: saved forward is stale")
+    if dy.shape != (cfg.tokens_per_step, cfg.model_dim) or dy.dtype != cfg.torch_dtype:
+        raise _lib.MoeError(_lib.MOE_EINVAL, "backward: expected (T, M) gradient in the layer dtype")
+    dev = dy.device
+    if dx is None:
+        dx = torch.empty_like(dy)
+    nE, M, V = cfg.local_experts, cfg.model_dim, cfg.hidden_dim
+    if dw1 is None:
+        dw1 = torch.empty(nE, M, V, device=dev, dtype=torch.float32)
+    if dw2 is None:
+        dw2 = torch.empty(nE, V, M, device=dev, dtype=torch.float32)
+    check(lib().moe_backward(state.handle, _ptr(dy), _ptr(dx), _ptr(dw1), _ptr(dw2),
+                             _stream(dev)), state.handle)
+    return LayerGrads(dx=dx, dw1=dw1, dw2=dw2)
+
+
+def forward_host(state: LayerState, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+    """forward with host (pinned) buffers: H2D + forward + D2H inside the call."""
+    check(lib().moe_forward_host(state.handle, _ptr(x_host), _ptr(y_host),
+                                 _stream(state.device)), state.handle)
+    state._step += 1
+
+
+def backward_host(state: LayerState, dy_host: torch.Tensor, dx_host: torch.Tensor) -> None:
+    check(lib().moe_backward_host(state.handle, _ptr(dy_host), _ptr(dx_host),
+                                  _stream(state.device)), state.handle)
