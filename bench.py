@@ -1,0 +1,398 @@
+#!/usr/bin/env python3
+"""Benchmark: MoE layer tokens/s (fwd+bwd) on B200, per BASELINE.json's metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W]
+
+N=1: the north-star SwinV2-MoE-B layer "TGT" (E=32, k=1, f=1.0, M=1024, V=4096, 32K tokens,
+bf16). N>1 (torchrun, one rank per GPU, NCCL): expert parallelism with the configs[3] per-GPU
+shape -- 8 experts and 64K tokens per GPU (E = 8N), flexible all-to-all + capacity pipelining --
+so per-GPU work is fixed as N grows (weak scaling).
+
+A step = gate -> encode -> dispatch -> expert FFN -> combine -> decode, then the full backward
+(dx and every expert dW), on synthetic inputs drawn with the reference Rng(402) recipe on the
+device. Timing: W untimed warm-up steps, barrier + synchronize, CUDA events around exactly K
+steps, max over ranks. The per-step working set (weights 512 MiB + activations > 1 GiB per GPU)
+is far larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+--impl reference times the reference algorithm on the host CPU: the fp64 oracle restatement
+(oracle/, "port") because the C++ reference needs Eigen, absent from this image; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (E, k, f, M, V, tokens per GPU, bpr, dtype)
+    "TGT": dict(E=32, k=1, f=1.0, M=1024, V=4096, T=32768, bpr=False, dtype="bf16",
+                desc="SwinV2-MoE-B layer (north-star target): E=32 k=1 f=1.0 M=1024 H=4096 32K tokens"),
+    "C1": dict(E=8, k=1, f=1.0, M=512, V=2048, T=4096, bpr=False, dtype="f32",
+               desc="configs[0]: single MoE layer fp32 E=8 k=1 f=1.0 M=512 H=2048 4096 tokens"),
+    "C2": dict(E=32, k=1, f=1.0, M=768, V=3072, T=32768, bpr=False, dtype="bf16",
+               desc="configs[1]: SwinV2-MoE-S layer E=32 k=1 f=1.0 M=768 H=3072 32K tokens"),
+    "C3": dict(E=32, k=2, f=1.25, M=1024, V=4096, T=32768, bpr=True, dtype="bf16",
+               desc="configs[2]: SwinV2-MoE-B top-2 + BPR E=32 k=2 f=1.25 M=1024 H=4096 32K tokens"),
+    "C4": dict(E=8, k=1, f=1.0, M=1024, V=4096, T=65536, bpr=False, dtype="bf16",
+               desc="configs[3] per GPU: 8 experts/GPU (E=8N) k=1 f=1.0 M=1024 H=4096 64K tokens/GPU"),
+}
+SEED = 402
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d["bf16_tflops_sustained"],
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def pick_workload(args, world):
+    if args.workload:
+        return args.workload
+    return "TGT" if world == 1 else "C4"
+
+
+def layer_dims(wl: str, world: int) -> dict:
+    d = dict(WORKLOADS[wl])
+    if wl == "C4":
+        d["E"] = 8 * world
+    elif world > 1:
+        d["E"] = d["E"] * world  # same per-GPU expert count
+    return d
+
+
+# ------------------------------------------------------------------ CPU reference leg
+def prepare_cpu(d: dict, sample_tokens: int):
+    """Inputs for the fp64 oracle (the reference algorithm restated in C, OpenMP) on a token
+    sample of the same layer; returns a callable running one fwd+bwd sample."""
+    import numpy as np
+    import oracle
+    from paper_2206_03382_b200 import rng
+    E, k, f, M, V = d["E"], d["k"], d["f"], d["M"], d["V"]
+    T = sample_tokens
+    off = rng.draw_offsets(M, E, V, 1, T)
+    wg = rng.uniform(SEED, off["wg"], M * E).reshape(M, E)
+    w1 = np.empty((E, M, V))
+    w2 = np.empty((E, V, M))
+    for e in range(E):
+        o = off["experts"] + e * off["expert_stride"]
+        w1[e] = rng.round_dtype(rng.uniform(SEED, o, M * V, -0.5, 0.5), d["dtype"]).reshape(M, V)
+        w2[e] = rng.round_dtype(rng.uniform(SEED, o + M * V, V * M, -0.5, 0.5),
+                                d["dtype"]).reshape(V, M)
+    x = rng.round_dtype(rng.uniform(SEED, off["x"], T * M), d["dtype"]).reshape(T, M)
+    dy = rng.round_dtype(rng.uniform(SEED, off["x"] + T * M, T * M), d["dtype"]).reshape(T, M)
+
+    def run():
+        oracle.layer_step(x, wg, w1, w2, dy, 1, k, 0, f, d["bpr"])
+    return run, oracle.num_threads()
+
+
+def cpu_reference(d: dict, sample_tokens: int, min_seconds: float, max_iters: int):
+    run, threads = prepare_cpu(d, sample_tokens)
+    run()  # warm
+    iters, t0 = 0, time.perf_counter()
+    while True:
+        run()
+        iters += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or iters >= max_iters:
+            break
+    return sample_tokens * iters / el, threads, el, iters
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    wl = pick_workload(args, world)
+    d = layer_dims(wl, world)
+    sample = max(256, d["T"] // 16)
+    run, threads = prepare_cpu(d, sample)
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    el = time.perf_counter() - t0
+    value = sample * args.steps / el
+    line = {
+        "impl": "reference", "metric": "MoE layer tokens/s (fwd+bwd)", "value": value,
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng(402) draw order)",
+        "config": {"workload": wl, "desc": d["desc"], "E": d["E"], "k": d["k"], "f": d["f"],
+                   "M": d["M"], "V": d["V"], "tokens_per_gpu": d["T"], "bpr": d["bpr"],
+                   "parallelism": f"ep{world}"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} of {d['T']} tokens per step (same E, k, f, M, V; "
+                                   f"capacity scales with tokens), fp64 oracle restatement "
+                                   f"(reference needs Eigen 3, absent)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--degree", type=int, default=0, help="pipelining degree (0: adaptive Alg. 1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_03382_b200 import LayerState, MoELayerConfig, backward, forward, ops, rng
+    from paper_2206_03382_b200 import layer as L
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = pick_workload(args, world)
+    d = layer_dims(wl, world)
+    E, k, f, M, V, T = d["E"], d["k"], d["f"], d["M"], d["V"], d["T"]
+    tdt = torch.bfloat16 if d["dtype"] == "bf16" else torch.float32
+    esz = 2 if d["dtype"] == "bf16" else 4
+
+    nccl_id = None
+    if world > 1:
+        obj = [LayerState.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    adaptive = world > 1 and args.degree == 0
+    cfg = MoELayerConfig(world_size=world, gpus_per_node=world, global_experts=E, model_dim=M,
+                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f,
+                         bpr=d["bpr"], dtype=d["dtype"], adaptive=adaptive,
+                         degree=args.degree if args.degree else 1)
+    state = LayerState.init(cfg, SEED, rank=rank, device=local, nccl_id=nccl_id)
+    off = rng.draw_offsets(M, E, V, world, T)
+    x = torch.empty(T, M, dtype=tdt, device=dev)
+    dy = torch.empty(T, M, dtype=tdt, device=dev)
+    ops.fill_uniform(x, SEED, off["x"] + rank * T * M)
+    ops.fill_uniform(dy, SEED, off["dy"] + rank * T * M)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    dw1 = torch.empty(cfg.local_experts, M, V, dtype=torch.float32, device=dev)
+    dw2 = torch.empty(cfg.local_experts, V, M, dtype=torch.float32, device=dev)
+
+    def step():
+        res = forward(state, x, y)
+        backward(state, res.saved, dy, dx, dw1, dw2)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    state.take_profile()  # drop warm-up records
+    state.set_profiling(True)
+    stream = torch.cuda.current_stream(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+    state.set_profiling(False)
+    ms = ev0.elapsed_time(ev1)
+    prof = state.take_profile()
+    launches_per_step = state.kernel_launches()
+    metrics = state.metrics()
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * T / (ms_step * 1e-3)
+
+    # roofline: expert GEMMs (tensor-bound) -- 12 * rows * M * V per step over capacity rows
+    peaks = load_peaks()
+    cap = metrics.capacity
+    rows = cfg.local_experts * world * cap  # capacity rows per GPU: dE * (W * dC)
+    gemm_flops = 12.0 * rows * M * V
+    gemm_names = ["gemm_up", "gemm_down", "gemm_dgrad_mask", "gemm_dgrad", "gemm_wgrad1",
+                  "gemm_wgrad2"]
+    gemm_ms = sum(prof[n][0] for n in gemm_names) / args.steps
+    gemm_launches = sum(prof[n][1] for n in gemm_names) / args.steps
+    achieved_tf = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(wl)
+        except Exception:
+            traffic = None
+    # dispatch/combine HBM rooflines (algorithmic bytes)
+    drops = metrics.drop_count
+    kept = T * k - drops
+    slots = E * cap if world == 1 else E * cap  # encode writes every slot of every expert
+    enc_bytes = (slots * M + kept * M) * esz + T * k * 8
+    dec_bytes = (kept * M + T * M) * esz + T * k * 16
+    enc_ms = prof["encode"][0] / args.steps
+    dec_ms = prof["decode"][0] / args.steps
+    dbwd_ms = prof["decode_bwd"][0] / args.steps
+    ebwd_ms = prof["encode_bwd"][0] / args.steps
+    gbs = lambda b, t: b / (t * 1e-3) / 1e9 if t > 0 else None  # noqa: E731
+    phases_ms = {n: round(prof[n][0] / args.steps, 4) for n in prof}
+
+    # end to end through the host-buffer C ABI (H2D of x, dy and D2H of y, dx every step)
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        dyh = dy.cpu().pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        dxh = torch.empty_like(xh).pin_memory()
+        for _ in range(2):
+            L.forward_host(state, xh, yh)
+            L.backward_host(state, dyh, dxh)
+        barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(3, args.steps // 2)
+        for _ in range(n_e2e):
+            L.forward_host(state, xh, yh)
+            L.backward_host(state, dyh, dxh)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * T * n_e2e / el, "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * T * M * esz, "d2h_bytes_per_step": 2 * T * M * esz,
+               "steps": n_e2e, "api": "moe_forward_host + moe_backward_host (C ABI, pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = max(256, T // 16)
+        v, thr, el, it = cpu_reference(d, sample, 10.0, 50)
+        cpu = {"value": v, "unit": "tokens/s", "cores": thr, "kind": "port",
+               "sample": f"{it} x {sample}-token fwd+bwd samples of {wl} ({el:.1f} s), fp64 oracle "
+                         f"restatement of the reference (Eigen absent, reference unbuildable)"}
+
+    if rank == 0:
+        line = {
+            "metric": "MoE layer tokens/s (fwd+bwd)", "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": d["dtype"], "data": "synthetic (reference Rng(402) draw order, on device)",
+            "config": {"workload": wl, "desc": d["desc"], "E": E, "k": k, "f": f, "M": M, "V": V,
+                       "tokens_per_gpu": T, "global_batch": world * T, "bpr": d["bpr"],
+                       "capacity": cap, "parallelism": f"ep{world}",
+                       "degree": metrics.degree, "adaptive": adaptive,
+                       "l2": "per-step working set >1 GiB/GPU >> 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_sus"],
+                         "unit": "TFLOP/s",
+                         "frac": achieved_tf / peaks["bf16_sus"] if achieved_tf else None,
+                         "traffic": traffic,
+                         "kernel": "gemm_bf16_kernel (tcgen05 expert GEMMs, 6 launches/step)",
+                         "algorithmic": f"12*rows*M*V per step, rows={rows} capacity rows/GPU",
+                         "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
+                         "peak_source": peaks["source"] + " bf16_tflops_sustained"},
+            "dispatch": {"encode_gbs": gbs(enc_bytes, enc_ms), "decode_gbs": gbs(dec_bytes, dec_ms),
+                         "decode_bwd_gbs": gbs(enc_bytes, dbwd_ms),
+                         "encode_bwd_gbs": gbs(dec_bytes, ebwd_ms), "hbm_peak_gbs": peaks["hbm"],
+                         "encode_frac": (gbs(enc_bytes, enc_ms) or 0) / peaks["hbm"],
+                         "decode_frac": (gbs(dec_bytes, dec_ms) or 0) / peaks["hbm"]},
+            "phases_ms": phases_ms,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "drop_count": drops,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    state.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -68,6 +68,8 @@ typedef struct moe_step_metrics {
   double seconds;      /* forward device time (CUDA events), 0 if not measured */
   double comm_bytes;   /* bytes this rank sent in the forward all-to-alls */
   int64_t drop_count;  /* dropped (token, expert) assignments on this rank */
+  int64_t relu_fixups; /* bf16 path: up-GEMM outputs re-decided in fp64 (ReLU-mask certificate,
+                          last chunk of the last forward) */
 } moe_step_metrics;
 
 typedef struct moe_handle moe_handle;
@@ -132,6 +134,14 @@ int moe_get_expert_grads(moe_handle* h, float* dw1_host, float* dw2_host);
 int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr);
 /* Number of kernels launched by the last forward + backward (benchmark bookkeeping). */
 int64_t moe_kernel_launches(const moe_handle* h);
+/* Measured timeline (replaces the simulated Timeline of pipeline.hpp:36-46): when on, every
+ * phase is bracketed by CUDA events on the stream it runs on. Phases, in order: gate, encode,
+ * gemm_up, gemm_down, decode, decode_bwd, gemm_dgrad_mask, gemm_dgrad, gemm_wgrad1,
+ * gemm_wgrad2, encode_bwd, a2a_fwd, a2a_bwd (MOE_NUM_PHASES). */
+#define MOE_NUM_PHASES 13
+int moe_set_profiling(moe_handle* h, int32_t on);
+/* Per-phase summed milliseconds and interval counts since the last call (synchronizes). */
+int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n);
 
 /* ---------------------------------------------------------------- stateless device ops
  * All pointers are device memory; each call is stream-ordered on `stream` and allocates its

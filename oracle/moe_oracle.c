@@ -319,56 +319,41 @@ void orc_flex_combine(const double* in, int64_t W, int64_t E, int64_t dC, int64_
 }
 
 /* ------------------------------------------------------------------ dense fp64 GEMMs */
-/* C (m,n) = A (m,kk) . B (kk,n), row-major, parallel over row blocks. */
-static void dgemm_nn(const double* A, const double* B, double* Cm, int64_t m, int64_t n,
-                     int64_t kk) {
-  const int64_t MB = 32, KB = 256, NB = 1024;
+/* C (m,n) = op(A) . B, row-major; op(A) = A (m,kk) or A^T with A (kk,m). Parallel over
+ * (row block, column block) tiles so small per-expert row counts still use every core. */
+static void dgemm_impl(const double* A, int trans_a, const double* B, double* Cm, int64_t m,
+                       int64_t n, int64_t kk) {
+  const int64_t MB = 16, KB = 256, NB = 256;
+  const int64_t mb = (m + MB - 1) / MB, nb = (n + NB - 1) / NB;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t i0 = 0; i0 < m; i0 += MB) {
-    const int64_t i1 = i0 + MB < m ? i0 + MB : m;
-    for (int64_t i = i0; i < i1; ++i) memset(Cm + i * n, 0, sizeof(double) * (size_t)n);
-    for (int64_t j0 = 0; j0 < n; j0 += NB) {
-      const int64_t j1 = j0 + NB < n ? j0 + NB : n;
-      for (int64_t k0 = 0; k0 < kk; k0 += KB) {
-        const int64_t k1 = k0 + KB < kk ? k0 + KB : kk;
-        for (int64_t i = i0; i < i1; ++i) {
-          double* c = Cm + i * n;
-          for (int64_t p = k0; p < k1; ++p) {
-            const double a = A[i * kk + p];
-            if (a == 0.0) continue;
-            const double* b = B + p * n;
-            for (int64_t j = j0; j < j1; ++j) c[j] += a * b[j];
-          }
+  for (int64_t tile = 0; tile < mb * nb; ++tile) {
+    const int64_t i0 = (tile / nb) * MB, j0 = (tile % nb) * NB;
+    const int64_t i1 = i0 + MB < m ? i0 + MB : m, j1 = j0 + NB < n ? j0 + NB : n;
+    for (int64_t i = i0; i < i1; ++i)
+      for (int64_t j = j0; j < j1; ++j) Cm[i * n + j] = 0.0;
+    for (int64_t k0 = 0; k0 < kk; k0 += KB) {
+      const int64_t k1 = k0 + KB < kk ? k0 + KB : kk;
+      for (int64_t i = i0; i < i1; ++i) {
+        double* c = Cm + i * n;
+        for (int64_t p = k0; p < k1; ++p) {
+          const double a = trans_a ? A[p * m + i] : A[i * kk + p];
+          const double* b = B + p * n;
+          for (int64_t j = j0; j < j1; ++j) c[j] += a * b[j];
         }
       }
     }
   }
 }
 
+static void dgemm_nn(const double* A, const double* B, double* Cm, int64_t m, int64_t n,
+                     int64_t kk) {
+  dgemm_impl(A, 0, B, Cm, m, n, kk);
+}
+
 /* C (m,n) = A^T . B with A (kk,m), B (kk,n). */
 static void dgemm_tn(const double* A, const double* B, double* Cm, int64_t m, int64_t n,
                      int64_t kk) {
-  const int64_t MB = 32, KB = 256, NB = 1024;
-#pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t i0 = 0; i0 < m; i0 += MB) {
-    const int64_t i1 = i0 + MB < m ? i0 + MB : m;
-    for (int64_t i = i0; i < i1; ++i) memset(Cm + i * n, 0, sizeof(double) * (size_t)n);
-    for (int64_t j0 = 0; j0 < n; j0 += NB) {
-      const int64_t j1 = j0 + NB < n ? j0 + NB : n;
-      for (int64_t k0 = 0; k0 < kk; k0 += KB) {
-        const int64_t k1 = k0 + KB < kk ? k0 + KB : kk;
-        for (int64_t i = i0; i < i1; ++i) {
-          double* c = Cm + i * n;
-          for (int64_t p = k0; p < k1; ++p) {
-            const double a = A[p * m + i];
-            if (a == 0.0) continue;
-            const double* b = B + p * n;
-            for (int64_t j = j0; j < j1; ++j) c[j] += a * b[j];
-          }
-        }
-      }
-    }
-  }
+  dgemm_impl(A, 1, B, Cm, m, n, kk);
 }
 
 static double* transpose(const double* A, int64_t r, int64_t c) {

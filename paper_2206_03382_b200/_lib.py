@@ -16,6 +16,9 @@ MOE_OK, MOE_EINVAL, MOE_ECUDA, MOE_ECOMM, MOE_ESTATE, MOE_ENOMEM = range(6)
 DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2
 CAP_FIXED, CAP_AUTO, CAP_BOUNDED = 0, 1, 2
 
+PHASES = ["gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd", "gemm_dgrad_mask",
+          "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2", "encode_bwd", "a2a_fwd", "a2a_bwd"]
+
 _ERRNAMES = {1: "EINVAL", 2: "ECUDA", 3: "ECOMM", 4: "ESTATE", 5: "ENOMEM"}
 
 
@@ -38,7 +41,7 @@ class StepMetrics(C.Structure):
     _fields_ = [
         ("f", C.c_double), ("capacity", C.c_int64), ("a2a_algo", C.c_int32),
         ("degree", C.c_int32), ("seconds", C.c_double), ("comm_bytes", C.c_double),
-        ("drop_count", C.c_int64),
+        ("drop_count", C.c_int64), ("relu_fixups", C.c_int64),
     ]
 
 
@@ -70,6 +73,8 @@ SIGNATURES = {
     "moe_get_expert_grads": (I32, [P, P, P]),
     "moe_get_weights_device": (I32, [P, I32, C.POINTER(P)]),
     "moe_kernel_launches": (I64, [P]),
+    "moe_set_profiling": (I32, [P, I32]),
+    "moe_take_profile": (I32, [P, PD, PI64, I32]),
     "moe_op_gating": (I32, [P, I32, P, I64, I64, I64, I64, I64, I32, D, I32, P, P, P, P, PI64,
                             PI64, P]),
     "moe_op_encode": (I32, [P, I32, I64, I64, I64, I64, I64, I64, I64, P, P, P, P]),

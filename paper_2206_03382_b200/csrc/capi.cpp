@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -114,6 +115,36 @@ void expert_gemm(int kind, int dtype, int use_tc, const void* A, const void* B, 
     rc = moe::gemm_bf16_simt(kind, A, B, D, a, st);
   }
   ckr(rc, "gemm");
+}
+
+// Up-projection with the ReLU-mask certificate on the bf16 path (see relu_fix.cu).
+void certified_up(int dtype, const void* x, const void* w1, void* act, moe::GemmArgs up,
+                  int64_t n, int64_t rows, int64_t M, int64_t V, cudaStream_t st, Scratch& sc) {
+  if (dtype != MOE_DTYPE_BF16) {
+    expert_gemm(moe::kGemmUp, dtype, -1, x, w1, act, up, static_cast<int>(n), st);
+    return;
+  }
+  float* colabs = sc.get<float>(static_cast<size_t>(n) * V);
+  void* w1t = sc.get<char>(static_cast<size_t>(n) * M * V * 2);
+  float* rowmax = sc.get<float>(static_cast<size_t>(n) * rows);
+  const unsigned int cap =
+      static_cast<unsigned int>(std::max<int64_t>(1 << 16, n * rows * V / 256));
+  auto* list = sc.get<unsigned long long>(cap);
+  auto* count = sc.get<unsigned int>(1);
+  ckr(moe::weight_stats_device(w1, static_cast<int>(n), static_cast<int>(M), static_cast<int>(V),
+                               colabs, w1t, st),
+      "weight stats");
+  ckr(moe::rowmax_device(x, n * rows, static_cast<int>(M), rowmax, st), "rowmax");
+  ck(cudaMemsetAsync(count, 0, sizeof(unsigned int), st), "memset");
+  up.rowmax = rowmax;
+  up.colabs = colabs;
+  up.fix_list = list;
+  up.fix_count = count;
+  up.fix_cap = cap;
+  expert_gemm(moe::kGemmUp, dtype, -1, x, w1, act, up, static_cast<int>(n), st);
+  ckr(moe::relu_fixup_device(x, w1t, static_cast<int>(n), static_cast<int>(rows),
+                             static_cast<int>(M), static_cast<int>(V), list, count, cap, act, st),
+      "relu_fixup");
 }
 
 moe::SlotGeom make_geom(int64_t blocks, int64_t T, int64_t M, int64_t E, int64_t k, int64_t cap,
@@ -246,6 +277,10 @@ int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr) {
   });
 }
 int64_t moe_kernel_launches(const moe_handle* h) { return h ? h->layer->launches() : 0; }
+int moe_set_profiling(moe_handle* h, int32_t on) { LAYER_CALL(h, h->layer->set_profiling(on != 0)); }
+int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n) {
+  LAYER_CALL(h, h->layer->take_profile(ms, counts, n));
+}
 
 // ------------------------------------------------------------------ stateless ops
 int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t blocks, int64_t T,
@@ -387,7 +422,7 @@ int moe_op_expert_ffn(const void* x, const void* w1, const void* w2, void* y, vo
     moe::GemmArgs down = up;
     down.N = M;
     down.K = V;
-    expert_gemm(moe::kGemmUp, dtype, -1, x, w1, a, up, static_cast<int>(n), st);
+    certified_up(dtype, x, w1, a, up, n, rows, M, V, st, sc);
     expert_gemm(moe::kGemmDown, dtype, -1, a, w2, y, down, static_cast<int>(n), st);
   });
 }
@@ -412,7 +447,7 @@ int moe_op_expert_ffn_backward(const void* x, const void* w1, const void* w2, co
     up.K = M;
     const int nseg = static_cast<int>(n);
     // recompute a = relu(x W1) (parallelism.cpp:135-136)
-    expert_gemm(moe::kGemmUp, dtype, -1, x, w1, a, up, nseg, st);
+    certified_up(dtype, x, w1, a, up, n, rows, M, V, st, sc);
     moe::GemmArgs dgm = up;
     dgm.aux = a;
     expert_gemm(moe::kGemmDgradMask, dtype, -1, dy, w2, dh, dgm, nseg, st);

@@ -93,7 +93,7 @@ __device__ __forceinline__ float from_f<float>(float v) {
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_kernel(SlotGeom g, const T* __restrict__ x, const int32_t* __restrict__ slot_token,
-                  T* __restrict__ z) {
+                  T* __restrict__ z, float* __restrict__ rowmax) {
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
       uint4* dst = reinterpret_cast<uint4*>(z + row * g.M);
+      float amax = 0.0f;
       if (t < 0) {
         for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
       } else {
@@ -123,14 +124,36 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 #pragma unroll
           for (int u = 0; u < kUnroll; ++u) {
             const int v = v0 + u * 32 + lane;
-            if (v < nv) dst[v] = buf[u];
+            if (v < nv) {
+              dst[v] = buf[u];
+              if (rowmax) {
+                float f[VN];
+                Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+                for (int q = 0; q < VN; ++q) amax = fmaxf(amax, fabsf(f[q]));
+              }
+            }
           }
         }
       }
+      if (rowmax) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) rowmax[row] = amax;
+      }
     } else {
       T* dst = z + row * g.M;
-      for (int m = lane; m < g.M; m += 32)
-        dst[m] = t < 0 ? from_f<T>(0.0f) : x[static_cast<size_t>(t) * g.M + m];
+      float amax = 0.0f;
+      for (int m = lane; m < g.M; m += 32) {
+        const T v = t < 0 ? from_f<T>(0.0f) : x[static_cast<size_t>(t) * g.M + m];
+        dst[m] = v;
+        amax = fmaxf(amax, fabsf(to_f(v)));
+      }
+      if (rowmax) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if (lane == 0) rowmax[row] = amax;
+      }
     }
   }
 }
@@ -361,17 +384,17 @@ bool vec_ok(int dtype, int M) { return (M * (dtype == 1 ? 4 : 2)) % 16 == 0; }
 }  // namespace
 
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st) {
+                  cudaStream_t st, float* rowmax) {
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) encode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z));
-    else encode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z));
+    if (v) encode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax);
+    else encode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax);
   } else {
     using B = __nv_bfloat16;
-    if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z));
-    else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z));
+    if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax);
+    else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

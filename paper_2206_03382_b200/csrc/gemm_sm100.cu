@@ -259,6 +259,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (uint32_t i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
           if constexpr (kEpi == kEpiReluBf16) {
+            if (args.fix_list != nullptr && row_ok) {
+              // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64 re-decision.
+              const float rmax = args.rowmax[static_cast<size_t>(seg) * args.seg_rows + row_in] *
+                                 kReluTauScale;
+              const float* ca = args.colabs + static_cast<size_t>(tc.g) * args.N + tc.n0 + c * 64;
+#pragma unroll
+              for (uint32_t i = 0; i < 64; ++i) {
+                if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
+                  const unsigned int slot = atomicAdd(args.fix_count, 1u);
+                  if (slot < args.fix_cap)
+                    args.fix_list[slot] = fix_pack(seg, row_in, tc.n0 + c * 64 + i);
+                }
+              }
+            }
 #pragma unroll
             for (uint32_t i = 0; i < 64; ++i) f[i] = fmaxf(f[i], 0.0f);
           }

@@ -26,7 +26,21 @@ struct GemmArgs {
   uint32_t K;         // reduction length (row-M kinds)
   uint32_t Mo;        // output rows (wgrad)
   const void* aux;    // kGemmDgradMask: saved activation, same layout as D
+  // kGemmUp ReLU-mask certificate (optional): outputs with |h| < tau = 2^-18 * rowmax[row] *
+  // colabs[g][col] are appended to fix_list for an fp64 sign re-decision (relu_fixup).
+  const float* rowmax;            // [nseg * seg_rows] max_m |X[row, m]|
+  const float* colabs;            // [G][N] sum_m |W1[g][m][col]|
+  unsigned long long* fix_list;   // packed (seg << 44) | (row << 24) | col
+  unsigned int* fix_count;
+  unsigned int fix_cap;
 };
+
+// Pack / unpack of one ReLU-fixup entry.
+__host__ __device__ inline unsigned long long fix_pack(uint32_t seg, uint32_t row, uint32_t col) {
+  return (static_cast<unsigned long long>(seg) << 44) | (static_cast<unsigned long long>(row) << 24) |
+         col;
+}
+constexpr float kReluTauScale = 1.0f / 262144.0f;  // 2^-18
 
 int gemm_validate(const GemmArgs& a, int kind);
 

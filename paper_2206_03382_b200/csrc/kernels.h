@@ -48,9 +48,10 @@ struct SlotGeom {
   int blocks, T, E, M, k, cap, cc, degree;
 };
 
-// dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype)
+// dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rowmax (optional, [z rows]):
+// max_m |z[row][m]| for the ReLU-mask certificate.
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st);
+                  cudaStream_t st, float* rowmax = nullptr);
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
                   const int32_t* locations, const double* gates, void* y, cudaStream_t st);
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
@@ -73,6 +74,14 @@ int fill_uniform_device(void* dst, int dtype /*0 bf16, 1 f32, 2 f64*/, int64_t n
 // Same stream, strided gather: dst[i*cols + j] = draw(offset + i*src_stride + j) for a sub-block.
 int fill_uniform_2d_device(void* dst, int dtype, int64_t rows, int64_t cols, int64_t src_stride,
                            uint64_t seed, uint64_t offset, double lo, double hi, cudaStream_t st);
+
+// ReLU-mask certificate support (relu_fix.cu).
+int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, void* w1t,
+                        cudaStream_t st);
+int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st);
+int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
+                      const unsigned long long* list, const unsigned int* count, unsigned int cap,
+                      void* act, cudaStream_t st);
 
 // fp32 SIMT GEMM path (the 1e-5 fp32 layer): same kinds/addressing as the bf16 tcgen05 GEMM.
 struct GemmArgs;

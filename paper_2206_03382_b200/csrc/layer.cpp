@@ -180,6 +180,15 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   dz_.alloc(rowsM);
   dh_.alloc(rowsV);
   dxe_.alloc(rowsM);
+  if (cfg.dtype == MOE_DTYPE_BF16) {
+    const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
+    colabs_.alloc(sizeof(float) * dE_ * V_);
+    w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
+    rowmax_.alloc(sizeof(float) * rows_all);
+    fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));
+    fix_list_.alloc(sizeof(unsigned long long) * fix_cap_);
+    fix_count_.alloc(sizeof(unsigned int));
+  }
   if (W_ > 1) {
     recv_.alloc(rowsM);
     ycomb_.alloc(rowsM);
@@ -188,7 +197,49 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   }
 }
 
+void Layer::prof_mark(int phase, bool begin, cudaStream_t st) {
+  if (!prof_) return;
+  cudaEvent_t e;
+  if (!ev_pool_.empty()) {
+    e = ev_pool_.back();
+    ev_pool_.pop_back();
+  } else {
+    ck(cudaEventCreateWithFlags(&e, cudaEventDefault), "event");
+  }
+  ck(cudaEventRecord(e, st), "event");
+  if (begin) {
+    prof_open_[phase] = e;
+  } else {
+    prof_recs_.push_back({phase, prof_open_[phase], e});
+    prof_open_[phase] = nullptr;
+  }
+}
+
+void Layer::take_profile(double* ms, int64_t* counts, int n) {
+  for (int i = 0; i < n; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  for (const auto& r : prof_recs_) {
+    ck(cudaEventSynchronize(r.b), "event sync");
+    float t = 0.0f;
+    ck(cudaEventElapsedTime(&t, r.a, r.b), "elapsed");
+    if (r.phase < n) {
+      ms[r.phase] += t;
+      counts[r.phase] += 1;
+    }
+    ev_pool_.push_back(r.a);
+    ev_pool_.push_back(r.b);
+  }
+  prof_recs_.clear();
+}
+
 Layer::~Layer() {
+  for (const auto& r : prof_recs_) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   if (comm_) ncclCommDestroy(comm_);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
   cudaEventDestroy(ev_fwd_start_);
@@ -219,6 +270,7 @@ void Layer::init_params(uint64_t seed) {
         "init w2");
   }
   ck(cudaDeviceSynchronize(), "init_params");
+  stats_dirty_ = true;
 }
 
 void Layer::set_router(const double* wg) {
@@ -244,6 +296,7 @@ void Layer::set_expert(int64_t le, const double* w1, const double* w2) {
   const size_t mv = static_cast<size_t>(M_) * V_;
   upload_weights(static_cast<char*>(w1_.p) + le * mv * esz_, w1, mv);
   upload_weights(static_cast<char*>(w2_.p) + le * mv * esz_, w2, mv);
+  stats_dirty_ = true;
 }
 
 // gather_computed_experts (parallelism.cpp:149-206) for per-rank placement: rank q holds slice q
@@ -295,6 +348,17 @@ void Layer::set_expert_slices(const double* w1s, const double* w2s) {
          "assemble w2");
     }
   ck(cudaDeviceSynchronize(), "set_expert_slices");
+  stats_dirty_ = true;
+}
+
+// Enables the ReLU-mask certificate on an up-GEMM launch (bf16 path only).
+void Layer::prepare_up(GemmArgs& up) {
+  if (cfg_.dtype != MOE_DTYPE_BF16) return;
+  up.rowmax = static_cast<const float*>(rowmax_.p);
+  up.colabs = static_cast<const float*>(colabs_.p);
+  up.fix_list = static_cast<unsigned long long*>(fix_list_.p);
+  up.fix_count = static_cast<unsigned int*>(fix_count_.p);
+  up.fix_cap = fix_cap_;
 }
 
 bool Layer::tc_ok(int kind, const GemmArgs& a) const {
@@ -398,12 +462,24 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   // --- gating: router GEMM + softmax + top-k + capacity + slots (per source block)
   GatingArgs ga = gating_args(x);
   GatingBuffers gb = gating_buffers();
+  prof_mark(kPhGate, true, st);
   ckr(run_gating_device(ga, gb, st), "gating");
   ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
+  prof_mark(kPhGate, false, st);
   launches_ += 3 + (cfg_.bpr ? 1 : 0);
 
+  const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
+  if (cert && stats_dirty_) {
+    ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colabs_.p), w1t_.p, st),
+        "weight stats");
+    stats_dirty_ = false;
+  }
   const SlotGeom g = geom();
-  ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st), "encode");
+  prof_mark(kPhEncode, true, st);
+  ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st,
+                    (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr),
+      "encode");
+  prof_mark(kPhEncode, false, st);
   ++launches_;
 
   const size_t seg = static_cast<size_t>(cc_) * M_;          // elements per (segment) block
@@ -418,19 +494,35 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   GemmArgs down = up;
   down.N = M_;
   down.K = V_;
+  prepare_up(up);
+  auto fixup = [&](void* xin) {
+    if (!cert) return;
+    ckr(relu_fixup_device(xin, w1t_.p, dE_, cc_, M_, V_,
+                          static_cast<const unsigned long long*>(fix_list_.p),
+                          static_cast<const unsigned int*>(fix_count_.p), fix_cap_, act_.p, st),
+        "relu_fixup");
+    ++launches_;
+  };
 
   void* recv = W_ > 1 ? recv_.p : z_.p;
   void* ycomb = W_ > 1 ? ycomb_.p : yexp_.p;
   if (W_ == 1) {
     up.seg_base = 0;
     down.seg_base = 0;
+    if (cert) ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
+    prof_mark(kPhUp, true, st);
     gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+    fixup(recv);
+    prof_mark(kPhUp, false, st);
+    prof_mark(kPhDown, true, st);
     gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+    prof_mark(kPhDown, false, st);
   } else {
     // Comm stream: all dispatches (chunk order), then all combines (reference FIFO order,
     // pipeline.cpp:180-190); compute stream: per chunk up+down GEMMs.
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+    prof_mark(kPhA2aFwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {
       // chunk i of z: [E][cc][M] at i*E*seg; peer p gets experts [p*dE, (p+1)*dE)
       exchange(static_cast<char*>(z_.p) + i * E_ * seg * esz_, dE_ * seg,
@@ -441,8 +533,22 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
       up.seg_base = i * W_;
       down.seg_base = i * W_;
+      if (cert) {
+        const size_t r0 = static_cast<size_t>(i) * W_ * dE_ * cc_;
+        ckr(rowmax_device(static_cast<char*>(recv) + r0 * M_ * esz_,
+                          static_cast<int64_t>(W_) * dE_ * cc_, M_,
+                          static_cast<float*>(rowmax_.p) + r0, st),
+            "rowmax");
+        ++launches_;
+        ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
+      }
+      prof_mark(kPhUp, true, st);
       gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+      fixup(recv);
+      prof_mark(kPhUp, false, st);
+      prof_mark(kPhDown, true, st);
       gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+      prof_mark(kPhDown, false, st);
       ck(cudaEventRecord(ev_b_[i], st), "event");
     }
     for (int i = 0; i < degree_; ++i) {
@@ -450,11 +556,14 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       exchange(static_cast<char*>(yexp_.p) + i * W_ * dE_ * seg * esz_, dE_ * seg,
                static_cast<char*>(ycomb) + i * E_ * seg * esz_, dE_ * seg, dE_ * seg);
     }
+    prof_mark(kPhA2aFwd, false, comm_stream_);
     ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
     ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
   }
   (void)segV;
+  prof_mark(kPhDecode, true, st);
   ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
+  prof_mark(kPhDecode, false, st);
   ++launches_;
   ck(cudaEventRecord(ev_fwd_end_, st), "event");
   fwd_done_ = true;
@@ -489,7 +598,9 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   const int64_t l0 = launches_;
 
   // dZ = decode^T(dy): slot-major gather of g * dy (fast_decode_backward_range)
+  prof_mark(kPhDecodeBwd, true, st);
   ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st), "decode_bwd");
+  prof_mark(kPhDecodeBwd, false, st);
   ++launches_;
 
   const size_t seg = static_cast<size_t>(cc_) * M_;
@@ -520,13 +631,22 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   void* drecv = W_ > 1 ? drecv_.p : dz_.p;
   void* dxcomb = W_ > 1 ? dxcomb_.p : dxe_.p;
   if (W_ == 1) {
+    prof_mark(kPhDgradMask, true, st);
     gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
+    prof_mark(kPhDgradMask, false, st);
+    prof_mark(kPhDgrad, true, st);
     gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+    prof_mark(kPhDgrad, false, st);
+    prof_mark(kPhWgrad1, true, st);
     gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
+    prof_mark(kPhWgrad1, false, st);
+    prof_mark(kPhWgrad2, true, st);
     gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
+    prof_mark(kPhWgrad2, false, st);
   } else {
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+    prof_mark(kPhA2aBwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {  // adjoint of combine
       exchange(static_cast<char*>(dz_.p) + i * E_ * seg * esz_, dE_ * seg,
                static_cast<char*>(drecv) + i * W_ * dE_ * seg * esz_, dE_ * seg, dE_ * seg);
@@ -536,8 +656,12 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
       ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
       dgm.seg_base = i * W_;
       dg.seg_base = i * W_;
+      prof_mark(kPhDgradMask, true, st);
       gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
+      prof_mark(kPhDgradMask, false, st);
+      prof_mark(kPhDgrad, true, st);
       gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+      prof_mark(kPhDgrad, false, st);
       ck(cudaEventRecord(ev_b_[i], st), "event");
     }
     for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
@@ -545,13 +669,20 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
       exchange(static_cast<char*>(dxe_.p) + i * W_ * dE_ * seg * esz_, dE_ * seg,
                static_cast<char*>(dxcomb) + i * E_ * seg * esz_, dE_ * seg, dE_ * seg);
     }
+    prof_mark(kPhA2aBwd, false, comm_stream_);
     ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
     // Weight gradients overlap the last return exchanges.
+    prof_mark(kPhWgrad1, true, st);
     gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
+    prof_mark(kPhWgrad1, false, st);
+    prof_mark(kPhWgrad2, true, st);
     gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
+    prof_mark(kPhWgrad2, false, st);
     ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
   }
+  prof_mark(kPhEncodeBwd, true, st);
   ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st), "encode_bwd");
+  prof_mark(kPhEncodeBwd, false, st);
   ++launches_;
   bwd_launches_ = launches_ - l0;
   if (dw1) last_dw1_ = nullptr; else last_dw1_ = gw1;
@@ -612,6 +743,13 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->seconds = ms * 1e-3;
   m->comm_bytes = comm_bytes_;
   m->drop_count = drops;
+  m->relu_fixups = 0;
+  if (cfg_.dtype == MOE_DTYPE_BF16) {
+    unsigned int nfix = 0;
+    ck(cudaMemcpy(&nfix, fix_count_.p, 4, cudaMemcpyDeviceToHost), "copy");
+    m->relu_fixups = nfix;
+    if (nfix > fix_cap_) throw MoeError(MOE_ESTATE, "ReLU-mask certificate list overflowed");
+  }
 }
 
 void Layer::get_grads(float* dw1, float* dw2) {

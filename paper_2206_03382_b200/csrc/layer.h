@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/moe_b200.h"
 #include "gemm_sm100.h"
@@ -34,6 +35,13 @@ uint16_t bf16_bits_rne(double x);
 int64_t expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts);
 void validate(const moe_config& c);
 
+// Phases timed with CUDA events on the compute stream when profiling is on (Timeline tracing,
+// pipeline.hpp:36-46 / pipeline.cpp:68-76, with measured instead of simulated intervals).
+enum Phase : int {
+  kPhGate = 0, kPhEncode, kPhUp, kPhDown, kPhDecode, kPhDecodeBwd, kPhDgradMask, kPhDgrad,
+  kPhWgrad1, kPhWgrad2, kPhEncodeBwd, kPhA2aFwd, kPhA2aBwd, kNumPhases
+};
+
 class Layer {
  public:
   Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device);
@@ -53,6 +61,9 @@ class Layer {
   void* w1() { return w1_.p; }
   void* w2() { return w2_.p; }
   int64_t launches() const { return launches_; }
+  void set_profiling(bool on) { prof_ = on; }
+  // Sums (ms) and counts per phase since the last call; synchronizes.
+  void take_profile(double* ms, int64_t* counts, int n);
 
   std::string err;
 
@@ -68,6 +79,7 @@ class Layer {
   void exchange(const void* send, size_t send_stride, void* recv, size_t recv_stride, size_t elems);
   double allreduce_max_host(double v);
   void ensure_io();
+  void prof_mark(int phase, bool begin, cudaStream_t st);
 
   moe_config cfg_;
   int rank_, device_;
@@ -94,6 +106,20 @@ class Layer {
   DevMem slot_token_, slot_gate_;
   DevMem z_, recv_, act_, yexp_, ycomb_, dz_, drecv_, dh_, dxe_, dxcomb_;
   DevMem io_x_, io_y_, io_dy_, io_dx_;
+  // ReLU-mask certificate state (relu_fix.cu)
+  DevMem colabs_, w1t_, rowmax_, fix_list_, fix_count_;
+  unsigned int fix_cap_ = 0;
+  bool stats_dirty_ = true;
+  void prepare_up(GemmArgs& up);
+
+  struct ProfRec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  bool prof_ = false;
+  std::vector<ProfRec> prof_recs_;
+  std::vector<cudaEvent_t> ev_pool_;
+  cudaEvent_t prof_open_[kNumPhases]{};
 };
 
 }  // namespace moe

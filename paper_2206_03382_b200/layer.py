@@ -67,6 +67,7 @@ class StepMetricsPy:
     seconds: float
     comm_bytes: float
     drop_count: int
+    relu_fixups: int = 0
 
 
 @dataclass
@@ -191,10 +192,23 @@ class LayerState:
         m = StepMetrics()
         check(lib().moe_get_metrics(self._h, C.byref(m)), self._h)
         return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
-                             m.seconds, m.comm_bytes, m.drop_count)
+                             m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups)
 
     def kernel_launches(self) -> int:
         return int(lib().moe_kernel_launches(self._h))
+
+    def set_profiling(self, on: bool) -> None:
+        check(lib().moe_set_profiling(self._h, int(on)), self._h)
+
+    def take_profile(self) -> dict:
+        """{phase: (total ms, intervals)} since the last call (measured timeline)."""
+        import numpy as np
+        n = len(_lib.PHASES)
+        ms = np.zeros(n, np.float64)
+        cnt = np.zeros(n, np.int64)
+        check(lib().moe_take_profile(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                     cnt.ctypes.data_as(C.POINTER(C.c_int64)), n), self._h)
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(_lib.PHASES)}
 
     @property
     def handle(self):
