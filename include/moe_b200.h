@@ -86,6 +86,15 @@ int moe_capacity_to_factor(int64_t capacity, int64_t experts, int64_t top_k, int
 /* Dims::validate, core.cpp:8-26 (per-rank placement). */
 int moe_validate_config(const moe_config* cfg);
 
+/* Flexible all-to-all plan (flex_all2all, collectives.cpp:116-162, over all2all_linear
+ * :48-56) for pipeline chunk `chunk`: element offsets of the block sent to / received from each
+ * peer (arrays of W) and the block size. phase 0 = dispatch: send buffer [degree][E][cc][M],
+ * peer p gets experts [p*E/W, (p+1)*E/W); receive buffer [degree][W][E/W][cc][M], i.e. expert
+ * e's gathered rows (source r, slot c) -- the (dE, W*cc, M) interleave -- without a copy.
+ * phase 1 = combine: the inverse. Host-only; the layer's NCCL exchanges use exactly this plan. */
+int moe_a2a_plan(int64_t W, int64_t E, int64_t cc, int64_t M, int64_t chunk, int32_t phase,
+                 int64_t* send_offsets, int64_t* recv_offsets, int64_t* elems);
+
 /* ---------------------------------------------------------------- layer (moe_layer.hpp) */
 /* NCCL unique id for W > 1 (128 bytes), created on rank 0 and broadcast by the caller. */
 int moe_get_unique_id(uint8_t* id128);

@@ -55,6 +55,7 @@ SIGNATURES = {
     "moe_resolve_capacity": (I32, [I32, D, PI64, I64, I64, I64, PI64]),
     "moe_capacity_to_factor": (I32, [I64, I64, I64, I64, PD]),
     "moe_validate_config": (I32, [C.POINTER(MoeConfig)]),
+    "moe_a2a_plan": (I32, [I64, I64, I64, I64, I64, I32, PI64, PI64, PI64]),
     "moe_get_unique_id": (I32, [C.c_char_p]),
     "moe_create": (I32, [C.POINTER(MoeConfig), I32, C.c_char_p, I32, C.POINTER(P)]),
     "moe_destroy": (I32, [P]),

@@ -201,6 +201,15 @@ int moe_capacity_to_factor(int64_t capacity, int64_t experts, int64_t top_k, int
   });
 }
 
+int moe_a2a_plan(int64_t W, int64_t E, int64_t cc, int64_t M, int64_t chunk, int32_t phase,
+                 int64_t* send_off, int64_t* recv_off, int64_t* elems) {
+  return guard(nullptr, [&] {
+    if (W < 1 || E < 1 || E % W != 0 || cc < 1 || M < 1 || chunk < 0 || (phase != 0 && phase != 1))
+      throw moe::MoeError(MOE_EINVAL, "flex_all2all: expert axis not divisible by W");
+    moe::a2a_plan(W, E, cc, M, chunk, phase, send_off, recv_off, elems);
+  });
+}
+
 int moe_validate_config(const moe_config* cfg) {
   return guard(nullptr, [&] {
     if (!cfg) throw moe::MoeError(MOE_EINVAL, "null config");

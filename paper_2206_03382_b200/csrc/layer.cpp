@@ -59,6 +59,19 @@ uint16_t bf16_bits_rne(double x) {
   return static_cast<uint16_t>(fb >> 16);
 }
 
+void a2a_plan(int64_t W, int64_t E, int64_t cc, int64_t M, int64_t chunk, int phase,
+              int64_t* send_off, int64_t* recv_off, int64_t* elems) {
+  const int64_t dE = E / W;
+  const int64_t blk = dE * cc * M;
+  for (int64_t p = 0; p < W; ++p) {
+    const int64_t zoff = (chunk * E + p * dE) * cc * M;  // [chunk][E][cc] block of peer p
+    const int64_t roff = (chunk * W + p) * blk;           // [chunk][W][dE][cc] block of peer p
+    send_off[p] = phase == 0 ? zoff : roff;
+    recv_off[p] = phase == 0 ? roff : zoff;
+  }
+  *elems = blk;
+}
+
 int64_t expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts) {
   if (k < 1 || tokens < 1 || experts < 1 || !(f > 0.0))
     throw MoeError(MOE_EINVAL, "expert_capacity: inputs must be positive");
@@ -430,17 +443,18 @@ SlotGeom Layer::geom() const {
   return g;
 }
 
-// One grouped exchange of W equal blocks (all2all_linear, collectives.cpp:48-56):
-// block p of `send` -> rank p, block p of `recv` <- rank p.
-void Layer::exchange(const void* send, size_t send_stride, void* recv, size_t recv_stride,
-                     size_t elems) {
+// One grouped exchange of chunk `chunk` (all2all_linear, collectives.cpp:48-56): block p of
+// `send` -> rank p, block p of `recv` <- rank p, offsets from a2a_plan.
+void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
   const ncclDataType_t dt = cfg_.dtype == MOE_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
+  std::vector<int64_t> so(W_), ro(W_);
+  int64_t elems = 0;
+  a2a_plan(W_, E_, cc_, M_, chunk, phase, so.data(), ro.data(), &elems);
   ckn(ncclGroupStart(), "ncclGroupStart");
   for (int p = 0; p < W_; ++p) {
-    ckn(ncclSend(static_cast<const char*>(send) + p * send_stride * esz_, elems, dt, p, comm_,
-                 comm_stream_),
+    ckn(ncclSend(static_cast<const char*>(send) + so[p] * esz_, elems, dt, p, comm_, comm_stream_),
         "ncclSend");
-    ckn(ncclRecv(static_cast<char*>(recv) + p * recv_stride * esz_, elems, dt, p, comm_, comm_stream_),
+    ckn(ncclRecv(static_cast<char*>(recv) + ro[p] * esz_, elems, dt, p, comm_, comm_stream_),
         "ncclRecv");
   }
   ckn(ncclGroupEnd(), "ncclGroupEnd");
@@ -482,8 +496,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   prof_mark(kPhEncode, false, st);
   ++launches_;
 
-  const size_t seg = static_cast<size_t>(cc_) * M_;          // elements per (segment) block
-  const size_t segV = static_cast<size_t>(cc_) * V_;
   const int nseg = degree_ * W_ * dE_;
   GemmArgs up{};
   up.G = dE_;
@@ -525,8 +537,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     prof_mark(kPhA2aFwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {
       // chunk i of z: [E][cc][M] at i*E*seg; peer p gets experts [p*dE, (p+1)*dE)
-      exchange(static_cast<char*>(z_.p) + i * E_ * seg * esz_, dE_ * seg,
-               static_cast<char*>(recv) + i * W_ * dE_ * seg * esz_, dE_ * seg, dE_ * seg);
+      exchange(z_.p, recv, i, 0);
       ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
     }
     for (int i = 0; i < degree_; ++i) {
@@ -553,14 +564,12 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     }
     for (int i = 0; i < degree_; ++i) {
       ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
-      exchange(static_cast<char*>(yexp_.p) + i * W_ * dE_ * seg * esz_, dE_ * seg,
-               static_cast<char*>(ycomb) + i * E_ * seg * esz_, dE_ * seg, dE_ * seg);
+      exchange(yexp_.p, ycomb, i, 1);
     }
     prof_mark(kPhA2aFwd, false, comm_stream_);
     ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
     ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
   }
-  (void)segV;
   prof_mark(kPhDecode, true, st);
   ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
   prof_mark(kPhDecode, false, st);
@@ -603,7 +612,6 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   prof_mark(kPhDecodeBwd, false, st);
   ++launches_;
 
-  const size_t seg = static_cast<size_t>(cc_) * M_;
   const int nseg = degree_ * W_ * dE_;
   GemmArgs dgm{};  // dh = (dY . W2^T) * [a > 0]
   dgm.G = dE_;
@@ -648,8 +656,7 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
     prof_mark(kPhA2aBwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {  // adjoint of combine
-      exchange(static_cast<char*>(dz_.p) + i * E_ * seg * esz_, dE_ * seg,
-               static_cast<char*>(drecv) + i * W_ * dE_ * seg * esz_, dE_ * seg, dE_ * seg);
+      exchange(dz_.p, drecv, i, 0);
       ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
     }
     for (int i = 0; i < degree_; ++i) {
@@ -666,8 +673,7 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     }
     for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
       ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
-      exchange(static_cast<char*>(dxe_.p) + i * W_ * dE_ * seg * esz_, dE_ * seg,
-               static_cast<char*>(dxcomb) + i * E_ * seg * esz_, dE_ * seg, dE_ * seg);
+      exchange(dxe_.p, dxcomb, i, 1);
     }
     prof_mark(kPhA2aBwd, false, comm_stream_);
     ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");

@@ -32,6 +32,13 @@ struct DevMem {
 };
 
 uint16_t bf16_bits_rne(double x);
+
+// Flexible all-to-all plan for pipeline chunk `chunk` (flex_all2all, collectives.cpp:116-162):
+// element offsets of the block sent to / received from each peer p and the block size.
+// phase 0 (dispatch): send [chunk][E][cc][M] experts [p*dE,(p+1)*dE) -> recv [chunk][W][dE][cc][M]
+// phase 1 (combine):  the inverse.
+void a2a_plan(int64_t W, int64_t E, int64_t cc, int64_t M, int64_t chunk, int phase,
+              int64_t* send_off, int64_t* recv_off, int64_t* elems);
 int64_t expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts);
 void validate(const moe_config& c);
 
@@ -76,7 +83,7 @@ class Layer {
   GatingArgs gating_args(const void* x) const;
   GatingBuffers gating_buffers();
   SlotGeom geom() const;
-  void exchange(const void* send, size_t send_stride, void* recv, size_t recv_stride, size_t elems);
+  void exchange(const void* send, void* recv, int chunk, int phase);
   double allreduce_max_host(double v);
   void ensure_io();
   void prof_mark(int phase, bool begin, cudaStream_t st);
