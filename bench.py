@@ -385,6 +385,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "drop_count": drops,
+            "relu_fixups_last_chunk": metrics.relu_fixups,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -60,7 +60,12 @@ void ck(cudaError_t e, const char* what) {
 }
 void ckr(int rc, const char* what) {
   if (rc == -1) throw moe::MoeError(MOE_EINVAL, std::string(what) + ": invalid arguments");
-  if (rc != 0) throw moe::MoeError(MOE_ECUDA, std::string(what) + ": launch failed");
+  if (rc != 0) {
+    cudaError_t e = moe::last_launch_error();
+    moe::last_launch_error() = cudaSuccess;
+    throw moe::MoeError(MOE_ECUDA, std::string(what) + ": launch failed (" +
+                                       cudaGetErrorString(e) + ")");
+  }
 }
 
 void require_device() {
@@ -118,13 +123,17 @@ void expert_gemm(int kind, int dtype, int use_tc, const void* A, const void* B, 
 }
 
 // Up-projection with the ReLU-mask certificate on the bf16 path (see relu_fix.cu).
-void certified_up(int dtype, const void* x, const void* w1, void* act, moe::GemmArgs up,
-                  int64_t n, int64_t rows, int64_t M, int64_t V, cudaStream_t st, Scratch& sc) {
+// Returns the ReLU bitmask (bf16 path) for a following kGemmDgradMask.
+unsigned long long* certified_up(int dtype, const void* x, const void* w1, void* act,
+                                 moe::GemmArgs up, int64_t n, int64_t rows, int64_t M, int64_t V,
+                                 cudaStream_t st, Scratch& sc) {
   if (dtype != MOE_DTYPE_BF16) {
     expert_gemm(moe::kGemmUp, dtype, -1, x, w1, act, up, static_cast<int>(n), st);
-    return;
+    return nullptr;
   }
   float* colabs = sc.get<float>(static_cast<size_t>(n) * V);
+  float* colabs_blk = sc.get<float>(static_cast<size_t>(n) * (V / 64 + 1));
+  auto* mask = sc.get<unsigned long long>(static_cast<size_t>(n) * rows * (V / 64 + 1));
   void* w1t = sc.get<char>(static_cast<size_t>(n) * M * V * 2);
   float* rowmax = sc.get<float>(static_cast<size_t>(n) * rows);
   const unsigned int cap =
@@ -132,19 +141,23 @@ void certified_up(int dtype, const void* x, const void* w1, void* act, moe::Gemm
   auto* list = sc.get<unsigned long long>(cap);
   auto* count = sc.get<unsigned int>(1);
   ckr(moe::weight_stats_device(w1, static_cast<int>(n), static_cast<int>(M), static_cast<int>(V),
-                               colabs, w1t, st),
+                               colabs, colabs_blk, w1t, st),
       "weight stats");
   ckr(moe::rowmax_device(x, n * rows, static_cast<int>(M), rowmax, st), "rowmax");
   ck(cudaMemsetAsync(count, 0, sizeof(unsigned int), st), "memset");
   up.rowmax = rowmax;
   up.colabs = colabs;
+  up.colabs_blk = colabs_blk;
+  up.relu_mask = mask;
   up.fix_list = list;
   up.fix_count = count;
   up.fix_cap = cap;
   expert_gemm(moe::kGemmUp, dtype, -1, x, w1, act, up, static_cast<int>(n), st);
   ckr(moe::relu_fixup_device(x, w1t, static_cast<int>(n), static_cast<int>(rows),
-                             static_cast<int>(M), static_cast<int>(V), list, count, cap, act, st),
+                             static_cast<int>(M), static_cast<int>(V), list, count, cap, act, mask,
+                             st),
       "relu_fixup");
+  return mask;
 }
 
 moe::SlotGeom make_geom(int64_t blocks, int64_t T, int64_t M, int64_t E, int64_t k, int64_t cap,
@@ -456,9 +469,10 @@ int moe_op_expert_ffn_backward(const void* x, const void* w1, const void* w2, co
     up.K = M;
     const int nseg = static_cast<int>(n);
     // recompute a = relu(x W1) (parallelism.cpp:135-136)
-    certified_up(dtype, x, w1, a, up, n, rows, M, V, st, sc);
+    unsigned long long* mask = certified_up(dtype, x, w1, a, up, n, rows, M, V, st, sc);
     moe::GemmArgs dgm = up;
     dgm.aux = a;
+    dgm.relu_mask = mask;
     expert_gemm(moe::kGemmDgradMask, dtype, -1, dy, w2, dh, dgm, nseg, st);
     moe::GemmArgs dg = up;
     dg.N = M;
@@ -494,6 +508,14 @@ int moe_op_gemm(int32_t kind, int32_t dtype, int32_t use_tc, const void* A, cons
     a.K = static_cast<uint32_t>(K);
     a.Mo = static_cast<uint32_t>(Mo);
     a.aux = aux;
+    Scratch sc(S(stream));
+    if (kind == moe::kGemmDgradMask && dtype == MOE_DTYPE_BF16 && use_tc != 0 && tc_shape_ok(kind, a)) {
+      if (!aux) throw moe::MoeError(MOE_EINVAL, "dgrad-mask needs the activation (aux)");
+      const int64_t rows = nseg_total * seg_rows;
+      a.relu_mask = sc.get<unsigned long long>(static_cast<size_t>(rows) * (N / 64));
+      ckr(moe::relu_mask_from_act_device(aux, rows, static_cast<int>(N), a.relu_mask, S(stream)),
+          "relu mask");
+    }
     expert_gemm(kind, dtype, use_tc, A, B, D, a, static_cast<int>(nseg_total), S(stream));
   });
 }

@@ -396,7 +396,7 @@ int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* sl
     if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax);
     else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
@@ -411,7 +411,7 @@ int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* id
     if (v) decode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
     else decode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
@@ -428,7 +428,7 @@ int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
     if (v) decode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz));
     else decode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz));
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
@@ -439,7 +439,7 @@ int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, co
     decode_bwd_gates_kernel<float><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), static_cast<const float*>(dy), idxs, locations, dgates);
   else
     decode_bwd_gates_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g, static_cast<const __nv_bfloat16*>(z), static_cast<const __nv_bfloat16*>(dy), idxs, locations, dgates);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
@@ -454,7 +454,7 @@ int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const i
     if (v) encode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
     else encode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 namespace {
@@ -485,7 +485,7 @@ int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* 
   const int grid = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
   build_slots_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(n, T, k, E, cap, idxs, locations, gates,
                                                          slot_token, slot_gate);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace moe

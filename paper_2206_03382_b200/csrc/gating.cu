@@ -54,15 +54,22 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // x: [blocks*T, M] (bf16 or f32), wg: [M, E] fp64 row-major.
 // Outputs idxs/gates [blocks*T, k], hist [n_cta, E] (per-CTA expert counts), optional probs.
+// Each warp owns 8 tokens; lane l owns experts l + 32j (j < EPL) and keeps the current Wg chunk in
+// registers, while the token values come from shared memory as warp broadcasts. The next chunk
+// of x / Wg is prefetched into registers during the current chunk's DFMAs (double-buffered smem,
+// one barrier per chunk). Summation per (token, expert) is a single sequential fma chain over m.
 template <typename TX, int EPL>
 __global__ void __launch_bounds__(kGateWarps * 32)
     gate_topk_kernel(const TX* __restrict__ x, const double* __restrict__ wg, int T, int M, int E,
                      int k, int cta_per_block, int32_t* __restrict__ idxs,
                      double* __restrict__ gates, int32_t* __restrict__ hist,
                      double* __restrict__ probs_out) {
-  constexpr int KC = 32 / EPL;  // k-chunk staged through smem
-  __shared__ double xs[kGateTok][KC];
-  __shared__ double ws[KC][32 * EPL];
+  constexpr int KC = 16 / EPL;  // k-chunk staged through smem (2 x 24 KiB static smem at EPL=1)
+  constexpr int NT = kGateWarps * 32;
+  constexpr int XPT = (kGateTok * KC + NT - 1) / NT;  // x elements per thread per chunk
+  constexpr int WPT = (KC * 32 * EPL + NT - 1) / NT;  // Wg elements per thread per chunk
+  __shared__ __align__(16) double xs[2][kGateTok][KC];
+  __shared__ __align__(16) double ws[2][KC][32 * EPL];
   extern __shared__ int32_t sh_hist[];  // [E]
 
   const int b = blockIdx.x / cta_per_block;
@@ -80,36 +87,63 @@ __global__ void __launch_bounds__(kGateWarps * 32)
 #pragma unroll
     for (int j = 0; j < EPL; ++j) acc[i][j] = 0.0;
 
-  for (int k0 = 0; k0 < M; k0 += KC) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < kGateTok * KC; i += blockDim.x) {
+  double xr[XPT], wrg[WPT];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int i = threadIdx.x + q * NT;
       const int tt = i / KC, kk = i % KC;
-      double v = 0.0;
-      if (tt < ntok && k0 + kk < M) v = to_f64(x[static_cast<size_t>(t_begin + tt) * M + k0 + kk]);
-      xs[tt][kk] = v;
+      xr[q] = (i < kGateTok * KC && tt < ntok && k0 + kk < M)
+                  ? to_f64(x[static_cast<size_t>(t_begin + tt) * M + k0 + kk])
+                  : 0.0;
     }
-    for (int i = threadIdx.x; i < KC * 32 * EPL; i += blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int i = threadIdx.x + q * NT;
       const int kk = i / (32 * EPL), e = i % (32 * EPL);
-      ws[kk][e] = (k0 + kk < M && e < E) ? wg[static_cast<size_t>(k0 + kk) * E + e] : 0.0;
+      wrg[q] = (i < KC * 32 * EPL && k0 + kk < M && e < E)
+                   ? __ldg(wg + static_cast<size_t>(k0 + kk) * E + e)
+                   : 0.0;
     }
-    __syncthreads();
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int i = threadIdx.x + q * NT;
+      if (i < kGateTok * KC) xs[buf][i / KC][i % KC] = xr[q];
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int i = threadIdx.x + q * NT;
+      if (i < KC * 32 * EPL) ws[buf][i / (32 * EPL)][i % (32 * EPL)] = wrg[q];
+    }
+  };
+
+  const int nchunks = (M + KC - 1) / KC;
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) load_chunk((ch + 1) * KC);  // global loads in flight during DFMAs
     double wr[KC][EPL];
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk)
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) wr[kk][j] = ws[kk][lane + 32 * j];
+      for (int j = 0; j < EPL; ++j) wr[kk][j] = ws[buf][kk][lane + 32 * j];
 #pragma unroll
     for (int i = 0; i < kGateTokPerWarp; ++i) {
       const int tt = warp * kGateTokPerWarp + i;
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        const double xv = xs[tt][kk];  // warp broadcast
+        const double xv = xs[buf][tt][kk];  // warp broadcast
 #pragma unroll
         for (int j = 0; j < EPL; ++j) acc[i][j] = fma(xv, wr[kk][j], acc[i][j]);
       }
     }
+    if (ch + 1 < nchunks) store_chunk(buf ^ 1);
+    __syncthreads();
   }
-  __syncthreads();
 
 #pragma unroll
   for (int i = 0; i < kGateTokPerWarp; ++i) {
@@ -171,25 +205,212 @@ __global__ void __launch_bounds__(kGateWarps * 32)
     hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
 }
 
+// FP64 tensor-core variant (E <= 64): mma.sync.m8n8k4.f64 (DMMA). A warp owns MT m8-tiles of
+// tokens x NT n8-tiles of experts; per 4-deep k step it loads MT A-fragments (x) and NT
+// B-fragments (Wg) from padded, conflict-free shared memory and issues MT*NT DMMAs (256 fp64
+// FMAs each). Products of the bf16/fp32 inputs with fp64 Wg are exact in fp64; only the
+// accumulation order differs from the reference's Eigen GEMM (ulp-level, below any routing tie).
+// Fragment layout (m8n8k4 .f64): A[r][c] with r = lane/4, c = lane%4; B[r][c] with r = lane%4,
+// c = lane/4; D[r][2*(lane%4) + i] with r = lane/4.
+constexpr int kDmWarps = 4, kDmMT = 2, kDmTok = kDmWarps * kDmMT * 8, kDmKC = 16;
+static_assert(kDmTok == kGateTok, "gate kernels must share the token-block partition of assign");
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename TX, int NT>
+__global__ void __launch_bounds__(kDmWarps * 32)
+    gate_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ wg, int T, int M, int E,
+                     int k, int cta_per_block, int32_t* __restrict__ idxs,
+                     double* __restrict__ gates, int32_t* __restrict__ hist,
+                     double* __restrict__ probs_out) {
+  constexpr int NTH = kDmWarps * 32;
+  constexpr int XS = kDmKC + 4;       // x row stride (doubles): conflict-free A fragments
+  constexpr int EP = 8 * NT + 4;      // Wg row stride: conflict-free B fragments
+  constexpr int XPT = kDmTok * kDmKC / NTH;
+  constexpr int WPT = (kDmKC * 8 * NT + NTH - 1) / NTH;
+  __shared__ __align__(16) double xs[2][kDmTok][XS];
+  __shared__ __align__(16) double ws[2][kDmKC][EP];
+  __shared__ int32_t sh_hist[8 * NT];
+
+  const int b = blockIdx.x / cta_per_block;
+  const int c = blockIdx.x % cta_per_block;
+  const int t_begin = b * T + c * kDmTok;
+  const int ntok = min(b * T + T, t_begin + kDmTok) - t_begin;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int e = threadIdx.x; e < 8 * NT; e += NTH) sh_hist[e] = 0;
+
+  double acc[kDmMT][NT][2];
+#pragma unroll
+  for (int i = 0; i < kDmMT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double xr[XPT], wr[WPT];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int i = threadIdx.x + q * NTH;
+      const int tt = i / kDmKC, kk = i % kDmKC;
+      xr[q] = (tt < ntok && k0 + kk < M) ? to_f64(x[static_cast<size_t>(t_begin + tt) * M + k0 + kk])
+                                         : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int i = threadIdx.x + q * NTH;
+      const int kk = i / (8 * NT), e = i % (8 * NT);
+      wr[q] = (i < kDmKC * 8 * NT && k0 + kk < M && e < E)
+                  ? __ldg(wg + static_cast<size_t>(k0 + kk) * E + e)
+                  : 0.0;
+    }
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int i = threadIdx.x + q * NTH;
+      xs[buf][i / kDmKC][i % kDmKC] = xr[q];
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int i = threadIdx.x + q * NTH;
+      if (i < kDmKC * 8 * NT) ws[buf][i / (8 * NT)][i % (8 * NT)] = wr[q];
+    }
+  };
+
+  const int nchunks = (M + kDmKC - 1) / kDmKC;
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  const int ar = lane >> 2, ac = lane & 3;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) load_chunk((ch + 1) * kDmKC);
+#pragma unroll
+    for (int ks = 0; ks < kDmKC; ks += 4) {
+      double a[kDmMT], bb[NT];
+#pragma unroll
+      for (int i = 0; i < kDmMT; ++i) a[i] = xs[buf][(warp * kDmMT + i) * 8 + ar][ks + ac];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bb[j] = ws[buf][ks + ac][j * 8 + ar];
+#pragma unroll
+      for (int i = 0; i < kDmMT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+    if (ch + 1 < nchunks) store_chunk(buf ^ 1);
+    __syncthreads();
+  }
+
+  // softmax + top-k: the 4 lanes of a quad (same lane/4) hold one token's 8*NT logits.
+#pragma unroll
+  for (int i = 0; i < kDmMT; ++i) {
+    const int tt = (warp * kDmMT + i) * 8 + ar;
+    const bool tok_ok = tt < ntok;
+    const int t = t_begin + tt;
+    double mx = -DBL_MAX;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (j * 8 + ac * 2 + h < E) mx = fmax(mx, acc[i][j][h]);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    double p[NT][2];
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        p[j][h] = (j * 8 + ac * 2 + h < E) ? exp(acc[i][j][h] - mx) : 0.0;
+        s += p[j][h];
+      }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        p[j][h] /= s;
+        const int e = j * 8 + ac * 2 + h;
+        if (probs_out && tok_ok && e < E) probs_out[static_cast<size_t>(t) * E + e] = p[j][h];
+      }
+    unsigned taken = 0;
+    for (int r = 0; r < k; ++r) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = j * 8 + ac * 2 + h;
+          if (e < E && !(taken & (1u << (j * 2 + h))) && (p[j][h] > bv || (p[j][h] == bv && e < bi))) {
+            bv = p[j][h];
+            bi = e;
+          }
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (((bi & 7) >> 1) == ac) taken |= 1u << ((bi >> 3) * 2 + (bi & 1));
+      if (ac == 0 && tok_ok) {
+        idxs[static_cast<size_t>(t) * k + r] = bi;
+        gates[static_cast<size_t>(t) * k + r] = bv;
+        atomicAdd(&sh_hist[bi], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += NTH) hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
+}
+
 // Per (block, expert): exclusive scan of CTA histograms, demand, resolved capacity, fill counts
-// and the member-list base used by BPR. One CTA.
-__global__ void scan_kernel(const int32_t* __restrict__ hist, int blocks, int cta_per_block, int E,
-                            int T, int k, int cap_kind, int cap_formula, int32_t* __restrict__ offs,
-                            int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
-                            int32_t* __restrict__ fill, int32_t* __restrict__ cap_out) {
+// and the member-list base used by BPR. One CTA; warp w scans the CTA-histogram columns of pairs
+// w, w+32, ... with warp shuffles (32 CTA counts per step, loads issued 4 steps ahead).
+__global__ void __launch_bounds__(1024)
+    scan_kernel(const int32_t* __restrict__ hist, int blocks, int cta_per_block, int E, int T,
+                int k, int cap_kind, int cap_formula, int32_t* __restrict__ offs,
+                int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
+                int32_t* __restrict__ fill, int32_t* __restrict__ cap_out) {
   extern __shared__ int32_t sh[];  // [E] max demand over blocks
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
   for (int e = threadIdx.x; e < E; e += blockDim.x) sh[e] = 0;
   __syncthreads();
-  for (int p = threadIdx.x; p < blocks * E; p += blockDim.x) {
+  for (int p = warp; p < blocks * E; p += nwarps) {
     const int b = p / E, e = p % E;
     int run = 0;
-    for (int c = 0; c < cta_per_block; ++c) {
-      const size_t idx = static_cast<size_t>(b * cta_per_block + c) * E + e;
-      offs[idx] = run;
-      run += hist[idx];
+    for (int c0 = 0; c0 < cta_per_block; c0 += 128) {
+      int v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 32 + lane;
+        v[u] = c < cta_per_block ? hist[static_cast<size_t>(b * cta_per_block + c) * E + e] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int inc = v[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int n = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += n;
+        }
+        const int c = c0 + u * 32 + lane;
+        if (c < cta_per_block) offs[static_cast<size_t>(b * cta_per_block + c) * E + e] = run + inc - v[u];
+        run += __shfl_sync(0xffffffffu, inc, 31);
+      }
     }
-    demand[p] = run;
-    atomicMax(&sh[e], run);
+    if (lane == 0) {
+      demand[p] = run;
+      atomicMax(&sh[e], run);
+    }
   }
   __syncthreads();
   __shared__ int32_t cap_sh;
@@ -329,10 +550,21 @@ __global__ void __launch_bounds__(256)
 template <typename TX>
 int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E, int k,
                 int32_t* idxs, double* gates, int32_t* hist, double* probs, cudaStream_t st) {
+  const TX* xp = static_cast<const TX*>(x);
+  if (E <= 64) {
+    const int cpb = (T + kDmTok - 1) / kDmTok;
+    const dim3 grid(blocks * cpb);
+    if (E <= 32)
+      gate_dmma_kernel<TX, 4><<<grid, kDmWarps * 32, 0, st>>>(xp, wg, T, M, E, k, cpb, idxs, gates,
+                                                              hist, probs);
+    else
+      gate_dmma_kernel<TX, 8><<<grid, kDmWarps * 32, 0, st>>>(xp, wg, T, M, E, k, cpb, idxs, gates,
+                                                              hist, probs);
+    return launch_status();
+  }
   const int cpb = (T + kGateTok - 1) / kGateTok;
   const dim3 grid(blocks * cpb);
   const size_t sh = static_cast<size_t>(E) * sizeof(int32_t);
-  const TX* xp = static_cast<const TX*>(x);
   if (E <= 32)
     gate_topk_kernel<TX, 1><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
                                                                 gates, hist, probs);
@@ -347,7 +579,7 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
                                                                 gates, hist, probs);
   else
     return -1;
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace
@@ -365,7 +597,7 @@ int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t 
   scan_kernel<<<1, 1024, a.E * sizeof(int32_t), st>>>(g.hist, a.blocks, cpb, a.E, a.T, a.k,
                                                       a.cap_kind, a.cap_formula, g.offs, g.demand,
                                                       g.list_base, g.fill, g.cap);
-  if (cudaGetLastError() != cudaSuccess) return -2;
+  if (launch_status() != 0) return -2;
   return 0;
 }
 
@@ -385,12 +617,12 @@ int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound
   assign_kernel<<<a.blocks * cpb, 256, sh, st>>>(g.idxs, g.gates, a.T, a.k, a.E, cpb, g.offs,
                                                  g.list_base, g.cap, a.bpr, g.locations,
                                                  g.slot_token, g.slot_gate, g.list, g.drops);
-  if (cudaGetLastError() != cudaSuccess) return -2;
+  if (launch_status() != 0) return -2;
   if (a.bpr) {
     const dim3 grid(a.blocks * a.E, (a.T + 255) / 256);
     bpr_rank_kernel<<<grid, 256, 0, st>>>(g.gates, a.k, a.E, g.demand, g.list_base, g.list, g.cap,
                                           g.locations, g.slot_token, g.slot_gate, g.drops);
-    if (cudaGetLastError() != cudaSuccess) return -2;
+    if (launch_status() != 0) return -2;
   }
   return 0;
 }

@@ -143,7 +143,7 @@ int launch_simt(int kind, const T* A, const T* B, TD* D, const GemmArgs& a, cuda
     case kGemmWgrad: gemm_simt_kernel<kGemmWgrad><<<grid, 256, 0, st>>>(A, B, D, a); break;
     default: return -1;
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace

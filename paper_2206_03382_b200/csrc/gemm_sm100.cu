@@ -20,6 +20,7 @@
 #include <cstdio>
 
 #include "gemm_sm100.h"
+#include "kernels.h"
 #include "ptx.cuh"
 
 namespace moe {
@@ -33,17 +34,16 @@ constexpr uint32_t UK = 16;   // K per tcgen05.mma (bf16)
 constexpr uint32_t kStages = 4;
 constexpr uint32_t kAccStages = 2;
 constexpr uint32_t kTmemCols = kAccStages * BN;  // 512
-constexpr uint32_t kThreads = 256;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-7 epilogue
-constexpr uint32_t kEpiThreads = 128;
+constexpr uint32_t kThreads = 384;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-11 epilogue
+constexpr uint32_t kEpiThreads = 256;
 
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
 constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
-constexpr uint32_t CD_STAGE_BYTES = BM * 128;     // 128 rows x 128 B
-constexpr uint32_t kCdStages = 2;
+constexpr uint32_t EPI_WARP_BYTES = 32 * 128;    // 32 rows x 128 B staging per epilogue warp
 constexpr uint32_t SMEM_A_OFF = 0;
 constexpr uint32_t SMEM_B_OFF = SMEM_A_OFF + kStages * A_STAGE_BYTES;
-constexpr uint32_t SMEM_CD_OFF = SMEM_B_OFF + kStages * B_STAGE_BYTES;
-constexpr uint32_t SMEM_BAR_OFF = SMEM_CD_OFF + kCdStages * CD_STAGE_BYTES;
+constexpr uint32_t SMEM_EPI_OFF = SMEM_B_OFF + kStages * B_STAGE_BYTES;
+constexpr uint32_t SMEM_BAR_OFF = SMEM_EPI_OFF + (kEpiThreads / 32) * EPI_WARP_BYTES;
 constexpr uint32_t SMEM_BYTES = SMEM_BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 
 struct TileCoord {
@@ -209,111 +209,122 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const uint32_t q = warp - 4;           // TMEM lane quadrant == warp % 4
-    const uint32_t row = q * 32 + lane;    // row inside the 128-row tile
-    constexpr uint32_t kColsPerChunk = (kEpi == kEpiF32) ? 32 : 64;  // 128 B of output
-    constexpr uint32_t kChunks = BN / kColsPerChunk;
-    uint32_t iter = 0, cd_stage = 0;
-    const bool leader = (threadIdx.x == 128);
+    // 8 warps: warp w reads TMEM lane quadrant w % 4 (32 rows) and column half (w - 4) / 4 of
+    // the 128 x 256 accumulator; each 128-byte-wide sub-chunk (64 bf16 / 32 fp32 columns) goes
+    // registers -> warp-private 128B-swizzled smem -> one TMA bulk store by lane 0.
+    const uint32_t q = warp % 4;
+    const uint32_t half = (warp - 4) / 4;
+    const uint32_t row = q * 32 + lane;
+    constexpr uint32_t kSub = (kEpi == kEpiF32) ? 32 : 64;  // columns per 128-byte sub-chunk
+    constexpr uint32_t kSubs = (BN / 2) / kSub;
+    uint8_t* stage = smem + SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES;
+    const uint32_t stage_row = ptx::smem_u32(stage) + lane * 128;
+    uint32_t iter = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
       const TileCoord tc = tile_coord<kRowK>(args, tile);
       const uint32_t acc = iter % kAccStages;
       const uint32_t acc_phase = (iter / kAccStages) & 1;
-      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
-      ptx::tc_fence_after();
-      const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16);
-      const int seg = kRowK ? static_cast<int>(tc.g)
-                            : static_cast<int>((args.seg_base + tc.s) * args.G + tc.g);
+      const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16) + half * (BN / 2);
+      const uint32_t seg = kRowK ? tc.g : (args.seg_base + tc.s) * args.G + tc.g;
       const uint32_t row_in = tc.m0 + row;
       const bool row_ok = kRowK || row_in < args.seg_rows;
+      const uint32_t col0 = tc.n0 + half * (BN / 2);
+      const size_t orow = static_cast<size_t>(seg) * args.seg_rows + row_in;  // row-M kinds
+      const size_t mrow = orow * (args.N / 64);
+      unsigned long long mw[kSubs];
+      if constexpr (kEpi == kEpiMaskBf16) {
+        // issued before the accumulator wait so their latency hides under the MMAs
+#pragma unroll
+        for (uint32_t c = 0; c < kSubs; ++c)
+          mw[c] = row_ok ? __ldg(args.relu_mask + mrow + col0 / 64 + c) : 0ull;
+      }
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::tc_fence_after();
 #pragma unroll 1
-      for (uint32_t c = 0; c < kChunks; ++c) {
-        uint32_t v[64];
-        if constexpr (kEpi == kEpiF32) {
-          uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
-          ptx::tmem_ld_32x32b_x32(tmem_row + c * 32, r0);
+      for (uint32_t c = 0; c < kSubs; ++c) {
+        uint32_t v[kSub];
+        if constexpr (kSub == 32) {
+          ptx::tmem_ld_32x32b_x32(tmem_row + c * kSub, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
         } else {
-          uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
-          uint32_t (&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32]);
-          ptx::tmem_ld_32x32b_x32(tmem_row + c * 64, r0);
-          ptx::tmem_ld_32x32b_x32(tmem_row + c * 64 + 32, r1);
+          ptx::tmem_ld_32x32b_x32(tmem_row + c * kSub, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          ptx::tmem_ld_32x32b_x32(tmem_row + c * kSub + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
         }
         ptx::tmem_ld_wait();
-        if (c == kChunks - 1) {
-          // Accumulator fully drained into registers: hand TMEM back to the MMA warp.
+        if (c == kSubs - 1) {
+          // accumulator drained into registers: hand TMEM back to the MMA warp
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty_bar[acc]);
         }
-        // Make sure the TMA store that last used this staging buffer has read it.
-        if (leader) ptx::tma_store_wait_read<kCdStages - 1>();
-        ptx::named_bar_sync(1, kEpiThreads);
-        uint8_t* cd = smem + SMEM_CD_OFF + cd_stage * CD_STAGE_BYTES;
-        const uint32_t cd_row = ptx::smem_u32(cd) + row * 128;
+        const uint32_t cols = col0 + c * kSub;
+        // the previous TMA store of this warp must have finished reading the staging buffer
+        if (lane == 0) ptx::tma_store_wait_read<0>();
+        __syncwarp();
         if constexpr (kEpi == kEpiF32) {
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
-            ptx::st_shared_v4(cd_row + ((j ^ (row & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
-                              v[4 * j + 3]);
+            ptx::st_shared_v4(stage_row + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1],
+                              v[4 * j + 2], v[4 * j + 3]);
         } else {
           float f[64];
 #pragma unroll
           for (uint32_t i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
           if constexpr (kEpi == kEpiReluBf16) {
             if (args.fix_list != nullptr && row_ok) {
-              // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64 re-decision.
-              const float rmax = args.rowmax[static_cast<size_t>(seg) * args.seg_rows + row_in] *
-                                 kReluTauScale;
-              const float* ca = args.colabs + static_cast<size_t>(tc.g) * args.N + tc.n0 + c * 64;
+              // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64
+              // re-decision. Prefilter against the 64-column block bound; per element on a hit.
+              const float rmax = args.rowmax[orow] * kReluTauScale;
+              const float tmax =
+                  rmax * __ldg(args.colabs_blk + static_cast<size_t>(tc.g) * (args.N / 64) + cols / 64);
+              float mn = fabsf(f[0]);
 #pragma unroll
-              for (uint32_t i = 0; i < 64; ++i) {
-                if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
-                  const unsigned int slot = atomicAdd(args.fix_count, 1u);
-                  if (slot < args.fix_cap)
-                    args.fix_list[slot] = fix_pack(seg, row_in, tc.n0 + c * 64 + i);
+              for (uint32_t i = 1; i < 64; ++i) mn = fminf(mn, fabsf(f[i]));
+              if (mn < tmax) {
+                const float* ca = args.colabs + static_cast<size_t>(tc.g) * args.N + cols;
+                for (uint32_t i = 0; i < 64; ++i) {
+                  if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
+                    const unsigned int slot = atomicAdd(args.fix_count, 1u);
+                    if (slot < args.fix_cap) args.fix_list[slot] = fix_pack(seg, row_in, cols + i);
+                  }
                 }
               }
             }
+            unsigned long long bits = 0ull;
 #pragma unroll
-            for (uint32_t i = 0; i < 64; ++i) f[i] = fmaxf(f[i], 0.0f);
+            for (uint32_t i = 0; i < 64; ++i) {
+              bits |= static_cast<unsigned long long>(f[i] > 0.0f) << i;
+              f[i] = fmaxf(f[i], 0.0f);
+            }
+            if (args.relu_mask != nullptr && row_ok) args.relu_mask[mrow + cols / 64] = bits;
           }
           if constexpr (kEpi == kEpiMaskBf16) {
-            // dh = (dY . W2^T) * [h > 0]; the saved activation a = relu(h) carries the mask.
-            if (row_ok) {
-              const uint4* aux = reinterpret_cast<const uint4*>(
-                  static_cast<const uint16_t*>(args.aux) +
-                  ((static_cast<size_t>(seg) * args.seg_rows + row_in) * args.N + tc.n0 + c * 64));
+            // dh = (dY . W2^T) * [h > 0]; the up-GEMM's ReLU bitmask carries [h > 0]
+            unsigned long long w = 0ull;
 #pragma unroll
-              for (uint32_t j = 0; j < 8; ++j) {
-                const uint4 w = __ldg(aux + j);
-                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+            for (uint32_t c2 = 0; c2 < kSubs; ++c2)
+              if (c2 == c) w = mw[c2];
 #pragma unroll
-                for (uint32_t h = 0; h < 4; ++h) {
-                  // bf16 > 0  <=>  sign bit clear and non-zero magnitude
-                  const uint32_t lo = ww[h] & 0xFFFFu, hi = ww[h] >> 16;
-                  if (!((lo & 0x8000u) == 0 && (lo & 0x7FFFu) != 0)) f[8 * j + 2 * h] = 0.0f;
-                  if (!((hi & 0x8000u) == 0 && (hi & 0x7FFFu) != 0)) f[8 * j + 2 * h + 1] = 0.0f;
-                }
-              }
-            }
+            for (uint32_t i = 0; i < 64; ++i)
+              if (!((w >> i) & 1ull)) f[i] = 0.0f;
           }
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
-            ptx::st_shared_v4(cd_row + ((j ^ (row & 7)) << 4), ptx::pack_bf16x2(f[8 * j], f[8 * j + 1]),
+            ptx::st_shared_v4(stage_row + ((j ^ (lane & 7)) << 4),
+                              ptx::pack_bf16x2(f[8 * j], f[8 * j + 1]),
                               ptx::pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
                               ptx::pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
                               ptx::pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
         }
         ptx::fence_proxy_async_smem();
-        ptx::named_bar_sync(1, kEpiThreads);
-        if (leader) {
-          ptx::tma_store_3d(&tmD, cd, static_cast<int>(tc.n0 + c * kColsPerChunk),
-                            static_cast<int>(tc.m0), seg);
+        __syncwarp();
+        if (lane == 0) {
+          // rows past the segment end are clipped by the tensor map bounds
+          ptx::tma_store_3d(&tmD, stage, static_cast<int>(cols), static_cast<int>(tc.m0 + q * 32),
+                            static_cast<int>(seg));
           ptx::tma_store_commit();
         }
-        cd_stage = (cd_stage + 1) % kCdStages;
       }
     }
-    if (leader) ptx::tma_store_wait_all<0>();
+    if (lane == 0) ptx::tma_store_wait_all<0>();
   }
 
   __syncwarp();
@@ -372,7 +383,7 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, con
   if (tiles == 0) return 0;
   const uint32_t grid = tiles < static_cast<uint32_t>(num_sms) ? tiles : num_sms;
   kern<<<grid, kThreads, SMEM_BYTES, stream>>>(a, b, d, args);
-  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+  return launch_status();
 }
 
 }  // namespace
@@ -389,9 +400,11 @@ int gemm_validate(const GemmArgs& a, int kind) {
 }
 
 // X:[nseg][seg_rows][K] bf16, W:[G][K][N] bf16 (row-major, N-major), D:[nseg][seg_rows][N]
-int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArgs& args,
+int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArgs& args_in,
              int nseg_total, int num_sms, cudaStream_t stream) {
-  if (gemm_validate(args, kind) != 0) return -1;
+  if (gemm_validate(args_in, kind) != 0) return -1;
+  GemmArgs args = args_in;
+  args.d_ptr = D;
   CUtensorMap ma, mb, md;
   const uint64_t nseg = static_cast<uint64_t>(nseg_total);
   int rc = 0;
@@ -400,16 +413,18 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
     case kGemmDown: {  // Y   = act . W2          A K-major, W2 [G][K=V][N=M] N-major
       rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
       rc |= make_map_3d(&mb, B, false, args.N, args.K, args.G, 64, 64);
-      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, BM);
+      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, 32);
       if (rc) return -2;
       return kind == kGemmUp ? launch<false, true, kEpiReluBf16, false>(ma, mb, md, args, num_sms, stream)
                              : launch<false, true, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
     }
     case kGemmDgradMask:  // dh = (dY . W2^T) * [a > 0]; W2 [G][V][M] == B K-major [G][N=V][K=M]
+      if (args.relu_mask == nullptr) return -1;
+      [[fallthrough]];
     case kGemmDgrad: {    // dX = dh . W1^T;             W1 [G][M][V] == B K-major [G][N=M][K=V]
       rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
       rc |= make_map_3d(&mb, B, false, args.K, args.N, args.G, 64, BN);
-      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, BM);
+      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, 32);
       if (rc) return -2;
       return kind == kGemmDgradMask
                  ? launch<false, false, kEpiMaskBf16, false>(ma, mb, md, args, num_sms, stream)
@@ -418,7 +433,7 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
     case kGemmWgrad: {  // dW[g] = A[g]^T . B[g] over all (segment, row); fp32 out [G][Mo][N]
       rc |= make_map_3d(&ma, A, false, args.Mo, args.seg_rows, nseg, 64, 64);
       rc |= make_map_3d(&mb, B, false, args.N, args.seg_rows, nseg, 64, 64);
-      rc |= make_map_3d(&md, D, true, args.N, args.Mo, args.G, 32, BM);
+      rc |= make_map_3d(&md, D, true, args.N, args.Mo, args.G, 32, 32);
       if (rc) return -2;
       return launch<true, true, kEpiF32, true>(ma, mb, md, args, num_sms, stream);
     }

@@ -8,6 +8,16 @@
 
 namespace moe {
 
+// Launch-error bookkeeping: cudaGetLastError() clears the error, so launch helpers record it
+// here for the caller's message (returns 0 on success, -2 on failure).
+cudaError_t& last_launch_error();
+inline int launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return 0;
+  last_launch_error() = e;
+  return -2;
+}
+
 struct GatingArgs {
   const void* x;       // [blocks*T, M] bf16 or f32
   int x_is_f32;
@@ -76,12 +86,14 @@ int fill_uniform_2d_device(void* dst, int dtype, int64_t rows, int64_t cols, int
                            uint64_t seed, uint64_t offset, double lo, double hi, cudaStream_t st);
 
 // ReLU-mask certificate support (relu_fix.cu).
-int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, void* w1t,
-                        cudaStream_t st);
+int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, float* colabs_blk,
+                        void* w1t, cudaStream_t st);
+int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned long long* mask,
+                              cudaStream_t st);
 int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st);
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
-                      void* act, cudaStream_t st);
+                      void* act, unsigned long long* relu_mask, cudaStream_t st);
 
 // fp32 SIMT GEMM path (the 1e-5 fp32 layer): same kinds/addressing as the bf16 tcgen05 GEMM.
 struct GemmArgs;

@@ -32,7 +32,9 @@ void ck(cudaError_t e, const char* what) {
 void ckr(int rc, const char* what) {
   if (rc == -1) throw MoeError(MOE_EINVAL, std::string(what) + ": invalid arguments");
   if (rc != 0) {
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = last_launch_error();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    last_launch_error() = cudaSuccess;
     throw MoeError(MOE_ECUDA, std::string(what) + ": launch failed (" + cudaGetErrorString(e) + ")");
   }
 }
@@ -41,6 +43,11 @@ void ckn(ncclResult_t r, const char* what) {
 }
 
 }  // namespace
+
+cudaError_t& last_launch_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
 
 // Round-to-nearest-even double -> bf16 bits without passing through fp32 (no double rounding).
 uint16_t bf16_bits_rne(double x) {
@@ -196,6 +203,8 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   if (cfg.dtype == MOE_DTYPE_BF16) {
     const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
     colabs_.alloc(sizeof(float) * dE_ * V_);
+    colabs_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
+    relu_mask_.alloc(sizeof(unsigned long long) * rows_all * (V_ / 64 + 1));
     w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
     rowmax_.alloc(sizeof(float) * rows_all);
     fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));
@@ -369,6 +378,8 @@ void Layer::prepare_up(GemmArgs& up) {
   if (cfg_.dtype != MOE_DTYPE_BF16) return;
   up.rowmax = static_cast<const float*>(rowmax_.p);
   up.colabs = static_cast<const float*>(colabs_.p);
+  up.colabs_blk = static_cast<const float*>(colabs_blk_.p);
+  up.relu_mask = static_cast<unsigned long long*>(relu_mask_.p);
   up.fix_list = static_cast<unsigned long long*>(fix_list_.p);
   up.fix_count = static_cast<unsigned int*>(fix_count_.p);
   up.fix_cap = fix_cap_;
@@ -478,13 +489,16 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   GatingBuffers gb = gating_buffers();
   prof_mark(kPhGate, true, st);
   ckr(run_gating_device(ga, gb, st), "gating");
-  ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
   prof_mark(kPhGate, false, st);
+  prof_mark(kPhAssign, true, st);
+  ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
+  prof_mark(kPhAssign, false, st);
   launches_ += 3 + (cfg_.bpr ? 1 : 0);
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
   if (cert && stats_dirty_) {
-    ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colabs_.p), w1t_.p, st),
+    ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colabs_.p),
+                            static_cast<float*>(colabs_blk_.p), w1t_.p, st),
         "weight stats");
     stats_dirty_ = false;
   }
@@ -509,10 +523,13 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   prepare_up(up);
   auto fixup = [&](void* xin) {
     if (!cert) return;
+    prof_mark(kPhReluFix, true, st);
     ckr(relu_fixup_device(xin, w1t_.p, dE_, cc_, M_, V_,
                           static_cast<const unsigned long long*>(fix_list_.p),
-                          static_cast<const unsigned int*>(fix_count_.p), fix_cap_, act_.p, st),
+                          static_cast<const unsigned int*>(fix_count_.p), fix_cap_, act_.p,
+                          static_cast<unsigned long long*>(relu_mask_.p), st),
         "relu_fixup");
+    prof_mark(kPhReluFix, false, st);
     ++launches_;
   };
 
@@ -524,8 +541,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     if (cert) ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
     prof_mark(kPhUp, true, st);
     gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
-    fixup(recv);
     prof_mark(kPhUp, false, st);
+    fixup(recv);
     prof_mark(kPhDown, true, st);
     gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
     prof_mark(kPhDown, false, st);
@@ -555,8 +572,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       }
       prof_mark(kPhUp, true, st);
       gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
-      fixup(recv);
       prof_mark(kPhUp, false, st);
+      fixup(recv);
       prof_mark(kPhDown, true, st);
       gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
       prof_mark(kPhDown, false, st);
@@ -619,11 +636,13 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   dgm.seg_rows = cc_;
   dgm.N = V_;
   dgm.K = M_;
-  dgm.aux = act_.p;
+  dgm.aux = act_.p;  // SIMT / fp32 paths read the activation's sign
+  dgm.relu_mask = static_cast<unsigned long long*>(relu_mask_.p);  // tcgen05 path: bitmask
   GemmArgs dg = dgm;  // dX = dh . W1^T
   dg.N = M_;
   dg.K = V_;
   dg.aux = nullptr;
+  dg.relu_mask = nullptr;
   GemmArgs wg1{};  // dW1 = X^T dh over every (chunk, source) segment
   wg1.G = dE_;
   wg1.S = degree_ * W_;

@@ -46,7 +46,7 @@ void validate(const moe_config& c);
 // pipeline.hpp:36-46 / pipeline.cpp:68-76, with measured instead of simulated intervals).
 enum Phase : int {
   kPhGate = 0, kPhEncode, kPhUp, kPhDown, kPhDecode, kPhDecodeBwd, kPhDgradMask, kPhDgrad,
-  kPhWgrad1, kPhWgrad2, kPhEncodeBwd, kPhA2aFwd, kPhA2aBwd, kNumPhases
+  kPhWgrad1, kPhWgrad2, kPhEncodeBwd, kPhA2aFwd, kPhA2aBwd, kPhAssign, kPhReluFix, kNumPhases
 };
 
 class Layer {
@@ -114,7 +114,7 @@ class Layer {
   DevMem z_, recv_, act_, yexp_, ycomb_, dz_, drecv_, dh_, dxe_, dxcomb_;
   DevMem io_x_, io_y_, io_dy_, io_dx_;
   // ReLU-mask certificate state (relu_fix.cu)
-  DevMem colabs_, w1t_, rowmax_, fix_list_, fix_count_;
+  DevMem colabs_, colabs_blk_, w1t_, rowmax_, fix_list_, fix_count_, relu_mask_;
   unsigned int fix_cap_ = 0;
   bool stats_dirty_ = true;
   void prepare_up(GemmArgs& up);

@@ -31,6 +31,18 @@ __global__ void colabs_kernel(const __nv_bfloat16* __restrict__ w1, int G, int M
   }
 }
 
+// blk[g][b] = max over the 64 columns of block b of colabs[g][:]
+__global__ void colabs_blk_kernel(const float* __restrict__ colabs, int G, int V,
+                                  float* __restrict__ blk) {
+  const int nb = V / 64;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G * nb; i += gridDim.x * blockDim.x) {
+    const float* c = colabs + static_cast<size_t>(i / nb) * V + (i % nb) * 64;
+    float m = 0.0f;
+    for (int j = 0; j < 64; ++j) m = fmaxf(m, c[j]);
+    blk[i] = m;
+  }
+}
+
 // out[g][c][r] = in[g][r][c] (bf16, 32x32 smem tiles)
 __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, int R, int Cc,
                                  __nv_bfloat16* __restrict__ out) {
@@ -71,7 +83,8 @@ __global__ void relu_fixup_kernel(const __nv_bfloat16* __restrict__ x,
                                   const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows, int M,
                                   int V, const unsigned long long* __restrict__ list,
                                   const unsigned int* __restrict__ count, unsigned int cap,
-                                  __nv_bfloat16* __restrict__ act) {
+                                  __nv_bfloat16* __restrict__ act,
+                                  unsigned long long* __restrict__ relu_mask) {
   const unsigned int n = min(*count, cap);
   const int lane = threadIdx.x % 32;
   for (unsigned int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n;
@@ -88,22 +101,54 @@ __global__ void relu_fixup_kernel(const __nv_bfloat16* __restrict__ x,
       s = fma(static_cast<double>(__bfloat162float(xr[m])), static_cast<double>(__bfloat162float(wr[m])), s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0)
-      act[(static_cast<size_t>(seg) * seg_rows + row) * V + col] = __double2bfloat16(s > 0.0 ? s : 0.0);
+    if (lane == 0) {
+      const size_t r = static_cast<size_t>(seg) * seg_rows + row;
+      act[r * V + col] = __double2bfloat16(s > 0.0 ? s : 0.0);
+      if (relu_mask) {
+        unsigned long long* w = relu_mask + r * (V / 64) + col / 64;
+        const unsigned long long bit = 1ull << (col % 64);
+        if (s > 0.0) atomicOr(w, bit);
+        else atomicAnd(w, ~bit);
+      }
+    }
+  }
+}
+
+// mask[r][w] bit i = act[r][64 w + i] > 0 (one thread per 64-column word)
+__global__ void mask_from_act_kernel(const __nv_bfloat16* __restrict__ act, int64_t rows, int V,
+                                     unsigned long long* __restrict__ mask) {
+  const int nw = V / 64;
+  const int64_t n = rows * nw;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const __nv_bfloat16* a = act + (i / nw) * V + (i % nw) * 64;
+    unsigned long long b = 0ull;
+    for (int j = 0; j < 64; ++j) b |= static_cast<unsigned long long>(__bfloat162float(a[j]) > 0.0f) << j;
+    mask[i] = b;
   }
 }
 
 }  // namespace
 
-int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, void* w1t,
-                        cudaStream_t st) {
+int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned long long* mask,
+                              cudaStream_t st) {
+  const int64_t n = rows * (V / 64);
+  const int grid = static_cast<int>(n / 256 + 1 < 148 * 16 ? n / 256 + 1 : 148 * 16);
+  mask_from_act_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(act), rows, V, mask);
+  return launch_status();
+}
+
+int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, float* colabs_blk,
+                        void* w1t, cudaStream_t st) {
   const int n = G * V;
   colabs_kernel<<<(n + 255) / 256, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w1), G, M, V,
                                                  colabs);
+  if (colabs_blk && V % 64 == 0)
+    colabs_blk_kernel<<<(G * V / 64 + 255) / 256, 256, 0, st>>>(colabs, G, V, colabs_blk);
   dim3 grid((V + 31) / 32, (M + 31) / 32, G);
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(static_cast<const __nv_bfloat16*>(w1), M, V,
                                                  static_cast<__nv_bfloat16*>(w1t));
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st) {
@@ -111,17 +156,17 @@ int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_
   const int64_t blocks = (rows + 7) / 8;
   const int grid = static_cast<int>(blocks < 148 * 16 ? blocks : 148 * 16);
   rowmax_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, M, rowmax);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
-                      void* act, cudaStream_t st) {
+                      void* act, unsigned long long* relu_mask, cudaStream_t st) {
   relu_fixup_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
                                              static_cast<const __nv_bfloat16*>(w1t), G, seg_rows,
                                              M, V, list, count, cap,
-                                             static_cast<__nv_bfloat16*>(act));
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+                                             static_cast<__nv_bfloat16*>(act), relu_mask);
+  return launch_status();
 }
 
 }  // namespace moe

@@ -67,7 +67,7 @@ int fill_uniform_2d_device(void* dst, int dtype, int64_t rows, int64_t cols, int
   else
     fill_kernel<double><<<grid, 256, 0, st>>>(static_cast<double*>(dst), rows, cols, src_stride,
                                               seed, offset, lo, hi);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int fill_uniform_device(void* dst, int dtype, int64_t n, uint64_t seed, uint64_t offset, double lo,

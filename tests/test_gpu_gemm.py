@@ -46,7 +46,8 @@ def test_row_m_kinds(cuda, use_tc, G, S, seg_rows, M, V):
     ref_y = torch.bmm(got_act.float(), W2.float())
     got_y = Y.view(S, G, seg_rows, M).permute(1, 0, 2, 3).reshape(G, S * seg_rows, M)
     assert rel(got_y, ref_y) < 1e-2
-    # dgrad with mask: dh = (dY W2^T) * [act > 0]
+    # dgrad with mask: dh = (dY W2^T) * [act > 0] -- via moe_op_expert_ffn_backward's path below;
+    # here the SIMT path (reads act) and, for tcgen05, an explicit bitmask built from act.
     dY = torch.randn(nseg, seg_rows, M, device=cuda).to(bf)
     dYg = dY.view(S, G, seg_rows, M).permute(1, 0, 2, 3).reshape(G, S * seg_rows, M).float()
     dh = torch.empty(nseg, seg_rows, V, device=cuda, dtype=bf)
