@@ -135,6 +135,7 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   k_ = static_cast<int>(cfg.top_k);
   esz_ = cfg.dtype == MOE_DTYPE_BF16 ? 2 : 4;
   if (rank < 0 || rank >= W_) throw MoeError(MOE_EINVAL, "rank out of range");
+  if (cfg.gpus_per_node == cfg.world_size) memo_.allowed = {0, 1, 2, 3};  // linear x {1,2,4,8}
   if (cfg.capacity_kind != MOE_CAP_FIXED)
     throw MoeError(MOE_EINVAL, "layer: Auto/Bounded capacity is available through moe_op_gating only");
   cap_ = static_cast<int>(expert_capacity(k_, cfg.capacity_factor, T_, E_));
@@ -594,7 +595,11 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ck(cudaEventRecord(ev_fwd_end_, st), "event");
   fwd_done_ = true;
   metrics_valid_ = false;
-  if (cfg_.adaptive) {
+  // Alg. 1 feedback (pipeline.cpp:227-237). Measuring needs a host sync (and, for W > 1, an
+  // all-reduce so every rank records the same time and picks the same strategy), so it runs
+  // while the f bucket is still exploring; once every strategy has a time the controller
+  // exploits the argmin without stalling the stream.
+  if (cfg_.adaptive && !strategy_settled(memo_, f_)) {
     ck(cudaEventSynchronize(ev_fwd_end_), "event sync");
     float ms = 0.0f;
     ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");

@@ -54,14 +54,32 @@ void recompute_buckets(StrategyMemo& memo, double f) {
   }
 }
 
+namespace {
+
+std::vector<int> allowed_of(const StrategyMemo& memo) {
+  if (!memo.allowed.empty()) return memo.allowed;
+  std::vector<int> all(strategy_space().size());
+  for (size_t i = 0; i < all.size(); ++i) all[i] = static_cast<int>(i);
+  return all;
+}
+
+bool complete(const std::map<int, double>& table, const std::vector<int>& allowed) {
+  for (int i : allowed)
+    if (table.find(i) == table.end()) return false;
+  return true;
+}
+
+}  // namespace
+
 Strategy get_strategy(StrategyMemo& memo, double f) {
   if (memo.per_f.find(f) == memo.per_f.end()) recompute_buckets(memo, f);
   const auto& space = strategy_space();
+  const std::vector<int> allowed = allowed_of(memo);
   auto argmin = [&](const std::map<int, double>& table) {
-    Strategy best = space.front();
+    Strategy best = space[allowed.front()];
     double best_t = std::numeric_limits<double>::infinity();
-    for (size_t i = 0; i < space.size(); ++i) {
-      auto it = table.find(static_cast<int>(i));
+    for (int i : allowed) {  // exploration order breaks ties
+      auto it = table.find(i);
       if (it != table.end() && it->second < best_t) {
         best = space[i];
         best_t = it->second;
@@ -70,13 +88,22 @@ Strategy get_strategy(StrategyMemo& memo, double f) {
     return best;
   };
   const auto& own = memo.per_f[f];
-  if (own.size() == space.size()) return argmin(own);
+  if (complete(own, allowed)) return argmin(own);
   StrategyMemo::Bucket* b = find_bucket(memo, f);
   if (!b) throw std::logic_error("get_strategy: f missing from every bucket");
-  if (b->table.size() == space.size()) return argmin(b->table);
-  for (size_t i = 0; i < space.size(); ++i)
-    if (b->table.find(static_cast<int>(i)) == b->table.end()) return space[i];
+  if (complete(b->table, allowed)) return argmin(b->table);
+  for (int i : allowed)
+    if (b->table.find(i) == b->table.end()) return space[i];
   return argmin(b->table);
+}
+
+bool strategy_settled(StrategyMemo& memo, double f) {
+  auto it = memo.per_f.find(f);
+  if (it == memo.per_f.end()) return false;
+  const std::vector<int> allowed = allowed_of(memo);
+  if (complete(it->second, allowed)) return true;
+  StrategyMemo::Bucket* b = find_bucket(memo, f);
+  return b && complete(b->table, allowed);
 }
 
 void optimize_strategy(StrategyMemo& memo, double f, const Strategy& s, double seconds) {

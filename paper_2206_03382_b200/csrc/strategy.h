@@ -18,6 +18,10 @@ int strategy_index(const Strategy& s);
 
 struct StrategyMemo {
   double bucket_length = 0.5;
+  // Strategy indices the search may use (empty = the reference's full space). Inside a single
+  // NVSwitch domain (gpus_per_node == W) 2DH is linear plus two local copies, so the layer
+  // restricts the search to the linear degrees.
+  std::vector<int> allowed;
   struct Bucket {
     double start = 0.0;
     std::vector<double> members;
@@ -30,5 +34,7 @@ struct StrategyMemo {
 void recompute_buckets(StrategyMemo& memo, double f);
 Strategy get_strategy(StrategyMemo& memo, double f);
 void optimize_strategy(StrategyMemo& memo, double f, const Strategy& s, double seconds);
+// True once f's own table or its bucket has a time for every strategy (get_strategy exploits).
+bool strategy_settled(StrategyMemo& memo, double f);
 
 }  // namespace moe

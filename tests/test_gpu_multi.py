@@ -1,0 +1,34 @@
+"""Expert parallelism on >= 2 GPUs (skipped on a 1-GPU box): tools/mp_parity.py under torchrun
+checks every rank's routing, y, dx and local dW against the fp64 oracle of the whole layer for
+pipelining degrees 1/2/4/8, an fp32 case and the adaptive Alg. 1 controller."""
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_expert_parallel_parity(cuda):
+    n = min(torch.cuda.device_count(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           str(ROOT / "tools" / "mp_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "FAIL" not in r.stdout and r.stdout.count("PASS") >= 6

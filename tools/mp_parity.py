@@ -1,0 +1,81 @@
+"""Expert-parallel parity on W GPUs (torchrun, one rank per GPU, NCCL): every rank's y / dx /
+routing and its local experts' dW1 / dW2 against the fp64 oracle of the whole W-block layer
+(moe_layer.cpp:171-319), for several pipelining degrees and the adaptive Alg. 1 controller."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+from paper_2206_03382_b200 import LayerState, MoELayerConfig, backward, forward  # noqa: E402
+from tests.helpers import layer_inputs  # noqa: E402
+
+
+def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, seed=402):
+    E = E_per * W
+    cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
+                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f, bpr=bpr,
+                         dtype=dt, degree=degree, adaptive=adaptive)
+    obj = [LayerState.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
+    inp = layer_inputs(seed, W, T, M, V, E, dt)
+    tdt = cfg.torch_dtype
+    xs = torch.as_tensor(inp["x"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
+    dys = torch.as_tensor(inp["dy"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
+    steps = 10 if adaptive else 1
+    for _ in range(steps):
+        res = forward(st, xs)
+        g = backward(st, res.saved, dys)
+    torch.cuda.synchronize()
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, 0, f, bpr)
+    sl = slice(rank * T, (rank + 1) * T)
+    el = slice(rank * E_per, (rank + 1) * E_per)
+    idxs, loc, gates, cap = st.routing()
+    tol = 1e-5 if dt == "f32" else 2e-2
+    errs = dict(
+        routing=int(not (np.array_equal(idxs, ref["idxs"][sl]) and np.array_equal(loc, ref["locations"][sl]))),
+        cap=int(cap != ref["capacity"]),
+        y=oracle.max_rel_diff(res.y.double().cpu().numpy(), ref["y"][sl]),
+        dx=oracle.max_rel_diff(g.dx.double().cpu().numpy(), ref["dx"][sl]),
+        dw1=oracle.max_rel_diff(g.dw1.double().cpu().numpy(), ref["dw1"][el]),
+        dw2=oracle.max_rel_diff(g.dw2.double().cpu().numpy(), ref["dw2"][el]),
+    )
+    m = st.metrics()
+    ok = errs["routing"] == 0 and errs["cap"] == 0 and all(errs[n] < tol for n in ("y", "dx", "dw1", "dw2"))
+    t = torch.tensor([0.0 if ok else 1.0], device=dev)
+    dist.all_reduce(t)
+    st.close()
+    return ok and t.item() == 0, errs, m
+
+
+def main():
+    rank, W, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    cases = [
+        # E_per, k, f, M, V, T, bpr, dtype, degree, adaptive
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 1, False),
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False),
+        (4, 1, 1.0, 256, 512, 1024, False, "bf16", 4, False),
+        (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False),   # drops, ragged chunks
+        (2, 2, 1.0, 64, 128, 200, True, "f32", 2, False),
+        (4, 1, 1.0, 512, 1024, 2048, False, "bf16", 1, True),  # Alg. 1 adaptive degree
+    ]
+    all_ok = True
+    for c in cases:
+        ok, errs, m = run(rank, W, dev, *c)
+        all_ok &= ok
+        if rank == 0:
+            print(("PASS" if ok else "FAIL"), c, {k: (round(v, 7) if isinstance(v, float) else v) for k, v in errs.items()},
+                  f"degree={m.degree} f={m.f:.3f} comm_bytes={m.comm_bytes:.0f}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if all_ok else 1)
+
+
+if __name__ == "__main__":
+    main()
