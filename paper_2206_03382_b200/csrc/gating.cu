@@ -372,55 +372,60 @@ __global__ void __launch_bounds__(kDmWarps * 32)
   for (int e = threadIdx.x; e < E; e += NTH) hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
 }
 
-// Per (block, expert): exclusive scan of CTA histograms, demand, resolved capacity, fill counts
-// and the member-list base used by BPR. One CTA; warp w scans the CTA-histogram columns of pairs
-// w, w+32, ... with warp shuffles (32 CTA counts per step, loads issued 4 steps ahead).
-__global__ void __launch_bounds__(1024)
-    scan_kernel(const int32_t* __restrict__ hist, int blocks, int cta_per_block, int E, int T,
-                int k, int cap_kind, int cap_formula, int32_t* __restrict__ offs,
-                int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
-                int32_t* __restrict__ fill, int32_t* __restrict__ cap_out) {
-  extern __shared__ int32_t sh[];  // [E] max demand over blocks
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) sh[e] = 0;
-  __syncthreads();
-  for (int p = warp; p < blocks * E; p += nwarps) {
-    const int b = p / E, e = p % E;
-    int run = 0;
-    for (int c0 = 0; c0 < cta_per_block; c0 += 128) {
-      int v[4];
+// Per (block, expert) column: exclusive scan of the CTA histograms -> offs, demand.
+// One CTA per column; each thread scans a contiguous run of CTA counts, then a block scan.
+__global__ void __launch_bounds__(256)
+    scan_cols_kernel(const int32_t* __restrict__ hist, int cta_per_block, int E,
+                     int32_t* __restrict__ offs, int32_t* __restrict__ demand) {
+  __shared__ int32_t wsum[8];
+  const int p = blockIdx.x, b = p / E, e = p % E;
+  const int per = (cta_per_block + blockDim.x - 1) / blockDim.x;
+  const int c0 = threadIdx.x * per;
+  int local[16];  // cta_per_block <= 4096 (T <= 256K tokens per block)
+  int sum = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * 32 + lane;
-        v[u] = c < cta_per_block ? hist[static_cast<size_t>(b * cta_per_block + c) * E + e] : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int inc = v[u];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int n = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += n;
-        }
-        const int c = c0 + u * 32 + lane;
-        if (c < cta_per_block) offs[static_cast<size_t>(b * cta_per_block + c) * E + e] = run + inc - v[u];
-        run += __shfl_sync(0xffffffffu, inc, 31);
-      }
-    }
-    if (lane == 0) {
-      demand[p] = run;
-      atomicMax(&sh[e], run);
-    }
+  for (int i = 0; i < 16; ++i) {
+    const int c = c0 + i;
+    local[i] = (i < per && c < cta_per_block) ? hist[static_cast<size_t>(b * cta_per_block + c) * E + e] : 0;
+    sum += local[i];
   }
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += n;
+  }
+  if (lane == 31) wsum[warp] = inc;
   __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  int run = base + inc - sum;  // exclusive prefix of this thread's run
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int c = c0 + i;
+    if (i < per && c < cta_per_block) offs[static_cast<size_t>(b * cta_per_block + c) * E + e] = run;
+    run += local[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) demand[p] = run;
+}
+
+// resolve_capacity (core.cpp:47-59) over the per-block max demand, fill counts and the BPR
+// member-list bases. One small CTA.
+__global__ void finalize_capacity_kernel(int blocks, int E, int T, int k, int cap_kind,
+                                         int cap_formula, const int32_t* __restrict__ demand,
+                                         int32_t* __restrict__ list_base,
+                                         int32_t* __restrict__ fill, int32_t* __restrict__ cap_out) {
   __shared__ int32_t cap_sh;
+  __shared__ int32_t mx_sh;
+  if (threadIdx.x == 0) mx_sh = 1;  // max demand floors at 1
+  __syncthreads();
+  for (int p = threadIdx.x; p < blocks * E; p += blockDim.x) atomicMax(&mx_sh, demand[p]);
+  __syncthreads();
   if (threadIdx.x == 0) {
-    // resolve_capacity (core.cpp:47-59): max demand floors at 1.
-    int mx = 1;
-    for (int e = 0; e < E; ++e) mx = max(mx, sh[e]);
     int cap = cap_formula;
-    if (cap_kind == 1) cap = mx;                      // Auto
-    if (cap_kind == 2) cap = min(mx, cap_formula);    // Bounded (formula at max_factor)
+    if (cap_kind == 1) cap = mx_sh;                      // Auto
+    if (cap_kind == 2) cap = min(mx_sh, cap_formula);    // Bounded (formula at max_factor)
     cap_sh = cap;
     *cap_out = cap;
   }
@@ -594,9 +599,11 @@ int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t 
                       : launch_gate<__nv_bfloat16>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k,
                                                    g.idxs, g.gates, g.hist, g.probs, st);
   if (rc) return rc;
-  scan_kernel<<<1, 1024, a.E * sizeof(int32_t), st>>>(g.hist, a.blocks, cpb, a.E, a.T, a.k,
-                                                      a.cap_kind, a.cap_formula, g.offs, g.demand,
-                                                      g.list_base, g.fill, g.cap);
+  if (cpb > 16 * 256) return -1;
+  scan_cols_kernel<<<a.blocks * a.E, 256, 0, st>>>(g.hist, cpb, a.E, g.offs, g.demand);
+  if (launch_status() != 0) return -2;
+  finalize_capacity_kernel<<<1, 256, 0, st>>>(a.blocks, a.E, a.T, a.k, a.cap_kind, a.cap_formula,
+                                             g.demand, g.list_base, g.fill, g.cap);
   if (launch_status() != 0) return -2;
   return 0;
 }

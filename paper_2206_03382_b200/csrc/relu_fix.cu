@@ -97,8 +97,25 @@ __global__ void relu_fixup_kernel(const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* xr = x + (static_cast<size_t>(seg) * seg_rows + row) * M;
     const __nv_bfloat16* wr = w1t + (static_cast<size_t>(g) * V + col) * M;
     double s = 0.0;
-    for (int m = lane; m < M; m += 32)
-      s = fma(static_cast<double>(__bfloat162float(xr[m])), static_cast<double>(__bfloat162float(wr[m])), s);
+    if ((M & 7) == 0) {
+      // 16-byte loads: 8 bf16 of x and of W1^T per lane per step
+      const uint4* xv = reinterpret_cast<const uint4*>(xr);
+      const uint4* wv = reinterpret_cast<const uint4*>(wr);
+      for (int v = lane; v < M / 8; v += 32) {
+        const uint4 a = __ldg(xv + v), w = __ldg(wv + v);
+        const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 af = __bfloat1622float2(ah[q]), wf = __bfloat1622float2(wh[q]);
+          s = fma(static_cast<double>(af.x), static_cast<double>(wf.x), s);
+          s = fma(static_cast<double>(af.y), static_cast<double>(wf.y), s);
+        }
+      }
+    } else {
+      for (int m = lane; m < M; m += 32)
+        s = fma(static_cast<double>(__bfloat162float(xr[m])), static_cast<double>(__bfloat162float(wr[m])), s);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
