@@ -229,6 +229,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--degree", type=int, default=0, help="pipelining degree (0: adaptive Alg. 1)")
+    ap.add_argument("--a2a", default="peer", choices=["peer", "nccl"],
+                    help="W>1 all-to-all: copy engines over NVLink peer memory, or NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -269,7 +271,7 @@ def run_gpu(args):
     cfg = MoELayerConfig(world_size=world, gpus_per_node=world, global_experts=E, model_dim=M,
                          hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f,
                          bpr=d["bpr"], dtype=d["dtype"], adaptive=adaptive,
-                         degree=args.degree if args.degree else 1)
+                         degree=args.degree if args.degree else 1, a2a_backend=args.a2a)
     state = LayerState.init(cfg, SEED, rank=rank, device=local, nccl_id=nccl_id)
     off = rng.draw_offsets(M, E, V, world, T)
     x = torch.empty(T, M, dtype=tdt, device=dev)
@@ -394,6 +396,7 @@ def run_gpu(args):
             "config": {"workload": wl, "desc": d["desc"], "E": E, "k": k, "f": f, "M": M, "V": V,
                        "tokens_per_gpu": T, "global_batch": world * T, "bpr": d["bpr"],
                        "capacity": cap, "parallelism": f"ep{world}",
+                       "a2a": args.a2a if world > 1 else None,
                        "degree": metrics.degree, "adaptive": adaptive,
                        "l2": "per-step working set >1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_sus"],

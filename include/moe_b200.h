@@ -57,7 +57,15 @@ typedef struct moe_config {
   int32_t dtype;           /* MOE_DTYPE_BF16 (tensor-core path) or MOE_DTYPE_F32 */
   int32_t adaptive;        /* StrategyControl::adaptive: Alg. 1 picks the pipelining degree */
   int32_t degree;          /* StrategyControl::fixed.degree (capacity chunks), 1..8 */
+  int32_t a2a_backend;     /* MOE_A2A_BACKEND_*: how W > 1 ranks exchange tokens */
 } moe_config;
+
+/* All-to-all transport for W > 1. PEER: copy engines push blocks into the peers' receive
+ * buffers over NVLink (CUDA IPC mappings), ordered by epoch flags -- no SMs are taken from the
+ * expert GEMMs it overlaps. NCCL: grouped ncclSend/ncclRecv. Same plan (moe_a2a_plan), same
+ * results bit for bit. */
+#define MOE_A2A_BACKEND_PEER 0
+#define MOE_A2A_BACKEND_NCCL 1
 
 /* StepMetrics (moe_layer.hpp:46-54); sim_seconds becomes measured device seconds. */
 typedef struct moe_step_metrics {

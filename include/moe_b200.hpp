@@ -45,6 +45,7 @@ struct Dims {  // core.hpp:32-56 (per-rank placement)
 struct StrategyControl {  // moe_layer.hpp:17-20
   bool adaptive = false;
   int degree = 1;
+  int a2a_backend = MOE_A2A_BACKEND_PEER;
 };
 
 struct MoELayerConfig {  // moe_layer.hpp:22-29
@@ -70,6 +71,7 @@ struct MoELayerConfig {  // moe_layer.hpp:22-29
     c.dtype = static_cast<int32_t>(dtype);
     c.adaptive = strategy.adaptive ? 1 : 0;
     c.degree = strategy.degree;
+    c.a2a_backend = strategy.a2a_backend;
     return c;
   }
 };

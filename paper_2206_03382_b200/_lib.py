@@ -35,6 +35,7 @@ class MoeConfig(C.Structure):
         ("model_dim", C.c_int64), ("hidden_dim", C.c_int64), ("tokens_per_step", C.c_int64),
         ("top_k", C.c_int64), ("capacity_kind", C.c_int32), ("capacity_factor", C.c_double),
         ("bpr", C.c_int32), ("dtype", C.c_int32), ("adaptive", C.c_int32), ("degree", C.c_int32),
+        ("a2a_backend", C.c_int32),
     ]
 
 

@@ -158,7 +158,10 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   for (int i = 0; i < 8; ++i) {
     ck(cudaEventCreateWithFlags(&ev_a_[i], cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ev_b_[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_c_[i], cudaEventDisableTiming), "event");
   }
+  for (int c = 0; c < PeerExchange::kChannels; ++c)
+    ck(cudaEventCreateWithFlags(&ev_freed_[c], cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_comm_done_, cudaEventDisableTiming), "event");
 
   if (W_ > 1) {
@@ -217,6 +220,12 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
     ycomb_.alloc(rowsM);
     drecv_.alloc(rowsM);
     dxcomb_.alloc(rowsM);
+    if (cfg.a2a_backend == MOE_A2A_BACKEND_PEER) {
+      void* bufs[PeerExchange::kChannels] = {recv_.p, ycomb_.p, drecv_.p, dxcomb_.p};
+      peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs);
+    } else if (cfg.a2a_backend != MOE_A2A_BACKEND_NCCL) {
+      throw MoeError(MOE_EINVAL, "unknown all-to-all backend");
+    }
   }
 }
 
@@ -258,6 +267,8 @@ void Layer::take_profile(double* ms, int64_t* counts, int n) {
 }
 
 Layer::~Layer() {
+  if (comm_stream_) cudaStreamSynchronize(comm_stream_);
+  peer_.reset();
   for (const auto& r : prof_recs_) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -272,7 +283,9 @@ Layer::~Layer() {
   for (int i = 0; i < 8; ++i) {
     cudaEventDestroy(ev_a_[i]);
     cudaEventDestroy(ev_b_[i]);
+    cudaEventDestroy(ev_c_[i]);
   }
+  for (int c = 0; c < PeerExchange::kChannels; ++c) cudaEventDestroy(ev_freed_[c]);
 }
 
 uint64_t Layer::expert_draw_offset(int64_t e) const {
@@ -473,6 +486,17 @@ void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
   comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
 }
 
+// Copy-engine version of exchange(): push chunk `chunk` of `src` into every peer's channel
+// buffer (same plan), then publish the chunk's ready flag.
+void Layer::peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch) {
+  std::vector<int64_t> so(W_), ro(W_);
+  int64_t elems = 0;
+  a2a_plan(W_, E_, cc_, M_, chunk, phase, so.data(), ro.data(), &elems);
+  peer_->push_chunk(comm_stream_, ch, chunk, src, so.data(), ro.data(),
+                    static_cast<size_t>(elems) * esz_, esz_, epoch);
+  comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
+}
+
 void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   launches_ = 0;
@@ -547,6 +571,61 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     prof_mark(kPhDown, true, st);
     gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
     prof_mark(kPhDown, false, st);
+  } else if (peer_) {
+    if (bwd_pending_) {
+      // The previous forward was not followed by a backward (inference): its saved expert
+      // inputs are dead, so release the receive buffer to the peers now (stream-ordered after
+      // that forward's GEMMs).
+      peer_->signal_freed(st, 0, epoch_[0]);
+      ck(cudaEventRecord(ev_freed_[0], st), "event");
+    }
+    // Copy engines over NVLink: all dispatches, then all combines (the reference's FIFO order,
+    // pipeline.cpp:180-190); each chunk's GEMMs start when its blocks have landed.
+    const uint32_t e0 = ++epoch_[0], e1 = ++epoch_[1];
+    ck(cudaEventRecord(ev_sync_, st), "event");
+    ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[0], 0), "wait");  // my recv buffer consumed
+    peer_->wait_peers_freed(comm_stream_, 0, e0);
+    prof_mark(kPhA2aFwd, true, comm_stream_);
+    for (int i = 0; i < degree_; ++i) {
+      peer_push(0, z_.p, i, 0, e0);
+      ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+    }
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
+      peer_->wait_chunk(st, 0, i, e0);
+      up.seg_base = i * W_;
+      down.seg_base = i * W_;
+      if (cert) {
+        const size_t r0 = static_cast<size_t>(i) * W_ * dE_ * cc_;
+        ckr(rowmax_device(static_cast<char*>(recv) + r0 * M_ * esz_,
+                          static_cast<int64_t>(W_) * dE_ * cc_, M_,
+                          static_cast<float*>(rowmax_.p) + r0, st),
+            "rowmax");
+        ++launches_;
+        ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
+      }
+      prof_mark(kPhUp, true, st);
+      gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+      prof_mark(kPhUp, false, st);
+      fixup(recv);
+      prof_mark(kPhDown, true, st);
+      gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+      prof_mark(kPhDown, false, st);
+      ck(cudaEventRecord(ev_b_[i], st), "event");
+    }
+    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[1], 0), "wait");  // my ycomb consumed
+    peer_->wait_peers_freed(comm_stream_, 1, e1);
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+      peer_push(1, yexp_.p, i, 1, e1);
+      ck(cudaEventRecord(ev_c_[i], comm_stream_), "event");
+    }
+    prof_mark(kPhA2aFwd, false, comm_stream_);
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_c_[i], 0), "wait");
+      peer_->wait_chunk(st, 1, i, e1);
+    }
   } else {
     // Comm stream: all dispatches (chunk order), then all combines (reference FIFO order,
     // pipeline.cpp:180-190); compute stream: per chunk up+down GEMMs.
@@ -592,6 +671,11 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
   prof_mark(kPhDecode, false, st);
   ++launches_;
+  if (peer_) {
+    peer_->signal_freed(st, 1, epoch_[1]);
+    ck(cudaEventRecord(ev_freed_[1], st), "event");
+    bwd_pending_ = true;
+  }
   ck(cudaEventRecord(ev_fwd_end_, st), "event");
   fwd_done_ = true;
   metrics_valid_ = false;
@@ -675,6 +759,54 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     prof_mark(kPhWgrad2, true, st);
     gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
     prof_mark(kPhWgrad2, false, st);
+  } else if (peer_) {
+    const uint32_t e2 = ++epoch_[2], e3 = ++epoch_[3];
+    ck(cudaEventRecord(ev_sync_, st), "event");
+    ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[2], 0), "wait");
+    peer_->wait_peers_freed(comm_stream_, 2, e2);
+    prof_mark(kPhA2aBwd, true, comm_stream_);
+    for (int i = 0; i < degree_; ++i) {  // adjoint of combine
+      peer_push(2, dz_.p, i, 0, e2);
+      ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+    }
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
+      peer_->wait_chunk(st, 2, i, e2);
+      dgm.seg_base = i * W_;
+      dg.seg_base = i * W_;
+      prof_mark(kPhDgradMask, true, st);
+      gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
+      prof_mark(kPhDgradMask, false, st);
+      prof_mark(kPhDgrad, true, st);
+      gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+      prof_mark(kPhDgrad, false, st);
+      ck(cudaEventRecord(ev_b_[i], st), "event");
+    }
+    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[3], 0), "wait");
+    peer_->wait_peers_freed(comm_stream_, 3, e3);
+    for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
+      ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+      peer_push(3, dxe_.p, i, 1, e3);
+      ck(cudaEventRecord(ev_c_[i], comm_stream_), "event");
+    }
+    prof_mark(kPhA2aBwd, false, comm_stream_);
+    // Weight gradients overlap the return pushes; then the receive buffers are released.
+    prof_mark(kPhWgrad1, true, st);
+    gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
+    prof_mark(kPhWgrad1, false, st);
+    peer_->signal_freed(st, 0, epoch_[0]);
+    ck(cudaEventRecord(ev_freed_[0], st), "event");
+    bwd_pending_ = false;
+    prof_mark(kPhWgrad2, true, st);
+    gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
+    prof_mark(kPhWgrad2, false, st);
+    peer_->signal_freed(st, 2, e2);
+    ck(cudaEventRecord(ev_freed_[2], st), "event");
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_c_[i], 0), "wait");
+      peer_->wait_chunk(st, 3, i, e3);
+    }
   } else {
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
@@ -714,6 +846,10 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st), "encode_bwd");
   prof_mark(kPhEncodeBwd, false, st);
   ++launches_;
+  if (peer_) {
+    peer_->signal_freed(st, 3, epoch_[3]);
+    ck(cudaEventRecord(ev_freed_[3], st), "event");
+  }
   bwd_launches_ = launches_ - l0;
   if (dw1) last_dw1_ = nullptr; else last_dw1_ = gw1;
   if (dw2) last_dw2_ = nullptr; else last_dw2_ = gw2;

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -12,6 +13,7 @@
 #include "../../include/moe_b200.h"
 #include "gemm_sm100.h"
 #include "kernels.h"
+#include "peer_a2a.h"
 #include "strategy.h"
 
 namespace moe {
@@ -84,6 +86,7 @@ class Layer {
   GatingBuffers gating_buffers();
   SlotGeom geom() const;
   void exchange(const void* send, void* recv, int chunk, int phase);
+  void peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch);
   double allreduce_max_host(double v);
   void ensure_io();
   void prof_mark(int phase, bool begin, cudaStream_t st);
@@ -106,7 +109,11 @@ class Layer {
   cudaStream_t comm_stream_ = nullptr;
   ncclComm_t comm_ = nullptr;
   cudaEvent_t ev_fwd_start_{}, ev_fwd_end_{}, ev_sync_{}, ev_comm_done_{};
-  cudaEvent_t ev_a_[8]{}, ev_b_[8]{};
+  cudaEvent_t ev_a_[8]{}, ev_b_[8]{}, ev_c_[8]{};
+  cudaEvent_t ev_freed_[PeerExchange::kChannels]{};
+  std::unique_ptr<PeerExchange> peer_;
+  uint32_t epoch_[PeerExchange::kChannels] = {0, 0, 0, 0};
+  bool bwd_pending_ = false;  // last forward's receive buffer still held for a backward
 
   DevMem wg_, w1_, w2_, dw1_, dw2_;
   DevMem idxs_, gates_, locs_, hist_, offs_, demand_, list_base_, fill_, list_, capd_, drops_;

@@ -1,0 +1,187 @@
+// Copy-engine all-to-all over NVLink peer memory. See peer_a2a.h.
+#include "peer_a2a.h"
+
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "layer.h"
+
+namespace moe {
+
+namespace {
+
+PFN_cuStreamWaitValue32_v11070 g_wait = nullptr;
+PFN_cuStreamWriteValue32_v11070 g_write = nullptr;
+bool g_resolved = false;
+
+void resolve() {
+  if (g_resolved) return;
+  g_resolved = true;
+  cudaDriverEntryPointQueryResult q{};
+  void* p = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_wait = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  p = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_write = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw MoeError(MOE_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kStageSlots = 2 * PeerExchange::kChannels;
+
+}  // namespace
+
+bool stream_memops_available() {
+  resolve();
+  return g_wait != nullptr && g_write != nullptr;
+}
+
+int stream_write_u32(cudaStream_t st, void* addr, uint32_t value) {
+  resolve();
+  if (!g_write) return -1;
+  return g_write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), value,
+                 CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS
+             ? 0
+             : -2;
+}
+
+int stream_wait_geq_u32(cudaStream_t st, const void* addr, uint32_t value) {
+  resolve();
+  if (!g_wait) return -1;
+  return g_wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), value,
+                CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
+             ? 0
+             : -2;
+}
+
+PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels])
+    : rank_(rank), world_(world) {
+  if (!stream_memops_available())
+    throw MoeError(MOE_ECUDA, "peer all-to-all: CUDA stream memory operations unavailable");
+  for (int c = 0; c < kChannels; ++c) local_bufs_[c] = bufs[c];
+  nflags_ = static_cast<size_t>(kChannels) * world * kMaxChunks + static_cast<size_t>(kChannels) * world +
+            kStageSlots;
+  ck(cudaMalloc(&flags_, nflags_ * sizeof(uint32_t) + 256), "cudaMalloc flags");
+  ck(cudaMemset(flags_, 0, nflags_ * sizeof(uint32_t) + 256), "memset flags");
+
+  // Exchange IPC handles of {flags, 4 receive buffers} through NCCL.
+  constexpr int kH = 1 + kChannels;
+  std::vector<cudaIpcMemHandle_t> mine(kH);
+  ck(cudaIpcGetMemHandle(&mine[0], flags_), "cudaIpcGetMemHandle");
+  for (int c = 0; c < kChannels; ++c) ck(cudaIpcGetMemHandle(&mine[1 + c], bufs[c]), "cudaIpcGetMemHandle");
+  const size_t hb = kH * sizeof(cudaIpcMemHandle_t);
+  void* dev = nullptr;
+  ck(cudaMalloc(&dev, hb * (world + 1)), "cudaMalloc handles");
+  ck(cudaMemcpy(dev, mine.data(), hb, cudaMemcpyHostToDevice), "copy handles");
+  cudaStream_t s;
+  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  if (ncclAllGather(dev, static_cast<char*>(dev) + hb, hb, ncclUint8, comm, s) != ncclSuccess)
+    throw MoeError(MOE_ECOMM, "peer all-to-all: handle all-gather failed");
+  ck(cudaStreamSynchronize(s), "sync");
+  cudaStreamDestroy(s);
+  std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(kH) * world);
+  ck(cudaMemcpy(all.data(), static_cast<char*>(dev) + hb, hb * world, cudaMemcpyDeviceToHost), "copy");
+  cudaFree(dev);
+
+  peer_flags_.assign(world, nullptr);
+  peer_bufs_.assign(kChannels, std::vector<void*>(world, nullptr));
+  for (int p = 0; p < world; ++p) {
+    if (p == rank) continue;
+    ck(cudaIpcOpenMemHandle(&peer_flags_[p], all[static_cast<size_t>(p) * kH], cudaIpcMemLazyEnablePeerAccess),
+       "cudaIpcOpenMemHandle(flags)");
+    for (int c = 0; c < kChannels; ++c)
+      ck(cudaIpcOpenMemHandle(&peer_bufs_[c][p], all[static_cast<size_t>(p) * kH + 1 + c],
+                              cudaIpcMemLazyEnablePeerAccess),
+         "cudaIpcOpenMemHandle(buffer)");
+  }
+}
+
+PeerExchange::~PeerExchange() {
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) continue;
+    if (peer_flags_[p]) cudaIpcCloseMemHandle(peer_flags_[p]);
+    for (int c = 0; c < kChannels; ++c)
+      if (peer_bufs_[c][p]) cudaIpcCloseMemHandle(peer_bufs_[c][p]);
+  }
+  if (flags_) cudaFree(flags_);
+}
+
+// Flag block layout (u32): ready[ch][src][chunk] | freed[ch][src] | stage[2*ch + kind]
+uint32_t* PeerExchange::ready_local(int ch, int src, int chunk) const {
+  return static_cast<uint32_t*>(flags_) + (static_cast<size_t>(ch) * world_ + src) * kMaxChunks + chunk;
+}
+uint32_t* PeerExchange::freed_local(int ch, int src) const {
+  return static_cast<uint32_t*>(flags_) + static_cast<size_t>(kChannels) * world_ * kMaxChunks +
+         static_cast<size_t>(ch) * world_ + src;
+}
+uint32_t* PeerExchange::ready_remote(int dst, int ch, int chunk) const {
+  return static_cast<uint32_t*>(peer_flags_[dst]) + (static_cast<size_t>(ch) * world_ + rank_) * kMaxChunks +
+         chunk;
+}
+uint32_t* PeerExchange::freed_remote(int dst, int ch) const {
+  return static_cast<uint32_t*>(peer_flags_[dst]) + static_cast<size_t>(kChannels) * world_ * kMaxChunks +
+         static_cast<size_t>(ch) * world_ + rank_;
+}
+uint32_t* PeerExchange::stage(int slot) const {
+  return static_cast<uint32_t*>(flags_) + static_cast<size_t>(kChannels) * world_ * kMaxChunks +
+         static_cast<size_t>(kChannels) * world_ + slot;
+}
+
+// Write epoch into a local stage word, then DMA it to each destination flag (all in stream
+// order, so the flags land after every earlier copy on this stream).
+void PeerExchange::publish(cudaStream_t st, int slot, uint32_t epoch, const std::vector<uint32_t*>& dsts) {
+  if (stream_write_u32(st, stage(slot), epoch) != 0) throw MoeError(MOE_ECUDA, "cuStreamWriteValue32 failed");
+  for (uint32_t* d : dsts)
+    ck(cudaMemcpyAsync(d, stage(slot), sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "flag copy");
+}
+
+void PeerExchange::wait_peers_freed(cudaStream_t copy, int ch, uint32_t epoch) {
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) continue;
+    if (stream_wait_geq_u32(copy, freed_local(ch, p), epoch - 1) != 0)
+      throw MoeError(MOE_ECUDA, "cuStreamWaitValue32 failed");
+  }
+}
+
+void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
+                              const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch) {
+  if (chunk >= kMaxChunks) throw MoeError(MOE_EINVAL, "peer all-to-all: too many chunks");
+  // Push model: peer p receives my block where it receives "from rank_", i.e. at ro[rank_] of
+  // the (source-symmetric) plan. Start with the next peer so all ranks spread over the links.
+  for (int i = 0; i < world_; ++i) {
+    const int p = (rank_ + i) % world_;
+    char* dst = static_cast<char*>(p == rank_ ? local_bufs_[ch] : peer_bufs_[ch][p]) + ro[rank_] * esz;
+    ck(cudaMemcpyAsync(dst, static_cast<const char*>(src) + so[p] * esz, block_bytes,
+                       cudaMemcpyDeviceToDevice, copy),
+       "peer copy");
+  }
+  std::vector<uint32_t*> dsts;
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_) dsts.push_back(ready_remote(p, ch, chunk));
+  publish(copy, 2 * ch, epoch, dsts);
+}
+
+void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch) {
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) continue;
+    if (stream_wait_geq_u32(st, ready_local(ch, p, chunk), epoch) != 0)
+      throw MoeError(MOE_ECUDA, "cuStreamWaitValue32 failed");
+  }
+}
+
+void PeerExchange::signal_freed(cudaStream_t st, int ch, uint32_t epoch) {
+  std::vector<uint32_t*> dsts;
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_) dsts.push_back(freed_remote(p, ch));
+  publish(st, 2 * ch + 1, epoch, dsts);
+}
+
+}  // namespace moe

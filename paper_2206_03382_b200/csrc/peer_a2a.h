@@ -1,0 +1,69 @@
+// Copy-engine flexible all-to-all over NVLink peer memory (one process per GPU).
+//
+// Every rank maps its peers' receive buffers (CUDA IPC) and pushes its blocks with
+// cudaMemcpyAsync on a dedicated copy stream: the DMA engines move the data over NVLink, so the
+// exchange takes no SMs from the persistent expert GEMMs it overlaps with. Ordering across
+// processes uses 32-bit epoch flags in each receiver's memory:
+//   ready[ch][src][chunk]  -- written (after the data) by src into dst's flags; dst's compute
+//                             stream waits with cuStreamWaitValue32(GEQ epoch).
+//   freed[ch][src]         -- written by src once it has consumed its channel-ch buffer for an
+//                             epoch; a sender waits on its own copy before overwriting src's buffer
+//                             in the next epoch.
+// Epochs are per channel and advance identically on every rank (SPMD call sequence).
+// Semantics are all2all_linear / flex_all2all (collectives.cpp:48-56, 116-162).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace moe {
+
+class PeerExchange {
+ public:
+  static constexpr int kChannels = 4;  // fwd dispatch, fwd combine, bwd dispatch, bwd combine
+  static constexpr int kMaxChunks = 8;
+
+  // bufs[ch]: this rank's receive buffer of channel ch (cudaMalloc base pointers).
+  PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels]);
+  ~PeerExchange();
+  PeerExchange(const PeerExchange&) = delete;
+  PeerExchange& operator=(const PeerExchange&) = delete;
+
+  // Copy stream: wait until every peer has freed its channel-ch buffer of epoch-1.
+  void wait_peers_freed(cudaStream_t copy, int ch, uint32_t epoch);
+  // Copy stream: push block p of `src` (offset so[p]) to peer p's channel buffer at the offset p
+  // receives from this rank, ro[rank] (moe_a2a_plan is source-symmetric), then publish
+  // ready[ch][me][chunk] = epoch to each peer.
+  void push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
+                  const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch);
+  // Compute stream: wait for every peer's chunk of this epoch.
+  void wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch);
+  // Stream st (after the consumers of channel ch's buffer): tell every peer it is free.
+  void signal_freed(cudaStream_t st, int ch, uint32_t epoch);
+
+ private:
+  uint32_t* ready_local(int ch, int src, int chunk) const;
+  uint32_t* freed_local(int ch, int src) const;
+  uint32_t* ready_remote(int dst, int ch, int chunk) const;  // my slot in dst's flags
+  uint32_t* freed_remote(int dst, int ch) const;
+  uint32_t* stage(int slot) const;
+  void publish(cudaStream_t st, int slot, uint32_t epoch, const std::vector<uint32_t*>& dsts);
+
+  int rank_, world_;
+  void* flags_ = nullptr;                       // this rank's flag block (IPC exported)
+  std::vector<void*> peer_flags_;               // mapped flag blocks of peers (nullptr for self)
+  std::vector<std::vector<void*>> peer_bufs_;   // [ch][peer] mapped receive buffers
+  void* local_bufs_[kChannels];
+  size_t nflags_ = 0;
+};
+
+// Driver stream memory operations (resolved through cudaGetDriverEntryPoint).
+bool stream_memops_available();
+int stream_write_u32(cudaStream_t st, void* addr, uint32_t value);
+int stream_wait_geq_u32(cudaStream_t st, const void* addr, uint32_t value);
+
+}  // namespace moe

@@ -38,12 +38,14 @@ class MoELayerConfig:
     dtype: str = "bf16"
     adaptive: bool = False
     degree: int = 1
+    a2a_backend: str = "peer"   # "peer" (copy engines over NVLink) or "nccl"
 
     def to_c(self) -> MoeConfig:
         return MoeConfig(self.world_size, self.gpus_per_node, self.global_experts, self.model_dim,
                          self.hidden_dim, self.tokens_per_step, self.top_k, _CAP[self.capacity],
                          float(self.capacity_factor), int(self.bpr), _DT[self.dtype],
-                         int(self.adaptive), int(self.degree))
+                         int(self.adaptive), int(self.degree),
+                         {"peer": 0, "nccl": 1}[self.a2a_backend])
 
     @property
     def local_experts(self) -> int:

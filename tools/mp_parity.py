@@ -14,11 +14,11 @@ from paper_2206_03382_b200 import LayerState, MoELayerConfig, backward, forward 
 from tests.helpers import layer_inputs  # noqa: E402
 
 
-def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, seed=402):
+def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, seed=402):
     E = E_per * W
     cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
                          hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f, bpr=bpr,
-                         dtype=dt, degree=degree, adaptive=adaptive)
+                         dtype=dt, degree=degree, adaptive=adaptive, a2a_backend=backend)
     obj = [LayerState.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
@@ -26,9 +26,11 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, seed=402)
     tdt = cfg.torch_dtype
     xs = torch.as_tensor(inp["x"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
     dys = torch.as_tensor(inp["dy"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
-    steps = 10 if adaptive else 1
-    for _ in range(steps):
+    steps = 10 if adaptive else 2
+    for it in range(steps):
         res = forward(st, xs)
+        if it == 0 and not adaptive:
+            res = forward(st, xs)  # inference-style forward without backward in between
         g = backward(st, res.saved, dys)
     torch.cuda.synchronize()
     ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, 0, f, bpr)
@@ -58,13 +60,15 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
     cases = [
-        # E_per, k, f, M, V, T, bpr, dtype, degree, adaptive
-        (2, 2, 1.25, 256, 512, 512, True, "bf16", 1, False),
-        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False),
-        (4, 1, 1.0, 256, 512, 1024, False, "bf16", 4, False),
-        (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False),   # drops, ragged chunks
-        (2, 2, 1.0, 64, 128, 200, True, "f32", 2, False),
-        (4, 1, 1.0, 512, 1024, 2048, False, "bf16", 1, True),  # Alg. 1 adaptive degree
+        # E_per, k, f, M, V, T, bpr, dtype, degree, adaptive, all-to-all backend
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 1, False, "peer"),
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer"),
+        (4, 1, 1.0, 256, 512, 1024, False, "bf16", 4, False, "peer"),
+        (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "peer"),   # drops, ragged chunks
+        (2, 2, 1.0, 64, 128, 200, True, "f32", 2, False, "peer"),
+        (4, 1, 1.0, 512, 1024, 2048, False, "bf16", 1, True, "peer"),  # Alg. 1 adaptive degree
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "nccl"),
+        (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "nccl"),
     ]
     all_ok = True
     for c in cases:
