@@ -7,10 +7,12 @@ fallback path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libmoe_b200.so"
+# MOE_LIB_PATH selects an alternative build of the same library (tuning variants); default in-tree.
+LIB_PATH = Path(os.environ.get("MOE_LIB_PATH", _PKG / "libmoe_b200.so"))
 
 MOE_OK, MOE_EINVAL, MOE_ECUDA, MOE_ECOMM, MOE_ESTATE, MOE_ENOMEM = range(6)
 DTYPE_BF16, DTYPE_F32, DTYPE_F64 = 0, 1, 2

@@ -16,8 +16,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "build"
-LIB = PKG / "libmoe_b200.so"
+OBJ = Path(os.environ.get("MOE_BUILD_DIR", PKG / "build"))
+LIB = Path(os.environ.get("MOE_LIB_OUT", PKG / "libmoe_b200.so"))
+EXTRA = os.environ.get("MOE_NVCC_EXTRA", "").split()  # e.g. tuning variants: -DMOE_GEMM_STAGES=4
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
@@ -42,7 +43,7 @@ def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
     obj = OBJ / (src.name + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
-    cmd = [nvcc()] + NVCC_FLAGS + ["-c", str(src), "-o", str(obj)]
+    cmd = [nvcc()] + NVCC_FLAGS + EXTRA + ["-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu":
         cmd.insert(1, "-Xptxas=-v") if verbose else None
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,7 +55,7 @@ def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
 
 
 def build(verbose: bool = False, force: bool = False) -> Path:
-    OBJ.mkdir(exist_ok=True)
+    OBJ.mkdir(parents=True, exist_ok=True)
     if force:
         for o in OBJ.glob("*.o"):
             o.unlink()

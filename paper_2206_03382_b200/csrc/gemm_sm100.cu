@@ -23,6 +23,13 @@
 #include "kernels.h"
 #include "ptx.cuh"
 
+#ifndef MOE_GEMM_STAGES
+#define MOE_GEMM_STAGES 4
+#endif
+#ifndef MOE_GEMM_EPI_BUFS
+#define MOE_GEMM_EPI_BUFS 1
+#endif
+
 namespace moe {
 
 namespace {
@@ -31,7 +38,8 @@ constexpr uint32_t BM = 128;  // UMMA M (TMEM lanes)
 constexpr uint32_t BN = 256;  // UMMA N
 constexpr uint32_t BK = 64;   // one 128-byte swizzle atom of bf16 along K
 constexpr uint32_t UK = 16;   // K per tcgen05.mma (bf16)
-constexpr uint32_t kStages = 4;
+constexpr uint32_t kStages = MOE_GEMM_STAGES;
+constexpr uint32_t kEpiBufs = MOE_GEMM_EPI_BUFS;  // staging buffers per epilogue warp
 constexpr uint32_t kAccStages = 2;
 constexpr uint32_t kTmemCols = kAccStages * BN;  // 512
 constexpr uint32_t kThreads = 384;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-11 epilogue
@@ -43,7 +51,7 @@ constexpr uint32_t EPI_WARP_BYTES = 32 * 128;    // 32 rows x 128 B staging per 
 constexpr uint32_t SMEM_A_OFF = 0;
 constexpr uint32_t SMEM_B_OFF = SMEM_A_OFF + kStages * A_STAGE_BYTES;
 constexpr uint32_t SMEM_EPI_OFF = SMEM_B_OFF + kStages * B_STAGE_BYTES;
-constexpr uint32_t SMEM_BAR_OFF = SMEM_EPI_OFF + (kEpiThreads / 32) * EPI_WARP_BYTES;
+constexpr uint32_t SMEM_BAR_OFF = SMEM_EPI_OFF + (kEpiThreads / 32) * EPI_WARP_BYTES * kEpiBufs;
 constexpr uint32_t SMEM_BYTES = SMEM_BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 
 struct TileCoord {
@@ -217,8 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = q * 32 + lane;
     constexpr uint32_t kSub = (kEpi == kEpiF32) ? 32 : 64;  // columns per 128-byte sub-chunk
     constexpr uint32_t kSubs = (BN / 2) / kSub;
-    uint8_t* stage = smem + SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES;
-    const uint32_t stage_row = ptx::smem_u32(stage) + lane * 128;
+    uint8_t* stage_base = smem + SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES * kEpiBufs;
+    uint32_t ebuf = 0;
     uint32_t iter = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
       const TileCoord tc = tile_coord<kRowK>(args, tile);
@@ -256,8 +264,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive(&tempty_bar[acc]);
         }
         const uint32_t cols = col0 + c * kSub;
-        // the previous TMA store of this warp must have finished reading the staging buffer
-        if (lane == 0) ptx::tma_store_wait_read<0>();
+        uint8_t* stage = stage_base + ebuf * EPI_WARP_BYTES;
+        const uint32_t stage_row = ptx::smem_u32(stage) + lane * 128;
+        ebuf = (ebuf + 1) % kEpiBufs;
+        // the TMA store that last used this staging buffer must have finished reading it
+        if (lane == 0) ptx::tma_store_wait_read<kEpiBufs - 1>();
         __syncwarp();
         if constexpr (kEpi == kEpiF32) {
 #pragma unroll

@@ -10,7 +10,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/moe_b200.h"
+#include "moe_b200.h"
 #include "gemm_sm100.h"
 #include "kernels.h"
 #include "peer_a2a.h"
