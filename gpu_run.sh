@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-echo "== 3 stages, 2 epi bufs"; timeout 300 python tools/gemm_bench.py 2>&1 | tail -3
-echo "== 4 stages, 1 epi buf"; MOE_LIB_PATH=gpurun_out/libmoe_v41.so timeout 300 python tools/gemm_bench.py 2>&1 | tail -3
-echo "== 2 stages, 2 epi bufs"; MOE_LIB_PATH=gpurun_out/libmoe_v42.so timeout 300 python tools/gemm_bench.py 2>&1 | tail -3
+mkdir -p gpurun_out
+timeout 300 python bench.py --steps 30 --no-cpu-baseline --no-e2e > gpurun_out/bench2.json 2> gpurun_out/bench2.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/bench2.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['phases_ms'])"
+tail -3 gpurun_out/bench2.err
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -5

@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "gemm_sm100.h"
 #include "kernels.h"
@@ -25,6 +26,9 @@
 
 #ifndef MOE_GEMM_STAGES
 #define MOE_GEMM_STAGES 4
+#endif
+#ifndef MOE_GEMM_STAGES_PAIR
+#define MOE_GEMM_STAGES_PAIR 6
 #endif
 #ifndef MOE_GEMM_EPI_BUFS
 #define MOE_GEMM_EPI_BUFS 1
@@ -34,57 +38,66 @@ namespace moe {
 
 namespace {
 
-constexpr uint32_t BM = 128;  // UMMA M (TMEM lanes)
+constexpr uint32_t BM = 128;  // accumulator rows per CTA (TMEM lanes)
 constexpr uint32_t BN = 256;  // UMMA N
 constexpr uint32_t BK = 64;   // one 128-byte swizzle atom of bf16 along K
 constexpr uint32_t UK = 16;   // K per tcgen05.mma (bf16)
-constexpr uint32_t kStages = MOE_GEMM_STAGES;
 constexpr uint32_t kEpiBufs = MOE_GEMM_EPI_BUFS;  // staging buffers per epilogue warp
 constexpr uint32_t kAccStages = 2;
 constexpr uint32_t kTmemCols = kAccStages * BN;  // 512
 constexpr uint32_t kThreads = 384;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-11 epilogue
 constexpr uint32_t kEpiThreads = 256;
-
-constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
-constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
+constexpr uint32_t kEpiWarps = kEpiThreads / 32;
 constexpr uint32_t EPI_WARP_BYTES = 32 * 128;    // 32 rows x 128 B staging per epilogue warp
-constexpr uint32_t SMEM_A_OFF = 0;
-constexpr uint32_t SMEM_B_OFF = SMEM_A_OFF + kStages * A_STAGE_BYTES;
-constexpr uint32_t SMEM_EPI_OFF = SMEM_B_OFF + kStages * B_STAGE_BYTES;
-constexpr uint32_t SMEM_BAR_OFF = SMEM_EPI_OFF + (kEpiThreads / 32) * EPI_WARP_BYTES * kEpiBufs;
-constexpr uint32_t SMEM_BYTES = SMEM_BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+
+// kCG = 1: one CTA computes a 128 x 256 tile. kCG = 2: a CTA pair (cluster of 2, cta_group::2)
+// computes 256 x 256: each CTA holds its 128 A rows and half (128 columns) of B, so B smem per
+// CTA halves and the pipeline gets deeper (6 stages instead of 4).
+template <int kCG>
+struct Cfg {
+  static constexpr uint32_t kStages = kCG == 1 ? MOE_GEMM_STAGES : MOE_GEMM_STAGES_PAIR;
+  static constexpr uint32_t TM = BM * kCG;   // tile rows per work unit
+  static constexpr uint32_t BNL = BN / kCG;  // B columns loaded per CTA
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BNL * BK * 2;
+  static constexpr uint32_t SMEM_A_OFF = 0;
+  static constexpr uint32_t SMEM_B_OFF = SMEM_A_OFF + kStages * A_BYTES;
+  static constexpr uint32_t SMEM_EPI_OFF = SMEM_B_OFF + kStages * B_BYTES;
+  static constexpr uint32_t SMEM_BAR_OFF = SMEM_EPI_OFF + kEpiWarps * EPI_WARP_BYTES * kEpiBufs;
+  static constexpr uint32_t SMEM_BYTES = SMEM_BAR_OFF + 256 + 1024;  // + barriers + alignment
+};
 
 struct TileCoord {
   uint32_t g, s, m0, n0;  // row-M: m0 = row within segment; row-K: m0 = output row
 };
 
-template <bool kRowK>
+template <bool kRowK, uint32_t TM>
 __device__ __forceinline__ TileCoord tile_coord(const GemmArgs& a, uint32_t tile) {
   const uint32_t n_tiles = a.N / BN;
   TileCoord c;
   c.n0 = (tile % n_tiles) * BN;
   uint32_t rest = tile / n_tiles;
   if constexpr (!kRowK) {
-    const uint32_t mts = (a.seg_rows + BM - 1) / BM;
-    c.m0 = (rest % mts) * BM;
+    const uint32_t mts = (a.seg_rows + TM - 1) / TM;
+    c.m0 = (rest % mts) * TM;
     rest /= mts;
     c.s = rest % a.S;
     c.g = rest / a.S;
   } else {
-    const uint32_t mts = a.Mo / BM;
-    c.m0 = (rest % mts) * BM;
+    const uint32_t mts = (a.Mo + TM - 1) / TM;
+    c.m0 = (rest % mts) * TM;
     c.g = rest / mts;
     c.s = 0;
   }
   return c;
 }
 
-template <bool kRowK>
-__device__ __forceinline__ uint32_t num_tiles(const GemmArgs& a) {
+template <bool kRowK, uint32_t TM>
+__host__ __device__ __forceinline__ uint32_t num_tiles(const GemmArgs& a) {
   if constexpr (!kRowK)
-    return a.G * a.S * ((a.seg_rows + BM - 1) / BM) * (a.N / BN);
+    return a.G * a.S * ((a.seg_rows + TM - 1) / TM) * (a.N / BN);
   else
-    return a.G * (a.Mo / BM) * (a.N / BN);
+    return a.G * ((a.Mo + TM - 1) / TM) * (a.N / BN);
 }
 
 template <bool kRowK>
@@ -95,14 +108,16 @@ __device__ __forceinline__ uint32_t num_kblocks(const GemmArgs& a) {
     return a.S * ((a.seg_rows + BK - 1) / BK);
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK>
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmD, const GemmArgs args) {
+  using C = Cfg<kCG>;
+  constexpr uint32_t kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + SMEM_BAR_OFF);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR_OFF);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + kAccStages;
@@ -110,55 +125,69 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
+  const uint32_t rank = kCG == 2 ? ptx::cluster_ctarank() : 0;  // CTA within the pair
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
     ptx::prefetch_tmap(&tmD);
     for (uint32_t i = 0; i < kStages; ++i) {
-      ptx::mbar_init(&full_bar[i], 1);
+      // pair: the leader's full barrier collects both CTAs' producer arrivals and TMA bytes
+      ptx::mbar_init(&full_bar[i], kCG == 2 && leader ? 2 : 1);
       ptx::mbar_init(&empty_bar[i], 1);
     }
     for (uint32_t i = 0; i < kAccStages; ++i) {
       ptx::mbar_init(&tfull_bar[i], 1);
-      ptx::mbar_init(&tempty_bar[i], kEpiThreads);
+      ptx::mbar_init(&tempty_bar[i], kEpiWarps * kCG);  // one arrival per epilogue warp (of the pair)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc<kTmemCols, kCG>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (kCG == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const uint32_t ntiles = num_tiles<kRowK>(args);
+  const uint32_t ntiles = num_tiles<kRowK, C::TM>(args);
   const uint32_t nkb = num_kblocks<kRowK>(args);
+  const uint32_t unit0 = blockIdx.x / kCG, unit_step = gridDim.x / kCG;
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ TMA producer
     uint32_t stage = 0, phase = 0;
     const uint32_t kb_per_seg = (args.seg_rows + BK - 1) / BK;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const TileCoord tc = tile_coord<kRowK>(args, tile);
+    auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+      if constexpr (kCG == 2)
+        ptx::tma_load_3d_pair(m, bar, dst, c0, c1, c2);
+      else
+        ptx::tma_load_3d(m, bar, dst, c0, c1, c2);
+    };
+    for (uint32_t tile = unit0; tile < ntiles; tile += unit_step) {
+      const TileCoord tc = tile_coord<kRowK, C::TM>(args, tile);
+      const uint32_t m0 = tc.m0 + rank * BM;       // this CTA's A rows
+      const uint32_t nb = tc.n0 + rank * C::BNL;   // this CTA's B columns
       for (uint32_t kb = 0; kb < nkb; ++kb) {
         ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* sa = smem + SMEM_A_OFF + stage * A_STAGE_BYTES;
-        uint8_t* sb = smem + SMEM_B_OFF + stage * B_STAGE_BYTES;
+        uint8_t* sa = smem + C::SMEM_A_OFF + stage * C::A_BYTES;
+        uint8_t* sb = smem + C::SMEM_B_OFF + stage * C::B_BYTES;
         if constexpr (!kRowK) {
           const int seg = static_cast<int>((args.seg_base + tc.s) * args.G + tc.g);
           const int k0 = static_cast<int>(kb * BK);
           // A: K-major [seg][seg_rows][K]
-          ptx::tma_load_3d(&tmA, &full_bar[stage], sa, k0, static_cast<int>(tc.m0), seg);
+          load(&tmA, &full_bar[stage], sa, k0, static_cast<int>(m0), seg);
           if constexpr (!kBMN) {
             // B: K-major [G][N][K]
-            ptx::tma_load_3d(&tmB, &full_bar[stage], sb, k0, static_cast<int>(tc.n0),
-                             static_cast<int>(tc.g));
+            load(&tmB, &full_bar[stage], sb, k0, static_cast<int>(nb), static_cast<int>(tc.g));
           } else {
-            // B: N-major [G][K][N], four 64-column atoms
+            // B: N-major [G][K][N], 64-column atoms
 #pragma unroll
-            for (uint32_t a = 0; a < BN / 64; ++a)
-              ptx::tma_load_3d(&tmB, &full_bar[stage], sb + a * (BK * 128),
-                               static_cast<int>(tc.n0 + a * 64), k0, static_cast<int>(tc.g));
+            for (uint32_t a = 0; a < C::BNL / 64; ++a)
+              load(&tmB, &full_bar[stage], sb + a * (BK * 128), static_cast<int>(nb + a * 64), k0,
+                   static_cast<int>(tc.g));
           }
         } else {
           const uint32_t s = kb / kb_per_seg;
@@ -167,27 +196,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           // A^T: rows are K, MN-major [seg][seg_rows][Mo]
 #pragma unroll
           for (uint32_t a = 0; a < BM / 64; ++a)
-            ptx::tma_load_3d(&tmA, &full_bar[stage], sa + a * (BK * 128),
-                             static_cast<int>(tc.m0 + a * 64), r0, seg);
+            load(&tmA, &full_bar[stage], sa + a * (BK * 128), static_cast<int>(m0 + a * 64), r0, seg);
           // B: N-major [seg][seg_rows][N]
 #pragma unroll
-          for (uint32_t a = 0; a < BN / 64; ++a)
-            ptx::tma_load_3d(&tmB, &full_bar[stage], sb + a * (BK * 128),
-                             static_cast<int>(tc.n0 + a * 64), r0, seg);
+          for (uint32_t a = 0; a < C::BNL / 64; ++a)
+            load(&tmB, &full_bar[stage], sb + a * (BK * 128), static_cast<int>(nb + a * 64), r0, seg);
         }
-        ptx::mbar_arrive_expect_tx(&full_bar[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+        if (leader)
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], (C::A_BYTES + C::B_BYTES) * kCG);
+        else
+          ptx::mbar_arrive_cluster(&full_bar[stage], 0);
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = ptx::make_idesc_bf16(BM, BN, kAMN, kBMN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(C::TM, BN, kAMN, kBMN);
     uint32_t stage = 0, phase = 0;
     uint32_t iter = 0;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+    for (uint32_t tile = unit0; tile < ntiles; tile += unit_step, ++iter) {
       const uint32_t acc = iter % kAccStages;
       const uint32_t acc_phase = (iter / kAccStages) & 1;
       ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -196,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t kb = 0; kb < nkb; ++kb) {
         ptx::mbar_wait(&full_bar[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + SMEM_A_OFF + stage * A_STAGE_BYTES);
-        const uint32_t sb = ptx::smem_u32(smem + SMEM_B_OFF + stage * B_STAGE_BYTES);
+        const uint32_t sa = ptx::smem_u32(smem + C::SMEM_A_OFF + stage * C::A_BYTES);
+        const uint32_t sb = ptx::smem_u32(smem + C::SMEM_B_OFF + stage * C::B_BYTES);
 #pragma unroll
         for (uint32_t k = 0; k < BK / UK; ++k) {
           // K-major: advance 32 B inside the swizzle atom. MN-major: advance 16 K-rows (2 KiB).
@@ -205,10 +235,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       : ptx::make_sw128_desc(sa + k * 32, 16, 1024);
           const uint64_t bdesc = kBMN ? ptx::make_sw128_desc(sb + k * 2048, BK * 128, 1024)
                                       : ptx::make_sw128_desc(sb + k * 32, 16, 1024);
-          ptx::umma_bf16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          if constexpr (kCG == 2)
+            ptx::umma_bf16_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          else
+            ptx::umma_bf16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
         }
-        ptx::umma_commit(&empty_bar[stage]);
-        if (kb == nkb - 1) ptx::umma_commit(&tfull_bar[acc]);
+        if constexpr (kCG == 2) {
+          ptx::umma_commit_pair(&empty_bar[stage]);
+          if (kb == nkb - 1) ptx::umma_commit_pair(&tfull_bar[acc]);
+        } else {
+          ptx::umma_commit(&empty_bar[stage]);
+          if (kb == nkb - 1) ptx::umma_commit(&tfull_bar[acc]);
+        }
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
@@ -225,11 +263,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = q * 32 + lane;
     constexpr uint32_t kSub = (kEpi == kEpiF32) ? 32 : 64;  // columns per 128-byte sub-chunk
     constexpr uint32_t kSubs = (BN / 2) / kSub;
-    uint8_t* stage_base = smem + SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES * kEpiBufs;
+    uint8_t* stage_base = smem + C::SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES * kEpiBufs;
     uint32_t ebuf = 0;
     uint32_t iter = 0;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
-      const TileCoord tc = tile_coord<kRowK>(args, tile);
+    for (uint32_t tile = unit0; tile < ntiles; tile += unit_step, ++iter) {
+      TileCoord tc = tile_coord<kRowK, C::TM>(args, tile);
+      tc.m0 += rank * BM;  // this CTA's rows of the pair tile
       const uint32_t acc = iter % kAccStages;
       const uint32_t acc_phase = (iter / kAccStages) & 1;
       const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16) + half * (BN / 2);
@@ -259,9 +298,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::tmem_ld_wait();
         if (c == kSubs - 1) {
-          // accumulator drained into registers: hand TMEM back to the MMA warp
+          // accumulator drained into registers: hand TMEM back to the (leader's) MMA warp
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty_bar[acc]);
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kCG == 2)
+              ptx::mbar_arrive_cluster(&tempty_bar[acc], 0);
+            else
+              ptx::mbar_arrive(&tempty_bar[acc]);
+          }
         }
         const uint32_t cols = col0 + c * kSub;
         uint8_t* stage = stage_base + ebuf * EPI_WARP_BYTES;
@@ -340,9 +385,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   __syncwarp();
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (kCG == 2)
+    ptx::cluster_sync();  // the peer's remote arrivals / MMA reads must be done before exit
+  else
+    __syncthreads();
   ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  if (warp == 2) ptx::tmem_dealloc<kTmemCols, kCG>(tmem_base);
 }
 
 // ---------------------------------------------------------------- host side
@@ -375,26 +423,53 @@ int make_map_3d(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK>
-int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
-           int num_sms, cudaStream_t stream) {
-  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK>;
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG>
+int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
+              int num_sms, cudaStream_t stream) {
+  using C = Cfg<kCG>;
+  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK, kCG>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) !=
         cudaSuccess)
       return -3;
     attr_set = true;
   }
-  uint32_t tiles;
-  if (!kRowK)
-    tiles = args.G * args.S * ((args.seg_rows + BM - 1) / BM) * (args.N / BN);
-  else
-    tiles = args.G * (args.Mo / BM) * (args.N / BN);
-  if (tiles == 0) return 0;
-  const uint32_t grid = tiles < static_cast<uint32_t>(num_sms) ? tiles : num_sms;
-  kern<<<grid, kThreads, SMEM_BYTES, stream>>>(a, b, d, args);
+  const uint32_t units = num_tiles<kRowK, C::TM>(args);
+  if (units == 0) return 0;
+  // persistent: one CTA (pair) per SM (pair of SMs)
+  const uint32_t max_units = static_cast<uint32_t>(num_sms) / kCG;
+  const uint32_t grid = (units < max_units ? units : max_units) * kCG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, d, args) != cudaSuccess) return launch_status() ? -2 : -2;
   return launch_status();
+}
+
+// CTA-pair (cta_group::2) kernel by default; MOE_GEMM_CG=1 selects the single-CTA kernel.
+int gemm_cta_group() {
+  static int cg = [] {
+    const char* e = std::getenv("MOE_GEMM_CG");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return cg;
+}
+
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK>
+int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
+           int num_sms, cudaStream_t stream) {
+  if (gemm_cta_group() == 2) return launch_cg<kAMN, kBMN, kEpi, kRowK, 2>(a, b, d, args, num_sms, stream);
+  return launch_cg<kAMN, kBMN, kEpi, kRowK, 1>(a, b, d, args, num_sms, stream);
 }
 
 }  // namespace
@@ -434,7 +509,7 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
       [[fallthrough]];
     case kGemmDgrad: {    // dX = dh . W1^T;             W1 [G][M][V] == B K-major [G][N=M][K=V]
       rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
-      rc |= make_map_3d(&mb, B, false, args.K, args.N, args.G, 64, BN);
+      rc |= make_map_3d(&mb, B, false, args.K, args.N, args.G, 64, BN / gemm_cta_group());
       rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, 32);
       if (rc) return -2;
       return kind == kGemmDgradMask
