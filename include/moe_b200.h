@@ -147,6 +147,11 @@ int moe_get_routing(moe_handle* h, int32_t* idxs, int32_t* locations, double* ga
 int moe_get_metrics(moe_handle* h, moe_step_metrics* out);
 /* Local expert gradients of the last backward, copied to host fp32 (E/W, M, V)+(E/W, V, M). */
 int moe_get_expert_grads(moe_handle* h, float* dw1_host, float* dw2_host);
+/* reduce_scatter_grads_p1 (parallelism.cpp:235-286): after a backward, route slice `rank` of
+ * every expert's weight gradient (dW1 columns / dW2 rows [rank*V/W, (rank+1)*V/W)) to this rank
+ * -- the ZeRO slice layout of moe_set_expert_slices. Device fp32 outputs: w1_slices
+ * [E][M][V/W], w2_slices [E][V/W][M]. Collective across ranks (NCCL); synchronizes `stream`. */
+int moe_get_expert_grad_slices(moe_handle* h, float* w1_slices, float* w2_slices, void* stream);
 /* Device pointer to local expert weights in the layer dtype: which=1 -> w1, 2 -> w2. */
 int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr);
 /* Number of kernels launched by the last forward + backward (benchmark bookkeeping). */

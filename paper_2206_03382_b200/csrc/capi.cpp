@@ -291,6 +291,9 @@ int moe_get_metrics(moe_handle* h, moe_step_metrics* out) { LAYER_CALL(h, h->lay
 int moe_get_expert_grads(moe_handle* h, float* dw1, float* dw2) {
   LAYER_CALL(h, h->layer->get_grads(dw1, dw2));
 }
+int moe_get_expert_grad_slices(moe_handle* h, float* w1_slices, float* w2_slices, void* stream) {
+  LAYER_CALL(h, h->layer->grad_slices(w1_slices, w2_slices, S(stream)));
+}
 int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr) {
   LAYER_CALL(h, {
     if (which == 1) *ptr = h->layer->w1();

@@ -587,7 +587,29 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
   return launch_status();
 }
 
+// resolve_capacity (core.cpp:47-59) from an (all-reduced) demand vector.
+__global__ void resolve_capacity_kernel(const int32_t* __restrict__ demand, int E, int cap_kind,
+                                        int cap_formula, int32_t* __restrict__ cap_out) {
+  __shared__ int32_t mx;
+  if (threadIdx.x == 0) mx = 1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) atomicMax(&mx, demand[e]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int cap = cap_formula;
+    if (cap_kind == 1) cap = mx;
+    if (cap_kind == 2) cap = min(mx, cap_formula);
+    *cap_out = cap;
+  }
+}
+
 }  // namespace
+
+int resolve_capacity_device(const int32_t* demand, int E, int cap_kind, int cap_formula,
+                            int32_t* cap_out, cudaStream_t st) {
+  resolve_capacity_kernel<<<1, 256, 0, st>>>(demand, E, cap_kind, cap_formula, cap_out);
+  return launch_status();
+}
 
 int gate_cta_per_block(int T) { return (T + kGateTok - 1) / kGateTok; }
 

@@ -48,6 +48,9 @@ struct GatingBuffers {
 int gate_cta_per_block(int T);
 // Router GEMM + softmax + top-k + histogram + capacity resolution (device scalar g.cap).
 int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t st);
+// Capacity from a (global, all-reduced) per-expert demand vector.
+int resolve_capacity_device(const int32_t* demand, int E, int cap_kind, int cap_formula,
+                            int32_t* cap_out, cudaStream_t st);
 // Location assignment (FIFO or BPR) + slot tables. cap_bound >= resolved capacity.
 int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound, cudaStream_t st);
 

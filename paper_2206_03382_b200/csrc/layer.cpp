@@ -136,11 +136,13 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   esz_ = cfg.dtype == MOE_DTYPE_BF16 ? 2 : 4;
   if (rank < 0 || rank >= W_) throw MoeError(MOE_EINVAL, "rank out of range");
   if (cfg.gpus_per_node == cfg.world_size) memo_.allowed = {0, 1, 2, 3};  // linear x {1,2,4,8}
-  if (cfg.capacity_kind != MOE_CAP_FIXED)
-    throw MoeError(MOE_EINVAL, "layer: Auto/Bounded capacity is available through moe_op_gating only");
-  cap_ = static_cast<int>(expert_capacity(k_, cfg.capacity_factor, T_, E_));
-  cap_alloc_ = 0;
-  for (int d : {1, 2, 4, 8}) cap_alloc_ = std::max(cap_alloc_, d * ((cap_ + d - 1) / d));
+  // Fixed: the formula; Bounded: its formula at max_factor bounds every step; Auto: start at the
+  // f = 1 capacity and grow (collectively) when a step's max demand exceeds the allocation.
+  if (cfg.capacity_kind == MOE_CAP_AUTO)
+    cap_ = static_cast<int>(expert_capacity(k_, 1.0, T_, E_));
+  else
+    cap_ = static_cast<int>(expert_capacity(k_, cfg.capacity_factor, T_, E_));
+  cap_formula_ = cfg.capacity_kind == MOE_CAP_AUTO ? 0 : cap_;
 
   int ndev = 0;
   ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -188,14 +190,36 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   hist_.alloc(4 * cpb * E_);
   offs_.alloc(4 * cpb * E_);
   demand_.alloc(4 * E_);
+  demand_max_.alloc(4 * E_);
   list_base_.alloc(4 * E_);
   fill_.alloc(4 * E_);
   list_.alloc(4 * Tk);
   capd_.alloc(4);
   drops_.alloc(4);
-  slot_token_.alloc(4 * static_cast<size_t>(E_) * cap_);
-  slot_gate_.alloc(4 * static_cast<size_t>(E_) * cap_);
+  ck(cudaMallocHost(&cap_host_, sizeof(int32_t)), "cudaMallocHost");
+  if (cfg.dtype == MOE_DTYPE_BF16) {
+    colabs_.alloc(sizeof(float) * dE_ * V_);
+    colabs_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
+    w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
+    fix_count_.alloc(sizeof(unsigned int));
+  }
+  if (W_ > 1 && cfg.a2a_backend != MOE_A2A_BACKEND_PEER && cfg.a2a_backend != MOE_A2A_BACKEND_NCCL)
+    throw MoeError(MOE_EINVAL, "unknown all-to-all backend");
+  alloc_capacity(cap_);
+}
 
+// (Re)allocates every capacity-sized buffer for capacity `cap` (and every pipelining degree's
+// padding), and for the peer all-to-all re-exports the receive buffers. Collective when W > 1 and
+// the peer backend is used: every rank reaches it at the same step (the capacity is global).
+void Layer::alloc_capacity(int cap) {
+  int ca = 0;
+  for (int d : {1, 2, 4, 8}) ca = std::max(ca, d * ((cap + d - 1) / d));
+  if (ca <= cap_alloc_) return;
+  ck(cudaDeviceSynchronize(), "sync before realloc");
+  peer_.reset();
+  cap_alloc_ = ca;
+  slot_token_.alloc(4 * static_cast<size_t>(E_) * cap_alloc_);
+  slot_gate_.alloc(4 * static_cast<size_t>(E_) * cap_alloc_);
   const size_t rowsM = static_cast<size_t>(E_) * cap_alloc_ * M_ * esz_;
   const size_t rowsV = static_cast<size_t>(E_) * cap_alloc_ * V_ * esz_;
   z_.alloc(rowsM);
@@ -204,29 +228,26 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   dz_.alloc(rowsM);
   dh_.alloc(rowsV);
   dxe_.alloc(rowsM);
-  if (cfg.dtype == MOE_DTYPE_BF16) {
+  if (cfg_.dtype == MOE_DTYPE_BF16) {
     const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
-    colabs_.alloc(sizeof(float) * dE_ * V_);
-    colabs_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
     relu_mask_.alloc(sizeof(unsigned long long) * rows_all * (V_ / 64 + 1));
-    w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
     rowmax_.alloc(sizeof(float) * rows_all);
     fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));
     fix_list_.alloc(sizeof(unsigned long long) * fix_cap_);
-    fix_count_.alloc(sizeof(unsigned int));
   }
   if (W_ > 1) {
     recv_.alloc(rowsM);
     ycomb_.alloc(rowsM);
     drecv_.alloc(rowsM);
     dxcomb_.alloc(rowsM);
-    if (cfg.a2a_backend == MOE_A2A_BACKEND_PEER) {
+    if (cfg_.a2a_backend == MOE_A2A_BACKEND_PEER) {
       void* bufs[PeerExchange::kChannels] = {recv_.p, ycomb_.p, drecv_.p, dxcomb_.p};
       peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs);
-    } else if (cfg.a2a_backend != MOE_A2A_BACKEND_NCCL) {
-      throw MoeError(MOE_EINVAL, "unknown all-to-all backend");
+      for (auto& e : epoch_) e = 0;  // fresh flag block on every rank
+      bwd_pending_ = false;
     }
   }
+  fwd_done_ = false;
 }
 
 void Layer::prof_mark(int phase, bool begin, cudaStream_t st) {
@@ -269,6 +290,7 @@ void Layer::take_profile(double* ms, int64_t* counts, int n) {
 Layer::~Layer() {
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);
   peer_.reset();
+  if (cap_host_) cudaFreeHost(cap_host_);
   for (const auto& r : prof_recs_) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -430,8 +452,8 @@ GatingArgs Layer::gating_args(const void* x) const {
   g.M = M_;
   g.E = E_;
   g.k = k_;
-  g.cap_kind = MOE_CAP_FIXED;
-  g.cap_formula = cap_;
+  g.cap_kind = cfg_.capacity_kind;
+  g.cap_formula = cfg_.capacity_kind == MOE_CAP_FIXED ? cap_ : cap_formula_;
   g.bpr = cfg_.bpr;
   return g;
 }
@@ -501,12 +523,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   launches_ = 0;
   comm_bytes_ = 0.0;
-  f_ = static_cast<double>(cap_) * E_ / (static_cast<double>(k_) * T_);  // capacity_to_factor
-  strategy_ = cfg_.adaptive ? get_strategy(memo_, f_) : Strategy{0, cfg_.degree};
-  // 2DH degenerates to the linear algorithm inside one NVSwitch domain (collectives.cpp:58-88
-  // with m == W); it is executed as linear and reported as chosen.
-  degree_ = W_ == 1 ? 1 : strategy_.degree;
-  cc_ = (cap_ + degree_ - 1) / degree_;
   ck(cudaEventRecord(ev_fwd_start_, st), "event");
 
   // --- gating: router GEMM + softmax + top-k + capacity + slots (per source block)
@@ -514,7 +530,29 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   GatingBuffers gb = gating_buffers();
   prof_mark(kPhGate, true, st);
   ckr(run_gating_device(ga, gb, st), "gating");
+  if (cfg_.capacity_kind != MOE_CAP_FIXED) {
+    // resolve_capacity over the max demand of all source blocks (run_gating_blocked,
+    // gating.cpp:141-148): one all-reduce(max) of E counts, then the host needs the value to
+    // size this step's buffers.
+    const int32_t* dmax = gb.demand;
+    if (W_ > 1) {
+      ckn(ncclAllReduce(gb.demand, demand_max_.p, E_, ncclInt32, ncclMax, comm_, st), "allreduce(max)");
+      dmax = static_cast<const int32_t*>(demand_max_.p);
+    }
+    ckr(resolve_capacity_device(dmax, E_, cfg_.capacity_kind, cap_formula_, gb.cap, st), "capacity");
+    ck(cudaMemcpyAsync(cap_host_, gb.cap, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
+    ck(cudaStreamSynchronize(st), "sync");
+    cap_ = *cap_host_;
+    alloc_capacity(cap_);  // collective growth when needed
+    gb = gating_buffers();
+  }
   prof_mark(kPhGate, false, st);
+  f_ = static_cast<double>(cap_) * E_ / (static_cast<double>(k_) * T_);  // capacity_to_factor
+  strategy_ = cfg_.adaptive ? get_strategy(memo_, f_) : Strategy{0, cfg_.degree};
+  // 2DH degenerates to the linear algorithm inside one NVSwitch domain (collectives.cpp:58-88
+  // with m == W); it is executed as linear and reported as chosen.
+  degree_ = W_ == 1 ? 1 : strategy_.degree;
+  cc_ = (cap_ + degree_ - 1) / degree_;
   prof_mark(kPhAssign, true, st);
   ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
   prof_mark(kPhAssign, false, st);
@@ -851,8 +889,50 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     ck(cudaEventRecord(ev_freed_[3], st), "event");
   }
   bwd_launches_ = launches_ - l0;
-  if (dw1) last_dw1_ = nullptr; else last_dw1_ = gw1;
-  if (dw2) last_dw2_ = nullptr; else last_dw2_ = gw2;
+  last_dw1_ = gw1;
+  last_dw2_ = gw2;
+}
+
+// reduce_scatter_grads_p1 (parallelism.cpp:235-286), per-rank placement: rank q receives slice
+// q (dW1 columns / dW2 rows [q*h, (q+1)*h), h = V/W) of every expert's gradient from the rank that
+// computed it -- pure routing, no sums. Output (device fp32): w1s [E][M][h], w2s [E][h][M].
+void Layer::grad_slices(float* w1s, float* w2s, cudaStream_t st) {
+  if (!last_dw1_) throw MoeError(MOE_ESTATE, "grad_slices: no backward yet");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  const int h = V_ / W_;
+  const size_t blk1 = static_cast<size_t>(dE_) * M_ * h;  // floats per (dst) block, each of w1/w2
+  DevMem pack;
+  pack.alloc(sizeof(float) * blk1 * 2 * W_);
+  float* p1 = static_cast<float*>(pack.p);
+  float* p2 = p1 + blk1 * W_;
+  for (int q = 0; q < W_; ++q)
+    for (int i = 0; i < dE_; ++i) {
+      // dW1[i][:, q*h:(q+1)*h] -> p1[q][i] (M x h): strided 2-D copy
+      ck(cudaMemcpy2DAsync(p1 + (static_cast<size_t>(q) * dE_ + i) * M_ * h, sizeof(float) * h,
+                           last_dw1_ + static_cast<size_t>(i) * M_ * V_ + static_cast<size_t>(q) * h,
+                           sizeof(float) * V_, sizeof(float) * h, M_, cudaMemcpyDeviceToDevice, st),
+         "pack dW1 slice");
+      // dW2[i][q*h:(q+1)*h, :] -> p2[q][i] (h x M): contiguous rows
+      ck(cudaMemcpyAsync(p2 + (static_cast<size_t>(q) * dE_ + i) * h * M_,
+                         last_dw2_ + static_cast<size_t>(i) * V_ * M_ + static_cast<size_t>(q) * h * M_,
+                         sizeof(float) * h * M_, cudaMemcpyDeviceToDevice, st),
+         "pack dW2 slice");
+    }
+  if (W_ == 1) {
+    ck(cudaMemcpyAsync(w1s, p1, sizeof(float) * blk1, cudaMemcpyDeviceToDevice, st), "copy");
+    ck(cudaMemcpyAsync(w2s, p2, sizeof(float) * blk1, cudaMemcpyDeviceToDevice, st), "copy");
+  } else {
+    // block from rank p holds experts [p*dE, (p+1)*dE): contiguous in the [E][..] outputs
+    ckn(ncclGroupStart(), "group");
+    for (int p = 0; p < W_; ++p) {
+      ckn(ncclSend(p1 + static_cast<size_t>(p) * blk1, blk1, ncclFloat32, p, comm_, st), "send");
+      ckn(ncclRecv(w1s + static_cast<size_t>(p) * blk1, blk1, ncclFloat32, p, comm_, st), "recv");
+      ckn(ncclSend(p2 + static_cast<size_t>(p) * blk1, blk1, ncclFloat32, p, comm_, st), "send");
+      ckn(ncclRecv(w2s + static_cast<size_t>(p) * blk1, blk1, ncclFloat32, p, comm_, st), "recv");
+    }
+    ckn(ncclGroupEnd(), "group");
+  }
+  ck(cudaStreamSynchronize(st), "sync");  // the pack buffer is freed on return
 }
 
 void Layer::ensure_io() {

@@ -67,6 +67,7 @@ class Layer {
   void get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* capacity);
   void get_metrics(moe_step_metrics* m);
   void get_grads(float* dw1, float* dw2);
+  void grad_slices(float* w1s, float* w2s, cudaStream_t st);
   void* w1() { return w1_.p; }
   void* w2() { return w2_.p; }
   int64_t launches() const { return launches_; }
@@ -89,12 +90,14 @@ class Layer {
   void peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch);
   double allreduce_max_host(double v);
   void ensure_io();
+  void alloc_capacity(int cap);
   void prof_mark(int phase, bool begin, cudaStream_t st);
 
   moe_config cfg_;
   int rank_, device_;
   int W_, E_, dE_, M_, V_, T_, k_, esz_;
-  int cap_, cap_alloc_;
+  int cap_, cap_alloc_ = 0, cap_formula_ = 0;
+  int32_t* cap_host_ = nullptr;
   int degree_ = 1, cc_ = 1;
   int num_sms_ = 148;
   double f_ = 1.0;
@@ -116,7 +119,8 @@ class Layer {
   bool bwd_pending_ = false;  // last forward's receive buffer still held for a backward
 
   DevMem wg_, w1_, w2_, dw1_, dw2_;
-  DevMem idxs_, gates_, locs_, hist_, offs_, demand_, list_base_, fill_, list_, capd_, drops_;
+  DevMem idxs_, gates_, locs_, hist_, offs_, demand_, demand_max_, list_base_, fill_, list_, capd_,
+      drops_;
   DevMem slot_token_, slot_gate_;
   DevMem z_, recv_, act_, yexp_, ycomb_, dz_, drecv_, dh_, dxe_, dxcomb_;
   DevMem io_x_, io_y_, io_dy_, io_dx_;

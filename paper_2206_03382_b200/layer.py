@@ -196,6 +196,17 @@ class LayerState:
         return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
                              m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups)
 
+    def grad_slices(self):
+        """reduce_scatter_grads_p1: this rank's slice of every expert's dW1 / dW2 (fp32 device),
+        shapes (E, M, V/W) and (E, V/W, M). Collective across ranks."""
+        cfg = self.config
+        h = cfg.hidden_dim // cfg.world_size
+        w1s = torch.empty(cfg.global_experts, cfg.model_dim, h, dtype=torch.float32, device=self.device)
+        w2s = torch.empty(cfg.global_experts, h, cfg.model_dim, dtype=torch.float32, device=self.device)
+        check(lib().moe_get_expert_grad_slices(self._h, _ptr(w1s), _ptr(w2s), _stream(self.device)),
+              self._h)
+        return w1s, w2s
+
     def kernel_launches(self) -> int:
         return int(lib().moe_kernel_launches(self._h))
 

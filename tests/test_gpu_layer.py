@@ -24,9 +24,10 @@ CASES = [
 ]
 
 
-def run_case(E, k, f, M, V, T, bpr, dt, seed=402, dev=0):
+def run_case(E, k, f, M, V, T, bpr, dt, seed=402, dev=0, cap="fixed"):
     cfg = MoELayerConfig(world_size=1, global_experts=E, model_dim=M, hidden_dim=V,
-                         tokens_per_step=T, top_k=k, capacity_factor=f, bpr=bpr, dtype=dt)
+                         tokens_per_step=T, top_k=k, capacity=cap, capacity_factor=f, bpr=bpr,
+                         dtype=dt)
     inp = layer_inputs(seed, 1, T, M, V, E, dt)
     st = LayerState.init(cfg, seed)
     tdt = cfg.torch_dtype
@@ -35,7 +36,8 @@ def run_case(E, k, f, M, V, T, bpr, dt, seed=402, dev=0):
     res = forward(st, x)
     g = backward(st, res.saved, dy)
     torch.cuda.synchronize()
-    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], 1, k, 0, f, bpr)
+    kind = {"fixed": 0, "auto": 1, "bounded": 2}[cap]
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], 1, k, kind, f, bpr)
     return st, res, g, ref, inp
 
 
@@ -58,6 +60,20 @@ def test_layer_forward_backward(cuda, case):
     assert oracle.max_rel_diff(g.dw2.double().cpu().numpy(), ref["dw2"]) < tol
     m = st.metrics()
     assert m.capacity == cap and m.drop_count == int((loc < 0).sum())
+
+
+@pytest.mark.parametrize("cap,f", [("auto", 1.0), ("bounded", 1.25), ("bounded", 0.5)])
+def test_layer_auto_bounded_capacity(cuda, cap, f):
+    """AutoCapacity / BoundedCapacity inside the layer (resolve_capacity, core.cpp:47-59): the
+    capacity follows the step's max demand (Auto grows the buffers), routing stays bit-exact."""
+    st, res, g, ref, _ = run_case(8, 2, f, 256, 512, 1024, True, "bf16", cap=cap)
+    idxs, loc, gates, capv = st.routing()
+    assert capv == ref["capacity"]
+    assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
+    if cap == "auto":
+        assert (loc >= 0).all()  # Auto never drops
+    for name, got in (("y", res.y), ("dx", g.dx), ("dw1", g.dw1), ("dw2", g.dw2)):
+        assert oracle.max_rel_diff(got.double().cpu().numpy(), ref[name]) < 2e-2, name
 
 
 def test_layer_deterministic(cuda):
@@ -96,6 +112,13 @@ def test_layer_slices_gather_single_rank(cuda):
     w1, w2 = s.weights()
     assert np.array_equal(w1.double().cpu().numpy(), inp["w1"])
     assert np.array_equal(w2.double().cpu().numpy(), inp["w2"])
+
+
+def test_grad_slices_single_rank(cuda):
+    """reduce_scatter_grads_p1 at W = 1: the slice is the whole gradient."""
+    st, res, g, ref, _ = run_case(4, 1, 1.0, 64, 256, 256, False, "f32")
+    w1s, w2s = st.grad_slices()
+    assert torch.equal(w1s, g.dw1) and torch.equal(w2s, g.dw2)
 
 
 def test_backward_without_forward_fails(cuda):

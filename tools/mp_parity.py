@@ -14,11 +14,13 @@ from paper_2206_03382_b200 import LayerState, MoELayerConfig, backward, forward 
 from tests.helpers import layer_inputs  # noqa: E402
 
 
-def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, seed=402):
+def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, cap="fixed",
+        seed=402):
     E = E_per * W
     cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
-                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f, bpr=bpr,
-                         dtype=dt, degree=degree, adaptive=adaptive, a2a_backend=backend)
+                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity=cap,
+                         capacity_factor=f, bpr=bpr, dtype=dt, degree=degree, adaptive=adaptive,
+                         a2a_backend=backend)
     obj = [LayerState.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
@@ -33,7 +35,8 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
             res = forward(st, xs)  # inference-style forward without backward in between
         g = backward(st, res.saved, dys)
     torch.cuda.synchronize()
-    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, 0, f, bpr)
+    kind = {"fixed": 0, "auto": 1, "bounded": 2}[cap]
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, kind, f, bpr)
     sl = slice(rank * T, (rank + 1) * T)
     el = slice(rank * E_per, (rank + 1) * E_per)
     idxs, loc, gates, cap = st.routing()
@@ -46,8 +49,13 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
         dw1=oracle.max_rel_diff(g.dw1.double().cpu().numpy(), ref["dw1"][el]),
         dw2=oracle.max_rel_diff(g.dw2.double().cpu().numpy(), ref["dw2"][el]),
     )
+    # ZeRO gradient slices (reduce_scatter_grads_p1): slice `rank` of every expert
+    h = V // W
+    w1s, w2s = st.grad_slices()
+    errs["dw1_slices"] = oracle.max_rel_diff(w1s.double().cpu().numpy(), ref["dw1"][:, :, rank * h:(rank + 1) * h])
+    errs["dw2_slices"] = oracle.max_rel_diff(w2s.double().cpu().numpy(), ref["dw2"][:, rank * h:(rank + 1) * h, :])
     m = st.metrics()
-    ok = errs["routing"] == 0 and errs["cap"] == 0 and all(errs[n] < tol for n in ("y", "dx", "dw1", "dw2"))
+    ok = errs["routing"] == 0 and errs["cap"] == 0 and all(errs[n] < tol for n in ("y", "dx", "dw1", "dw2", "dw1_slices", "dw2_slices"))
     t = torch.tensor([0.0 if ok else 1.0], device=dev)
     dist.all_reduce(t)
     st.close()
@@ -69,6 +77,8 @@ def main():
         (4, 1, 1.0, 512, 1024, 2048, False, "bf16", 1, True, "peer"),  # Alg. 1 adaptive degree
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "nccl"),
         (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "nccl"),
+        (2, 2, 1.0, 256, 512, 512, True, "bf16", 2, False, "peer", "auto"),
+        (2, 1, 1.25, 128, 256, 400, False, "bf16", 4, False, "nccl", "bounded"),
     ]
     all_ok = True
     for c in cases:
