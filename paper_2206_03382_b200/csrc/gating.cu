@@ -372,6 +372,183 @@ __global__ void __launch_bounds__(kDmWarps * 32)
   for (int e = threadIdx.x; e < E; e += NTH) hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
 }
 
+// Pipelined DMMA gate (E <= 64, 16-byte aligned rows): raw x / Wg tiles stream into a 3-stage
+// shared-memory ring with cp.async (no register staging; two chunks in flight while the DMMAs
+// of the current one run); x is converted bf16/f32 -> fp64 when the A fragment is loaded.
+constexpr int kD2KC = 32, kD2Stages = 3;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const int sz = pred ? 16 : 0;  // src-size 0: zero-fill (token / k / expert tail)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename TX>
+__device__ __forceinline__ double ld_x(const TX* p);
+template <>
+__device__ __forceinline__ double ld_x<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return static_cast<double>(__bfloat162float(*p));
+}
+template <>
+__device__ __forceinline__ double ld_x<float>(const float* p) {
+  return static_cast<double>(*p);
+}
+
+template <typename TX, int NT>
+struct D2Cfg {
+  static constexpr int XROW = kD2KC * sizeof(TX) + 16;       // bytes per staged token row (padded)
+  static constexpr int EP = 8 * NT + 4;                       // Wg row stride (doubles)
+  static constexpr int XBYTES = kDmTok * XROW;
+  static constexpr int WBYTES = kD2KC * EP * 8;
+  static constexpr int STAGE = XBYTES + WBYTES;
+  static constexpr int SMEM = kD2Stages * STAGE + 8 * NT * 4 + 16;
+};
+
+template <typename TX, int NT>
+__global__ void __launch_bounds__(kDmWarps * 32)
+    gate_dmma2_kernel(const TX* __restrict__ x, const double* __restrict__ wg, int T, int M, int E,
+                      int k, int cta_per_block, int32_t* __restrict__ idxs,
+                      double* __restrict__ gates, int32_t* __restrict__ hist,
+                      double* __restrict__ probs_out) {
+  using Cf = D2Cfg<TX, NT>;
+  constexpr int NTH = kDmWarps * 32;
+  constexpr int XCH = kD2KC * sizeof(TX) / 16;  // 16-byte chunks per token row
+  constexpr int WCH = 8 * NT * 8 / 16;          // 16-byte chunks per Wg row (8*NT doubles)
+  extern __shared__ __align__(16) uint8_t sm[];
+  int32_t* sh_hist = reinterpret_cast<int32_t*>(sm + kD2Stages * Cf::STAGE);
+
+  const int b = blockIdx.x / cta_per_block;
+  const int c = blockIdx.x % cta_per_block;
+  const int t_begin = b * T + c * kDmTok;
+  const int ntok = min(b * T + T, t_begin + kDmTok) - t_begin;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int e = threadIdx.x; e < 8 * NT; e += NTH) sh_hist[e] = 0;
+
+  auto issue = [&](int ch) {
+    const int k0 = ch * kD2KC;
+    uint8_t* st = sm + (ch % kD2Stages) * Cf::STAGE;
+    for (int i = threadIdx.x; i < kDmTok * XCH; i += NTH) {
+      const int tt = i / XCH, q = i % XCH;
+      const int kk = q * (16 / static_cast<int>(sizeof(TX)));
+      const bool ok = tt < ntok && k0 + kk < M;
+      const TX* src = ok ? x + static_cast<size_t>(t_begin + tt) * M + k0 + kk : x;
+      cp_async16(st + tt * Cf::XROW + q * 16, src, ok);
+    }
+    double* ws = reinterpret_cast<double*>(st + Cf::XBYTES);
+    for (int i = threadIdx.x; i < kD2KC * WCH; i += NTH) {
+      const int kk = i / WCH, q = i % WCH;
+      const int e = q * 2;
+      const bool ok = k0 + kk < M && e < E;
+      const double* src = ok ? wg + static_cast<size_t>(k0 + kk) * E + e : wg;
+      cp_async16(ws + kk * Cf::EP + e, src, ok);
+    }
+  };
+
+  double acc[kDmMT][NT][2];
+#pragma unroll
+  for (int i = 0; i < kDmMT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nch = (M + kD2KC - 1) / kD2KC;
+  issue(0);
+  cp_async_commit();
+  if (nch > 1) issue(1);
+  cp_async_commit();
+  const int ar = lane >> 2, ac = lane & 3;
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait<1>();  // chunk ch has landed (this thread's copies)
+    __syncthreads();     // ... and everyone's; buffer (ch+2)%3 is free
+    if (ch + 2 < nch) issue(ch + 2);
+    cp_async_commit();
+    const uint8_t* st = sm + (ch % kD2Stages) * Cf::STAGE;
+    const double* ws = reinterpret_cast<const double*>(st + Cf::XBYTES);
+#pragma unroll
+    for (int ks = 0; ks < kD2KC; ks += 4) {
+      double a[kDmMT], bb[NT];
+#pragma unroll
+      for (int i = 0; i < kDmMT; ++i)
+        a[i] = ld_x<TX>(reinterpret_cast<const TX*>(st + ((warp * kDmMT + i) * 8 + ar) * Cf::XROW) + ks + ac);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bb[j] = ws[(ks + ac) * Cf::EP + j * 8 + ar];
+#pragma unroll
+      for (int i = 0; i < kDmMT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+  }
+
+  // softmax + top-k: the 4 lanes of a quad (same lane/4) hold one token's 8*NT logits.
+#pragma unroll
+  for (int i = 0; i < kDmMT; ++i) {
+    const int tt = (warp * kDmMT + i) * 8 + ar;
+    const bool tok_ok = tt < ntok;
+    const int t = t_begin + tt;
+    double mx = -DBL_MAX;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (j * 8 + ac * 2 + h < E) mx = fmax(mx, acc[i][j][h]);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    double p[NT][2];
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        p[j][h] = (j * 8 + ac * 2 + h < E) ? exp(acc[i][j][h] - mx) : 0.0;
+        s += p[j][h];
+      }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        p[j][h] /= s;
+        const int e = j * 8 + ac * 2 + h;
+        if (probs_out && tok_ok && e < E) probs_out[static_cast<size_t>(t) * E + e] = p[j][h];
+      }
+    unsigned taken = 0;
+    for (int r = 0; r < k; ++r) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = j * 8 + ac * 2 + h;
+          if (e < E && !(taken & (1u << (j * 2 + h))) && (p[j][h] > bv || (p[j][h] == bv && e < bi))) {
+            bv = p[j][h];
+            bi = e;
+          }
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (((bi & 7) >> 1) == ac) taken |= 1u << ((bi >> 3) * 2 + (bi & 1));
+      if (ac == 0 && tok_ok) {
+        idxs[static_cast<size_t>(t) * k + r] = bi;
+        gates[static_cast<size_t>(t) * k + r] = bv;
+        atomicAdd(&sh_hist[bi], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += NTH) hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
+}
+
 // Per (block, expert) column: exclusive scan of the CTA histograms -> offs, demand.
 // One CTA per column; each thread scans a contiguous run of CTA counts, then a block scan.
 __global__ void __launch_bounds__(256)
@@ -556,6 +733,31 @@ template <typename TX>
 int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E, int k,
                 int32_t* idxs, double* gates, int32_t* hist, double* probs, cudaStream_t st) {
   const TX* xp = static_cast<const TX*>(x);
+  if (E <= 64 && (M * static_cast<int>(sizeof(TX))) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
+    const int cpb = (T + kDmTok - 1) / kDmTok;
+    const dim3 grid(blocks * cpb);
+    if (E <= 32) {
+      using Cf = D2Cfg<TX, 4>;
+      static bool set = false;
+      if (!set) {
+        cudaFuncSetAttribute(gate_dmma2_kernel<TX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+        set = true;
+      }
+      gate_dmma2_kernel<TX, 4><<<grid, kDmWarps * 32, Cf::SMEM, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+                                                                     gates, hist, probs);
+    } else {
+      using Cf = D2Cfg<TX, 8>;
+      static bool set = false;
+      if (!set) {
+        cudaFuncSetAttribute(gate_dmma2_kernel<TX, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+        set = true;
+      }
+      gate_dmma2_kernel<TX, 8><<<grid, kDmWarps * 32, Cf::SMEM, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+                                                                     gates, hist, probs);
+    }
+    return launch_status();
+  }
   if (E <= 64) {
     const int cpb = (T + kDmTok - 1) / kDmTok;
     const dim3 grid(blocks * cpb);
