@@ -458,6 +458,35 @@ int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const i
 }
 
 namespace {
+// Rows of tokens with no surviving assignment (all k locations < 0) are zeroed: the fused
+// single-rank path scatters expert outputs straight to token rows and never visits them.
+__global__ void zero_dropped_kernel(int T, int k, const int32_t* __restrict__ locations, int row_vecs,
+                                    uint4* __restrict__ out) {
+  // one thread checks one token; the warp then zeroes its dropped tokens' rows together
+  const int lane = threadIdx.x % 32;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool dropped = t < T;
+  for (int j = 0; j < k && dropped; ++j) dropped = __ldg(locations + static_cast<size_t>(t) * k + j) < 0;
+  unsigned m = __ballot_sync(0xffffffffu, dropped);
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    uint4* r = out + static_cast<size_t>(t - lane + src) * row_vecs;
+    for (int v = lane; v < row_vecs; v += 32) r[v] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+}  // namespace
+
+int zero_dropped_device(int T, int k, const int32_t* locations, size_t row_bytes, void* out,
+                        cudaStream_t st) {
+  if (row_bytes % 16 != 0) return -1;
+  zero_dropped_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, k, locations,
+                                                        static_cast<int>(row_bytes / 16),
+                                                        static_cast<uint4*>(out));
+  return launch_status();
+}
+
+namespace {
 __global__ void build_slots_kernel(int n, int T, int k, int E, int cap,
                                    const int32_t* __restrict__ idxs,
                                    const int32_t* __restrict__ locations,

@@ -33,6 +33,21 @@
 #ifndef MOE_GEMM_EPI_BUFS
 #define MOE_GEMM_EPI_BUFS 1
 #endif
+#ifndef MOE_EPI_DIRECT
+#define MOE_EPI_DIRECT 0  // 1: bf16 epilogues store rows straight from registers (no smem staging)
+#endif
+
+// MOE_GEMM_TRACE (debug builds only): per-role barrier wait cycles, printed by CTAs 0 and 1.
+#ifdef MOE_GEMM_TRACE
+#define TRACE_WAIT(acc, call)          \
+  do {                                 \
+    const long long t0_ = clock64();   \
+    call;                              \
+    acc += clock64() - t0_;            \
+  } while (0)
+#else
+#define TRACE_WAIT(acc, call) call
+#endif
 
 namespace moe {
 
@@ -42,7 +57,6 @@ constexpr uint32_t BM = 128;  // accumulator rows per CTA (TMEM lanes)
 constexpr uint32_t BN = 256;  // UMMA N
 constexpr uint32_t BK = 64;   // one 128-byte swizzle atom of bf16 along K
 constexpr uint32_t UK = 16;   // K per tcgen05.mma (bf16)
-constexpr uint32_t kEpiBufs = MOE_GEMM_EPI_BUFS;  // staging buffers per epilogue warp
 constexpr uint32_t kAccStages = 2;
 constexpr uint32_t kTmemCols = kAccStages * BN;  // 512
 constexpr uint32_t kThreads = 384;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-11 epilogue
@@ -53,9 +67,13 @@ constexpr uint32_t EPI_WARP_BYTES = 32 * 128;    // 32 rows x 128 B staging per 
 // kCG = 1: one CTA computes a 128 x 256 tile. kCG = 2: a CTA pair (cluster of 2, cta_group::2)
 // computes 256 x 256: each CTA holds its 128 A rows and half (128 columns) of B, so B smem per
 // CTA halves and the pipeline gets deeper (6 stages instead of 4).
-template <int kCG>
+// kPeer: the fused-combine kernels store over NVLink, where a bulk store holds its staging
+// buffer longer -- two staging buffers per epilogue warp, one pipeline stage fewer.
+template <int kCG, bool kPeer = false>
 struct Cfg {
-  static constexpr uint32_t kStages = kCG == 1 ? MOE_GEMM_STAGES : MOE_GEMM_STAGES_PAIR;
+  static constexpr uint32_t kEpiBufs = kPeer ? 2 : MOE_GEMM_EPI_BUFS;  // staging buffers per warp
+  static constexpr uint32_t kStages =
+      (kCG == 1 ? MOE_GEMM_STAGES : MOE_GEMM_STAGES_PAIR) - (kPeer && MOE_GEMM_EPI_BUFS == 1 ? 1 : 0);
   static constexpr uint32_t TM = BM * kCG;   // tile rows per work unit
   static constexpr uint32_t BNL = BN / kCG;  // B columns loaded per CTA
   static constexpr uint32_t A_BYTES = BM * BK * 2;
@@ -65,6 +83,10 @@ struct Cfg {
   static constexpr uint32_t SMEM_EPI_OFF = SMEM_B_OFF + kStages * B_BYTES;
   static constexpr uint32_t SMEM_BAR_OFF = SMEM_EPI_OFF + kEpiWarps * EPI_WARP_BYTES * kEpiBufs;
   static constexpr uint32_t SMEM_BYTES = SMEM_BAR_OFF + 256 + 1024;  // + barriers + alignment
+};
+
+struct PeerMaps {
+  CUtensorMap m[kMaxPeers];
 };
 
 struct TileCoord {
@@ -108,12 +130,14 @@ __device__ __forceinline__ uint32_t num_kblocks(const GemmArgs& a) {
     return a.S * ((a.seg_rows + BK - 1) / BK);
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG>
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG, uint32_t kIdx>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmD, const GemmArgs args) {
-  using C = Cfg<kCG>;
+                     const __grid_constant__ CUtensorMap tmD, const GemmArgs args,
+                     const __grid_constant__ PeerMaps pm) {
+  using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0>;
   constexpr uint32_t kStages = C::kStages;
+  constexpr uint32_t kEpiBufs = C::kEpiBufs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -155,6 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t ntiles = num_tiles<kRowK, C::TM>(args);
   const uint32_t nkb = num_kblocks<kRowK>(args);
   const uint32_t unit0 = blockIdx.x / kCG, unit_step = gridDim.x / kCG;
+  long long w_prod = 0, w_full = 0, w_tempty = 0, w_tfull = 0;
+#ifdef MOE_GEMM_TRACE
+  const long long t_start = clock64();
+#endif
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -171,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t m0 = tc.m0 + rank * BM;       // this CTA's A rows
       const uint32_t nb = tc.n0 + rank * C::BNL;   // this CTA's B columns
       for (uint32_t kb = 0; kb < nkb; ++kb) {
-        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        TRACE_WAIT(w_prod, ptx::mbar_wait(&empty_bar[stage], phase ^ 1));
         uint8_t* sa = smem + C::SMEM_A_OFF + stage * C::A_BYTES;
         uint8_t* sb = smem + C::SMEM_B_OFF + stage * C::B_BYTES;
         if constexpr (!kRowK) {
@@ -220,11 +248,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t tile = unit0; tile < ntiles; tile += unit_step, ++iter) {
       const uint32_t acc = iter % kAccStages;
       const uint32_t acc_phase = (iter / kAccStages) & 1;
-      ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      TRACE_WAIT(w_tempty, ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1));
       ptx::tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
       for (uint32_t kb = 0; kb < nkb; ++kb) {
-        ptx::mbar_wait(&full_bar[stage], phase);
+        TRACE_WAIT(w_full, ptx::mbar_wait(&full_bar[stage], phase));
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + C::SMEM_A_OFF + stage * C::A_BYTES);
         const uint32_t sb = ptx::smem_u32(smem + C::SMEM_B_OFF + stage * C::B_BYTES);
@@ -263,6 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = q * 32 + lane;
     constexpr uint32_t kSub = (kEpi == kEpiF32) ? 32 : 64;  // columns per 128-byte sub-chunk
     constexpr uint32_t kSubs = (BN / 2) / kSub;
+    constexpr uint32_t kStoreLanes = (kIdx & kIdxScatterD) ? 8 : 1;  // lanes issuing bulk stores
+    constexpr bool kDirect = MOE_EPI_DIRECT != 0 && kEpi != kEpiF32;
     uint8_t* stage_base = smem + C::SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES * kEpiBufs;
     uint32_t ebuf = 0;
     uint32_t iter = 0;
@@ -278,6 +308,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t col0 = tc.n0 + half * (BN / 2);
       const size_t orow = static_cast<size_t>(seg) * args.seg_rows + row_in;  // row-M kinds
       const size_t mrow = orow * (args.N / 64);
+      // token-indexed epilogue: the row's token (scatter) and gate scale
+      int tok = -1;
+      float scale = 1.0f;
+      if constexpr ((kIdx & kIdxScatterD) != 0)
+        tok = row_ok ? __ldg(args.row_token + orow) : -1;
+      if constexpr ((kIdx & kIdxScaleRow) != 0)
+        scale = row_ok ? __ldg(args.row_scale + orow) : 0.0f;
+      int st_tok[4];
+      if constexpr ((kIdx & kIdxScatterD) != 0) {
+        // lane j < 8 stores rows 4j .. 4j + 3 of this warp's 32 with one scatter4
+        const int t = tok < 0 ? static_cast<int>(args.gather_rows) : tok;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st_tok[i] = __shfl_sync(0xffffffffu, t, 4 * (lane & 7) + i);
+      }
+      // ReLU certificate inputs of this tile (row bound, 64-column block bounds), loaded before the
+      // accumulator wait like the mask words
+      float rmax = 0.0f, tblk[kSubs];
+      const bool cert = kEpi == kEpiReluBf16 && args.fix_list != nullptr && row_ok;
+      if constexpr (kEpi == kEpiReluBf16) {
+        if (cert) {
+          rmax = __ldg(args.rowmax + orow) * kReluTauScale;
+#pragma unroll
+          for (uint32_t c = 0; c < kSubs; ++c)
+            tblk[c] = rmax * __ldg(args.colabs_blk + static_cast<size_t>(tc.g) * (args.N / 64) + col0 / 64 + c);
+        }
+      }
       unsigned long long mw[kSubs];
       if constexpr (kEpi == kEpiMaskBf16) {
         // issued before the accumulator wait so their latency hides under the MMAs
@@ -285,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t c = 0; c < kSubs; ++c)
           mw[c] = row_ok ? __ldg(args.relu_mask + mrow + col0 / 64 + c) : 0ull;
       }
-      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      TRACE_WAIT(w_tfull, ptx::mbar_wait(&tfull_bar[acc], acc_phase));
       ptx::tc_fence_after();
 #pragma unroll 1
       for (uint32_t c = 0; c < kSubs; ++c) {
@@ -312,9 +368,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* stage = stage_base + ebuf * EPI_WARP_BYTES;
         const uint32_t stage_row = ptx::smem_u32(stage) + lane * 128;
         ebuf = (ebuf + 1) % kEpiBufs;
-        // the TMA store that last used this staging buffer must have finished reading it
-        if (lane == 0) ptx::tma_store_wait_read<kEpiBufs - 1>();
-        __syncwarp();
+        if constexpr (!kDirect) {
+          // the TMA store that last used this staging buffer must have finished reading it
+          if (lane < kStoreLanes) ptx::tma_store_wait_read<kEpiBufs - 1>();
+          __syncwarp();
+        }
         if constexpr (kEpi == kEpiF32) {
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
@@ -325,12 +383,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (uint32_t i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
           if constexpr (kEpi == kEpiReluBf16) {
-            if (args.fix_list != nullptr && row_ok) {
+            if (cert) {
               // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64
               // re-decision. Prefilter against the 64-column block bound; per element on a hit.
-              const float rmax = args.rowmax[orow] * kReluTauScale;
-              const float tmax =
-                  rmax * __ldg(args.colabs_blk + static_cast<size_t>(tc.g) * (args.N / 64) + cols / 64);
+              float tmax = 0.0f;
+#pragma unroll
+              for (uint32_t c2 = 0; c2 < kSubs; ++c2)
+                if (c2 == c) tmax = tblk[c2];
               float mn = fabsf(f[0]);
 #pragma unroll
               for (uint32_t i = 1; i < 64; ++i) mn = fminf(mn, fabsf(f[i]));
@@ -352,6 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (args.relu_mask != nullptr && row_ok) args.relu_mask[mrow + cols / 64] = bits;
           }
+          if constexpr ((kIdx & kIdxScaleRow) != 0) {
+            // fused decode: y[token] = g * (act . W2)[slot]
+#pragma unroll
+            for (uint32_t i = 0; i < 64; ++i) f[i] *= scale;
+          }
           if constexpr (kEpi == kEpiMaskBf16) {
             // dh = (dY . W2^T) * [h > 0]; the up-GEMM's ReLU bitmask carries [h > 0]
             unsigned long long w = 0ull;
@@ -361,6 +425,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (uint32_t i = 0; i < 64; ++i)
               if (!((w >> i) & 1ull)) f[i] = 0.0f;
+          }
+          if constexpr (kDirect) {
+            // one 128-byte row segment per thread, straight to global memory
+            const long long drow = (kIdx & kIdxScatterD) ? static_cast<long long>(tok)
+                                                         : (row_ok ? static_cast<long long>(orow) : -1);
+            if (row_ok && drow >= 0) {
+              uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.d_ptr) +
+                                                    static_cast<size_t>(drow) * args.N + cols);
+#pragma unroll
+              for (uint32_t j = 0; j < 8; ++j)
+                dst[j] = make_uint4(ptx::pack_bf16x2(f[8 * j], f[8 * j + 1]),
+                                    ptx::pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                                    ptx::pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
+                                    ptx::pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+            }
+            continue;
           }
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
@@ -372,7 +452,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if constexpr ((kIdx & kIdxScatterD) != 0) {
+          if (lane < 8) {
+            // rows to token positions; empty slots / rows past the segment end are out of bounds
+            ptx::tma_scatter4(&tmD, stage + lane * 512, static_cast<int>(cols), st_tok[0],
+                              st_tok[1], st_tok[2], st_tok[3]);
+            ptx::tma_store_commit();
+          }
+        } else if constexpr ((kIdx & kIdxPeerD) != 0) {
+          if (lane == 0) {
+            // fused combine: this tile's rows go straight to the source rank's combine buffer
+            const uint32_t sidx = args.seg_base + tc.s;  // chunk * W + src
+            const uint32_t src = sidx % args.peer_world;
+            const uint32_t oseg = (sidx / args.peer_world) * args.peer_world * args.G +
+                                  args.peer_rank * args.G + tc.g;
+            ptx::tma_store_3d(&pm.m[src], stage, static_cast<int>(cols),
+                              static_cast<int>(tc.m0 + q * 32), static_cast<int>(oseg));
+            ptx::tma_store_commit();
+          }
+        } else if (lane == 0) {
           // rows past the segment end are clipped by the tensor map bounds
           ptx::tma_store_3d(&tmD, stage, static_cast<int>(cols), static_cast<int>(tc.m0 + q * 32),
                             static_cast<int>(seg));
@@ -380,9 +478,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (lane == 0) ptx::tma_store_wait_all<0>();
+    if (lane < kStoreLanes) {
+      ptx::tma_store_wait_all<0>();
+      // peer stores: performed system-wide before the stream publishes the ready flags
+      if constexpr ((kIdx & kIdxPeerD) != 0) __threadfence_system();
+    }
   }
 
+#ifdef MOE_GEMM_TRACE
+  if (blockIdx.x < 2 && lane == 0 && (warp <= 1 || warp == 4 || warp == 11))
+    printf("trace cta %d warp %d: total %lld prod_empty %lld mma_full %lld mma_tempty %lld epi_tfull %lld\n",
+           blockIdx.x, warp, clock64() - t_start, w_prod, w_full, w_tempty, w_tfull);
+#endif
+  (void)w_prod; (void)w_full; (void)w_tempty; (void)w_tfull;
   __syncwarp();
   ptx::tc_fence_before();
   if constexpr (kCG == 2)
@@ -423,11 +531,25 @@ int make_map_3d(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG>
+// 2-D [rows][cols] bf16 map with a one-row box: the row-scatter (tile::scatter4) target.
+int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG, uint32_t kIdx>
 int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
-              int num_sms, cudaStream_t stream) {
-  using C = Cfg<kCG>;
-  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK, kCG>;
+              const PeerMaps& pm, int num_sms, cudaStream_t stream) {
+  using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0>;
+  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK, kCG, kIdx>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) !=
@@ -452,7 +574,7 @@ int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, a, b, d, args) != cudaSuccess) return launch_status() ? -2 : -2;
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, d, args, pm) != cudaSuccess) return launch_status() ? -2 : -2;
   return launch_status();
 }
 
@@ -465,11 +587,14 @@ int gemm_cta_group() {
   return cg;
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK>
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, uint32_t kIdx = 0>
 int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
-           int num_sms, cudaStream_t stream) {
-  if (gemm_cta_group() == 2) return launch_cg<kAMN, kBMN, kEpi, kRowK, 2>(a, b, d, args, num_sms, stream);
-  return launch_cg<kAMN, kBMN, kEpi, kRowK, 1>(a, b, d, args, num_sms, stream);
+           int num_sms, cudaStream_t stream, const PeerMaps* pm = nullptr) {
+  static const PeerMaps none{};
+  const PeerMaps& p = pm ? *pm : none;
+  if (gemm_cta_group() == 2)
+    return launch_cg<kAMN, kBMN, kEpi, kRowK, 2, kIdx>(a, b, d, args, p, num_sms, stream);
+  return launch_cg<kAMN, kBMN, kEpi, kRowK, 1, kIdx>(a, b, d, args, p, num_sms, stream);
 }
 
 }  // namespace
@@ -494,15 +619,41 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
   CUtensorMap ma, mb, md;
   const uint64_t nseg = static_cast<uint64_t>(nseg_total);
   int rc = 0;
+  const uint32_t im = args.idx_mode;
+  if ((im & kIdxScatterD) && (args.row_token == nullptr || args.gather_rows == 0)) return -1;
+  if ((im & kIdxScaleRow) && args.row_scale == nullptr) return -1;
+  PeerMaps pm{};
+  if (im & kIdxPeerD) {
+    if (kind != kGemmDown && kind != kGemmDgrad) return -1;
+    if (args.peer_world < 2 || args.peer_world > kMaxPeers || args.peer_rank >= args.peer_world ||
+        args.S != args.peer_world || args.peer_out_segs == 0)
+      return -1;
+    for (uint32_t p = 0; p < args.peer_world; ++p) {
+      if (args.peer_d[p] == nullptr) return -1;
+      if (make_map_3d(&pm.m[p], args.peer_d[p], false, args.N, args.seg_rows, args.peer_out_segs, 64, 32))
+        return -2;
+    }
+  }
+  auto map_d = [&](CUtensorMap* m) {
+    return (im & kIdxScatterD) ? make_map_rows(m, D, args.N, args.gather_rows)
+                               : make_map_3d(m, D, false, args.N, args.seg_rows, nseg, 64, 32);
+  };
   switch (kind) {
     case kGemmUp:      // act = relu(X . W1)      A K-major, W1 [G][K=M][N=V] N-major
     case kGemmDown: {  // Y   = act . W2          A K-major, W2 [G][K=V][N=M] N-major
       rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
       rc |= make_map_3d(&mb, B, false, args.N, args.K, args.G, 64, 64);
-      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, 32);
+      rc |= map_d(&md);
       if (rc) return -2;
-      return kind == kGemmUp ? launch<false, true, kEpiReluBf16, false>(ma, mb, md, args, num_sms, stream)
-                             : launch<false, true, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
+      if (kind == kGemmUp)
+        return im == 0 ? launch<false, true, kEpiReluBf16, false>(ma, mb, md, args, num_sms, stream) : -1;
+      if (im == 0) return launch<false, true, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
+      if (im == (kIdxScatterD | kIdxScaleRow))  // fused decode
+        return launch<false, true, kEpiBf16, false, kIdxScatterD | kIdxScaleRow>(ma, mb, md, args,
+                                                                                 num_sms, stream);
+      if (im == kIdxPeerD)  // fused combine
+        return launch<false, true, kEpiBf16, false, kIdxPeerD>(ma, mb, md, args, num_sms, stream, &pm);
+      return -1;
     }
     case kGemmDgradMask:  // dh = (dY . W2^T) * [a > 0]; W2 [G][V][M] == B K-major [G][N=V][K=M]
       if (args.relu_mask == nullptr) return -1;
@@ -510,13 +661,19 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
     case kGemmDgrad: {    // dX = dh . W1^T;             W1 [G][M][V] == B K-major [G][N=M][K=V]
       rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
       rc |= make_map_3d(&mb, B, false, args.K, args.N, args.G, 64, BN / gemm_cta_group());
-      rc |= make_map_3d(&md, D, false, args.N, args.seg_rows, nseg, 64, 32);
+      rc |= map_d(&md);
       if (rc) return -2;
-      return kind == kGemmDgradMask
-                 ? launch<false, false, kEpiMaskBf16, false>(ma, mb, md, args, num_sms, stream)
-                 : launch<false, false, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
+      if (kind == kGemmDgradMask)
+        return im == 0 ? launch<false, false, kEpiMaskBf16, false>(ma, mb, md, args, num_sms, stream) : -1;
+      if (im == 0) return launch<false, false, kEpiBf16, false>(ma, mb, md, args, num_sms, stream);
+      if (im == kIdxScatterD)  // fused encode-backward
+        return launch<false, false, kEpiBf16, false, kIdxScatterD>(ma, mb, md, args, num_sms, stream);
+      if (im == kIdxPeerD)  // fused backward combine
+        return launch<false, false, kEpiBf16, false, kIdxPeerD>(ma, mb, md, args, num_sms, stream, &pm);
+      return -1;
     }
     case kGemmWgrad: {  // dW[g] = A[g]^T . B[g] over all (segment, row); fp32 out [G][Mo][N]
+      if (im != 0) return -1;
       rc |= make_map_3d(&ma, A, false, args.Mo, args.seg_rows, nseg, 64, 64);
       rc |= make_map_3d(&mb, B, false, args.N, args.seg_rows, nseg, 64, 64);
       rc |= make_map_3d(&md, D, true, args.N, args.Mo, args.G, 32, 32);

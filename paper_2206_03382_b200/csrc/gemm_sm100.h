@@ -17,6 +17,18 @@ enum GemmKind : int {
 
 enum EpiKind : int { kEpiBf16 = 0, kEpiReluBf16 = 1, kEpiMaskBf16 = 2, kEpiF32 = 3 };
 
+// Token-indexed output (single-rank fused decode / encode-backward; GemmArgs::idx_mode bits). A
+// slot row (segment s, row r) maps to token row_token[s * seg_rows + r] (< 0: empty slot).
+enum IdxMode : uint32_t {
+  kIdxScatterD = 4,  // row-M: D rows are written to token rows of D:[gather_rows][N]
+  kIdxScaleRow = 8,  // row-M: output row scaled by row_scale[slot] (the slot's gate)
+  // row-M, expert-parallel combine fused into the epilogue: segment (chunk, src, g) of the
+  // receive layout is stored straight into rank src's combine buffer (peer memory over NVLink),
+  // at its [chunk][E][cap chunk][N] position (collectives.cpp:116-162 combine, reversed plan).
+  kIdxPeerD = 16,
+};
+constexpr int kMaxPeers = 8;
+
 struct GemmArgs {
   uint32_t G;         // groups (local experts)
   uint32_t S;         // capacity segments per group (pipeline chunks x source ranks)
@@ -38,6 +50,14 @@ struct GemmArgs {
   unsigned long long* fix_list;   // packed (seg << 44) | (row << 24) | col
   unsigned int* fix_count;
   unsigned int fix_cap;
+  // token-indexed output (IdxMode)
+  uint32_t idx_mode;
+  uint32_t gather_rows;       // token rows of the scattered tensor
+  const int32_t* row_token;   // [nseg * seg_rows]
+  const float* row_scale;     // [nseg * seg_rows]
+  // kIdxPeerD: destination combine buffer of every rank (this rank's own for src == rank)
+  uint32_t peer_world, peer_rank, peer_out_segs;  // out_segs = chunks * E
+  void* peer_d[kMaxPeers];
 };
 
 // Pack / unpack of one ReLU-fixup entry.

@@ -74,6 +74,8 @@ int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
 int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
                                  const int32_t* idxs, const int32_t* locations, double* dgates,
                                  cudaStream_t st);
+int zero_dropped_device(int T, int k, const int32_t* locations, size_t row_bytes, void* out,
+                        cudaStream_t st);
 int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
                            const int32_t* locations, void* dx, cudaStream_t st);
 
@@ -93,7 +95,12 @@ int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, floa
                         void* w1t, cudaStream_t st);
 int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned long long* mask,
                               cudaStream_t st);
-int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st);
+struct FlagWait;
+// wait: optional fused receive wait (peer flags, see peer_flags.cuh); reset: optional counter
+// zeroed by the kernel (the ReLU fixup count)
+int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st,
+                  const FlagWait* wait = nullptr, unsigned int* reset = nullptr);
+int wait_flags_device(const FlagWait& w, cudaStream_t st);
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
                       void* act, unsigned long long* relu_mask, cudaStream_t st);

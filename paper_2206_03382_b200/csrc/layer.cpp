@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -20,6 +22,7 @@
 
 #include "gemm_sm100.h"
 #include "kernels.h"
+#include "peer_flags.h"
 
 namespace moe {
 
@@ -152,6 +155,15 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   if (prop.major != 10) throw MoeError(MOE_ECUDA, "sm_100 (B200) device required");
   num_sms_ = prop.multiProcessorCount;
+  {
+    const char* t = std::getenv("MOE_TIMELINE");
+    tl_on_ = t && t[0] == '1';
+  }
+  {
+    const char* e = std::getenv("MOE_FUSED");  // MOE_FUSED=0: unfused single-rank path (A/B runs)
+    fused_ = !(e && e[0] == '0') && W_ == 1 && k_ == 1 && cfg.dtype == MOE_DTYPE_BF16 &&
+             M_ % 256 == 0 && V_ % 256 == 0;
+  }
 
   ck(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "stream");
   ck(cudaEventCreateWithFlags(&ev_fwd_start_, cudaEventDefault), "event");
@@ -222,12 +234,14 @@ void Layer::alloc_capacity(int cap) {
   slot_gate_.alloc(4 * static_cast<size_t>(E_) * cap_alloc_);
   const size_t rowsM = static_cast<size_t>(E_) * cap_alloc_ * M_ * esz_;
   const size_t rowsV = static_cast<size_t>(E_) * cap_alloc_ * V_ * esz_;
-  z_.alloc(rowsM);
   act_.alloc(rowsV);
-  yexp_.alloc(rowsM);
-  dz_.alloc(rowsM);
   dh_.alloc(rowsV);
-  dxe_.alloc(rowsM);
+  z_.alloc(rowsM);
+  dz_.alloc(rowsM);
+  if (!fused_) {  // the fused path never materialises expert-output rows
+    yexp_.alloc(rowsM);
+    dxe_.alloc(rowsM);
+  }
   if (cfg_.dtype == MOE_DTYPE_BF16) {
     const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
     relu_mask_.alloc(sizeof(unsigned long long) * rows_all * (V_ / 64 + 1));
@@ -243,6 +257,9 @@ void Layer::alloc_capacity(int cap) {
     if (cfg_.a2a_backend == MOE_A2A_BACKEND_PEER) {
       void* bufs[PeerExchange::kChannels] = {recv_.p, ycomb_.p, drecv_.p, dxcomb_.p};
       peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs);
+      const char* e = std::getenv("MOE_FUSED_COMBINE");  // =0: copy-engine combine (A/B runs)
+      fused_combine_ = !(e && e[0] == '0') && cfg_.dtype == MOE_DTYPE_BF16 && W_ <= kMaxPeers &&
+                       M_ % 256 == 0 && V_ % 64 == 0;
       for (auto& e : epoch_) e = 0;  // fresh flag block on every rank
       bwd_pending_ = false;
     }
@@ -250,7 +267,35 @@ void Layer::alloc_capacity(int cap) {
   fwd_done_ = false;
 }
 
+void Layer::tl_mark(const std::string& name, cudaStream_t st) {
+  if (!tl_on_) return;
+  cudaEvent_t e;
+  ck(cudaEventCreateWithFlags(&e, cudaEventDefault), "event");
+  ck(cudaEventRecord(e, st), "event");
+  tl_.emplace_back(name, e);
+}
+
+void Layer::tl_flush() {
+  if (!tl_on_ || tl_.empty()) return;
+  ck(cudaDeviceSynchronize(), "sync");
+  for (auto& [n, e] : tl_) {
+    float t = 0.0f;
+    ck(cudaEventElapsedTime(&t, tl_.front().second, e), "elapsed");
+    std::fprintf(stderr, "[timeline r%d] %9.3f ms  %s\n", rank_, t, n.c_str());
+  }
+  for (auto& pe : tl_) cudaEventDestroy(pe.second);
+  tl_.clear();
+}
+
 void Layer::prof_mark(int phase, bool begin, cudaStream_t st) {
+  if (tl_on_) {
+    static const char* names[] = {"gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd",
+                                  "gemm_dgrad_mask", "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2",
+                                  "encode_bwd", "a2a_fwd", "a2a_bwd", "assign", "relu_fixup"};
+    tl_mark(std::string(phase < 15 ? names[phase] : "?") + (begin ? " >" : " <") +
+                (st == comm_stream_ ? " [comm]" : ""),
+            st);
+  }
   if (!prof_) return;
   cudaEvent_t e;
   if (!ev_pool_.empty()) {
@@ -510,12 +555,24 @@ void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
 
 // Copy-engine version of exchange(): push chunk `chunk` of `src` into every peer's channel
 // buffer (same plan), then publish the chunk's ready flag.
-void Layer::peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch) {
+// Fused-combine GEMM arguments: segment (chunk, src, g) goes to rank src's channel-ch buffer.
+GemmArgs Layer::peer_args(const GemmArgs& a, int ch) const {
+  GemmArgs d = a;
+  d.idx_mode = kIdxPeerD;
+  d.peer_world = static_cast<uint32_t>(W_);
+  d.peer_rank = static_cast<uint32_t>(rank_);
+  d.peer_out_segs = static_cast<uint32_t>(degree_ * E_);
+  for (int p = 0; p < W_; ++p) d.peer_d[p] = peer_->buffer(ch, p);
+  return d;
+}
+
+void Layer::peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch,
+                      cudaEvent_t local_done) {
   std::vector<int64_t> so(W_), ro(W_);
   int64_t elems = 0;
   a2a_plan(W_, E_, cc_, M_, chunk, phase, so.data(), ro.data(), &elems);
   peer_->push_chunk(comm_stream_, ch, chunk, src, so.data(), ro.data(),
-                    static_cast<size_t>(elems) * esz_, esz_, epoch);
+                    static_cast<size_t>(elems) * esz_, esz_, epoch, local_done);
   comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
 }
 
@@ -524,6 +581,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   launches_ = 0;
   comm_bytes_ = 0.0;
   ck(cudaEventRecord(ev_fwd_start_, st), "event");
+  tl_mark("forward start", st);
 
   // --- gating: router GEMM + softmax + top-k + capacity + slots (per source block)
   GatingArgs ga = gating_args(x);
@@ -598,7 +656,28 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
 
   void* recv = W_ > 1 ? recv_.p : z_.p;
   void* ycomb = W_ > 1 ? ycomb_.p : yexp_.p;
-  if (W_ == 1) {
+  if (fused_) {
+    // decode fused into the down GEMM: y[token] = g * (act . W2)[slot], rows scattered by TMA;
+    // tokens without a slot get zero rows (the decode's dropped-token case).
+    up.seg_base = 0;
+    down.seg_base = 0;
+    down.idx_mode = kIdxScatterD | kIdxScaleRow;
+    down.gather_rows = static_cast<uint32_t>(T_);
+    down.row_token = gb.slot_token;
+    down.row_scale = gb.slot_gate;
+    ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
+    prof_mark(kPhUp, true, st);
+    gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+    prof_mark(kPhUp, false, st);
+    fixup(recv);
+    prof_mark(kPhDecode, true, st);
+    ckr(zero_dropped_device(T_, k_, gb.locations, static_cast<size_t>(M_) * esz_, y, st), "zero rows");
+    prof_mark(kPhDecode, false, st);
+    ++launches_;
+    prof_mark(kPhDown, true, st);
+    gemm(kGemmDown, act_.p, w2_.p, y, down, nseg, st);
+    prof_mark(kPhDown, false, st);
+  } else if (W_ == 1) {
     up.seg_base = 0;
     down.seg_base = 0;
     if (cert) ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
@@ -626,44 +705,64 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     peer_->wait_peers_freed(comm_stream_, 0, e0);
     prof_mark(kPhA2aFwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {
-      peer_push(0, z_.p, i, 0, e0);
-      ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+      peer_push(0, z_.p, i, 0, e0, ev_a_[i]);  // ev_a_[i]: my own block of chunk i copied
+      tl_mark("dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
     for (int i = 0; i < degree_; ++i) {
       ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
-      peer_->wait_chunk(st, 0, i, e0);
+      // the peers' blocks: polled on the device by the first kernel of the chunk
+      const FlagWait fw = peer_->ready_wait(0, i, e0);
       up.seg_base = i * W_;
       down.seg_base = i * W_;
       if (cert) {
         const size_t r0 = static_cast<size_t>(i) * W_ * dE_ * cc_;
         ckr(rowmax_device(static_cast<char*>(recv) + r0 * M_ * esz_,
                           static_cast<int64_t>(W_) * dE_ * cc_, M_,
-                          static_cast<float*>(rowmax_.p) + r0, st),
+                          static_cast<float*>(rowmax_.p) + r0, st, &fw,
+                          static_cast<unsigned int*>(fix_count_.p)),
             "rowmax");
-        ++launches_;
-        ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
+      } else {
+        ckr(wait_flags_device(fw, st), "wait");
       }
+      ++launches_;
+      tl_mark("dispatch landed " + std::to_string(i), st);
       prof_mark(kPhUp, true, st);
       gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
       prof_mark(kPhUp, false, st);
       fixup(recv);
       prof_mark(kPhDown, true, st);
-      gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+      if (fused_combine_) {
+        // combine fused into the down GEMM: tiles are stored into the source ranks' ycomb over
+        // NVLink as they complete; the chunk's ready flags follow the kernel
+        if (i == 0) {
+          ckr(wait_flags_device(peer_->freed_wait(1, e1 - 1), st), "wait");
+          ++launches_;
+        }
+        GemmArgs dn = peer_args(down, 1);
+        gemm(kGemmDown, act_.p, w2_.p, ycomb, dn, nseg, st);
+        peer_->signal_ready(st, 1, i, e1);
+        comm_bytes_ += static_cast<double>(dE_) * cc_ * M_ * esz_ * (W_ - 1);
+      } else {
+        gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
+      }
       prof_mark(kPhDown, false, st);
       ck(cudaEventRecord(ev_b_[i], st), "event");
     }
-    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[1], 0), "wait");  // my ycomb consumed
-    peer_->wait_peers_freed(comm_stream_, 1, e1);
-    for (int i = 0; i < degree_; ++i) {
-      ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
-      peer_push(1, yexp_.p, i, 1, e1);
-      ck(cudaEventRecord(ev_c_[i], comm_stream_), "event");
+    if (!fused_combine_) {
+      ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[1], 0), "wait");  // my ycomb consumed
+      peer_->wait_peers_freed(comm_stream_, 1, e1);
+      for (int i = 0; i < degree_; ++i) {
+        ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+        peer_push(1, yexp_.p, i, 1, e1, ev_c_[i]);
+        tl_mark("combine pushed " + std::to_string(i) + " [comm]", comm_stream_);
+      }
+      ck(cudaStreamWaitEvent(st, ev_c_[degree_ - 1], 0), "wait");
     }
     prof_mark(kPhA2aFwd, false, comm_stream_);
-    for (int i = 0; i < degree_; ++i) {
-      ck(cudaStreamWaitEvent(st, ev_c_[i], 0), "wait");
-      peer_->wait_chunk(st, 1, i, e1);
-    }
+    // blocks of one source land in chunk order: the last chunk's flags cover all
+    ckr(wait_flags_device(peer_->ready_wait(1, degree_ - 1, e1), st), "wait");
+    ++launches_;
+    tl_mark("combine landed", st);
   } else {
     // Comm stream: all dispatches (chunk order), then all combines (reference FIFO order,
     // pipeline.cpp:180-190); compute stream: per chunk up+down GEMMs.
@@ -705,10 +804,12 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
     ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
   }
-  prof_mark(kPhDecode, true, st);
-  ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
-  prof_mark(kPhDecode, false, st);
-  ++launches_;
+  if (!fused_) {
+    prof_mark(kPhDecode, true, st);
+    ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
+    prof_mark(kPhDecode, false, st);
+    ++launches_;
+  }
   if (peer_) {
     peer_->signal_freed(st, 1, epoch_[1]);
     ck(cudaEventRecord(ev_freed_[1], st), "event");
@@ -784,7 +885,29 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   void* recv = W_ > 1 ? recv_.p : z_.p;
   void* drecv = W_ > 1 ? drecv_.p : dz_.p;
   void* dxcomb = W_ > 1 ? dxcomb_.p : dxe_.p;
-  if (W_ == 1) {
+  if (fused_) {
+    // encode-backward fused into the dgrad GEMM: dx[token] = (dh . W1^T)[slot], rows scattered
+    // by TMA; dropped tokens get zero rows.
+    dg.idx_mode = kIdxScatterD;
+    dg.gather_rows = static_cast<uint32_t>(T_);
+    dg.row_token = gb.slot_token;
+    prof_mark(kPhDgradMask, true, st);
+    gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
+    prof_mark(kPhDgradMask, false, st);
+    prof_mark(kPhEncodeBwd, true, st);
+    ckr(zero_dropped_device(T_, k_, gb.locations, static_cast<size_t>(M_) * esz_, dx, st), "zero rows");
+    prof_mark(kPhEncodeBwd, false, st);
+    ++launches_;
+    prof_mark(kPhDgrad, true, st);
+    gemm(kGemmDgrad, dh_.p, w1_.p, dx, dg, nseg, st);
+    prof_mark(kPhDgrad, false, st);
+    prof_mark(kPhWgrad1, true, st);
+    gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
+    prof_mark(kPhWgrad1, false, st);
+    prof_mark(kPhWgrad2, true, st);
+    gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
+    prof_mark(kPhWgrad2, false, st);
+  } else if (W_ == 1) {
     prof_mark(kPhDgradMask, true, st);
     gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
     prof_mark(kPhDgradMask, false, st);
@@ -805,31 +928,47 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     peer_->wait_peers_freed(comm_stream_, 2, e2);
     prof_mark(kPhA2aBwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {  // adjoint of combine
-      peer_push(2, dz_.p, i, 0, e2);
-      ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+      peer_push(2, dz_.p, i, 0, e2, ev_a_[i]);
+      tl_mark("bwd dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
     for (int i = 0; i < degree_; ++i) {
       ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
-      peer_->wait_chunk(st, 2, i, e2);
+      ckr(wait_flags_device(peer_->ready_wait(2, i, e2), st), "wait");
+      ++launches_;
+      tl_mark("bwd dispatch landed " + std::to_string(i), st);
       dgm.seg_base = i * W_;
       dg.seg_base = i * W_;
       prof_mark(kPhDgradMask, true, st);
       gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
       prof_mark(kPhDgradMask, false, st);
       prof_mark(kPhDgrad, true, st);
-      gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+      if (fused_combine_) {
+        // backward combine fused into the dgrad GEMM (dx blocks straight to the source ranks)
+        if (i == 0) {
+          ckr(wait_flags_device(peer_->freed_wait(3, e3 - 1), st), "wait");
+          ++launches_;
+        }
+        GemmArgs d2 = peer_args(dg, 3);
+        gemm(kGemmDgrad, dh_.p, w1_.p, dxcomb, d2, nseg, st);
+        peer_->signal_ready(st, 3, i, e3);
+        comm_bytes_ += static_cast<double>(dE_) * cc_ * M_ * esz_ * (W_ - 1);
+      } else {
+        gemm(kGemmDgrad, dh_.p, w1_.p, dxe_.p, dg, nseg, st);
+      }
       prof_mark(kPhDgrad, false, st);
       ck(cudaEventRecord(ev_b_[i], st), "event");
     }
-    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[3], 0), "wait");
-    peer_->wait_peers_freed(comm_stream_, 3, e3);
-    for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
-      ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
-      peer_push(3, dxe_.p, i, 1, e3);
-      ck(cudaEventRecord(ev_c_[i], comm_stream_), "event");
+    if (!fused_combine_) {
+      ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[3], 0), "wait");
+      peer_->wait_peers_freed(comm_stream_, 3, e3);
+      for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
+        ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+        peer_push(3, dxe_.p, i, 1, e3, ev_c_[i]);
+        tl_mark("bwd combine pushed " + std::to_string(i) + " [comm]", comm_stream_);
+      }
     }
     prof_mark(kPhA2aBwd, false, comm_stream_);
-    // Weight gradients overlap the return pushes; then the receive buffers are released.
+    // Weight gradients overlap the return transfers; then the receive buffers are released.
     prof_mark(kPhWgrad1, true, st);
     gemm(kGemmWgrad, recv, dh_.p, gw1, wg1, nseg, st);
     prof_mark(kPhWgrad1, false, st);
@@ -841,10 +980,10 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     prof_mark(kPhWgrad2, false, st);
     peer_->signal_freed(st, 2, e2);
     ck(cudaEventRecord(ev_freed_[2], st), "event");
-    for (int i = 0; i < degree_; ++i) {
-      ck(cudaStreamWaitEvent(st, ev_c_[i], 0), "wait");
-      peer_->wait_chunk(st, 3, i, e3);
-    }
+    if (!fused_combine_) ck(cudaStreamWaitEvent(st, ev_c_[degree_ - 1], 0), "wait");
+    ckr(wait_flags_device(peer_->ready_wait(3, degree_ - 1, e3), st), "wait");
+    ++launches_;
+    tl_mark("bwd combine landed", st);
   } else {
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
@@ -880,15 +1019,19 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     prof_mark(kPhWgrad2, false, st);
     ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
   }
-  prof_mark(kPhEncodeBwd, true, st);
-  ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st), "encode_bwd");
-  prof_mark(kPhEncodeBwd, false, st);
-  ++launches_;
+  if (!fused_) {
+    prof_mark(kPhEncodeBwd, true, st);
+    ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st), "encode_bwd");
+    prof_mark(kPhEncodeBwd, false, st);
+    ++launches_;
+  }
   if (peer_) {
     peer_->signal_freed(st, 3, epoch_[3]);
     ck(cudaEventRecord(ev_freed_[3], st), "event");
   }
   bwd_launches_ = launches_ - l0;
+  tl_mark("backward end", st);
+  tl_flush();
   last_dw1_ = gw1;
   last_dw2_ = gw2;
 }

@@ -87,11 +87,16 @@ class Layer {
   GatingBuffers gating_buffers();
   SlotGeom geom() const;
   void exchange(const void* send, void* recv, int chunk, int phase);
-  void peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch);
+  void peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch, cudaEvent_t local_done);
   double allreduce_max_host(double v);
   void ensure_io();
   void alloc_capacity(int cap);
   void prof_mark(int phase, bool begin, cudaStream_t st);
+  // MOE_TIMELINE=1 (debug): event timeline of one forward + backward, printed after backward.
+  void tl_mark(const std::string& name, cudaStream_t st);
+  void tl_flush();
+  bool tl_on_ = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> tl_;
 
   moe_config cfg_;
   int rank_, device_;
@@ -129,6 +134,14 @@ class Layer {
   unsigned int fix_cap_ = 0;
   bool stats_dirty_ = true;
   void prepare_up(GemmArgs& up);
+  // Single-rank fused path (W = 1, k = 1, bf16 tcgen05 shapes): decode runs in the down GEMM's
+  // epilogue (gate scale + TMA row scatter to token rows) and encode-backward in the dgrad
+  // GEMM's epilogue (row scatter), so expert-output rows are never materialised.
+  bool fused_ = false;
+  // W > 1 peer backend: combine (fwd) / dx combine (bwd) fused into the down / dgrad GEMM
+  // epilogues, which store straight into the source ranks' buffers over NVLink.
+  bool fused_combine_ = false;
+  GemmArgs peer_args(const GemmArgs& a, int ch) const;
 
   struct ProfRec {
     int phase;

@@ -35,6 +35,8 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw MoeError(MOE_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// stage words: [2 * channel + kind][destination] (one per destination stream: an epoch written
+// for one peer can never be published to another by a lagging stream)
 constexpr int kStageSlots = 2 * PeerExchange::kChannels;
 
 }  // namespace
@@ -68,7 +70,7 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
     throw MoeError(MOE_ECUDA, "peer all-to-all: CUDA stream memory operations unavailable");
   for (int c = 0; c < kChannels; ++c) local_bufs_[c] = bufs[c];
   nflags_ = static_cast<size_t>(kChannels) * world * kMaxChunks + static_cast<size_t>(kChannels) * world +
-            kStageSlots;
+            static_cast<size_t>(kStageSlots) * world;
   ck(cudaMalloc(&flags_, nflags_ * sizeof(uint32_t) + 256), "cudaMalloc flags");
   ck(cudaMemset(flags_, 0, nflags_ * sizeof(uint32_t) + 256), "memset flags");
 
@@ -91,6 +93,14 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
   ck(cudaMemcpy(all.data(), static_cast<char*>(dev) + hb, hb * world, cudaMemcpyDeviceToHost), "copy");
   cudaFree(dev);
 
+  pstreams_.assign(world, nullptr);
+  ev_out_.assign(world, nullptr);
+  for (int p = 0; p < world; ++p) {
+    ck(cudaStreamCreateWithFlags(&pstreams_[p], cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ev_out_[p], cudaEventDisableTiming), "event");
+  }
+  ck(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming), "event");
+
   peer_flags_.assign(world, nullptr);
   peer_bufs_.assign(kChannels, std::vector<void*>(world, nullptr));
   for (int p = 0; p < world; ++p) {
@@ -111,6 +121,11 @@ PeerExchange::~PeerExchange() {
     for (int c = 0; c < kChannels; ++c)
       if (peer_bufs_[c][p]) cudaIpcCloseMemHandle(peer_bufs_[c][p]);
   }
+  for (auto st : pstreams_)
+    if (st) cudaStreamDestroy(st);
+  for (auto e : ev_out_)
+    if (e) cudaEventDestroy(e);
+  if (ev_in_) cudaEventDestroy(ev_in_);
   if (flags_) cudaFree(flags_);
 }
 
@@ -138,9 +153,15 @@ uint32_t* PeerExchange::stage(int slot) const {
 // Write epoch into a local stage word, then DMA it to each destination flag (all in stream
 // order, so the flags land after every earlier copy on this stream).
 void PeerExchange::publish(cudaStream_t st, int slot, uint32_t epoch, const std::vector<uint32_t*>& dsts) {
-  if (stream_write_u32(st, stage(slot), epoch) != 0) throw MoeError(MOE_ECUDA, "cuStreamWriteValue32 failed");
+  uint32_t* w = stage(slot * world_ + rank_);
+  if (stream_write_u32(st, w, epoch) != 0) throw MoeError(MOE_ECUDA, "cuStreamWriteValue32 failed");
   for (uint32_t* d : dsts)
-    ck(cudaMemcpyAsync(d, stage(slot), sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "flag copy");
+    ck(cudaMemcpyAsync(d, w, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "flag copy");
+}
+
+void PeerExchange::publish_one(cudaStream_t st, int slot, uint32_t epoch, uint32_t* dst) {
+  if (stream_write_u32(st, stage(slot), epoch) != 0) throw MoeError(MOE_ECUDA, "cuStreamWriteValue32 failed");
+  ck(cudaMemcpyAsync(dst, stage(slot), sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "flag copy");
 }
 
 void PeerExchange::wait_peers_freed(cudaStream_t copy, int ch, uint32_t epoch) {
@@ -152,21 +173,26 @@ void PeerExchange::wait_peers_freed(cudaStream_t copy, int ch, uint32_t epoch) {
 }
 
 void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
-                              const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch) {
+                              const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch,
+                              cudaEvent_t local_done) {
   if (chunk >= kMaxChunks) throw MoeError(MOE_EINVAL, "peer all-to-all: too many chunks");
   // Push model: peer p receives my block where it receives "from rank_", i.e. at ro[rank_] of
-  // the (source-symmetric) plan. Start with the next peer so all ranks spread over the links.
+  // the (source-symmetric) plan. One stream per destination: the blocks move concurrently, and
+  // each peer's ready flag follows its own block.
+  ck(cudaEventRecord(ev_in_, copy), "event");
   for (int i = 0; i < world_; ++i) {
     const int p = (rank_ + i) % world_;
+    cudaStream_t ps = pstreams_[p];
+    ck(cudaStreamWaitEvent(ps, ev_in_, 0), "wait");
     char* dst = static_cast<char*>(p == rank_ ? local_bufs_[ch] : peer_bufs_[ch][p]) + ro[rank_] * esz;
     ck(cudaMemcpyAsync(dst, static_cast<const char*>(src) + so[p] * esz, block_bytes,
-                       cudaMemcpyDeviceToDevice, copy),
+                       cudaMemcpyDeviceToDevice, ps),
        "peer copy");
+    if (p != rank_) publish_one(ps, (2 * ch) * world_ + p, epoch, ready_remote(p, ch, chunk));
+    else if (local_done) ck(cudaEventRecord(local_done, ps), "event");
+    ck(cudaEventRecord(ev_out_[p], ps), "event");
   }
-  std::vector<uint32_t*> dsts;
-  for (int p = 0; p < world_; ++p)
-    if (p != rank_) dsts.push_back(ready_remote(p, ch, chunk));
-  publish(copy, 2 * ch, epoch, dsts);
+  for (int p = 0; p < world_; ++p) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
 }
 
 void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch) {
@@ -175,6 +201,33 @@ void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch
     if (stream_wait_geq_u32(st, ready_local(ch, p, chunk), epoch) != 0)
       throw MoeError(MOE_ECUDA, "cuStreamWaitValue32 failed");
   }
+}
+
+FlagWait PeerExchange::ready_wait(int ch, int chunk, uint32_t epoch) const {
+  FlagWait w;
+  w.base = ready_local(ch, 0, chunk);
+  w.stride = kMaxChunks;
+  w.world = world_;
+  w.rank = rank_;
+  w.epoch = epoch;
+  return w;
+}
+
+FlagWait PeerExchange::freed_wait(int ch, uint32_t epoch) const {
+  FlagWait w;
+  w.base = freed_local(ch, 0);
+  w.stride = 1;
+  w.world = world_;
+  w.rank = rank_;
+  w.epoch = epoch;
+  return w;
+}
+
+void PeerExchange::signal_ready(cudaStream_t st, int ch, int chunk, uint32_t epoch) {
+  std::vector<uint32_t*> dsts;
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_) dsts.push_back(ready_remote(p, ch, chunk));
+  publish(st, 2 * ch, epoch, dsts);  // stage column `rank` of slot 2ch: unused by the push streams
 }
 
 void PeerExchange::signal_freed(cudaStream_t st, int ch, uint32_t epoch) {

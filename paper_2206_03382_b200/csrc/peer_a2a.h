@@ -1,8 +1,9 @@
 // Copy-engine flexible all-to-all over NVLink peer memory (one process per GPU).
 //
 // Every rank maps its peers' receive buffers (CUDA IPC) and pushes its blocks with
-// cudaMemcpyAsync on a dedicated copy stream: the DMA engines move the data over NVLink, so the
-// exchange takes no SMs from the persistent expert GEMMs it overlaps with. Ordering across
+// cudaMemcpyAsync, one copy stream per destination so the W blocks of a chunk move on separate
+// DMA engines at once: the copy engines drive NVLink, so the exchange takes no SMs from the
+// persistent expert GEMMs it overlaps with. Ordering across
 // processes uses 32-bit epoch flags in each receiver's memory:
 //   ready[ch][src][chunk]  -- written (after the data) by src into dst's flags; dst's compute
 //                             stream waits with cuStreamWaitValue32(GEQ epoch).
@@ -19,6 +20,8 @@
 
 #include <cstdint>
 #include <vector>
+
+#include "peer_flags.h"
 
 namespace moe {
 
@@ -38,12 +41,25 @@ class PeerExchange {
   // Copy stream: push block p of `src` (offset so[p]) to peer p's channel buffer at the offset p
   // receives from this rank, ro[rank] (moe_a2a_plan is source-symmetric), then publish
   // ready[ch][me][chunk] = epoch to each peer.
+  // local_done (optional) is recorded right after this rank's own block has been copied.
   void push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
-                  const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch);
-  // Compute stream: wait for every peer's chunk of this epoch.
+                  const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch,
+                  cudaEvent_t local_done = nullptr);
+  // Compute stream: wait for every peer's chunk of this epoch (stream memory operations).
   void wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch);
+  // The same wait as a device-side poll (fused into the first consuming kernel, or
+  // wait_flags_device). Flags of one source arrive in chunk order, so waiting for chunk c also
+  // covers every earlier chunk of the channel.
+  FlagWait ready_wait(int ch, int chunk, uint32_t epoch) const;
   // Stream st (after the consumers of channel ch's buffer): tell every peer it is free.
   void signal_freed(cudaStream_t st, int ch, uint32_t epoch);
+  // Fused-combine protocol: the producing kernel stores into the peers' channel buffers itself;
+  // before the first store, every peer's buffer must be free (device poll of freed[ch][*]) ...
+  FlagWait freed_wait(int ch, uint32_t epoch) const;
+  // ... and after each chunk's kernel, stream st publishes ready[ch][me][chunk] to every peer.
+  void signal_ready(cudaStream_t st, int ch, int chunk, uint32_t epoch);
+  // Channel-ch receive buffer of rank p (this rank's own for p == rank).
+  void* buffer(int ch, int p) const { return p == rank_ ? local_bufs_[ch] : peer_bufs_[ch][p]; }
 
  private:
   uint32_t* ready_local(int ch, int src, int chunk) const;
@@ -52,6 +68,7 @@ class PeerExchange {
   uint32_t* freed_remote(int dst, int ch) const;
   uint32_t* stage(int slot) const;
   void publish(cudaStream_t st, int slot, uint32_t epoch, const std::vector<uint32_t*>& dsts);
+  void publish_one(cudaStream_t st, int slot, uint32_t epoch, uint32_t* dst);
 
   int rank_, world_;
   void* flags_ = nullptr;                       // this rank's flag block (IPC exported)
@@ -59,6 +76,9 @@ class PeerExchange {
   std::vector<std::vector<void*>> peer_bufs_;   // [ch][peer] mapped receive buffers
   void* local_bufs_[kChannels];
   size_t nflags_ = 0;
+  std::vector<cudaStream_t> pstreams_;  // per-destination copy streams
+  cudaEvent_t ev_in_ = nullptr;
+  std::vector<cudaEvent_t> ev_out_;
 };
 
 // Driver stream memory operations (resolved through cudaGetDriverEntryPoint).

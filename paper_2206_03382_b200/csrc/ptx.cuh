@@ -107,6 +107,17 @@ __device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap* m, uint64_t*
       : "memory");
 }
 
+// Row scatter (tile::scatter4): 4 consecutive box rows at smem -> rows r0..r3 (rows out of
+// bounds are dropped: empty capacity slots).
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap* m, const void* smem, int c0, int r0,
+                                             int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group"
+      " [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(smem)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* smem, int c0, int c1,
                                              int c2) {
   asm volatile(

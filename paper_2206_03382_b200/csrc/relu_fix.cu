@@ -13,6 +13,7 @@
 
 #include "gemm_sm100.h"
 #include "kernels.h"
+#include "peer_flags.cuh"
 
 namespace moe {
 
@@ -63,19 +64,41 @@ __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, int R, in
 }
 
 // rowmax[i] = max_m |x[i][m]| (one warp per row)
+// max_m |x[r][m]| per row. Optionally first waits for the chunk's peer flags (fused receive
+// wait) and resets the fixup counter. bf16 |x| order == order of (bits & 0x7fff) for finite x,
+// so 8 columns reduce with packed integer max.
 __global__ void rowmax_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int M,
-                              float* __restrict__ rowmax) {
+                              float* __restrict__ rowmax, FlagWait fw, unsigned int* reset) {
+  if (fw.base != nullptr) {
+    if (threadIdx.x < 32) wait_flags_warp(fw);
+    __syncthreads();
+  }
+  if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0u;
   const int lane = threadIdx.x % 32;
+  const bool vec = (M % 8) == 0;
   for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
     const __nv_bfloat16* p = x + r * M;
-    float m = 0.0f;
-    for (int i = lane; i < M; i += 32) m = fmaxf(m, fabsf(__bfloat162float(p[i])));
+    uint32_t mb = 0u;
+    if (vec) {
+      const uint4* v = reinterpret_cast<const uint4*>(p);
+      for (int i = lane; i < M / 8; i += 32) {
+        const uint4 a = __ldg(v + i);
+        mb = __vmaxu2(mb, __vmaxu2(__vmaxu2(a.x & 0x7fff7fffu, a.y & 0x7fff7fffu),
+                                   __vmaxu2(a.z & 0x7fff7fffu, a.w & 0x7fff7fffu)));
+      }
+    } else {
+      const uint16_t* q = reinterpret_cast<const uint16_t*>(p);
+      for (int i = lane; i < M; i += 32) mb = max(mb, static_cast<uint32_t>(q[i] & 0x7fffu));
+    }
+    mb = max(mb & 0xffffu, mb >> 16);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) rowmax[r] = m;
+    for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    if (lane == 0) rowmax[r] = __uint_as_float(mb << 16);
   }
 }
+
+__global__ void wait_flags_kernel(FlagWait fw) { wait_flags_warp(fw); }
 
 // For each listed (seg, row, col): h = sum_m X[seg][row][m] * W1T[g][col][m] in fp64, then
 // act[seg][row][col] = bf16(max(h, 0)). One warp per entry.
@@ -168,11 +191,18 @@ int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, floa
   return launch_status();
 }
 
-int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st) {
+int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st,
+                  const FlagWait* wait, unsigned int* reset) {
   if (rows <= 0) return 0;
   const int64_t blocks = (rows + 7) / 8;
-  const int grid = static_cast<int>(blocks < 148 * 16 ? blocks : 148 * 16);
-  rowmax_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, M, rowmax);
+  const int grid = static_cast<int>(blocks < 148 * 4 ? blocks : 148 * 4);
+  rowmax_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, M, rowmax,
+                                      wait ? *wait : FlagWait{}, reset);
+  return launch_status();
+}
+
+int wait_flags_device(const FlagWait& w, cudaStream_t st) {
+  wait_flags_kernel<<<1, 32, 0, st>>>(w);
   return launch_status();
 }
 

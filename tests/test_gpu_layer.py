@@ -144,3 +144,30 @@ def test_layer_full_size_configs(cuda, name, E, k, f, M, V, bpr):
     assert oracle.max_rel_diff(g.dx.double().cpu().numpy(), ref["dx"]) < 2e-2
     assert oracle.max_rel_diff(g.dw1.double().cpu().numpy(), ref["dw1"]) < 2e-2
     assert oracle.max_rel_diff(g.dw2.double().cpu().numpy(), ref["dw2"]) < 2e-2
+
+
+def test_fused_decode_matches_unfused(cuda, monkeypatch):
+    """W = 1, k = 1: decode / encode-backward fused into the down / dgrad GEMM epilogues (TMA row
+    scatter to token rows) against the unfused kernels (MOE_FUSED=0) and the oracle; drops
+    included (f = 0.75), so dropped tokens' zero rows are exercised."""
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MOE_FUSED", mode)
+        st, res, g, ref, _ = run_case(16, 1, 0.75, 512, 1024, 4096, False, "bf16", seed=77)
+        idxs, loc, gates, cap = st.routing()
+        assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
+        assert (loc < 0).any()
+        y = res.y.double().cpu().numpy()
+        dx = g.dx.double().cpu().numpy()
+        dropped = (ref["locations"] < 0).all(axis=1)
+        assert (y[dropped] == 0).all() and (dx[dropped] == 0).all()
+        for name, got in (("y", y), ("dx", dx), ("dw1", g.dw1), ("dw2", g.dw2)):
+            got = got if isinstance(got, np.ndarray) else got.double().cpu().numpy()
+            assert oracle.max_rel_diff(got, ref[name]) < 2e-2, (mode, name)
+        outs[mode] = (res.y, g.dx, g.dw1, g.dw2)
+    # same GEMMs, only the epilogue's rounding point of g * out differs
+    assert torch.equal(outs["1"][1], outs["0"][1])      # dx: scatter of identical rows
+    assert torch.equal(outs["1"][2], outs["0"][2]) and torch.equal(outs["1"][3], outs["0"][3])
+    # y: one bf16 rounding (g * acc) vs two (acc, then g * out): within a couple of bf16 ulps
+    assert oracle.max_rel_diff(outs["1"][0].double().cpu().numpy(),
+                               outs["0"][0].double().cpu().numpy()) < 1e-2

@@ -17,6 +17,10 @@ from tests.helpers import layer_inputs  # noqa: E402
 def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, cap="fixed",
         seed=402):
     E = E_per * W
+    ce = backend == "peer-ce"  # peer backend with the copy-engine combine (fused combine off)
+    if ce:
+        backend = "peer"
+        os.environ["MOE_FUSED_COMBINE"] = "0"
     cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
                          hidden_dim=V, tokens_per_step=T, top_k=k, capacity=cap,
                          capacity_factor=f, bpr=bpr, dtype=dt, degree=degree, adaptive=adaptive,
@@ -24,6 +28,7 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     obj = [LayerState.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
+    os.environ.pop("MOE_FUSED_COMBINE", None)
     inp = layer_inputs(seed, W, T, M, V, E, dt)
     tdt = cfg.torch_dtype
     xs = torch.as_tensor(inp["x"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
@@ -69,8 +74,10 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     cases = [
         # E_per, k, f, M, V, T, bpr, dtype, degree, adaptive, all-to-all backend
+        # (peer: M % 256 == 0 runs the combine fused into the GEMM epilogues; peer-ce: copy engines)
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 1, False, "peer"),
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer"),
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer-ce"),
         (4, 1, 1.0, 256, 512, 1024, False, "bf16", 4, False, "peer"),
         (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "peer"),   # drops, ragged chunks
         (2, 2, 1.0, 64, 128, 200, True, "f32", 2, False, "peer"),
