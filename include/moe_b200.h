@@ -78,7 +78,11 @@ typedef struct moe_step_metrics {
   int64_t drop_count;  /* dropped (token, expert) assignments on this rank */
   int64_t relu_fixups; /* bf16 path: up-GEMM outputs re-decided in fp64 (ReLU-mask certificate,
                           last chunk of the last forward) */
+  int32_t fused;       /* MOE_FUSED_* bits: which exchanges ran inside the GEMM epilogues */
+  int32_t reserved;
 } moe_step_metrics;
+#define MOE_FUSED_DECODE 1  /* W = 1, k = 1: decode / encode-backward = down / dgrad epilogue scatter */
+#define MOE_FUSED_COMBINE 2 /* W > 1 peer backend: combine = down / dgrad epilogue NVLink stores */
 
 typedef struct moe_handle moe_handle;
 
@@ -140,6 +144,14 @@ int moe_backward(moe_handle* h, const void* dy, void* dx, float* dw1, float* dw2
  * device->host copy of the result happen inside the call, as a reference caller would see. */
 int moe_forward_host(moe_handle* h, const void* x_host, void* y_host, void* stream);
 int moe_backward_host(moe_handle* h, const void* dy_host, void* dx_host, void* stream);
+/* Pipelined variants for a stream of steps (a data loader feeding the layer): they return after
+ * enqueueing; the upload of the input and the download of the result run on the handle's own
+ * copy streams and overlap the neighbouring steps' compute (double-buffered device staging).
+ * Host buffers must be pinned and stay untouched (inputs) / unread (outputs) until
+ * moe_host_sync, which waits for every enqueued download. */
+int moe_forward_host_async(moe_handle* h, const void* x_host, void* y_host, void* stream);
+int moe_backward_host_async(moe_handle* h, const void* dy_host, void* dx_host, void* stream);
+int moe_host_sync(moe_handle* h);
 
 /* Routing of the last forward (GateOutput, gating.hpp:14-23): host buffers (T, k). */
 int moe_get_routing(moe_handle* h, int32_t* idxs, int32_t* locations, double* gates,

@@ -45,7 +45,8 @@ class StepMetrics(C.Structure):
     _fields_ = [
         ("f", C.c_double), ("capacity", C.c_int64), ("a2a_algo", C.c_int32),
         ("degree", C.c_int32), ("seconds", C.c_double), ("comm_bytes", C.c_double),
-        ("drop_count", C.c_int64), ("relu_fixups", C.c_int64),
+        ("drop_count", C.c_int64), ("relu_fixups", C.c_int64), ("fused", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -73,6 +74,9 @@ SIGNATURES = {
     "moe_backward": (I32, [P, P, P, P, P, P]),
     "moe_forward_host": (I32, [P, P, P, P]),
     "moe_backward_host": (I32, [P, P, P, P]),
+    "moe_forward_host_async": (I32, [P, P, P, P]),
+    "moe_backward_host_async": (I32, [P, P, P, P]),
+    "moe_host_sync": (I32, [P]),
     "moe_get_routing": (I32, [P, P, P, P, PI64]),
     "moe_get_metrics": (I32, [P, C.POINTER(StepMetrics)]),
     "moe_get_expert_grads": (I32, [P, P, P]),

@@ -284,6 +284,13 @@ int moe_forward_host(moe_handle* h, const void* xh, void* yh, void* stream) {
 int moe_backward_host(moe_handle* h, const void* dyh, void* dxh, void* stream) {
   LAYER_CALL(h, h->layer->backward_host(dyh, dxh, S(stream)));
 }
+int moe_forward_host_async(moe_handle* h, const void* xh, void* yh, void* stream) {
+  LAYER_CALL(h, h->layer->forward_host_async(xh, yh, S(stream)));
+}
+int moe_backward_host_async(moe_handle* h, const void* dyh, void* dxh, void* stream) {
+  LAYER_CALL(h, h->layer->backward_host_async(dyh, dxh, S(stream)));
+}
+int moe_host_sync(moe_handle* h) { LAYER_CALL(h, h->layer->host_sync()); }
 int moe_get_routing(moe_handle* h, int32_t* idxs, int32_t* locs, double* gates, int64_t* cap) {
   LAYER_CALL(h, h->layer->get_routing(idxs, locs, gates, cap));
 }

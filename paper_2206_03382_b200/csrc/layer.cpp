@@ -334,6 +334,13 @@ void Layer::take_profile(double* ms, int64_t* counts, int n) {
 
 Layer::~Layer() {
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);
+  if (d2h_) cudaStreamSynchronize(d2h_);
+  for (auto& p : pipe_)
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {p.in_ready[i], p.in_free[i], p.out_ready[i], p.out_free[i]})
+        if (e) cudaEventDestroy(e);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
   peer_.reset();
   if (cap_host_) cudaFreeHost(cap_host_);
   for (const auto& r : prof_recs_) {
@@ -614,7 +621,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   prof_mark(kPhAssign, true, st);
   ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
   prof_mark(kPhAssign, false, st);
-  launches_ += 3 + (cfg_.bpr ? 1 : 0);
+  // gate + column scan + capacity finalize, assign (+ BPR rank), (+ resolve_capacity)
+  launches_ += 4 + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
   if (cert && stats_dirty_) {
@@ -1106,6 +1114,50 @@ void Layer::backward_host(const void* dyh, void* dxh, cudaStream_t st) {
   ck(cudaStreamSynchronize(st), "sync");
 }
 
+void Layer::pipe_call(int dir, const void* inh, void* outh, cudaStream_t st) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  const size_t n = static_cast<size_t>(T_) * M_ * esz_;
+  HostPipe& p = pipe_[dir];
+  if (!h2d_) {
+    ck(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "stream");
+  }
+  if (!p.in_ready[0]) {
+    for (int i = 0; i < 2; ++i) {
+      p.in[i].alloc(n);
+      p.out[i].alloc(n);
+      for (cudaEvent_t* e : {&p.in_ready[i], &p.in_free[i], &p.out_ready[i], &p.out_free[i]})
+        ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    }
+  }
+  const int s = p.slot;
+  p.slot ^= 1;
+  // upload once the call that last read this staging buffer is done with it
+  ck(cudaStreamWaitEvent(h2d_, p.in_free[s], 0), "wait");
+  ck(cudaMemcpyAsync(p.in[s].p, inh, n, cudaMemcpyHostToDevice, h2d_), "h2d");
+  ck(cudaEventRecord(p.in_ready[s], h2d_), "event");
+  ck(cudaStreamWaitEvent(st, p.in_ready[s], 0), "wait");
+  ck(cudaStreamWaitEvent(st, p.out_free[s], 0), "wait");
+  if (dir == 0)
+    forward(p.in[s].p, p.out[s].p, st);
+  else
+    backward(p.in[s].p, p.out[s].p, nullptr, nullptr, st);
+  ck(cudaEventRecord(p.in_free[s], st), "event");
+  ck(cudaEventRecord(p.out_ready[s], st), "event");
+  ck(cudaStreamWaitEvent(d2h_, p.out_ready[s], 0), "wait");
+  ck(cudaMemcpyAsync(outh, p.out[s].p, n, cudaMemcpyDeviceToHost, d2h_), "d2h");
+  ck(cudaEventRecord(p.out_free[s], d2h_), "event");
+}
+
+void Layer::forward_host_async(const void* xh, void* yh, cudaStream_t st) { pipe_call(0, xh, yh, st); }
+void Layer::backward_host_async(const void* dyh, void* dxh, cudaStream_t st) { pipe_call(1, dyh, dxh, st); }
+
+void Layer::host_sync() {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (d2h_) ck(cudaStreamSynchronize(d2h_), "sync");
+  if (h2d_) ck(cudaStreamSynchronize(h2d_), "sync");
+}
+
 void Layer::get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* capacity) {
   if (!fwd_done_) throw MoeError(MOE_ESTATE, "get_routing: no forward yet");
   ck(cudaSetDevice(device_), "cudaSetDevice");
@@ -1133,6 +1185,8 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->comm_bytes = comm_bytes_;
   m->drop_count = drops;
   m->relu_fixups = 0;
+  m->fused = (fused_ ? MOE_FUSED_DECODE : 0) | (peer_ && fused_combine_ ? MOE_FUSED_COMBINE : 0);
+  m->reserved = 0;
   if (cfg_.dtype == MOE_DTYPE_BF16) {
     unsigned int nfix = 0;
     ck(cudaMemcpy(&nfix, fix_count_.p, 4, cudaMemcpyDeviceToHost), "copy");

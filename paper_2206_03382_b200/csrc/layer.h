@@ -64,6 +64,12 @@ class Layer {
   void backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStream_t st);
   void forward_host(const void* xh, void* yh, cudaStream_t st);
   void backward_host(const void* dyh, void* dxh, cudaStream_t st);
+  // Pipelined host-buffer calls: return after enqueueing; the input upload (H2D stream) and the
+  // result download (D2H stream) overlap the neighbouring steps' compute through double-buffered
+  // device staging. Host buffers must stay untouched / unread until host_sync().
+  void forward_host_async(const void* xh, void* yh, cudaStream_t st);
+  void backward_host_async(const void* dyh, void* dxh, cudaStream_t st);
+  void host_sync();
   void get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* capacity);
   void get_metrics(moe_step_metrics* m);
   void get_grads(float* dw1, float* dw2);
@@ -129,6 +135,14 @@ class Layer {
   DevMem slot_token_, slot_gate_;
   DevMem z_, recv_, act_, yexp_, ycomb_, dz_, drecv_, dh_, dxe_, dxcomb_;
   DevMem io_x_, io_y_, io_dy_, io_dx_;
+  struct HostPipe {
+    DevMem in[2], out[2];
+    cudaEvent_t in_ready[2]{}, in_free[2]{}, out_ready[2]{}, out_free[2]{};
+    int slot = 0;
+  };
+  HostPipe pipe_[2];  // [forward, backward]
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+  void pipe_call(int dir, const void* inh, void* outh, cudaStream_t st);
   // ReLU-mask certificate state (relu_fix.cu)
   DevMem colabs_, colabs_blk_, w1t_, rowmax_, fix_list_, fix_count_, relu_mask_;
   unsigned int fix_cap_ = 0;

@@ -101,53 +101,68 @@ __global__ void rowmax_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
 __global__ void wait_flags_kernel(FlagWait fw) { wait_flags_warp(fw); }
 
 // For each listed (seg, row, col): h = sum_m X[seg][row][m] * W1T[g][col][m] in fp64, then
-// act[seg][row][col] = bf16(max(h, 0)). One warp per entry.
-__global__ void relu_fixup_kernel(const __nv_bfloat16* __restrict__ x,
-                                  const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows, int M,
-                                  int V, const unsigned long long* __restrict__ list,
-                                  const unsigned int* __restrict__ count, unsigned int cap,
-                                  __nv_bfloat16* __restrict__ act,
-                                  unsigned long long* __restrict__ relu_mask) {
+// act[seg][row][col] = bf16(max(h, 0)) and the ReLU bit. One warp per entry, two entries in
+// flight per warp (the kernel is load-latency bound: two rows of x / W1^T per entry).
+__device__ __forceinline__ double fixup_dot(const __nv_bfloat16* xr, const __nv_bfloat16* wr, int M,
+                                            int lane) {
+  double s = 0.0;
+  if ((M & 7) == 0) {
+    const uint4* xv = reinterpret_cast<const uint4*>(xr);
+    const uint4* wv = reinterpret_cast<const uint4*>(wr);
+    for (int v = lane; v < M / 8; v += 32) {
+      const uint4 a = __ldg(xv + v), w = __ldg(wv + v);
+      const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 af = __bfloat1622float2(ah[q]), wf = __bfloat1622float2(wh[q]);
+        s = fma(static_cast<double>(af.x), static_cast<double>(wf.x), s);
+        s = fma(static_cast<double>(af.y), static_cast<double>(wf.y), s);
+      }
+    }
+  } else {
+    for (int m = lane; m < M; m += 32)
+      s = fma(static_cast<double>(__bfloat162float(xr[m])), static_cast<double>(__bfloat162float(wr[m])), s);
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(256) relu_fixup_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows,
+    int M, int V, const unsigned long long* __restrict__ list, const unsigned int* __restrict__ count,
+    unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
   const unsigned int n = min(*count, cap);
   const int lane = threadIdx.x % 32;
-  for (unsigned int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n;
-       i += gridDim.x * blockDim.x / 32) {
-    const unsigned long long e = list[i];
-    const uint32_t seg = static_cast<uint32_t>(e >> 44);
-    const uint32_t row = static_cast<uint32_t>((e >> 24) & 0xFFFFF);
-    const uint32_t col = static_cast<uint32_t>(e & 0xFFFFFF);
-    const uint32_t g = seg % G;
-    const __nv_bfloat16* xr = x + (static_cast<size_t>(seg) * seg_rows + row) * M;
-    const __nv_bfloat16* wr = w1t + (static_cast<size_t>(g) * V + col) * M;
-    double s = 0.0;
-    if ((M & 7) == 0) {
-      // 16-byte loads: 8 bf16 of x and of W1^T per lane per step
-      const uint4* xv = reinterpret_cast<const uint4*>(xr);
-      const uint4* wv = reinterpret_cast<const uint4*>(wr);
-      for (int v = lane; v < M / 8; v += 32) {
-        const uint4 a = __ldg(xv + v), w = __ldg(wv + v);
-        const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&w);
+  const unsigned int nw = gridDim.x * blockDim.x / 32;
+  for (unsigned int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n; i += 2 * nw) {
+    const bool two = i + nw < n;
+    const unsigned long long e[2] = {list[i], two ? list[i + nw] : list[i]};
+    size_t r[2];
+    uint32_t col[2];
+    double s[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 af = __bfloat1622float2(ah[q]), wf = __bfloat1622float2(wh[q]);
-          s = fma(static_cast<double>(af.x), static_cast<double>(wf.x), s);
-          s = fma(static_cast<double>(af.y), static_cast<double>(wf.y), s);
-        }
-      }
-    } else {
-      for (int m = lane; m < M; m += 32)
-        s = fma(static_cast<double>(__bfloat162float(xr[m])), static_cast<double>(__bfloat162float(wr[m])), s);
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t seg = static_cast<uint32_t>(e[j] >> 44);
+      const uint32_t row = static_cast<uint32_t>((e[j] >> 24) & 0xFFFFF);
+      col[j] = static_cast<uint32_t>(e[j] & 0xFFFFFF);
+      r[j] = static_cast<size_t>(seg) * seg_rows + row;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      const size_t r = static_cast<size_t>(seg) * seg_rows + row;
-      act[r * V + col] = __double2bfloat16(s > 0.0 ? s : 0.0);
+    for (int j = 0; j < 2; ++j)
+      s[j] = fixup_dot(x + r[j] * M, w1t + (static_cast<size_t>(static_cast<uint32_t>(e[j] >> 44) % G) * V + col[j]) * M,
+                       M, lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);
+      s[1] += __shfl_xor_sync(0xffffffffu, s[1], o);
+    }
+    if (lane < (two ? 2 : 1)) {
+      const int j = lane;
+      act[r[j] * V + col[j]] = __double2bfloat16(s[j] > 0.0 ? s[j] : 0.0);
       if (relu_mask) {
-        unsigned long long* w = relu_mask + r * (V / 64) + col / 64;
-        const unsigned long long bit = 1ull << (col % 64);
-        if (s > 0.0) atomicOr(w, bit);
+        unsigned long long* w = relu_mask + r[j] * (V / 64) + col[j] / 64;
+        const unsigned long long bit = 1ull << (col[j] % 64);
+        if (s[j] > 0.0) atomicOr(w, bit);
         else atomicAnd(w, ~bit);
       }
     }
@@ -209,7 +224,7 @@ int wait_flags_device(const FlagWait& w, cudaStream_t st) {
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
                       void* act, unsigned long long* relu_mask, cudaStream_t st) {
-  relu_fixup_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+  relu_fixup_kernel<<<148 * 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
                                              static_cast<const __nv_bfloat16*>(w1t), G, seg_rows,
                                              M, V, list, count, cap,
                                              static_cast<__nv_bfloat16*>(act), relu_mask);

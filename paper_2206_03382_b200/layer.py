@@ -70,6 +70,7 @@ class StepMetricsPy:
     comm_bytes: float
     drop_count: int
     relu_fixups: int = 0
+    fused: int = 0  # MOE_FUSED_DECODE (1) | MOE_FUSED_COMBINE (2)
 
 
 @dataclass
@@ -194,7 +195,7 @@ class LayerState:
         m = StepMetrics()
         check(lib().moe_get_metrics(self._h, C.byref(m)), self._h)
         return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
-                             m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups)
+                             m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups, m.fused)
 
     def grad_slices(self):
         """reduce_scatter_grads_p1: this rank's slice of every expert's dW1 / dW2 (fp32 device),
@@ -284,3 +285,21 @@ def forward_host(state: LayerState, x_host: torch.Tensor, y_host: torch.Tensor) 
 def backward_host(state: LayerState, dy_host: torch.Tensor, dx_host: torch.Tensor) -> None:
     check(lib().moe_backward_host(state.handle, _ptr(dy_host), _ptr(dx_host),
                                   _stream(state.device)), state.handle)
+
+
+def forward_host_async(state: LayerState, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+    """Pipelined forward on pinned host buffers: returns after enqueueing; the upload / download
+    overlap neighbouring steps. y_host is valid after host_sync(state)."""
+    state._step += 1
+    check(lib().moe_forward_host_async(state.handle, _ptr(x_host), _ptr(y_host),
+                                       _stream(state.device)), state.handle)
+
+
+def backward_host_async(state: LayerState, dy_host: torch.Tensor, dx_host: torch.Tensor) -> None:
+    check(lib().moe_backward_host_async(state.handle, _ptr(dy_host), _ptr(dx_host),
+                                        _stream(state.device)), state.handle)
+
+
+def host_sync(state: LayerState) -> None:
+    """Wait for every download enqueued by the *_host_async calls."""
+    check(lib().moe_host_sync(state.handle), state.handle)

@@ -171,3 +171,25 @@ def test_fused_decode_matches_unfused(cuda, monkeypatch):
     # y: one bf16 rounding (g * acc) vs two (acc, then g * out): within a couple of bf16 ulps
     assert oracle.max_rel_diff(outs["1"][0].double().cpu().numpy(),
                                outs["0"][0].double().cpu().numpy()) < 1e-2
+
+
+def test_host_async_pipeline_matches_device_calls(cuda):
+    """moe_forward_host_async / moe_backward_host_async (pipelined uploads / downloads, double-
+    buffered staging) return exactly what the device-pointer calls return, step after step."""
+    from paper_2206_03382_b200 import layer as L
+    E, M, V, T = 8, 256, 512, 1024
+    cfg = MoELayerConfig(global_experts=E, model_dim=M, hidden_dim=V, tokens_per_step=T, top_k=1)
+    st = LayerState.init(cfg, 21)
+    xs = [(torch.rand(T, M) * 2 - 1).to(torch.bfloat16).pin_memory() for _ in range(3)]
+    dys = [(torch.rand(T, M) * 2 - 1).to(torch.bfloat16).pin_memory() for _ in range(3)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    dxs = [torch.empty_like(x).pin_memory() for x in xs]
+    for i in range(3):
+        L.forward_host_async(st, xs[i], ys[i])
+        L.backward_host_async(st, dys[i], dxs[i])
+    L.host_sync(st)
+    ref = LayerState.init(cfg, 21)
+    for i in range(3):
+        r = forward(ref, xs[i].cuda())
+        g = backward(ref, r.saved, dys[i].cuda())
+        assert torch.equal(r.y.cpu(), ys[i]) and torch.equal(g.dx.cpu(), dxs[i])
