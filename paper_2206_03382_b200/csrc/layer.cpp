@@ -160,6 +160,8 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
     tl_on_ = t && t[0] == '1';
   }
   {
+    const char* lf = std::getenv("MOE_LOCAL_FIRST");  // =0: chunk 0 waits for every source
+    local_first_ = !(lf && lf[0] == '0');
     const char* e = std::getenv("MOE_FUSED");  // MOE_FUSED=0: unfused single-rank path (A/B runs)
     fused_ = !(e && e[0] == '0') && W_ == 1 && k_ == 1 && cfg.dtype == MOE_DTYPE_BF16 &&
              M_ % 256 == 0 && V_ % 256 == 0;
@@ -716,27 +718,42 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       peer_push(0, z_.p, i, 0, e0, ev_a_[i]);  // ev_a_[i]: my own block of chunk i copied
       tl_mark("dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
-    for (int i = 0; i < degree_; ++i) {
-      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
-      // the peers' blocks: polled on the device by the first kernel of the chunk
-      const FlagWait fw = peer_->ready_wait(0, i, e0);
-      up.seg_base = i * W_;
-      down.seg_base = i * W_;
+    // up GEMM over sources [s0, s1) of chunk i; the range's first kernel (the certificate's row
+    // max, or a bare wait) polls the peers' ready flags when `fw` is given
+    auto up_range = [&](int i, int s0, int s1, const FlagWait* fw, bool reset) {
+      if (s1 <= s0) return;
+      GemmArgs u = up;
+      u.seg_base = static_cast<uint32_t>(i * W_ + s0);
+      u.S = static_cast<uint32_t>(s1 - s0);
       if (cert) {
-        const size_t r0 = static_cast<size_t>(i) * W_ * dE_ * cc_;
+        const size_t r0 = static_cast<size_t>(i * W_ + s0) * dE_ * cc_;
         ckr(rowmax_device(static_cast<char*>(recv) + r0 * M_ * esz_,
-                          static_cast<int64_t>(W_) * dE_ * cc_, M_,
-                          static_cast<float*>(rowmax_.p) + r0, st, &fw,
-                          static_cast<unsigned int*>(fix_count_.p)),
+                          static_cast<int64_t>(s1 - s0) * dE_ * cc_, M_,
+                          static_cast<float*>(rowmax_.p) + r0, st, fw,
+                          reset ? static_cast<unsigned int*>(fix_count_.p) : nullptr),
             "rowmax");
-      } else {
-        ckr(wait_flags_device(fw, st), "wait");
+        ++launches_;
+      } else if (fw) {
+        ckr(wait_flags_device(*fw, st), "wait");
+        ++launches_;
       }
-      ++launches_;
-      tl_mark("dispatch landed " + std::to_string(i), st);
+      if (fw) tl_mark("dispatch landed " + std::to_string(i), st);
       prof_mark(kPhUp, true, st);
-      gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
+      gemm(kGemmUp, recv, w1_.p, act_.p, u, nseg, st);
       prof_mark(kPhUp, false, st);
+    };
+    for (int i = 0; i < degree_; ++i) {
+      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");  // my own block of chunk i is in place
+      const FlagWait fw = peer_->ready_wait(0, i, e0);
+      down.seg_base = i * W_;
+      if (i == 0 && local_first_) {
+        // this rank's own source segment first: it hides the first chunk's NVLink transfer
+        up_range(0, rank_, rank_ + 1, nullptr, true);
+        up_range(0, 0, rank_, &fw, false);
+        up_range(0, rank_ + 1, W_, rank_ > 0 ? nullptr : &fw, false);
+      } else {
+        up_range(i, 0, W_, &fw, true);
+      }
       fixup(recv);
       prof_mark(kPhDown, true, st);
       if (fused_combine_) {
@@ -941,14 +958,29 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     }
     for (int i = 0; i < degree_; ++i) {
       ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
-      ckr(wait_flags_device(peer_->ready_wait(2, i, e2), st), "wait");
-      ++launches_;
-      tl_mark("bwd dispatch landed " + std::to_string(i), st);
-      dgm.seg_base = i * W_;
+      const FlagWait fw = peer_->ready_wait(2, i, e2);
       dg.seg_base = i * W_;
-      prof_mark(kPhDgradMask, true, st);
-      gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
-      prof_mark(kPhDgradMask, false, st);
+      auto dgm_range = [&](int s0, int s1, bool wait) {
+        if (s1 <= s0) return;
+        if (wait) {
+          ckr(wait_flags_device(fw, st), "wait");
+          ++launches_;
+          tl_mark("bwd dispatch landed " + std::to_string(i), st);
+        }
+        GemmArgs a = dgm;
+        a.seg_base = static_cast<uint32_t>(i * W_ + s0);
+        a.S = static_cast<uint32_t>(s1 - s0);
+        prof_mark(kPhDgradMask, true, st);
+        gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, a, nseg, st);
+        prof_mark(kPhDgradMask, false, st);
+      };
+      if (i == 0 && local_first_) {
+        dgm_range(rank_, rank_ + 1, false);
+        dgm_range(0, rank_, true);
+        dgm_range(rank_ + 1, W_, rank_ == 0);
+      } else {
+        dgm_range(0, W_, true);
+      }
       prof_mark(kPhDgrad, true, st);
       if (fused_combine_) {
         // backward combine fused into the dgrad GEMM (dx blocks straight to the source ranks)

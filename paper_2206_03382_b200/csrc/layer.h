@@ -155,6 +155,7 @@ class Layer {
   // W > 1 peer backend: combine (fwd) / dx combine (bwd) fused into the down / dgrad GEMM
   // epilogues, which store straight into the source ranks' buffers over NVLink.
   bool fused_combine_ = false;
+  bool local_first_ = true;  // W > 1: chunk 0 computes this rank's own source segment first
   GemmArgs peer_args(const GemmArgs& a, int ch) const;
 
   struct ProfRec {
