@@ -88,12 +88,34 @@ __device__ __forceinline__ float from_f<float>(float v) {
   return v;
 }
 
+// Zero the rows of fully dropped tokens (one thread checks one token, the warp writes its
+// dropped tokens' rows together). Warp-uniform loop: every lane takes part in the ballot.
+__device__ __forceinline__ void zero_dropped_rows(const DropZero& d) {
+  if (d.out == nullptr) return;
+  const int lane = threadIdx.x % 32;
+  const int vecs = static_cast<int>(d.row_bytes / 16);
+  for (int base = blockIdx.x * blockDim.x + threadIdx.x - lane; base < d.T;
+       base += gridDim.x * blockDim.x) {
+    const int t = base + lane;
+    bool dropped = t < d.T;
+    for (int j = 0; j < d.k && dropped; ++j) dropped = __ldg(d.locations + static_cast<size_t>(t) * d.k + j) < 0;
+    unsigned m = __ballot_sync(0xffffffffu, dropped);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      uint4* r = static_cast<uint4*>(d.out) + static_cast<size_t>(base + src) * vecs;
+      for (int v = lane; v < vecs; v += 32) r[v] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ encode
 // Z[row] = x[slot_token[row]] or 0. Rows enumerate [block][chunk][expert][cc].
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_kernel(SlotGeom g, const T* __restrict__ x, const int32_t* __restrict__ slot_token,
-                  T* __restrict__ z, float* __restrict__ rowmax) {
+                  T* __restrict__ z, float* __restrict__ rowmax, DropZero dzero) {
+  zero_dropped_rows(dzero);
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
@@ -227,7 +249,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     decode_bwd_kernel(SlotGeom g, const T* __restrict__ dy, const int32_t* __restrict__ slot_token,
-                      const float* __restrict__ slot_gate, T* __restrict__ dz) {
+                      const float* __restrict__ slot_gate, T* __restrict__ dz, DropZero dzero) {
+  zero_dropped_rows(dzero);
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
@@ -384,17 +407,18 @@ bool vec_ok(int dtype, int M) { return (M * (dtype == 1 ? 4 : 2)) % 16 == 0; }
 }  // namespace
 
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax) {
+                  cudaStream_t st, float* rowmax, const DropZero& dzero) {
+  if (dzero.out && dzero.row_bytes % 16 != 0) return -1;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) encode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax);
-    else encode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax);
+    if (v) encode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero);
+    else encode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero);
   } else {
     using B = __nv_bfloat16;
-    if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax);
-    else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax);
+    if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero);
+    else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero);
   }
   return launch_status();
 }
@@ -416,17 +440,18 @@ int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* id
 
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
                            const int32_t* slot_token, const float* slot_gate, void* dz,
-                           cudaStream_t st) {
+                           cudaStream_t st, const DropZero& dzero) {
+  if (dzero.out && dzero.row_bytes % 16 != 0) return -1;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) decode_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz));
-    else decode_bwd_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz));
+    if (v) decode_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
+    else decode_bwd_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
   } else {
     using B = __nv_bfloat16;
-    if (v) decode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz));
-    else decode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz));
+    if (v) decode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
+    else decode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
   }
   return launch_status();
 }
@@ -454,35 +479,6 @@ int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const i
     if (v) encode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
     else encode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
   }
-  return launch_status();
-}
-
-namespace {
-// Rows of tokens with no surviving assignment (all k locations < 0) are zeroed: the fused
-// single-rank path scatters expert outputs straight to token rows and never visits them.
-__global__ void zero_dropped_kernel(int T, int k, const int32_t* __restrict__ locations, int row_vecs,
-                                    uint4* __restrict__ out) {
-  // one thread checks one token; the warp then zeroes its dropped tokens' rows together
-  const int lane = threadIdx.x % 32;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  bool dropped = t < T;
-  for (int j = 0; j < k && dropped; ++j) dropped = __ldg(locations + static_cast<size_t>(t) * k + j) < 0;
-  unsigned m = __ballot_sync(0xffffffffu, dropped);
-  while (m) {
-    const int src = __ffs(m) - 1;
-    m &= m - 1;
-    uint4* r = out + static_cast<size_t>(t - lane + src) * row_vecs;
-    for (int v = lane; v < row_vecs; v += 32) r[v] = make_uint4(0u, 0u, 0u, 0u);
-  }
-}
-}  // namespace
-
-int zero_dropped_device(int T, int k, const int32_t* locations, size_t row_bytes, void* out,
-                        cudaStream_t st) {
-  if (row_bytes % 16 != 0) return -1;
-  zero_dropped_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, k, locations,
-                                                        static_cast<int>(row_bytes / 16),
-                                                        static_cast<uint4*>(out));
   return launch_status();
 }
 

@@ -25,7 +25,19 @@ namespace moe {
 
 namespace {
 
-constexpr int kGateWarps = 8;
+#ifndef MOE_GATE_WARPS
+#define MOE_GATE_WARPS 8  // token block of the gate / assign partition = 8 tokens per warp
+#endif
+// DMMA gate CTA: MOE_DM_WARPS warps x MOE_DM_MT 8-token m-tiles = the 64-token block. Measured
+// at TGT: 8 warps x 1 m-tile 113 us, 4 x 2 123 us, 32-token blocks (2 x 2 / 4 x 1) 122-148 us,
+// K split over two warp groups 120 us -- warps in flight beat operand reuse here.
+#ifndef MOE_DM_WARPS
+#define MOE_DM_WARPS 8
+#endif
+#ifndef MOE_DM_MT
+#define MOE_DM_MT 1
+#endif
+constexpr int kGateWarps = MOE_GATE_WARPS;
 constexpr int kGateTokPerWarp = 8;
 constexpr int kGateTok = kGateWarps * kGateTokPerWarp;  // 64 tokens per CTA
 
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(kGateWarps * 32)
 // accumulation order differs from the reference's Eigen GEMM (ulp-level, below any routing tie).
 // Fragment layout (m8n8k4 .f64): A[r][c] with r = lane/4, c = lane%4; B[r][c] with r = lane%4,
 // c = lane/4; D[r][2*(lane%4) + i] with r = lane/4.
-constexpr int kDmWarps = 4, kDmMT = 2, kDmTok = kDmWarps * kDmMT * 8, kDmKC = 16;
+constexpr int kDmWarps = MOE_DM_WARPS, kDmMT = MOE_DM_MT, kDmTok = kDmWarps * kDmMT * 8, kDmKC = 16;
 static_assert(kDmTok == kGateTok, "gate kernels must share the token-block partition of assign");
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -480,7 +492,6 @@ __global__ void __launch_bounds__(kDmWarps * 32)
         for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
     }
   }
-
   // softmax + top-k: the 4 lanes of a quad (same lane/4) hold one token's 8*NT logits.
 #pragma unroll
   for (int i = 0; i < kDmMT; ++i) {

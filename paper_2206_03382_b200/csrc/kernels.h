@@ -61,21 +61,28 @@ struct SlotGeom {
   int blocks, T, E, M, k, cap, cc, degree;
 };
 
+// Optional side task of the slot-major gathers: zero the [T][row_bytes] rows of tokens whose k
+// assignments were all dropped (the fused decode / encode-backward path never writes them).
+struct DropZero {
+  const int32_t* locations = nullptr;  // [T][k]
+  int T = 0, k = 0;
+  void* out = nullptr;                 // [T] rows of row_bytes (multiple of 16)
+  size_t row_bytes = 0;
+};
+
 // dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rowmax (optional, [z rows]):
 // max_m |z[row][m]| for the ReLU-mask certificate.
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax = nullptr);
+                  cudaStream_t st, float* rowmax = nullptr, const DropZero& dzero = DropZero{});
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
                   const int32_t* locations, const double* gates, void* y, cudaStream_t st);
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
                            const int32_t* slot_token, const float* slot_gate, void* dz,
-                           cudaStream_t st);
+                           cudaStream_t st, const DropZero& dzero = DropZero{});
 // Optional d_gates[t, j] = <Z[e, loc], dy[t]> (dispatch.cpp:143-156); 0 for dropped.
 int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
                                  const int32_t* idxs, const int32_t* locations, double* dgates,
                                  cudaStream_t st);
-int zero_dropped_device(int T, int k, const int32_t* locations, size_t row_bytes, void* out,
-                        cudaStream_t st);
 int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
                            const int32_t* locations, void* dx, cudaStream_t st);
 

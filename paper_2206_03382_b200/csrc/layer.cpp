@@ -634,9 +634,17 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     stats_dirty_ = false;
   }
   const SlotGeom g = geom();
+  DropZero yzero;  // fused decode: the encode pass also zeroes the dropped tokens' y rows
+  if (fused_) {
+    yzero.locations = gb.locations;
+    yzero.T = T_;
+    yzero.k = k_;
+    yzero.out = y;
+    yzero.row_bytes = static_cast<size_t>(M_) * esz_;
+  }
   prof_mark(kPhEncode, true, st);
   ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st,
-                    (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr),
+                    (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr, yzero),
       "encode");
   prof_mark(kPhEncode, false, st);
   ++launches_;
@@ -680,10 +688,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
     prof_mark(kPhUp, false, st);
     fixup(recv);
-    prof_mark(kPhDecode, true, st);
-    ckr(zero_dropped_device(T_, k_, gb.locations, static_cast<size_t>(M_) * esz_, y, st), "zero rows");
-    prof_mark(kPhDecode, false, st);
-    ++launches_;
     prof_mark(kPhDown, true, st);
     gemm(kGemmDown, act_.p, w2_.p, y, down, nseg, st);
     prof_mark(kPhDown, false, st);
@@ -877,8 +881,17 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   const int64_t l0 = launches_;
 
   // dZ = decode^T(dy): slot-major gather of g * dy (fast_decode_backward_range)
+  DropZero dxzero;  // fused encode-backward: this pass also zeroes the dropped tokens' dx rows
+  if (fused_) {
+    dxzero.locations = gb.locations;
+    dxzero.T = T_;
+    dxzero.k = k_;
+    dxzero.out = dx;
+    dxzero.row_bytes = static_cast<size_t>(M_) * esz_;
+  }
   prof_mark(kPhDecodeBwd, true, st);
-  ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st), "decode_bwd");
+  ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st, dxzero),
+      "decode_bwd");
   prof_mark(kPhDecodeBwd, false, st);
   ++launches_;
 
@@ -919,10 +932,6 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     prof_mark(kPhDgradMask, true, st);
     gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, dgm, nseg, st);
     prof_mark(kPhDgradMask, false, st);
-    prof_mark(kPhEncodeBwd, true, st);
-    ckr(zero_dropped_device(T_, k_, gb.locations, static_cast<size_t>(M_) * esz_, dx, st), "zero rows");
-    prof_mark(kPhEncodeBwd, false, st);
-    ++launches_;
     prof_mark(kPhDgrad, true, st);
     gemm(kGemmDgrad, dh_.p, w1_.p, dx, dg, nseg, st);
     prof_mark(kPhDgrad, false, st);
