@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "pdl.cuh"
 
 namespace moe {
 
@@ -114,7 +115,10 @@ __device__ __forceinline__ void zero_dropped_rows(const DropZero& d) {
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_kernel(SlotGeom g, const T* __restrict__ x, const int32_t* __restrict__ slot_token,
-                  T* __restrict__ z, float* __restrict__ rowmax, DropZero dzero) {
+                  T* __restrict__ z, float* __restrict__ rowmax, DropZero dzero,
+                  unsigned int* __restrict__ reset) {
+  pdl_entry();
+  if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0u;
   zero_dropped_rows(dzero);
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
@@ -187,6 +191,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     decode_kernel(SlotGeom g, const T* __restrict__ z, const int32_t* __restrict__ idxs,
                   const int32_t* __restrict__ locations, const double* __restrict__ gates,
                   T* __restrict__ y) {
+  pdl_entry();
   const int lane = threadIdx.x % 32;
   const int ntok = g.blocks * g.T;
   for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
@@ -250,6 +255,7 @@ template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     decode_bwd_kernel(SlotGeom g, const T* __restrict__ dy, const int32_t* __restrict__ slot_token,
                       const float* __restrict__ slot_gate, T* __restrict__ dz, DropZero dzero) {
+  pdl_entry();
   zero_dropped_rows(dzero);
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
@@ -310,6 +316,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     decode_bwd_gates_kernel(SlotGeom g, const T* __restrict__ z, const T* __restrict__ dy,
                             const int32_t* __restrict__ idxs, const int32_t* __restrict__ locations,
                             double* __restrict__ dgates) {
+  pdl_entry();
   const int lane = threadIdx.x % 32;
   const int n = g.blocks * g.T * g.k;
   for (int f = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; f < n; f += gridDim.x * kWarpsPerCta) {
@@ -334,6 +341,7 @@ template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_bwd_kernel(SlotGeom g, const T* __restrict__ dz, const int32_t* __restrict__ idxs,
                       const int32_t* __restrict__ locations, T* __restrict__ dx) {
+  pdl_entry();
   const int lane = threadIdx.x % 32;
   const int ntok = g.blocks * g.T;
   for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
@@ -407,18 +415,18 @@ bool vec_ok(int dtype, int M) { return (M * (dtype == 1 ? 4 : 2)) % 16 == 0; }
 }  // namespace
 
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax, const DropZero& dzero) {
+                  cudaStream_t st, float* rowmax, const DropZero& dzero, unsigned int* reset) {
   if (dzero.out && dzero.row_bytes % 16 != 0) return -1;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) encode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero);
-    else encode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero);
+    if (v) launch_k(encode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset);
+    else launch_k(encode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset);
   } else {
     using B = __nv_bfloat16;
-    if (v) encode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero);
-    else encode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero);
+    if (v) launch_k(encode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset);
+    else launch_k(encode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset);
   }
   return launch_status();
 }
@@ -428,12 +436,12 @@ int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* id
   const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) decode_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
-    else decode_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
+    if (v) launch_k(decode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
+    else launch_k(decode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
   } else {
     using B = __nv_bfloat16;
-    if (v) decode_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
-    else decode_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
+    if (v) launch_k(decode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
+    else launch_k(decode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
   }
   return launch_status();
 }
@@ -446,12 +454,12 @@ int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) decode_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
-    else decode_bwd_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
+    if (v) launch_k(decode_bwd_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
+    else launch_k(decode_bwd_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
   } else {
     using B = __nv_bfloat16;
-    if (v) decode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
-    else decode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
+    if (v) launch_k(decode_bwd_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
+    else launch_k(decode_bwd_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
   }
   return launch_status();
 }
@@ -461,9 +469,9 @@ int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, co
                                  cudaStream_t st) {
   const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T * g.k);
   if (dtype == 1)
-    decode_bwd_gates_kernel<float><<<grid, 256, 0, st>>>(g, static_cast<const float*>(z), static_cast<const float*>(dy), idxs, locations, dgates);
+    launch_k(decode_bwd_gates_kernel<float>, grid, 256, 0, st, g, static_cast<const float*>(z), static_cast<const float*>(dy), idxs, locations, dgates);
   else
-    decode_bwd_gates_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(g, static_cast<const __nv_bfloat16*>(z), static_cast<const __nv_bfloat16*>(dy), idxs, locations, dgates);
+    launch_k(decode_bwd_gates_kernel<__nv_bfloat16>, grid, 256, 0, st, g, static_cast<const __nv_bfloat16*>(z), static_cast<const __nv_bfloat16*>(dy), idxs, locations, dgates);
   return launch_status();
 }
 
@@ -472,12 +480,12 @@ int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const i
   const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) encode_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
-    else encode_bwd_kernel<float, false><<<grid, 256, 0, st>>>(g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
+    if (v) launch_k(encode_bwd_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
+    else launch_k(encode_bwd_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
   } else {
     using B = __nv_bfloat16;
-    if (v) encode_bwd_kernel<B, true><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
-    else encode_bwd_kernel<B, false><<<grid, 256, 0, st>>>(g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
+    if (v) launch_k(encode_bwd_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
+    else launch_k(encode_bwd_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
   }
   return launch_status();
 }
@@ -488,6 +496,7 @@ __global__ void build_slots_kernel(int n, int T, int k, int E, int cap,
                                    const int32_t* __restrict__ locations,
                                    const double* __restrict__ gates, int32_t* __restrict__ slot_token,
                                    float* __restrict__ slot_gate) {
+  pdl_entry();
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
     const int loc = locations[f];
     if (loc < 0) continue;
@@ -508,7 +517,7 @@ int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* 
   if (cudaMemsetAsync(slot_gate, 0, ns * sizeof(float), st) != cudaSuccess) return -2;
   const int n = blocks * T * k;
   const int grid = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
-  build_slots_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(n, T, k, E, cap, idxs, locations, gates,
+  launch_k(build_slots_kernel, grid > 0 ? grid : 1, 256, 0, st, n, T, k, E, cap, idxs, locations, gates,
                                                          slot_token, slot_gate);
   return launch_status();
 }

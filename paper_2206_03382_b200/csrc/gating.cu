@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "pdl.cuh"
 
 namespace moe {
 
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(kGateWarps * 32)
                      int k, int cta_per_block, int32_t* __restrict__ idxs,
                      double* __restrict__ gates, int32_t* __restrict__ hist,
                      double* __restrict__ probs_out) {
+  pdl_entry();
   constexpr int KC = 16 / EPL;  // k-chunk staged through smem (2 x 24 KiB static smem at EPL=1)
   constexpr int NT = kGateWarps * 32;
   constexpr int XPT = (kGateTok * KC + NT - 1) / NT;  // x elements per thread per chunk
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(kDmWarps * 32)
                      int k, int cta_per_block, int32_t* __restrict__ idxs,
                      double* __restrict__ gates, int32_t* __restrict__ hist,
                      double* __restrict__ probs_out) {
+  pdl_entry();
   constexpr int NTH = kDmWarps * 32;
   constexpr int XS = kDmKC + 4;       // x row stride (doubles): conflict-free A fragments
   constexpr int EP = 8 * NT + 4;      // Wg row stride: conflict-free B fragments
@@ -425,6 +428,7 @@ __global__ void __launch_bounds__(kDmWarps * 32)
                       int k, int cta_per_block, int32_t* __restrict__ idxs,
                       double* __restrict__ gates, int32_t* __restrict__ hist,
                       double* __restrict__ probs_out) {
+  pdl_entry();
   using Cf = D2Cfg<TX, NT>;
   constexpr int NTH = kDmWarps * 32;
   constexpr int XCH = kD2KC * sizeof(TX) / 16;  // 16-byte chunks per token row
@@ -565,6 +569,7 @@ __global__ void __launch_bounds__(kDmWarps * 32)
 __global__ void __launch_bounds__(256)
     scan_cols_kernel(const int32_t* __restrict__ hist, int cta_per_block, int E,
                      int32_t* __restrict__ offs, int32_t* __restrict__ demand) {
+  pdl_entry();
   __shared__ int32_t wsum[8];
   const int p = blockIdx.x, b = p / E, e = p % E;
   const int per = (cta_per_block + blockDim.x - 1) / blockDim.x;
@@ -603,7 +608,10 @@ __global__ void __launch_bounds__(256)
 __global__ void finalize_capacity_kernel(int blocks, int E, int T, int k, int cap_kind,
                                          int cap_formula, const int32_t* __restrict__ demand,
                                          int32_t* __restrict__ list_base,
-                                         int32_t* __restrict__ fill, int32_t* __restrict__ cap_out) {
+                                         int32_t* __restrict__ fill, int32_t* __restrict__ cap_out,
+                                         int32_t* __restrict__ drops) {
+  pdl_entry();
+  if (threadIdx.x == 0) *drops = 0;  // the assign pass accumulates this step's drops
   __shared__ int32_t cap_sh;
   __shared__ int32_t mx_sh;
   if (threadIdx.x == 0) mx_sh = 1;  // max demand floors at 1
@@ -638,7 +646,8 @@ __global__ void __launch_bounds__(256)
                   const int32_t* __restrict__ list_base, const int32_t* __restrict__ cap_ptr,
                   int bpr, int32_t* __restrict__ locations, int32_t* __restrict__ slot_token,
                   float* __restrict__ slot_gate, int32_t* __restrict__ list,
-                  int32_t* __restrict__ drops) {
+                  int32_t* __restrict__ drops, const int32_t* __restrict__ demand) {
+  pdl_entry();
   extern __shared__ int32_t sh[];  // cnt[E] + wcnt[8][E]
   int32_t* cnt = sh;
   int32_t* wcnt = sh + E;
@@ -649,6 +658,18 @@ __global__ void __launch_bounds__(256)
   const int f_begin = t_begin * k, f_end = t_end * k;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int cap = *cap_ptr;
+  if (c == 0) {
+    // slots [min(demand, cap), cap) of this block's experts stay empty (FIFO and BPR both fill
+    // 0 .. min(demand, cap) - 1): token -1, gate 0 -- encode zero-fills those rows
+    for (int e = 0; e < E; ++e) {
+      const int d0 = min(demand[static_cast<size_t>(b) * E + e], cap);
+      for (int s = d0 + threadIdx.x; s < cap; s += blockDim.x) {
+        const size_t slot = static_cast<size_t>(b * E + e) * cap + s;
+        slot_token[slot] = -1;
+        slot_gate[slot] = 0.0f;
+      }
+    }
+  }
   for (int e = threadIdx.x; e < E; e += blockDim.x)
     cnt[e] = offs[static_cast<size_t>(blockIdx.x) * E + e];
   int my_drops = 0;
@@ -698,6 +719,7 @@ __global__ void __launch_bounds__(256)
                     const int32_t* __restrict__ list, const int32_t* __restrict__ cap_ptr,
                     int32_t* __restrict__ locations, int32_t* __restrict__ slot_token,
                     float* __restrict__ slot_gate, int32_t* __restrict__ drops) {
+  pdl_entry();
   constexpr int kTile = 1024;
   __shared__ double keys[kTile];
   const int be = blockIdx.x;
@@ -755,7 +777,7 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
         cudaFuncSetAttribute(gate_dmma2_kernel<TX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
         set = true;
       }
-      gate_dmma2_kernel<TX, 4><<<grid, kDmWarps * 32, Cf::SMEM, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+      launch_k(gate_dmma2_kernel<TX, 4>, grid, kDmWarps * 32, Cf::SMEM, st, xp, wg, T, M, E, k, cpb, idxs,
                                                                      gates, hist, probs);
     } else {
       using Cf = D2Cfg<TX, 8>;
@@ -764,7 +786,7 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
         cudaFuncSetAttribute(gate_dmma2_kernel<TX, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
         set = true;
       }
-      gate_dmma2_kernel<TX, 8><<<grid, kDmWarps * 32, Cf::SMEM, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+      launch_k(gate_dmma2_kernel<TX, 8>, grid, kDmWarps * 32, Cf::SMEM, st, xp, wg, T, M, E, k, cpb, idxs,
                                                                      gates, hist, probs);
     }
     return launch_status();
@@ -773,10 +795,10 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
     const int cpb = (T + kDmTok - 1) / kDmTok;
     const dim3 grid(blocks * cpb);
     if (E <= 32)
-      gate_dmma_kernel<TX, 4><<<grid, kDmWarps * 32, 0, st>>>(xp, wg, T, M, E, k, cpb, idxs, gates,
+      launch_k(gate_dmma_kernel<TX, 4>, grid, kDmWarps * 32, 0, st, xp, wg, T, M, E, k, cpb, idxs, gates,
                                                               hist, probs);
     else
-      gate_dmma_kernel<TX, 8><<<grid, kDmWarps * 32, 0, st>>>(xp, wg, T, M, E, k, cpb, idxs, gates,
+      launch_k(gate_dmma_kernel<TX, 8>, grid, kDmWarps * 32, 0, st, xp, wg, T, M, E, k, cpb, idxs, gates,
                                                               hist, probs);
     return launch_status();
   }
@@ -784,16 +806,16 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
   const dim3 grid(blocks * cpb);
   const size_t sh = static_cast<size_t>(E) * sizeof(int32_t);
   if (E <= 32)
-    gate_topk_kernel<TX, 1><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+    launch_k(gate_topk_kernel<TX, 1>, grid, kGateWarps * 32, sh, st, xp, wg, T, M, E, k, cpb, idxs,
                                                                 gates, hist, probs);
   else if (E <= 64)
-    gate_topk_kernel<TX, 2><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+    launch_k(gate_topk_kernel<TX, 2>, grid, kGateWarps * 32, sh, st, xp, wg, T, M, E, k, cpb, idxs,
                                                                 gates, hist, probs);
   else if (E <= 128)
-    gate_topk_kernel<TX, 4><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+    launch_k(gate_topk_kernel<TX, 4>, grid, kGateWarps * 32, sh, st, xp, wg, T, M, E, k, cpb, idxs,
                                                                 gates, hist, probs);
   else if (E <= 256)
-    gate_topk_kernel<TX, 8><<<grid, kGateWarps * 32, sh, st>>>(xp, wg, T, M, E, k, cpb, idxs,
+    launch_k(gate_topk_kernel<TX, 8>, grid, kGateWarps * 32, sh, st, xp, wg, T, M, E, k, cpb, idxs,
                                                                 gates, hist, probs);
   else
     return -1;
@@ -803,6 +825,7 @@ int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E
 // resolve_capacity (core.cpp:47-59) from an (all-reduced) demand vector.
 __global__ void resolve_capacity_kernel(const int32_t* __restrict__ demand, int E, int cap_kind,
                                         int cap_formula, int32_t* __restrict__ cap_out) {
+  pdl_entry();
   __shared__ int32_t mx;
   if (threadIdx.x == 0) mx = 1;
   __syncthreads();
@@ -820,7 +843,7 @@ __global__ void resolve_capacity_kernel(const int32_t* __restrict__ demand, int 
 
 int resolve_capacity_device(const int32_t* demand, int E, int cap_kind, int cap_formula,
                             int32_t* cap_out, cudaStream_t st) {
-  resolve_capacity_kernel<<<1, 256, 0, st>>>(demand, E, cap_kind, cap_formula, cap_out);
+  launch_k(resolve_capacity_kernel, 1, 256, 0, st, demand, E, cap_kind, cap_formula, cap_out);
   return launch_status();
 }
 
@@ -835,10 +858,10 @@ int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t 
                                                    g.idxs, g.gates, g.hist, g.probs, st);
   if (rc) return rc;
   if (cpb > 16 * 256) return -1;
-  scan_cols_kernel<<<a.blocks * a.E, 256, 0, st>>>(g.hist, cpb, a.E, g.offs, g.demand);
+  launch_k(scan_cols_kernel, a.blocks * a.E, 256, 0, st, g.hist, cpb, a.E, g.offs, g.demand);
   if (launch_status() != 0) return -2;
-  finalize_capacity_kernel<<<1, 256, 0, st>>>(a.blocks, a.E, a.T, a.k, a.cap_kind, a.cap_formula,
-                                             g.demand, g.list_base, g.fill, g.cap);
+  launch_k(finalize_capacity_kernel, 1, 256, 0, st, a.blocks, a.E, a.T, a.k, a.cap_kind, a.cap_formula,
+                                             g.demand, g.list_base, g.fill, g.cap, g.drops);
   if (launch_status() != 0) return -2;
   return 0;
 }
@@ -846,23 +869,16 @@ int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t 
 int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound,
                       cudaStream_t st) {
   const int cpb = gate_cta_per_block(a.T);
-  // Slots not claimed by a token stay -1 (empty capacity rows are zero-filled by encode).
-  if (cudaMemsetAsync(g.slot_token, 0xFF,
-                      static_cast<size_t>(a.blocks) * a.E * cap_bound * sizeof(int32_t), st) !=
-      cudaSuccess)
-    return -2;
-  if (cudaMemsetAsync(g.slot_gate, 0, static_cast<size_t>(a.blocks) * a.E * cap_bound * sizeof(float),
-                      st) != cudaSuccess)
-    return -2;
-  if (cudaMemsetAsync(g.drops, 0, sizeof(int32_t), st) != cudaSuccess) return -2;
+  // Slots not claimed by a token are set to -1 by the assign pass itself (no memsets: they
+  // would break the programmatic-dependent-launch chain); empty rows are zero-filled by encode.
   const size_t sh = static_cast<size_t>(9) * a.E * sizeof(int32_t);
-  assign_kernel<<<a.blocks * cpb, 256, sh, st>>>(g.idxs, g.gates, a.T, a.k, a.E, cpb, g.offs,
+  launch_k(assign_kernel, a.blocks * cpb, 256, sh, st, g.idxs, g.gates, a.T, a.k, a.E, cpb, g.offs,
                                                  g.list_base, g.cap, a.bpr, g.locations,
-                                                 g.slot_token, g.slot_gate, g.list, g.drops);
+                                                 g.slot_token, g.slot_gate, g.list, g.drops, g.demand);
   if (launch_status() != 0) return -2;
   if (a.bpr) {
     const dim3 grid(a.blocks * a.E, (a.T + 255) / 256);
-    bpr_rank_kernel<<<grid, 256, 0, st>>>(g.gates, a.k, a.E, g.demand, g.list_base, g.list, g.cap,
+    launch_k(bpr_rank_kernel, grid, 256, 0, st, g.gates, a.k, a.E, g.demand, g.list_base, g.list, g.cap,
                                           g.locations, g.slot_token, g.slot_gate, g.drops);
     if (launch_status() != 0) return -2;
   }

@@ -22,6 +22,7 @@
 
 #include "gemm_sm100.h"
 #include "kernels.h"
+#include "pdl.cuh"
 #include "ptx.cuh"
 
 #ifndef MOE_GEMM_STAGES
@@ -175,6 +176,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous kernel's tail;
+  // operands produced by it are read only after this wait
+  pdl_entry();
 
   const uint32_t ntiles = num_tiles<kRowK, C::TM>(args);
   const uint32_t nkb = num_kblocks<kRowK>(args);
@@ -567,13 +571,15 @@ int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (cudaLaunchKernelEx(&cfg, kern, a, b, d, args, pm) != cudaSuccess) return launch_status() ? -2 : -2;
   return launch_status();
 }

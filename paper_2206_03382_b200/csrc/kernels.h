@@ -72,8 +72,10 @@ struct DropZero {
 
 // dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rowmax (optional, [z rows]):
 // max_m |z[row][m]| for the ReLU-mask certificate.
+// reset (optional): a counter zeroed by the pass (the ReLU-fixup count; no memset node).
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax = nullptr, const DropZero& dzero = DropZero{});
+                  cudaStream_t st, float* rowmax = nullptr, const DropZero& dzero = DropZero{},
+                  unsigned int* reset = nullptr);
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
                   const int32_t* locations, const double* gates, void* y, cudaStream_t st);
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,

@@ -644,7 +644,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   prof_mark(kPhEncode, true, st);
   ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st,
-                    (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr, yzero),
+                    (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr, yzero,
+                    (cert && W_ == 1) ? static_cast<unsigned int*>(fix_count_.p) : nullptr),
       "encode");
   prof_mark(kPhEncode, false, st);
   ++launches_;
@@ -683,7 +684,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     down.gather_rows = static_cast<uint32_t>(T_);
     down.row_token = gb.slot_token;
     down.row_scale = gb.slot_gate;
-    ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
     prof_mark(kPhUp, true, st);
     gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
     prof_mark(kPhUp, false, st);
@@ -694,7 +694,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   } else if (W_ == 1) {
     up.seg_base = 0;
     down.seg_base = 0;
-    if (cert) ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
     prof_mark(kPhUp, true, st);
     gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
     prof_mark(kPhUp, false, st);

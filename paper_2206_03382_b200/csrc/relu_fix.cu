@@ -13,6 +13,7 @@
 
 #include "gemm_sm100.h"
 #include "kernels.h"
+#include "pdl.cuh"
 #include "peer_flags.cuh"
 
 namespace moe {
@@ -22,6 +23,7 @@ namespace {
 // colabs[g][v] = sum_m |W1[g][m][v]|
 __global__ void colabs_kernel(const __nv_bfloat16* __restrict__ w1, int G, int M, int V,
                               float* __restrict__ colabs) {
+  pdl_entry();
   const int n = G * V;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int g = i / V, v = i % V;
@@ -35,6 +37,7 @@ __global__ void colabs_kernel(const __nv_bfloat16* __restrict__ w1, int G, int M
 // blk[g][b] = max over the 64 columns of block b of colabs[g][:]
 __global__ void colabs_blk_kernel(const float* __restrict__ colabs, int G, int V,
                                   float* __restrict__ blk) {
+  pdl_entry();
   const int nb = V / 64;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < G * nb; i += gridDim.x * blockDim.x) {
     const float* c = colabs + static_cast<size_t>(i / nb) * V + (i % nb) * 64;
@@ -47,6 +50,7 @@ __global__ void colabs_blk_kernel(const float* __restrict__ colabs, int G, int V
 // out[g][c][r] = in[g][r][c] (bf16, 32x32 smem tiles)
 __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, int R, int Cc,
                                  __nv_bfloat16* __restrict__ out) {
+  pdl_entry();
   __shared__ __nv_bfloat16 tile[32][33];
   const size_t g = blockIdx.z;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
@@ -69,6 +73,7 @@ __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, int R, in
 // so 8 columns reduce with packed integer max.
 __global__ void rowmax_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int M,
                               float* __restrict__ rowmax, FlagWait fw, unsigned int* reset) {
+  pdl_entry();
   if (fw.base != nullptr) {
     if (threadIdx.x < 32) wait_flags_warp(fw);
     __syncthreads();
@@ -98,7 +103,8 @@ __global__ void rowmax_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
   }
 }
 
-__global__ void wait_flags_kernel(FlagWait fw) { wait_flags_warp(fw); }
+__global__ void wait_flags_kernel(FlagWait fw) {
+  pdl_entry(); wait_flags_warp(fw); }
 
 // For each listed (seg, row, col): h = sum_m X[seg][row][m] * W1T[g][col][m] in fp64, then
 // act[seg][row][col] = bf16(max(h, 0)) and the ReLU bit. One warp per entry, two entries in
@@ -131,6 +137,7 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows,
     int M, int V, const unsigned long long* __restrict__ list, const unsigned int* __restrict__ count,
     unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
+  pdl_entry();
   const unsigned int n = min(*count, cap);
   const int lane = threadIdx.x % 32;
   const unsigned int nw = gridDim.x * blockDim.x / 32;
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
 // mask[r][w] bit i = act[r][64 w + i] > 0 (one thread per 64-column word)
 __global__ void mask_from_act_kernel(const __nv_bfloat16* __restrict__ act, int64_t rows, int V,
                                      unsigned long long* __restrict__ mask) {
+  pdl_entry();
   const int nw = V / 64;
   const int64_t n = rows * nw;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -189,19 +197,19 @@ int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned lon
                               cudaStream_t st) {
   const int64_t n = rows * (V / 64);
   const int grid = static_cast<int>(n / 256 + 1 < 148 * 16 ? n / 256 + 1 : 148 * 16);
-  mask_from_act_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(act), rows, V, mask);
+  launch_k(mask_from_act_kernel, grid, 256, 0, st, static_cast<const __nv_bfloat16*>(act), rows, V, mask);
   return launch_status();
 }
 
 int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, float* colabs_blk,
                         void* w1t, cudaStream_t st) {
   const int n = G * V;
-  colabs_kernel<<<(n + 255) / 256, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w1), G, M, V,
+  launch_k(colabs_kernel, (n + 255) / 256, 256, 0, st, static_cast<const __nv_bfloat16*>(w1), G, M, V,
                                                  colabs);
   if (colabs_blk && V % 64 == 0)
-    colabs_blk_kernel<<<(G * V / 64 + 255) / 256, 256, 0, st>>>(colabs, G, V, colabs_blk);
+    launch_k(colabs_blk_kernel, (G * V / 64 + 255) / 256, 256, 0, st, colabs, G, V, colabs_blk);
   dim3 grid((V + 31) / 32, (M + 31) / 32, G);
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(static_cast<const __nv_bfloat16*>(w1), M, V,
+  launch_k(transpose_kernel, grid, dim3(32, 8), 0, st, static_cast<const __nv_bfloat16*>(w1), M, V,
                                                  static_cast<__nv_bfloat16*>(w1t));
   return launch_status();
 }
@@ -211,20 +219,20 @@ int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_
   if (rows <= 0) return 0;
   const int64_t blocks = (rows + 7) / 8;
   const int grid = static_cast<int>(blocks < 148 * 4 ? blocks : 148 * 4);
-  rowmax_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, M, rowmax,
+  launch_k(rowmax_kernel, grid, 256, 0, st, static_cast<const __nv_bfloat16*>(x), rows, M, rowmax,
                                       wait ? *wait : FlagWait{}, reset);
   return launch_status();
 }
 
 int wait_flags_device(const FlagWait& w, cudaStream_t st) {
-  wait_flags_kernel<<<1, 32, 0, st>>>(w);
+  launch_k(wait_flags_kernel, 1, 32, 0, st, w);
   return launch_status();
 }
 
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
                       void* act, unsigned long long* relu_mask, cudaStream_t st) {
-  relu_fixup_kernel<<<148 * 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+  launch_k(relu_fixup_kernel, 148 * 8, 256, 0, st, static_cast<const __nv_bfloat16*>(x),
                                              static_cast<const __nv_bfloat16*>(w1t), G, seg_rows,
                                              M, V, list, count, cap,
                                              static_cast<__nv_bfloat16*>(act), relu_mask);
