@@ -34,9 +34,6 @@
 #ifndef MOE_GEMM_EPI_BUFS
 #define MOE_GEMM_EPI_BUFS 1
 #endif
-#ifndef MOE_EPI_DIRECT
-#define MOE_EPI_DIRECT 0  // 1: bf16 epilogues store rows straight from registers (no smem staging)
-#endif
 
 // MOE_GEMM_TRACE (debug builds only): per-role barrier wait cycles, printed by CTAs 0 and 1.
 #ifdef MOE_GEMM_TRACE
@@ -296,7 +293,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kSub = (kEpi == kEpiF32) ? 32 : 64;  // columns per 128-byte sub-chunk
     constexpr uint32_t kSubs = (BN / 2) / kSub;
     constexpr uint32_t kStoreLanes = (kIdx & kIdxScatterD) ? 8 : 1;  // lanes issuing bulk stores
-    constexpr bool kDirect = MOE_EPI_DIRECT != 0 && kEpi != kEpiF32;
     uint8_t* stage_base = smem + C::SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES * kEpiBufs;
     uint32_t ebuf = 0;
     uint32_t iter = 0;
@@ -372,11 +368,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* stage = stage_base + ebuf * EPI_WARP_BYTES;
         const uint32_t stage_row = ptx::smem_u32(stage) + lane * 128;
         ebuf = (ebuf + 1) % kEpiBufs;
-        if constexpr (!kDirect) {
-          // the TMA store that last used this staging buffer must have finished reading it
-          if (lane < kStoreLanes) ptx::tma_store_wait_read<kEpiBufs - 1>();
-          __syncwarp();
-        }
+        // the TMA store that last used this staging buffer must have finished reading it
+        if (lane < kStoreLanes) ptx::tma_store_wait_read<kEpiBufs - 1>();
+        __syncwarp();
         if constexpr (kEpi == kEpiF32) {
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
@@ -386,18 +380,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           float f[64];
 #pragma unroll
           for (uint32_t i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]);
+          if constexpr ((kIdx & kIdxScaleRow) != 0) {
+            // fused decode: y[token] = g * (act . W2)[slot]
+#pragma unroll
+            for (uint32_t i = 0; i < 64; ++i) f[i] *= scale;
+          }
+          uint32_t w[32];  // the 64 outputs as bf16 pairs (round to nearest even)
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j) w[j] = ptx::pack_bf16x2(f[2 * j], f[2 * j + 1]);
           if constexpr (kEpi == kEpiReluBf16) {
             if (cert) {
               // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64
-              // re-decision. Prefilter against the 64-column block bound; per element on a hit.
+              // re-decision. Prefilter: min |bf16(h)| over the 64 columns (magnitude order ==
+              // unsigned order of the 15 low bits) against the block bound widened by 2^-7 for
+              // the rounding; on a hit, the exact per-element test on the fp32 values.
               float tmax = 0.0f;
 #pragma unroll
               for (uint32_t c2 = 0; c2 < kSubs; ++c2)
                 if (c2 == c) tmax = tblk[c2];
-              float mn = fabsf(f[0]);
+              uint32_t m2 = w[0] & 0x7fff7fffu;
 #pragma unroll
-              for (uint32_t i = 1; i < 64; ++i) mn = fminf(mn, fabsf(f[i]));
-              if (mn < tmax) {
+              for (uint32_t j = 1; j < 32; ++j) m2 = __vminu2(m2, w[j] & 0x7fff7fffu);
+              const float mn = __uint_as_float(min(m2 & 0xffffu, m2 >> 16) << 16);
+              if (mn < tmax * (1.0f + 1.0f / 128.0f)) {
                 const float* ca = args.colabs + static_cast<size_t>(tc.g) * args.N + cols;
                 for (uint32_t i = 0; i < 64; ++i) {
                   if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
@@ -407,52 +412,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
-            unsigned long long bits = 0ull;
+            // [h > 0] bits from the fp32 values (exact zeros stay 0), relu on the pairs
+            uint32_t lo = 0u, hi = 0u;
 #pragma unroll
-            for (uint32_t i = 0; i < 64; ++i) {
-              bits |= static_cast<unsigned long long>(f[i] > 0.0f) << i;
-              f[i] = fmaxf(f[i], 0.0f);
+            for (uint32_t i = 0; i < 32; ++i) {
+              lo |= static_cast<uint32_t>(f[i] > 0.0f) << i;
+              hi |= static_cast<uint32_t>(f[32 + i] > 0.0f) << i;
             }
-            if (args.relu_mask != nullptr && row_ok) args.relu_mask[mrow + cols / 64] = bits;
-          }
-          if constexpr ((kIdx & kIdxScaleRow) != 0) {
-            // fused decode: y[token] = g * (act . W2)[slot]
+            if (args.relu_mask != nullptr && row_ok)
+              args.relu_mask[mrow + cols / 64] = (static_cast<unsigned long long>(hi) << 32) | lo;
 #pragma unroll
-            for (uint32_t i = 0; i < 64; ++i) f[i] *= scale;
+            for (uint32_t j = 0; j < 32; ++j) w[j] = __vmaxs2(w[j], 0u);  // int16 max == bf16 relu
           }
           if constexpr (kEpi == kEpiMaskBf16) {
             // dh = (dY . W2^T) * [h > 0]; the up-GEMM's ReLU bitmask carries [h > 0]
-            unsigned long long w = 0ull;
+            unsigned long long mk = 0ull;
 #pragma unroll
             for (uint32_t c2 = 0; c2 < kSubs; ++c2)
-              if (c2 == c) w = mw[c2];
+              if (c2 == c) mk = mw[c2];
+            const uint32_t mlo = static_cast<uint32_t>(mk), mhi = static_cast<uint32_t>(mk >> 32);
 #pragma unroll
-            for (uint32_t i = 0; i < 64; ++i)
-              if (!((w >> i) & 1ull)) f[i] = 0.0f;
-          }
-          if constexpr (kDirect) {
-            // one 128-byte row segment per thread, straight to global memory
-            const long long drow = (kIdx & kIdxScatterD) ? static_cast<long long>(tok)
-                                                         : (row_ok ? static_cast<long long>(orow) : -1);
-            if (row_ok && drow >= 0) {
-              uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.d_ptr) +
-                                                    static_cast<size_t>(drow) * args.N + cols);
-#pragma unroll
-              for (uint32_t j = 0; j < 8; ++j)
-                dst[j] = make_uint4(ptx::pack_bf16x2(f[8 * j], f[8 * j + 1]),
-                                    ptx::pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                                    ptx::pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
-                                    ptx::pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+            for (uint32_t j = 0; j < 32; ++j) {
+              const uint32_t b2 = ((j < 16 ? mlo : mhi) >> (2 * (j % 16))) & 3u;
+              w[j] &= (b2 & 1u ? 0x0000ffffu : 0u) | (b2 & 2u ? 0xffff0000u : 0u);
             }
-            continue;
           }
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
-            ptx::st_shared_v4(stage_row + ((j ^ (lane & 7)) << 4),
-                              ptx::pack_bf16x2(f[8 * j], f[8 * j + 1]),
-                              ptx::pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                              ptx::pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
-                              ptx::pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+            ptx::st_shared_v4(stage_row + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1],
+                              w[4 * j + 2], w[4 * j + 3]);
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
