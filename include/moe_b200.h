@@ -58,7 +58,15 @@ typedef struct moe_config {
   int32_t adaptive;        /* StrategyControl::adaptive: Alg. 1 picks the pipelining degree */
   int32_t degree;          /* StrategyControl::fixed.degree (capacity chunks), 1..8 */
   int32_t a2a_backend;     /* MOE_A2A_BACKEND_*: how W > 1 ranks exchange tokens */
+  int32_t router;          /* MOE_ROUTER_* (RouterKind, moe_layer.hpp:10) */
 } moe_config;
+
+/* Router (route_probabilities, moe_layer.cpp:165-169). COSINE: softmax of
+ * cos(x . P, C_e) / max(temperature, 0.01) (gate_cosine, gating.cpp:37-56), P (M, 256),
+ * C (E, 256), fp64; the DMMA kernels support E <= 64 (even). */
+#define MOE_ROUTER_LINEAR 0
+#define MOE_ROUTER_COSINE 1
+#define MOE_COSINE_DIM 256
 
 /* All-to-all transport for W > 1. PEER: copy engines push blocks into the peers' receive
  * buffers over NVLink (CUDA IPC mappings), ordered by epoch flags -- no SMs are taken from the
@@ -125,6 +133,12 @@ const char* moe_last_error_global(void);
 int moe_init_params(moe_handle* h, uint64_t seed);
 /* RouterParams::linear_weight (gating.hpp:25-30); host fp64 (M, E). */
 int moe_set_router(moe_handle* h, const double* wg_host);
+/* RouterParams::cosine_proj (M, 256), cosine_experts (E, 256), temperature (host fp64). A
+ * zero-norm expert row is rejected (MOE_EINVAL, as gate_cosine's invalid_argument); a
+ * zero-norm projected token is detected on the device and reported by the next
+ * moe_get_metrics / moe_get_routing call (MOE_EINVAL). */
+int moe_set_cosine_router(moe_handle* h, const double* proj_host, const double* experts_host,
+                          double temperature);
 /* Full weights of local expert `local_e` (global index rank*E/W + local_e); host fp64
  * w1 (M, V), w2 (V, M) -- ExpertParams::assemble layout (parallelism.cpp:80-90). */
 int moe_set_expert(moe_handle* h, int64_t local_e, const double* w1_host, const double* w2_host);
@@ -188,6 +202,14 @@ int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t bloc
                   int64_t M, int64_t E, int64_t k, int32_t capacity_kind, double capacity_factor,
                   int32_t bpr, int32_t* idxs, double* gates, int32_t* locations, double* probs,
                   int64_t* capacity, int64_t* drops, void* stream);
+
+/* gate_cosine + run_gating_blocked: as moe_op_gating with the cosine router (proj (M, D),
+ * experts (E, D), device fp64). */
+int moe_op_gating_cosine(const void* x, int32_t x_dtype, const double* proj, const double* experts,
+                         int64_t D, double temperature, int64_t blocks, int64_t T, int64_t M,
+                         int64_t E, int64_t k, int32_t capacity_kind, double capacity_factor,
+                         int32_t bpr, int32_t* idxs, double* gates, int32_t* locations,
+                         double* probs, int64_t* capacity, int64_t* drops, void* stream);
 
 /* fast_encode_range per block (dispatch.cpp:51-62) + partition_capacity (pipeline.cpp:33-51):
  * z = [blocks][degree][E][cc][M], cc = ceil(capacity/degree), padded slots zero. */

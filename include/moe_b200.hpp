@@ -48,9 +48,12 @@ struct StrategyControl {  // moe_layer.hpp:17-20
   int a2a_backend = MOE_A2A_BACKEND_PEER;
 };
 
+enum class RouterKind { Linear = MOE_ROUTER_LINEAR, Cosine = MOE_ROUTER_COSINE };  // moe_layer.hpp:10
+
 struct MoELayerConfig {  // moe_layer.hpp:22-29
   Dims dims;
   CapacityKind capacity = CapacityKind::Fixed;
+  RouterKind router = RouterKind::Linear;
   double capacity_factor = 1.0;
   bool bpr = false;
   DType dtype = DType::BF16;
@@ -72,6 +75,7 @@ struct MoELayerConfig {  // moe_layer.hpp:22-29
     c.adaptive = strategy.adaptive ? 1 : 0;
     c.degree = strategy.degree;
     c.a2a_backend = strategy.a2a_backend;
+    c.router = static_cast<int32_t>(router);
     return c;
   }
 };

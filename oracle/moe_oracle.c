@@ -75,6 +75,65 @@ void orc_gate_linear(const double* x, const double* wg, int64_t T, int64_t M, in
   }
 }
 
+/* gating.cpp:37-56 (gate_cosine): proj = x . P (T, D); logits[t][e] = <proj_t, C_e> /
+ * (|proj_t| |C_e| max(tau, 0.01)); row softmax. Returns -1 on a zero-norm projected token or
+ * expert row (the reference's std::invalid_argument), 0 otherwise. */
+int32_t orc_gate_cosine(const double* x, const double* proj_w, const double* experts,
+                        double temperature, int64_t T, int64_t M, int64_t E, int64_t D,
+                        double* probs) {
+  const double tau = temperature > 0.01 ? temperature : 0.01;
+  double* en = (double*)malloc(sizeof(double) * (size_t)E);
+  for (int64_t e = 0; e < E; ++e) {
+    double s = 0.0;
+    for (int64_t d = 0; d < D; ++d) s += experts[e * D + d] * experts[e * D + d];
+    en[e] = sqrt(s);
+    if (en[e] == 0.0) {
+      free(en);
+      return -1;
+    }
+  }
+  int32_t bad = 0;
+#pragma omp parallel
+  {
+    double* pr = (double*)malloc(sizeof(double) * (size_t)D);
+#pragma omp for schedule(static)
+    for (int64_t t = 0; t < T; ++t) {
+      for (int64_t d = 0; d < D; ++d) pr[d] = 0.0;
+      for (int64_t m = 0; m < M; ++m) {
+        const double xv = x[t * M + m];
+        const double* w = proj_w + m * D;
+        for (int64_t d = 0; d < D; ++d) pr[d] += xv * w[d];
+      }
+      double s = 0.0;
+      for (int64_t d = 0; d < D; ++d) s += pr[d] * pr[d];
+      const double tn = sqrt(s);
+      if (tn == 0.0) {
+#pragma omp atomic write
+        bad = 1;
+        continue;
+      }
+      double* row = probs + t * E;
+      for (int64_t e = 0; e < E; ++e) {
+        double dot = 0.0;
+        for (int64_t d = 0; d < D; ++d) dot += pr[d] * experts[e * D + d];
+        row[e] = dot / (tn * en[e] * tau);
+      }
+      double mx = row[0];
+      for (int64_t e = 1; e < E; ++e)
+        if (row[e] > mx) mx = row[e];
+      double z = 0.0;
+      for (int64_t e = 0; e < E; ++e) {
+        row[e] = exp(row[e] - mx);
+        z += row[e];
+      }
+      for (int64_t e = 0; e < E; ++e) row[e] /= z;
+    }
+    free(pr);
+  }
+  free(en);
+  return bad ? -1 : 0;
+}
+
 /* gating.cpp:58-78: stable sort by (prob desc, id asc) == repeated selection with that order. */
 void orc_topk_select(const double* probs, int64_t T, int64_t E, int64_t k, int64_t* idxs,
                      double* gates) {
@@ -437,17 +496,14 @@ void orc_frozen_plan_forward(const double* x, int64_t Ttot, int64_t M, int64_t V
 }
 
 /* ------------------------------------------------------------------ moe_layer.cpp:171-319 */
-int64_t orc_layer_step(const double* x, const double* wg, const double* w1, const double* w2,
-                       const double* dy, int64_t W, int64_t T, int64_t M, int64_t V, int64_t E,
-                       int64_t k, int32_t cap_kind, double factor, int32_t bpr, double* y,
-                       int64_t* idxs, int64_t* locations, double* gates, double* dx,
-                       double* dw1, double* dw2) {
-  const int64_t Ttot = W * T;
-  double* probs = (double*)malloc(sizeof(double) * (size_t)(Ttot * E));
-  orc_gate_linear(x, wg, Ttot, M, E, probs);
+/* moe_layer.cpp:171-319 from the router's probabilities (route_probabilities, :165-169). */
+int64_t orc_layer_step_probs(const double* x, const double* probs, const double* w1,
+                             const double* w2, const double* dy, int64_t W, int64_t T, int64_t M,
+                             int64_t V, int64_t E, int64_t k, int32_t cap_kind, double factor,
+                             int32_t bpr, double* y, int64_t* idxs, int64_t* locations,
+                             double* gates, double* dx, double* dw1, double* dw2) {
   const int64_t cap = orc_run_gating_blocked(probs, W, T, E, k, cap_kind, factor, bpr, idxs, gates,
                                              locations);
-  free(probs);
   const int64_t rows = W * cap; /* gathered capacity C = W * dC per expert */
   const size_t zsz = (size_t)(W * E * cap * M);
   double* z = (double*)malloc(sizeof(double) * zsz);
@@ -473,6 +529,20 @@ int64_t orc_layer_step(const double* x, const double* wg, const double* w1, cons
   free(z);
   free(xe);
   free(ye);
+  return cap;
+}
+
+int64_t orc_layer_step(const double* x, const double* wg, const double* w1, const double* w2,
+                       const double* dy, int64_t W, int64_t T, int64_t M, int64_t V, int64_t E,
+                       int64_t k, int32_t cap_kind, double factor, int32_t bpr, double* y,
+                       int64_t* idxs, int64_t* locations, double* gates, double* dx,
+                       double* dw1, double* dw2) {
+  const int64_t Ttot = W * T;
+  double* probs = (double*)malloc(sizeof(double) * (size_t)(Ttot * E));
+  orc_gate_linear(x, wg, Ttot, M, E, probs);
+  const int64_t cap = orc_layer_step_probs(x, probs, w1, w2, dy, W, T, M, V, E, k, cap_kind,
+                                           factor, bpr, y, idxs, locations, gates, dx, dw1, dw2);
+  free(probs);
   return cap;
 }
 

@@ -36,6 +36,9 @@ double orc_capacity_to_factor(int64_t cap, int64_t E, int64_t k, int64_t T);
 void orc_gate_linear(const double* x, const double* wg, int64_t T, int64_t M, int64_t E,
                      double* probs);
 /* gating.cpp:58-78 */
+int32_t orc_gate_cosine(const double* x, const double* proj_w, const double* experts,
+                        double temperature, int64_t T, int64_t M, int64_t E, int64_t D,
+                        double* probs);
 void orc_topk_select(const double* probs, int64_t T, int64_t E, int64_t k, int64_t* idxs,
                      double* gates);
 /* gating.cpp:80-112 */
@@ -101,6 +104,11 @@ void orc_frozen_plan_forward(const double* x, int64_t Ttot, int64_t M, int64_t V
  * linear router): gate -> encode -> per-expert FFN over the gathered capacity rows -> decode,
  * and the reverse pass (gates frozen; d_gates discarded). w1 (E,M,V), w2 (E,V,M).
  * Outputs: y (W*T, M); routing (W*T, k); dx (W*T, M), dw1, dw2 (if dy != NULL). */
+int64_t orc_layer_step_probs(const double* x, const double* probs, const double* w1,
+                             const double* w2, const double* dy, int64_t W, int64_t T, int64_t M,
+                             int64_t V, int64_t E, int64_t k, int32_t cap_kind, double factor,
+                             int32_t bpr, double* y, int64_t* idxs, int64_t* locations,
+                             double* gates, double* dx, double* dw1, double* dw2);
 int64_t orc_layer_step(const double* x, const double* wg, const double* w1, const double* w2,
                        const double* dy, int64_t W, int64_t T, int64_t M, int64_t V, int64_t E,
                        int64_t k, int32_t cap_kind, double factor, int32_t bpr, double* y,

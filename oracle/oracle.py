@@ -42,6 +42,8 @@ def lib() -> C.CDLL:
         _l.orc_run_gating_blocked.restype = C.c_int64
         _l.orc_drop_count.restype = C.c_int64
         _l.orc_layer_step.restype = C.c_int64
+        _l.orc_layer_step_probs.restype = C.c_int64
+        _l.orc_gate_cosine.restype = C.c_int32
         _l.orc_num_threads.restype = C.c_int32
         _l.orc_next_u64.restype = C.c_uint64
         _l.orc_uniform.restype = C.c_double
@@ -95,6 +97,19 @@ def gate_linear(x, wg) -> np.ndarray:
     E = wg.shape[1]
     out = np.empty((T, E), np.float64)
     lib().orc_gate_linear(_p(x), _p(wg), I64(T), I64(M), I64(E), _p(out))
+    return out
+
+
+def gate_cosine(x, proj, experts, temperature=1.0) -> np.ndarray:
+    """gating.cpp:37-56; raises ValueError on a zero-norm token / expert (invalid_argument)."""
+    x, proj, experts = _f64(x), _f64(proj), _f64(experts)
+    T, M = x.shape
+    E, Dd = experts.shape
+    out = np.empty((T, E), np.float64)
+    rc = lib().orc_gate_cosine(_p(x), _p(proj), _p(experts), D(temperature), I64(T), I64(M),
+                               I64(E), I64(Dd), _p(out))
+    if rc != 0:
+        raise ValueError("gate_cosine: zero-norm projected token or expert row")
     return out
 
 
@@ -254,8 +269,9 @@ def frozen_plan_forward(x, k, idxs, locations, gates, w1, w2):
     return y
 
 
-def layer_step(x, wg, w1, w2, dy, W, k, cap_kind=0, factor=1.0, bpr=False):
-    """Whole layer over W source blocks; returns dict of y, routing and (if dy) dx, dw1, dw2."""
+def layer_step(x, wg, w1, w2, dy, W, k, cap_kind=0, factor=1.0, bpr=False, cosine=None):
+    """Whole layer over W source blocks; returns dict of y, routing and (if dy) dx, dw1, dw2.
+    cosine = (proj (M, D), experts (E, D), temperature) selects RouterKind::Cosine."""
     x, wg, w1, w2 = _f64(x), _f64(wg), _f64(w1), _f64(w2)
     n, M = x.shape
     T = n // W
@@ -268,10 +284,11 @@ def layer_step(x, wg, w1, w2, dy, W, k, cap_kind=0, factor=1.0, bpr=False):
     dx = np.empty((n, M), np.float64) if dy is not None else None
     dw1 = np.empty((E, M, V), np.float64) if dy is not None else None
     dw2 = np.empty((E, V, M), np.float64) if dy is not None else None
-    cap = lib().orc_layer_step(_p(x), _p(wg), _p(w1), _p(w2), _p(dyy), I64(W), I64(T), I64(M),
-                               I64(V), I64(E), I64(k), C.c_int32(cap_kind), D(factor),
-                               C.c_int32(int(bpr)), _p(y), _p(idxs), _p(loc), _p(gates), _p(dx),
-                               _p(dw1), _p(dw2))
+    probs = gate_cosine(x, *cosine) if cosine is not None else gate_linear(x, wg)
+    cap = lib().orc_layer_step_probs(_p(x), _p(probs), _p(w1), _p(w2), _p(dyy), I64(W), I64(T),
+                                     I64(M), I64(V), I64(E), I64(k), C.c_int32(cap_kind),
+                                     D(factor), C.c_int32(int(bpr)), _p(y), _p(idxs), _p(loc),
+                                     _p(gates), _p(dx), _p(dw1), _p(dw2))
     return dict(y=y, idxs=idxs, locations=loc, gates=gates, capacity=int(cap), dx=dx, dw1=dw1,
                 dw2=dw2)
 

@@ -37,7 +37,7 @@ class MoeConfig(C.Structure):
         ("model_dim", C.c_int64), ("hidden_dim", C.c_int64), ("tokens_per_step", C.c_int64),
         ("top_k", C.c_int64), ("capacity_kind", C.c_int32), ("capacity_factor", C.c_double),
         ("bpr", C.c_int32), ("dtype", C.c_int32), ("adaptive", C.c_int32), ("degree", C.c_int32),
-        ("a2a_backend", C.c_int32),
+        ("a2a_backend", C.c_int32), ("router", C.c_int32),
     ]
 
 
@@ -68,6 +68,7 @@ SIGNATURES = {
     "moe_last_error_global": (C.c_char_p, []),
     "moe_init_params": (I32, [P, U64]),
     "moe_set_router": (I32, [P, P]),
+    "moe_set_cosine_router": (I32, [P, P, P, D]),
     "moe_set_expert": (I32, [P, I64, P, P]),
     "moe_set_expert_slices": (I32, [P, P, P]),
     "moe_forward": (I32, [P, P, P, P]),
@@ -87,6 +88,8 @@ SIGNATURES = {
     "moe_take_profile": (I32, [P, PD, PI64, I32]),
     "moe_op_gating": (I32, [P, I32, P, I64, I64, I64, I64, I64, I32, D, I32, P, P, P, P, PI64,
                             PI64, P]),
+    "moe_op_gating_cosine": (I32, [P, I32, P, P, I64, D, I64, I64, I64, I64, I64, I32, D, I32, P, P,
+                                   P, P, PI64, PI64, P]),
     "moe_op_encode": (I32, [P, I32, I64, I64, I64, I64, I64, I64, I64, P, P, P, P]),
     "moe_op_decode": (I32, [P, I32, I64, I64, I64, I64, I64, I64, I64, P, P, P, P, P]),
     "moe_op_decode_backward": (I32, [P, P, I32, I64, I64, I64, I64, I64, I64, I64, P, P, P, P, P,

@@ -266,6 +266,9 @@ const char* moe_last_error_global(void) { return g_err.c_str(); }
 
 int moe_init_params(moe_handle* h, uint64_t seed) { LAYER_CALL(h, h->layer->init_params(seed)); }
 int moe_set_router(moe_handle* h, const double* wg) { LAYER_CALL(h, h->layer->set_router(wg)); }
+int moe_set_cosine_router(moe_handle* h, const double* proj, const double* experts, double temperature) {
+  LAYER_CALL(h, h->layer->set_cosine_router(proj, experts, temperature));
+}
 int moe_set_expert(moe_handle* h, int64_t le, const double* w1, const double* w2) {
   LAYER_CALL(h, h->layer->set_expert(le, w1, w2));
 }
@@ -315,10 +318,17 @@ int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n) {
 }
 
 // ------------------------------------------------------------------ stateless ops
-int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t blocks, int64_t T,
-                  int64_t M, int64_t E, int64_t k, int32_t capacity_kind, double capacity_factor,
-                  int32_t bpr, int32_t* idxs, double* gates, int32_t* locations, double* probs,
-                  int64_t* capacity, int64_t* drops, void* stream) {
+namespace {
+struct CosineOp {
+  const double* proj = nullptr;
+  const double* experts = nullptr;
+  int64_t D = 0;
+  double temperature = 1.0;
+};
+int op_gating(const void* x, int32_t x_dtype, const double* wg, const CosineOp* cos, int64_t blocks,
+              int64_t T, int64_t M, int64_t E, int64_t k, int32_t capacity_kind,
+              double capacity_factor, int32_t bpr, int32_t* idxs, double* gates, int32_t* locations,
+              double* probs, int64_t* capacity, int64_t* drops, void* stream) {
   return guard(nullptr, [&] {
     require_device();
     check_dtype(x_dtype);
@@ -357,7 +367,32 @@ int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t bloc
     g.list = sc.get<int32_t>(Tk);
     g.cap = sc.get<int32_t>(1);
     g.drops = sc.get<int32_t>(1);
+    int32_t* err = nullptr;
+    if (cos) {
+      if (E > 64 || E % 2 || cos->D < 2 || cos->D % 2) throw moe::MoeError(MOE_EINVAL, "cosine gating: E <= 64 (even), even D");
+      a.router = 1;
+      a.cos_proj = cos->proj;
+      a.cos_dim = static_cast<int>(cos->D);
+      a.cos_tau = std::max(cos->temperature, 0.01);
+      double* ct = sc.get<double>(static_cast<size_t>(E) * cos->D);
+      double* en = sc.get<double>(static_cast<size_t>(E));
+      err = sc.get<int32_t>(1);
+      ck(cudaMemsetAsync(err, 0, 4, st), "memset");
+      ckr(moe::cosine_prep_device(cos->experts, static_cast<int>(E), static_cast<int>(cos->D), ct, en, err, st),
+          "cosine prep");
+      a.cos_ct = ct;
+      a.cos_en = en;
+      a.cos_buf = sc.get<double>(static_cast<size_t>(blocks) * T * cos->D);
+      a.err = err;
+    }
     ckr(moe::run_gating_device(a, g, st), "gating");
+    if (err) {
+      int32_t e = 0;
+      ck(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, st), "copy");
+      ck(cudaStreamSynchronize(st), "sync");
+      if (e == 2) throw moe::MoeError(MOE_EINVAL, "gate_cosine: zero-norm expert row");
+      if (e) throw moe::MoeError(MOE_EINVAL, "gate_cosine: zero-norm projected token");
+    }
     int32_t cap = a.cap_formula;
     if (capacity_kind != MOE_CAP_FIXED) {
       ck(cudaMemcpyAsync(&cap, g.cap, 4, cudaMemcpyDeviceToHost, st), "copy");
@@ -372,6 +407,29 @@ int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t bloc
     if (capacity) *capacity = cap;
     if (drops) *drops = nd;
   });
+}
+}  // namespace
+
+int moe_op_gating(const void* x, int32_t x_dtype, const double* wg, int64_t blocks, int64_t T,
+                  int64_t M, int64_t E, int64_t k, int32_t capacity_kind, double capacity_factor,
+                  int32_t bpr, int32_t* idxs, double* gates, int32_t* locations, double* probs,
+                  int64_t* capacity, int64_t* drops, void* stream) {
+  return op_gating(x, x_dtype, wg, nullptr, blocks, T, M, E, k, capacity_kind, capacity_factor, bpr,
+                   idxs, gates, locations, probs, capacity, drops, stream);
+}
+
+int moe_op_gating_cosine(const void* x, int32_t x_dtype, const double* proj, const double* experts,
+                         int64_t D, double temperature, int64_t blocks, int64_t T, int64_t M,
+                         int64_t E, int64_t k, int32_t capacity_kind, double capacity_factor,
+                         int32_t bpr, int32_t* idxs, double* gates, int32_t* locations,
+                         double* probs, int64_t* capacity, int64_t* drops, void* stream) {
+  CosineOp c;
+  c.proj = proj;
+  c.experts = experts;
+  c.D = D;
+  c.temperature = temperature;
+  return op_gating(x, x_dtype, nullptr, &c, blocks, T, M, E, k, capacity_kind, capacity_factor, bpr,
+                   idxs, gates, locations, probs, capacity, drops, stream);
 }
 
 int moe_op_encode(const void* x, int32_t dtype, int64_t blocks, int64_t T, int64_t M, int64_t E,

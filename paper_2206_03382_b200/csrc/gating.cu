@@ -17,7 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.h"
 #include "pdl.cuh"
@@ -412,34 +414,60 @@ __device__ __forceinline__ double ld_x<float>(const float* p) {
   return static_cast<double>(*p);
 }
 
+template <>
+__device__ __forceinline__ double ld_x<double>(const double* p) {
+  return *p;
+}
+
 template <typename TX, int NT>
 struct D2Cfg {
   static constexpr int XROW = kD2KC * sizeof(TX) + 16;       // bytes per staged token row (padded)
-  static constexpr int EP = 8 * NT + 4;                       // Wg row stride (doubles)
+  static constexpr int EP = 8 * NT + 4;                       // W row stride in smem (doubles)
   static constexpr int XBYTES = kDmTok * XROW;
   static constexpr int WBYTES = kD2KC * EP * 8;
   static constexpr int STAGE = XBYTES + WBYTES;
   static constexpr int SMEM = kD2Stages * STAGE + 8 * NT * 4 + 16;
 };
 
-template <typename TX, int NT>
-__global__ void __launch_bounds__(kDmWarps * 32)
-    gate_dmma2_kernel(const TX* __restrict__ x, const double* __restrict__ wg, int T, int M, int E,
-                      int k, int cta_per_block, int32_t* __restrict__ idxs,
-                      double* __restrict__ gates, int32_t* __restrict__ hist,
-                      double* __restrict__ probs_out) {
+// Epilogue of the pipelined DMMA x . W kernel.
+enum DmmaMode : int {
+  kDmGate = 0,    // logits -> softmax -> top-k + per-CTA histogram (gate_linear, gating.cpp:29-35)
+  kDmRaw = 1,     // fp64 rows out (the cosine router's projection x . P, gating.cpp:43)
+  kDmCosine = 2,  // logits / (|a_t| |C_e| tau) -> softmax -> top-k (gate_cosine, gating.cpp:50-55)
+};
+
+struct DmmaArgs {
+  const void* x;        // A: [rows][K] (bf16 / f32 / f64), rows of the 64-token blocks
+  const double* w;      // W: [K][ldw] fp64, columns [0, ncols)
+  int ldw, ncols, T, K, k, cpb;
+  int32_t* idxs;        // gate modes
+  double* gates;
+  int32_t* hist;
+  double* probs_out;
+  double* out;          // kDmRaw: [rows][ldo]
+  int ldo;
+  const double* en;     // kDmCosine: |C_e|
+  double tau;           // kDmCosine: max(temperature, 0.01)
+  int32_t* err;         // kDmCosine: set to 1 on a zero-norm projected token
+};
+
+template <typename TX, int NT, int kMode>
+__global__ void __launch_bounds__(kDmWarps * 32) gate_dmma2_kernel(DmmaArgs a) {
   pdl_entry();
   using Cf = D2Cfg<TX, NT>;
   constexpr int NTH = kDmWarps * 32;
   constexpr int XCH = kD2KC * sizeof(TX) / 16;  // 16-byte chunks per token row
-  constexpr int WCH = 8 * NT * 8 / 16;          // 16-byte chunks per Wg row (8*NT doubles)
+  constexpr int WCH = 8 * NT * 8 / 16;          // 16-byte chunks per W row (8*NT doubles)
   extern __shared__ __align__(16) uint8_t sm[];
   int32_t* sh_hist = reinterpret_cast<int32_t*>(sm + kD2Stages * Cf::STAGE);
+  const TX* __restrict__ x = static_cast<const TX*>(a.x);
+  const int M = a.K, E = a.ncols;
+  const int n0 = kMode == kDmRaw ? blockIdx.y * 8 * NT : 0;
 
-  const int b = blockIdx.x / cta_per_block;
-  const int c = blockIdx.x % cta_per_block;
-  const int t_begin = b * T + c * kDmTok;
-  const int ntok = min(b * T + T, t_begin + kDmTok) - t_begin;
+  const int b = blockIdx.x / a.cpb;
+  const int c = blockIdx.x % a.cpb;
+  const int t_begin = b * a.T + c * kDmTok;
+  const int ntok = min(b * a.T + a.T, t_begin + kDmTok) - t_begin;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int e = threadIdx.x; e < 8 * NT; e += NTH) sh_hist[e] = 0;
 
@@ -457,17 +485,20 @@ __global__ void __launch_bounds__(kDmWarps * 32)
     for (int i = threadIdx.x; i < kD2KC * WCH; i += NTH) {
       const int kk = i / WCH, q = i % WCH;
       const int e = q * 2;
-      const bool ok = k0 + kk < M && e < E;
-      const double* src = ok ? wg + static_cast<size_t>(k0 + kk) * E + e : wg;
+      const bool ok = k0 + kk < M && n0 + e < E;
+      const double* src = ok ? a.w + static_cast<size_t>(k0 + kk) * a.ldw + n0 + e : a.w;
       cp_async16(ws + kk * Cf::EP + e, src, ok);
     }
   };
 
   double acc[kDmMT][NT][2];
+  double ss[kDmMT];  // kDmCosine: sum of squares of this lane's A elements (token norm)
 #pragma unroll
-  for (int i = 0; i < kDmMT; ++i)
+  for (int i = 0; i < kDmMT; ++i) {
+    ss[i] = 0.0;
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
 
   const int nch = (M + kD2KC - 1) / kD2KC;
   issue(0);
@@ -484,18 +515,62 @@ __global__ void __launch_bounds__(kDmWarps * 32)
     const double* ws = reinterpret_cast<const double*>(st + Cf::XBYTES);
 #pragma unroll
     for (int ks = 0; ks < kD2KC; ks += 4) {
-      double a[kDmMT], bb[NT];
+      double av[kDmMT], bb[NT];
 #pragma unroll
-      for (int i = 0; i < kDmMT; ++i)
-        a[i] = ld_x<TX>(reinterpret_cast<const TX*>(st + ((warp * kDmMT + i) * 8 + ar) * Cf::XROW) + ks + ac);
+      for (int i = 0; i < kDmMT; ++i) {
+        av[i] = ld_x<TX>(reinterpret_cast<const TX*>(st + ((warp * kDmMT + i) * 8 + ar) * Cf::XROW) + ks + ac);
+        if constexpr (kMode == kDmCosine) ss[i] = fma(av[i], av[i], ss[i]);
+      }
 #pragma unroll
       for (int j = 0; j < NT; ++j) bb[j] = ws[(ks + ac) * Cf::EP + j * 8 + ar];
 #pragma unroll
       for (int i = 0; i < kDmMT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], av[i], bb[j]);
     }
   }
+  if constexpr (kMode == kDmRaw) {
+    // fragment (i, j, h) = row (warp * MT + i) * 8 + ar, column j * 8 + ac * 2 + h
+#pragma unroll
+    for (int i = 0; i < kDmMT; ++i) {
+      const int tt = (warp * kDmMT + i) * 8 + ar;
+      if (tt >= ntok) continue;
+      double* orow = a.out + static_cast<size_t>(t_begin + tt) * a.ldo;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = n0 + j * 8 + ac * 2 + h;
+          if (e < E) orow[e] = acc[i][j][h];
+        }
+    }
+    return;
+  }
+  if constexpr (kMode == kDmCosine) {
+    // logits[t][e] = <a_t, C_e> / (|a_t| |C_e| tau) (gating.cpp:50-54)
+#pragma unroll
+    for (int i = 0; i < kDmMT; ++i) {
+      double q = ss[i];
+      q += __shfl_xor_sync(0xffffffffu, q, 1);
+      q += __shfl_xor_sync(0xffffffffu, q, 2);
+      const double tn = sqrt(q);
+      const int tt = (warp * kDmMT + i) * 8 + ar;
+      if (tn == 0.0 && tt < ntok && ac == 0) atomicExch(a.err, 1);
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = j * 8 + ac * 2 + h;
+          if (e < E) acc[i][j][h] = acc[i][j][h] / (tn * __ldg(a.en + e) * a.tau);
+        }
+    }
+  }
+  const int T = a.T, k = a.k;
+  int32_t* __restrict__ idxs = a.idxs;
+  double* __restrict__ gates = a.gates;
+  int32_t* __restrict__ hist = a.hist;
+  double* __restrict__ probs_out = a.probs_out;
+  (void)T;
   // softmax + top-k: the 4 lanes of a quad (same lane/4) hold one token's 8*NT logits.
 #pragma unroll
   for (int i = 0; i < kDmMT; ++i) {
@@ -762,34 +837,47 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Pipelined DMMA x . W launch: NT = 4 (<= 32 columns per CTA) or 8 (<= 64).
+template <typename TX, int kMode>
+int launch_dmma(const DmmaArgs& da, int gx, int gy, cudaStream_t st) {
+  const int cols = kMode == kDmRaw ? 64 : da.ncols;
+  auto go = [&](auto nt_tag) -> int {
+    constexpr int NT = decltype(nt_tag)::value;
+    using Cf = D2Cfg<TX, NT>;
+    auto kern = gate_dmma2_kernel<TX, NT, kMode>;
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+      set = true;
+    }
+    launch_k(kern, dim3(gx, gy), dim3(kDmWarps * 32), Cf::SMEM, st, da);
+    return launch_status();
+  };
+  if (cols <= 32) return go(std::integral_constant<int, 4>{});
+  return go(std::integral_constant<int, 8>{});
+}
+
 template <typename TX>
 int launch_gate(const void* x, const double* wg, int blocks, int T, int M, int E, int k,
                 int32_t* idxs, double* gates, int32_t* hist, double* probs, cudaStream_t st) {
   const TX* xp = static_cast<const TX*>(x);
-  if (E <= 64 && (M * static_cast<int>(sizeof(TX))) % 16 == 0 &&
+  if (E <= 64 && E % 2 == 0 && (M * static_cast<int>(sizeof(TX))) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
     const int cpb = (T + kDmTok - 1) / kDmTok;
-    const dim3 grid(blocks * cpb);
-    if (E <= 32) {
-      using Cf = D2Cfg<TX, 4>;
-      static bool set = false;
-      if (!set) {
-        cudaFuncSetAttribute(gate_dmma2_kernel<TX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-        set = true;
-      }
-      launch_k(gate_dmma2_kernel<TX, 4>, grid, kDmWarps * 32, Cf::SMEM, st, xp, wg, T, M, E, k, cpb, idxs,
-                                                                     gates, hist, probs);
-    } else {
-      using Cf = D2Cfg<TX, 8>;
-      static bool set = false;
-      if (!set) {
-        cudaFuncSetAttribute(gate_dmma2_kernel<TX, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-        set = true;
-      }
-      launch_k(gate_dmma2_kernel<TX, 8>, grid, kDmWarps * 32, Cf::SMEM, st, xp, wg, T, M, E, k, cpb, idxs,
-                                                                     gates, hist, probs);
-    }
-    return launch_status();
+    DmmaArgs da{};
+    da.x = xp;
+    da.w = wg;
+    da.ldw = E;
+    da.ncols = E;
+    da.T = T;
+    da.K = M;
+    da.k = k;
+    da.cpb = cpb;
+    da.idxs = idxs;
+    da.gates = gates;
+    da.hist = hist;
+    da.probs_out = probs;
+    return launch_dmma<TX, kDmGate>(da, blocks * cpb, 1, st);
   }
   if (E <= 64) {
     const int cpb = (T + kDmTok - 1) / kDmTok;
@@ -849,13 +937,113 @@ int resolve_capacity_device(const int32_t* demand, int E, int cap_kind, int cap_
 
 int gate_cta_per_block(int T) { return (T + kGateTok - 1) / kGateTok; }
 
+namespace {
+
+__global__ void cosine_prep_kernel(const double* __restrict__ ce, int E, int D,
+                                   double* __restrict__ ct, double* __restrict__ en,
+                                   int32_t* __restrict__ err) {
+  pdl_entry();
+  const int lane = threadIdx.x % 32;
+  for (int e = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; e < E;
+       e += gridDim.x * (blockDim.x / 32)) {
+    double s = 0.0;
+    for (int d = lane; d < D; d += 32) {
+      const double v = ce[static_cast<size_t>(e) * D + d];
+      ct[static_cast<size_t>(d) * E + e] = v;
+      s = fma(v, v, s);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      en[e] = sqrt(s);
+      if (s == 0.0) atomicExch(err, 2);
+    }
+  }
+}
+
+// x . P for token rows that are not 16-byte aligned (tiny M): one fp64 output per thread.
+template <typename TX>
+__global__ void proj_simt_kernel(const TX* __restrict__ x, const double* __restrict__ P, int64_t n,
+                                 int M, int D, double* __restrict__ out) {
+  pdl_entry();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n * D;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / D;
+    const int d = static_cast<int>(i % D);
+    double s = 0.0;
+    for (int m = 0; m < M; ++m) s = fma(ld_x<TX>(x + t * M + m), P[static_cast<size_t>(m) * D + d], s);
+    out[i] = s;
+  }
+}
+
+// RouterKind::Cosine: proj = x . P (DMMA, fp64 rows), then cos(proj_t, C_e) / tau -> softmax
+// -> top-k with the same 64-token CTA partition / histograms as the linear gate.
+template <typename TX>
+int launch_cosine_gate(const GatingArgs& a, const GatingBuffers& g, cudaStream_t st) {
+  const int D = a.cos_dim;
+  if (a.E > 64 || a.E % 2 || D % 2 || !a.cos_proj || !a.cos_ct || !a.cos_en || !a.cos_buf)
+    return -1;
+  const int cpb = gate_cta_per_block(a.T);
+  int rc;
+  if ((a.M * static_cast<int>(sizeof(TX))) % 16 == 0 && reinterpret_cast<uintptr_t>(a.x) % 16 == 0) {
+    DmmaArgs p{};
+    p.x = a.x;
+    p.w = a.cos_proj;
+    p.ldw = D;
+    p.ncols = D;
+    p.T = a.T;
+    p.K = a.M;
+    p.k = a.k;
+    p.cpb = cpb;
+    p.out = a.cos_buf;
+    p.ldo = D;
+    rc = launch_dmma<TX, kDmRaw>(p, a.blocks * cpb, (D + 63) / 64, st);
+  } else {
+    const int64_t n = static_cast<int64_t>(a.blocks) * a.T;
+    const int64_t tot = n * D;
+    const int grid = static_cast<int>(std::min<int64_t>((tot + 255) / 256, 148 * 16));
+    launch_k(proj_simt_kernel<TX>, dim3(grid), dim3(256), 0, st, static_cast<const TX*>(a.x),
+             a.cos_proj, n, a.M, D, a.cos_buf);
+    rc = launch_status();
+  }
+  if (rc) return rc;
+  DmmaArgs q{};
+  q.x = a.cos_buf;
+  q.w = a.cos_ct;
+  q.ldw = a.E;
+  q.ncols = a.E;
+  q.T = a.T;
+  q.K = D;
+  q.k = a.k;
+  q.cpb = cpb;
+  q.idxs = g.idxs;
+  q.gates = g.gates;
+  q.hist = g.hist;
+  q.probs_out = g.probs;
+  q.en = a.cos_en;
+  q.tau = a.cos_tau;
+  q.err = a.err;
+  return launch_dmma<double, kDmCosine>(q, a.blocks * cpb, 1, st);
+}
+
+}  // namespace
+
+int cosine_prep_device(const double* ce, int E, int D, double* ct, double* en, int32_t* err,
+                       cudaStream_t st) {
+  launch_k(cosine_prep_kernel, dim3((E + 7) / 8), dim3(256), 0, st, ce, E, D, ct, en, err);
+  return launch_status();
+}
+
 int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t st) {
   if (a.E < 1 || a.k < 1 || a.k > a.E || a.k > 32 || a.T < 1 || a.M < 1 || a.blocks < 1) return -1;
   const int cpb = gate_cta_per_block(a.T);
-  int rc = a.x_is_f32 ? launch_gate<float>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k, g.idxs,
-                                           g.gates, g.hist, g.probs, st)
-                      : launch_gate<__nv_bfloat16>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k,
-                                                   g.idxs, g.gates, g.hist, g.probs, st);
+  int rc;
+  if (a.router == 1)
+    rc = a.x_is_f32 ? launch_cosine_gate<float>(a, g, st) : launch_cosine_gate<__nv_bfloat16>(a, g, st);
+  else
+    rc = a.x_is_f32 ? launch_gate<float>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k, g.idxs, g.gates,
+                                         g.hist, g.probs, st)
+                    : launch_gate<__nv_bfloat16>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k, g.idxs,
+                                                 g.gates, g.hist, g.probs, st);
   if (rc) return rc;
   if (cpb > 16 * 256) return -1;
   launch_k(scan_cols_kernel, a.blocks * a.E, 256, 0, st, g.hist, cpb, a.E, g.offs, g.demand);

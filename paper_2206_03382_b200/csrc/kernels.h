@@ -26,7 +26,20 @@ struct GatingArgs {
   int cap_kind;        // 0 fixed, 1 auto, 2 bounded
   int cap_formula;     // expert_capacity(k, f, T, E) (fixed) or at max_factor (bounded)
   int bpr;
+  // RouterKind::Cosine (moe_layer.hpp:10, gating.cpp:37-56); router == 0: linear (wg)
+  int router;
+  const double* cos_proj;  // [M][D]
+  const double* cos_ct;    // [D][E]: the expert embeddings transposed
+  const double* cos_en;    // [E]: |C_e|
+  double cos_tau;          // max(temperature, 0.01)
+  int cos_dim;             // D
+  double* cos_buf;         // [blocks*T][D] fp64 scratch: x . P
+  int32_t* err;            // set to 1 on a zero-norm projected token
 };
+
+// Cosine router weights: ct = C^T, en[e] = |C_e|; err = 2 if an expert row has zero norm.
+int cosine_prep_device(const double* ce, int E, int D, double* ct, double* en, int32_t* err,
+                       cudaStream_t st);
 
 struct GatingBuffers {
   int32_t* idxs;        // [blocks*T, k]

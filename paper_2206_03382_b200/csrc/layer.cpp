@@ -105,6 +105,10 @@ void validate(const moe_config& c) {
   if (c.top_k > 32) throw MoeError(MOE_EINVAL, "top_k > 32 unsupported");
   if (c.global_experts > 256) throw MoeError(MOE_EINVAL, "E > 256 unsupported by the gate kernel");
   if (c.dtype != MOE_DTYPE_BF16 && c.dtype != MOE_DTYPE_F32) throw MoeError(MOE_EINVAL, "dtype");
+  if (c.router != MOE_ROUTER_LINEAR && c.router != MOE_ROUTER_COSINE)
+    throw MoeError(MOE_EINVAL, "router kind");
+  if (c.router == MOE_ROUTER_COSINE && (c.global_experts > 64 || c.global_experts % 2 != 0))
+    throw MoeError(MOE_EINVAL, "cosine router: E <= 64 (even) supported");
   if (c.capacity_kind < 0 || c.capacity_kind > 2) throw MoeError(MOE_EINVAL, "capacity kind");
   if (c.capacity_kind != MOE_CAP_AUTO && !(c.capacity_factor > 0.0))
     throw MoeError(MOE_EINVAL, "capacity factor must be positive");
@@ -190,6 +194,16 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   const size_t Tk = static_cast<size_t>(T_) * k_;
   const size_t cpb = gate_cta_per_block(T_);
   wg_.alloc(sizeof(double) * M_ * E_);
+  gate_err_.alloc(sizeof(int32_t));
+  ck(cudaMemset(gate_err_.p, 0, sizeof(int32_t)), "memset");
+  if (cfg_.router == MOE_ROUTER_COSINE) {
+    const size_t D = MOE_COSINE_DIM;
+    cos_p_.alloc(sizeof(double) * M_ * D);
+    cos_ce_.alloc(sizeof(double) * E_ * D);
+    cos_ct_.alloc(sizeof(double) * E_ * D);
+    cos_en_.alloc(sizeof(double) * E_);
+    cos_buf_.alloc(sizeof(double) * static_cast<size_t>(T_) * D);
+  }
   w1_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
   w2_.alloc(static_cast<size_t>(esz_) * dE_ * V_ * M_);
   dw1_.alloc(sizeof(float) * dE_ * M_ * V_);
@@ -381,8 +395,54 @@ void Layer::init_params(uint64_t seed) {
     ckr(fill_uniform_device(static_cast<char*>(w2_.p) + le * mv * esz_, dt, mv, seed, o + mv, -0.5, 0.5, 0),
         "init w2");
   }
+  if (cfg_.router == MOE_ROUTER_COSINE) {
+    // RouterParams draws (moe_layer.cpp:154-160): cosine_proj (M x 256), cosine_experts (E x 256)
+    const int64_t D = MOE_COSINE_DIM;
+    const uint64_t o = static_cast<uint64_t>(M_) * E_;
+    ckr(fill_uniform_device(cos_p_.p, MOE_DTYPE_F64, static_cast<int64_t>(M_) * D, seed, o, -1.0, 1.0, 0),
+        "init cosine proj");
+    ckr(fill_uniform_device(cos_ce_.p, MOE_DTYPE_F64, static_cast<int64_t>(E_) * D, seed,
+                            o + static_cast<uint64_t>(M_) * D, -1.0, 1.0, 0),
+        "init cosine experts");
+    cos_tau_ = 1.0;  // RouterParams::temperature at init
+    ckr(cosine_prep_device(static_cast<const double*>(cos_ce_.p), E_, static_cast<int>(D),
+                           static_cast<double*>(cos_ct_.p), static_cast<double*>(cos_en_.p),
+                           static_cast<int32_t*>(gate_err_.p), 0),
+        "cosine prep");
+  }
   ck(cudaDeviceSynchronize(), "init_params");
   stats_dirty_ = true;
+}
+
+void Layer::set_cosine_router(const double* proj, const double* experts, double temperature) {
+  if (cfg_.router != MOE_ROUTER_COSINE) throw MoeError(MOE_ESTATE, "set_cosine_router: layer uses the linear router");
+  const int64_t D = MOE_COSINE_DIM;
+  for (int64_t e = 0; e < E_; ++e) {
+    double s = 0.0;
+    for (int64_t d = 0; d < D; ++d) s += experts[e * D + d] * experts[e * D + d];
+    if (s == 0.0) throw MoeError(MOE_EINVAL, "gate_cosine: zero-norm expert row");
+  }
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaMemcpy(cos_p_.p, proj, sizeof(double) * M_ * D, cudaMemcpyHostToDevice), "set_cosine_router");
+  ck(cudaMemcpy(cos_ce_.p, experts, sizeof(double) * E_ * D, cudaMemcpyHostToDevice), "set_cosine_router");
+  cos_tau_ = std::max(temperature, 0.01);  // clamped as gating.cpp:42
+  ckr(cosine_prep_device(static_cast<const double*>(cos_ce_.p), E_, static_cast<int>(D),
+                         static_cast<double*>(cos_ct_.p), static_cast<double*>(cos_en_.p),
+                         static_cast<int32_t*>(gate_err_.p), 0),
+      "cosine prep");
+  ck(cudaDeviceSynchronize(), "set_cosine_router");
+}
+
+// The cosine gate flags a zero-norm projected token on the device (no host sync in forward);
+// the reference throws invalid_argument from gate_cosine -- reported at the next host read.
+void Layer::check_gate_error() {
+  int32_t err = 0;
+  ck(cudaMemcpy(&err, gate_err_.p, sizeof(err), cudaMemcpyDeviceToHost), "copy");
+  if (err) {
+    ck(cudaMemset(gate_err_.p, 0, sizeof(int32_t)), "memset");
+    throw MoeError(MOE_EINVAL, err == 2 ? "gate_cosine: zero-norm expert row"
+                                        : "gate_cosine: zero-norm projected token");
+  }
 }
 
 void Layer::set_router(const double* wg) {
@@ -509,6 +569,16 @@ GatingArgs Layer::gating_args(const void* x) const {
   g.cap_kind = cfg_.capacity_kind;
   g.cap_formula = cfg_.capacity_kind == MOE_CAP_FIXED ? cap_ : cap_formula_;
   g.bpr = cfg_.bpr;
+  g.router = cfg_.router;
+  if (cfg_.router == MOE_ROUTER_COSINE) {
+    g.cos_proj = static_cast<const double*>(cos_p_.p);
+    g.cos_ct = static_cast<const double*>(cos_ct_.p);
+    g.cos_en = static_cast<const double*>(cos_en_.p);
+    g.cos_tau = cos_tau_;
+    g.cos_dim = MOE_COSINE_DIM;
+    g.cos_buf = static_cast<double*>(cos_buf_.p);
+  }
+  g.err = static_cast<int32_t*>(gate_err_.p);
   return g;
 }
 
@@ -1202,6 +1272,7 @@ void Layer::get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* ca
   if (!fwd_done_) throw MoeError(MOE_ESTATE, "get_routing: no forward yet");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ck(cudaDeviceSynchronize(), "sync");
+  check_gate_error();
   const size_t Tk = static_cast<size_t>(T_) * k_;
   if (idxs) ck(cudaMemcpy(idxs, idxs_.p, 4 * Tk, cudaMemcpyDeviceToHost), "copy");
   if (locs) ck(cudaMemcpy(locs, locs_.p, 4 * Tk, cudaMemcpyDeviceToHost), "copy");
@@ -1213,6 +1284,7 @@ void Layer::get_metrics(moe_step_metrics* m) {
   if (!fwd_done_) throw MoeError(MOE_ESTATE, "get_metrics: no forward yet");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ck(cudaEventSynchronize(ev_fwd_end_), "sync");
+  check_gate_error();
   float ms = 0.0f;
   ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");
   int32_t drops = 0;

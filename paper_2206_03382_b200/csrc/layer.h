@@ -58,6 +58,7 @@ class Layer {
 
   void init_params(uint64_t seed);
   void set_router(const double* wg);
+  void set_cosine_router(const double* proj, const double* experts, double temperature);
   void set_expert(int64_t le, const double* w1, const double* w2);
   void set_expert_slices(const double* w1s, const double* w2s);
   void forward(const void* x, void* y, cudaStream_t st);
@@ -130,6 +131,10 @@ class Layer {
   bool bwd_pending_ = false;  // last forward's receive buffer still held for a backward
 
   DevMem wg_, w1_, w2_, dw1_, dw2_;
+  // cosine router (RouterParams, gating.hpp:25-30): P [M][256], C [E][256], C^T, |C_e|, x . P
+  DevMem cos_p_, cos_ce_, cos_ct_, cos_en_, cos_buf_, gate_err_;
+  double cos_tau_ = 1.0;
+  void check_gate_error();
   DevMem idxs_, gates_, locs_, hist_, offs_, demand_, demand_max_, list_base_, fill_, list_, capd_,
       drops_;
   DevMem slot_token_, slot_gate_;

@@ -39,13 +39,15 @@ class MoELayerConfig:
     adaptive: bool = False
     degree: int = 1
     a2a_backend: str = "peer"   # "peer" (copy engines over NVLink) or "nccl"
+    router: str = "linear"      # RouterKind (moe_layer.hpp:10): "linear" or "cosine"
 
     def to_c(self) -> MoeConfig:
         return MoeConfig(self.world_size, self.gpus_per_node, self.global_experts, self.model_dim,
                          self.hidden_dim, self.tokens_per_step, self.top_k, _CAP[self.capacity],
                          float(self.capacity_factor), int(self.bpr), _DT[self.dtype],
                          int(self.adaptive), int(self.degree),
-                         {"peer": 0, "nccl": 1}[self.a2a_backend])
+                         {"peer": 0, "nccl": 1}[self.a2a_backend],
+                         {"linear": 0, "cosine": 1}[self.router])
 
     @property
     def local_experts(self) -> int:
@@ -148,6 +150,14 @@ class LayerState:
         import numpy as np
         a = np.ascontiguousarray(wg, np.float64)
         check(lib().moe_set_router(self._h, a.ctypes.data_as(C.c_void_p)), self._h)
+
+    def set_cosine_router(self, proj, experts, temperature: float = 1.0) -> None:
+        """RouterParams cosine_proj (M, 256), cosine_experts (E, 256), temperature."""
+        import numpy as np
+        a = np.ascontiguousarray(proj, np.float64)
+        b = np.ascontiguousarray(experts, np.float64)
+        check(lib().moe_set_cosine_router(self._h, a.ctypes.data_as(C.c_void_p),
+                                          b.ctypes.data_as(C.c_void_p), float(temperature)), self._h)
 
     def set_expert(self, local_e: int, w1, w2) -> None:
         import numpy as np

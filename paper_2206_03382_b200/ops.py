@@ -54,6 +54,30 @@ def gating(x: torch.Tensor, wg: torch.Tensor, blocks: int, k: int, capacity: str
     return idxs, gates, loc, cap.value, drops.value, probs
 
 
+def gating_cosine(x: torch.Tensor, proj: torch.Tensor, experts: torch.Tensor, blocks: int, k: int,
+                  temperature: float = 1.0, capacity: str = "fixed", factor: float = 1.0,
+                  bpr: bool = False, want_probs: bool = False):
+    """gate_cosine + run_gating_blocked (gating.cpp:37-56, 134-162): proj (M, D), experts (E, D)
+    fp64; same outputs as gating()."""
+    _need(x, "x"); _need(proj, "proj"); _need(experts, "experts")
+    n, M = x.shape
+    E, D = experts.shape
+    if n % blocks:
+        raise _lib.MoeError(_lib.MOE_EINVAL, "run_gating_blocked: rows must split into equal blocks")
+    T = n // blocks
+    dev = x.device
+    idxs = torch.empty(n, k, dtype=torch.int32, device=dev)
+    gates = torch.empty(n, k, dtype=torch.float64, device=dev)
+    loc = torch.empty(n, k, dtype=torch.int32, device=dev)
+    probs = torch.empty(n, E, dtype=torch.float64, device=dev) if want_probs else None
+    cap, drops = C.c_int64(), C.c_int64()
+    check(lib().moe_op_gating_cosine(_p(x), _DT[x.dtype], _p(proj), _p(experts), D,
+                                     float(temperature), blocks, T, M, E, k, _CAP[capacity],
+                                     float(factor), int(bpr), _p(idxs), _p(gates), _p(loc),
+                                     _p(probs), C.byref(cap), C.byref(drops), _st(x)))
+    return idxs, gates, loc, cap.value, drops.value, probs
+
+
 def encode(x, blocks, E, k, capacity, degree, idxs, locations):
     """fast_encode_range per block + partition_capacity -> (blocks, degree, E, cc, M)."""
     _need(x, "x")

@@ -56,6 +56,14 @@ def draw_offsets(M: int, E: int, V: int, W: int, T: int) -> dict:
                 expert_stride=2 * M * V)
 
 
+def cosine_params(seed: int, M: int, E: int):
+    """RouterParams cosine_proj (M, 256) and cosine_experts (E, 256) (moe_layer.cpp:154-160)."""
+    off = draw_offsets(M, E, 1, 1, 1)
+    proj = uniform(seed, off["cosine_proj"], M * COSINE_DIM).reshape(M, COSINE_DIM)
+    experts = uniform(seed, off["cosine_experts"], E * COSINE_DIM).reshape(E, COSINE_DIM)
+    return proj, experts
+
+
 def layer_params(seed: int, M: int, E: int, V: int, experts=None):
     """Wg (M,E) fp64 and w1 (n,M,V), w2 (n,V,M) fp64 for the given global experts."""
     off = draw_offsets(M, E, V, 1, 1)

@@ -14,7 +14,9 @@ def layer_inputs(seed, W, T, M, V, E, dtype="bf16", with_dy=True, experts=None):
     x = rng.uniform(seed, off["x"], W * T * M).reshape(W * T, M)
     dy = rng.uniform(seed, off["dy"], W * T * M).reshape(W * T, M) if with_dy else None
     r = lambda a: rng.round_dtype(a, dtype)  # noqa: E731
-    return dict(wg=wg, w1=r(w1), w2=r(w2), x=r(x), dy=r(dy) if with_dy else None)
+    cp, ce = rng.cosine_params(seed, M, E)
+    return dict(wg=wg, w1=r(w1), w2=r(w2), x=r(x), dy=r(dy) if with_dy else None,
+                cos_proj=cp, cos_experts=ce)
 
 
 def probs_to_inputs(probs):

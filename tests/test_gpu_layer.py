@@ -193,3 +193,53 @@ def test_host_async_pipeline_matches_device_calls(cuda):
         r = forward(ref, xs[i].cuda())
         g = backward(ref, r.saved, dys[i].cuda())
         assert torch.equal(r.y.cpu(), ys[i]) and torch.equal(g.dx.cpu(), dxs[i])
+
+
+@pytest.mark.parametrize("E,k,f,M,V,T,bpr,dt,cap", [
+    (4, 1, 1.0, 3, 8, 8, False, "f32", "auto"),           # test_moe_layer.cpp:62-66 shape, W=1
+    (16, 2, 1.25, 256, 512, 2048, True, "bf16", "fixed"),
+    (32, 1, 1.0, 1024, 4096, 4096, False, "bf16", "auto"),
+])
+def test_layer_cosine_router(cuda, E, k, f, M, V, T, bpr, dt, cap):
+    """RouterKind::Cosine inside the layer (route_probabilities, moe_layer.cpp:165-169; draws
+    moe_layer.cpp:154-160): routing bit-exact, outputs / gradients at the dtype tolerance."""
+    cfg = MoELayerConfig(world_size=1, global_experts=E, model_dim=M, hidden_dim=V,
+                         tokens_per_step=T, top_k=k, capacity=cap, capacity_factor=f, bpr=bpr,
+                         dtype=dt, router="cosine")
+    inp = layer_inputs(402, 1, T, M, V, E, dt)
+    st = LayerState.init(cfg, 402)
+    tdt = cfg.torch_dtype
+    res = forward(st, torch.as_tensor(inp["x"]).to(tdt).cuda())
+    g = backward(st, res.saved, torch.as_tensor(inp["dy"]).to(tdt).cuda())
+    kind = {"fixed": 0, "auto": 1, "bounded": 2}[cap]
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], 1, k, kind, f,
+                            bpr, cosine=(inp["cos_proj"], inp["cos_experts"], 1.0))
+    idxs, loc, gates, capv = st.routing()
+    assert capv == ref["capacity"]
+    assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
+    np.testing.assert_allclose(gates, ref["gates"], rtol=1e-12, atol=0)
+    tol = 1e-5 if dt == "f32" else 2e-2
+    for name, got in (("y", res.y), ("dx", g.dx), ("dw1", g.dw1), ("dw2", g.dw2)):
+        assert oracle.max_rel_diff(got.double().cpu().numpy(), ref[name]) < tol, name
+
+
+def test_layer_cosine_router_set_params(cuda):
+    """moe_set_cosine_router (explicit RouterParams, temperature clamp) == on-device init draw."""
+    E, M, V, T = 8, 64, 128, 256
+    cfg = MoELayerConfig(global_experts=E, model_dim=M, hidden_dim=V, tokens_per_step=T,
+                         top_k=2, router="cosine")
+    inp = layer_inputs(9, 1, T, M, V, E, "bf16")
+    a = LayerState.init(cfg, 9)
+    b = LayerState.init(cfg, 9)
+    b.set_cosine_router(inp["cos_proj"], inp["cos_experts"], 1.0)
+    x = torch.as_tensor(inp["x"]).to(torch.bfloat16).cuda()
+    assert torch.equal(forward(a, x).y, forward(b, x).y)
+    b.set_cosine_router(inp["cos_proj"], inp["cos_experts"], 1e-9)   # clamped to 0.01
+    ya = forward(b, x).y
+    b.set_cosine_router(inp["cos_proj"], inp["cos_experts"], 0.01)
+    assert torch.equal(ya, forward(b, x).y)
+    from paper_2206_03382_b200 import MoeError
+    bad = inp["cos_experts"].copy()
+    bad[1] = 0.0
+    with pytest.raises(MoeError):
+        b.set_cosine_router(inp["cos_proj"], bad, 1.0)

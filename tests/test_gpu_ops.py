@@ -208,3 +208,53 @@ def test_fill_uniform_matches_host_stream(cuda):
     ops.fill_uniform(ob, 402, 12345, -0.5, 0.5)
     assert np.array_equal(ob.double().cpu().numpy(),
                           rng.round_bf16(rng.uniform(402, 12345, 100000, -0.5, 0.5)))
+
+
+# ---------------------------------------------------------------- cosine router parity
+COSINE_CASES = [
+    # blocks, T, M, E, k, cap kind, factor, bpr, dtype, temperature
+    (1, 2048, 256, 8, 1, "fixed", 1.0, False, "bf16", 1.0),
+    (2, 1000, 64, 32, 2, "auto", 1.0, True, "bf16", 0.07),
+    (3, 333, 40, 64, 2, "fixed", 0.5, True, "f32", 1e-9),   # temperature clamped to 0.01
+    (1, 32768, 1024, 32, 1, "fixed", 1.0, False, "bf16", 1.0),  # TGT shape
+]
+
+
+@pytest.mark.parametrize("case", COSINE_CASES, ids=str)
+def test_cosine_gating_matches_oracle(cuda, case):
+    """gate_cosine (gating.cpp:37-56) + run_gating_blocked on the GPU (fp64 DMMA projection and
+    cosine logits) against the oracle: routing bit-exact, gates to 1e-12."""
+    from paper_2206_03382_b200 import ops
+    blocks, T, M, E, k, cap, f, bpr, dt, tau = case
+    seed = 77 + T + E
+    x = rng.round_dtype(rng.uniform(seed, 0, blocks * T * M).reshape(blocks * T, M), dt)
+    proj = rng.uniform(seed, blocks * T * M, M * 256).reshape(M, 256)
+    experts = rng.uniform(seed, blocks * T * M + M * 256, E * 256).reshape(E, 256)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    xi = torch.as_tensor(x).to(tdt).cuda()
+    idxs, gates, loc, gcap, drops, probs = ops.gating_cosine(
+        xi, torch.as_tensor(proj).cuda(), torch.as_tensor(experts).cuda(), blocks, k, tau, cap, f,
+        bpr, want_probs=True)
+    oprobs = oracle.gate_cosine(x, proj, experts, tau)
+    np.testing.assert_allclose(probs.cpu().numpy(), oprobs, rtol=1e-11, atol=1e-300)
+    kind = {"fixed": 0, "auto": 1, "bounded": 2}[cap]
+    oi, og, ol, ocap = oracle.run_gating_blocked(oprobs, blocks, k, kind, f, bpr)
+    assert gcap == ocap
+    assert np.array_equal(idxs.cpu().numpy(), oi) and np.array_equal(loc.cpu().numpy(), ol)
+    assert drops == int((ol < 0).sum())
+    np.testing.assert_allclose(gates.cpu().numpy(), og, rtol=1e-12, atol=0)
+
+
+def test_cosine_gating_rejects_zero_norms(cuda):
+    """A zero-norm expert row or projected token raises invalid_argument (gating.cpp:46-49)."""
+    from paper_2206_03382_b200 import ops, MoeError
+    x = torch.rand(128, 64, device="cuda").to(torch.bfloat16)
+    proj = torch.rand(64, 256, device="cuda", dtype=torch.float64) - 0.5
+    experts = torch.rand(8, 256, device="cuda", dtype=torch.float64) - 0.5
+    experts[3] = 0.0
+    with pytest.raises(MoeError):
+        ops.gating_cosine(x, proj, experts, 1, 1)
+    experts[3] = 1.0
+    x[5] = 0.0
+    with pytest.raises(MoeError):
+        ops.gating_cosine(x, proj, experts, 1, 1)

@@ -233,3 +233,24 @@ def test_bf16_rounding_is_nearest_even():
     lo_even = ((u >> np.uint64(45)) & np.uint64(1)) == 0
     want = np.where(dlo < dhi, lo, np.where(dhi < dlo, hi, np.where(lo_even, lo, hi)))
     assert np.array_equal(rng.round_bf16(x), want)
+
+
+def test_cosine_gate_kat():
+    """test_gating.cpp:38-53: the temperature clamps at 0.01, rows sum to 1, a zero-norm expert
+    row is rejected (invalid_argument)."""
+    rng = np.random.default_rng(13)
+    x = rng.uniform(-1, 1, (4, 3))
+    proj = rng.uniform(-1, 1, (3, 6))
+    experts = rng.uniform(-1, 1, (5, 6))
+    p = oracle.gate_cosine(x, proj, experts, 1e-9)
+    p2 = oracle.gate_cosine(x, proj, experts, 0.01)
+    assert np.abs(p - p2).max() == 0.0
+    np.testing.assert_allclose(p.sum(axis=1), 1.0, rtol=1e-12)
+    experts[2] = 0.0
+    with pytest.raises(ValueError):
+        oracle.gate_cosine(x, proj, experts, 1.0)
+    # zero-norm projected token (x row of zeros) is rejected as well (gating.cpp:46-47)
+    experts[2] = 1.0
+    x[1] = 0.0
+    with pytest.raises(ValueError):
+        oracle.gate_cosine(x, proj, experts, 1.0)

@@ -15,7 +15,7 @@ from tests.helpers import layer_inputs  # noqa: E402
 
 
 def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, cap="fixed",
-        seed=402):
+        router="linear", seed=402):
     E = E_per * W
     ce = backend == "peer-ce"  # peer backend with the copy-engine combine (fused combine off)
     if ce:
@@ -24,7 +24,7 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
                          hidden_dim=V, tokens_per_step=T, top_k=k, capacity=cap,
                          capacity_factor=f, bpr=bpr, dtype=dt, degree=degree, adaptive=adaptive,
-                         a2a_backend=backend)
+                         a2a_backend=backend, router=router)
     obj = [LayerState.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
@@ -41,7 +41,9 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
         g = backward(st, res.saved, dys)
     torch.cuda.synchronize()
     kind = {"fixed": 0, "auto": 1, "bounded": 2}[cap]
-    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, kind, f, bpr)
+    cos = (inp["cos_proj"], inp["cos_experts"], 1.0) if router == "cosine" else None
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, kind, f, bpr,
+                            cosine=cos)
     sl = slice(rank * T, (rank + 1) * T)
     el = slice(rank * E_per, (rank + 1) * E_per)
     idxs, loc, gates, cap = st.routing()
@@ -86,6 +88,9 @@ def main():
         (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "nccl"),
         (2, 2, 1.0, 256, 512, 512, True, "bf16", 2, False, "peer", "auto"),
         (2, 1, 1.25, 128, 256, 400, False, "bf16", 4, False, "nccl", "bounded"),
+        # test_moe_layer.cpp:62-66: cosine router, auto capacity, base_config(2, 2, 2, T=4, M=3, V=8)
+        (2, 1, 1.0, 3, 8, 4, False, "f32", 1, False, "peer", "auto", "cosine"),
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer", "fixed", "cosine"),
     ]
     all_ok = True
     for c in cases:
