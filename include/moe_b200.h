@@ -139,6 +139,9 @@ int moe_set_router(moe_handle* h, const double* wg_host);
  * moe_get_metrics / moe_get_routing call (MOE_EINVAL). */
 int moe_set_cosine_router(moe_handle* h, const double* proj_host, const double* experts_host,
                           double temperature);
+/* FixedCapacity{f} from the next forward on (the scenario runner's per-step trace,
+ * bench.cpp:199-201). Collective when W > 1 (buffers may grow): every rank calls it. */
+int moe_set_capacity_factor(moe_handle* h, double f);
 /* Full weights of local expert `local_e` (global index rank*E/W + local_e); host fp64
  * w1 (M, V), w2 (V, M) -- ExpertParams::assemble layout (parallelism.cpp:80-90). */
 int moe_set_expert(moe_handle* h, int64_t local_e, const double* w1_host, const double* w2_host);

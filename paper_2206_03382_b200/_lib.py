@@ -69,6 +69,7 @@ SIGNATURES = {
     "moe_init_params": (I32, [P, U64]),
     "moe_set_router": (I32, [P, P]),
     "moe_set_cosine_router": (I32, [P, P, P, D]),
+    "moe_set_capacity_factor": (I32, [P, D]),
     "moe_set_expert": (I32, [P, I64, P, P]),
     "moe_set_expert_slices": (I32, [P, P, P]),
     "moe_forward": (I32, [P, P, P, P]),

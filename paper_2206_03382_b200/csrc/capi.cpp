@@ -266,6 +266,7 @@ const char* moe_last_error_global(void) { return g_err.c_str(); }
 
 int moe_init_params(moe_handle* h, uint64_t seed) { LAYER_CALL(h, h->layer->init_params(seed)); }
 int moe_set_router(moe_handle* h, const double* wg) { LAYER_CALL(h, h->layer->set_router(wg)); }
+int moe_set_capacity_factor(moe_handle* h, double f) { LAYER_CALL(h, h->layer->set_capacity_factor(f)); }
 int moe_set_cosine_router(moe_handle* h, const double* proj, const double* experts, double temperature) {
   LAYER_CALL(h, h->layer->set_cosine_router(proj, experts, temperature));
 }

@@ -414,6 +414,17 @@ void Layer::init_params(uint64_t seed) {
   stats_dirty_ = true;
 }
 
+void Layer::set_capacity_factor(double f) {
+  if (cfg_.capacity_kind != MOE_CAP_FIXED)
+    throw MoeError(MOE_ESTATE, "set_capacity_factor: layer capacity policy is not Fixed");
+  if (!(f > 0.0)) throw MoeError(MOE_EINVAL, "capacity factor must be positive");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  cfg_.capacity_factor = f;
+  cap_ = static_cast<int>(expert_capacity(k_, f, T_, E_));
+  cap_formula_ = cap_;
+  alloc_capacity(cap_);  // collective growth when needed
+}
+
 void Layer::set_cosine_router(const double* proj, const double* experts, double temperature) {
   if (cfg_.router != MOE_ROUTER_COSINE) throw MoeError(MOE_ESTATE, "set_cosine_router: layer uses the linear router");
   const int64_t D = MOE_COSINE_DIM;

@@ -59,6 +59,7 @@ class Layer {
   void init_params(uint64_t seed);
   void set_router(const double* wg);
   void set_cosine_router(const double* proj, const double* experts, double temperature);
+  void set_capacity_factor(double f);
   void set_expert(int64_t le, const double* w1, const double* w2);
   void set_expert_slices(const double* w1s, const double* w2s);
   void forward(const void* x, void* y, cudaStream_t st);

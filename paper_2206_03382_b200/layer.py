@@ -151,6 +151,10 @@ class LayerState:
         a = np.ascontiguousarray(wg, np.float64)
         check(lib().moe_set_router(self._h, a.ctypes.data_as(C.c_void_p)), self._h)
 
+    def set_capacity_factor(self, f: float) -> None:
+        """FixedCapacity{f} from the next forward on (collective for W > 1)."""
+        check(lib().moe_set_capacity_factor(self._h, float(f)), self._h)
+
     def set_cosine_router(self, proj, experts, temperature: float = 1.0) -> None:
         """RouterParams cosine_proj (M, 256), cosine_experts (E, 256), temperature."""
         import numpy as np

@@ -32,3 +32,23 @@ def test_expert_parallel_parity(cuda):
     print(r.stdout[-4000:], r.stderr[-2000:])
     assert r.returncode == 0
     assert "FAIL" not in r.stdout and r.stdout.count("PASS") >= 10
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_scenario_runner_two_ranks(cuda, tmp_path):
+    """moe_bench run on the reference's W = 2 "tiny" scenario (test_bench.cpp:104-121), one
+    process per GPU: 4 records, capacity follows the f cycle, measured seconds > 0."""
+    from paper_2206_03382_b200 import scenario as S
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "-m",
+           "paper_2206_03382_b200.scenario", "run", str(ROOT / "tests" / "golden" / "scenario_tiny.json"),
+           "--out", str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    recs = S.parse_records_csv((tmp_path / "records.csv").read_text())
+    assert [x.step for x in recs] == [0, 1, 2, 3]
+    assert [x.f for x in recs] == [1.0, 2.0, 1.0, 2.0]
+    assert recs[0].capacity < recs[1].capacity
+    assert all(x.sim_seconds > 0 and x.strategy == "linearx1" for x in recs)
