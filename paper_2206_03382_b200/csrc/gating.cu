@@ -33,7 +33,8 @@ namespace {
 #endif
 // DMMA gate CTA: MOE_DM_WARPS warps x MOE_DM_MT 8-token m-tiles = the 64-token block. Measured
 // at TGT: 8 warps x 1 m-tile 113 us, 4 x 2 123 us, 32-token blocks (2 x 2 / 4 x 1) 122-148 us,
-// K split over two warp groups 120 us -- warps in flight beat operand reuse here.
+// K split over two warp groups 120 us -- warps in flight beat operand reuse here. sm_100a has
+// only the DMMA.8x8x4 unit (mma.m16n8k16.f64 compiles to 8 of them), so m8n8k4 loses nothing.
 #ifndef MOE_DM_WARPS
 #define MOE_DM_WARPS 8
 #endif
