@@ -195,42 +195,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       else
         ptx::tma_load_3d(m, bar, dst, c0, c1, c2);
     };
-    for (uint32_t tile = unit0; tile < ntiles; tile += unit_step) {
-      const TileCoord tc = tile_coord<kRowK, C::TM>(args, tile);
+    // the (A, B) boxes of k-block kb of a tile into one smem stage
+    auto issue = [&](const TileCoord& tc, uint32_t kb, uint8_t* sa, uint8_t* sb, uint64_t* bar) {
       const uint32_t m0 = tc.m0 + rank * BM;       // this CTA's A rows
       const uint32_t nb = tc.n0 + rank * C::BNL;   // this CTA's B columns
-      for (uint32_t kb = 0; kb < nkb; ++kb) {
-        TRACE_WAIT(w_prod, ptx::mbar_wait(&empty_bar[stage], phase ^ 1));
-        uint8_t* sa = smem + C::SMEM_A_OFF + stage * C::A_BYTES;
-        uint8_t* sb = smem + C::SMEM_B_OFF + stage * C::B_BYTES;
-        if constexpr (!kRowK) {
-          const int seg = static_cast<int>((args.seg_base + tc.s) * args.G + tc.g);
-          const int k0 = static_cast<int>(kb * BK);
-          // A: K-major [seg][seg_rows][K]
-          load(&tmA, &full_bar[stage], sa, k0, static_cast<int>(m0), seg);
-          if constexpr (!kBMN) {
-            // B: K-major [G][N][K]
-            load(&tmB, &full_bar[stage], sb, k0, static_cast<int>(nb), static_cast<int>(tc.g));
-          } else {
-            // B: N-major [G][K][N], 64-column atoms
-#pragma unroll
-            for (uint32_t a = 0; a < C::BNL / 64; ++a)
-              load(&tmB, &full_bar[stage], sb + a * (BK * 128), static_cast<int>(nb + a * 64), k0,
-                   static_cast<int>(tc.g));
-          }
+      auto go = [&](const CUtensorMap* m, void* dst, int c0, int c1, int c2) {
+        load(m, bar, dst, c0, c1, c2);
+      };
+      if constexpr (!kRowK) {
+        const int seg = static_cast<int>((args.seg_base + tc.s) * args.G + tc.g);
+        const int k0 = static_cast<int>(kb * BK);
+        // A: K-major [seg][seg_rows][K]
+        go(&tmA, sa, k0, static_cast<int>(m0), seg);
+        if constexpr (!kBMN) {
+          // B: K-major [G][N][K]
+          go(&tmB, sb, k0, static_cast<int>(nb), static_cast<int>(tc.g));
         } else {
-          const uint32_t s = kb / kb_per_seg;
-          const int r0 = static_cast<int>((kb % kb_per_seg) * BK);
-          const int seg = static_cast<int>((args.seg_base + s) * args.G + tc.g);
-          // A^T: rows are K, MN-major [seg][seg_rows][Mo]
-#pragma unroll
-          for (uint32_t a = 0; a < BM / 64; ++a)
-            load(&tmA, &full_bar[stage], sa + a * (BK * 128), static_cast<int>(m0 + a * 64), r0, seg);
-          // B: N-major [seg][seg_rows][N]
+          // B: N-major [G][K][N], 64-column atoms
 #pragma unroll
           for (uint32_t a = 0; a < C::BNL / 64; ++a)
-            load(&tmB, &full_bar[stage], sb + a * (BK * 128), static_cast<int>(nb + a * 64), r0, seg);
+            go(&tmB, sb + a * (BK * 128), static_cast<int>(nb + a * 64), k0, static_cast<int>(tc.g));
         }
+      } else {
+        const uint32_t s = kb / kb_per_seg;
+        const int r0 = static_cast<int>((kb % kb_per_seg) * BK);
+        const int seg = static_cast<int>((args.seg_base + s) * args.G + tc.g);
+        // A^T: rows are K, MN-major [seg][seg_rows][Mo]
+#pragma unroll
+        for (uint32_t a = 0; a < BM / 64; ++a)
+          go(&tmA, sa + a * (BK * 128), static_cast<int>(m0 + a * 64), r0, seg);
+        // B: N-major [seg][seg_rows][N]
+#pragma unroll
+        for (uint32_t a = 0; a < C::BNL / 64; ++a)
+          go(&tmB, sb + a * (BK * 128), static_cast<int>(nb + a * 64), r0, seg);
+      }
+    };
+    for (uint32_t tile = unit0; tile < ntiles; tile += unit_step) {
+      const TileCoord tc = tile_coord<kRowK, C::TM>(args, tile);
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + C::SMEM_A_OFF + stage * C::A_BYTES;
+        uint8_t* sb = smem + C::SMEM_B_OFF + stage * C::B_BYTES;
+        issue(tc, kb, sa, sb, &full_bar[stage]);
         if (leader)
           ptx::mbar_arrive_expect_tx(&full_bar[stage], (C::A_BYTES + C::B_BYTES) * kCG);
         else
