@@ -110,13 +110,26 @@ __device__ __forceinline__ void zero_dropped_rows(const DropZero& d) {
   }
 }
 
+// Destination row of slot-major row `row` = (block b, chunk i, expert e, slot c % cc): the send
+// buffer, or (this rank's experts, LocalDest) the receive buffer's own-source segment.
+template <typename T>
+__device__ __forceinline__ T* gather_dst(T* z, const LocalDest& ld, const SlotGeom& g, size_t row,
+                                         int i, int e, int rem) {
+  if (ld.recv != nullptr && e / ld.dE == ld.rank) {
+    const size_t rrow = (static_cast<size_t>(i * ld.W + ld.rank) * ld.dE + (e - ld.rank * ld.dE)) * g.cc +
+                        rem % g.cc;
+    return static_cast<T*>(ld.recv) + rrow * g.M;
+  }
+  return z + row * g.M;
+}
+
 // ------------------------------------------------------------------ encode
 // Z[row] = x[slot_token[row]] or 0. Rows enumerate [block][chunk][expert][cc].
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_kernel(SlotGeom g, const T* __restrict__ x, const int32_t* __restrict__ slot_token,
                   T* __restrict__ z, float* __restrict__ rowmax, DropZero dzero,
-                  unsigned int* __restrict__ reset) {
+                  unsigned int* __restrict__ reset, LocalDest ld) {
   pdl_entry();
   if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0u;
   zero_dropped_rows(dzero);
@@ -134,7 +147,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     if constexpr (kVec) {
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
-      uint4* dst = reinterpret_cast<uint4*>(z + row * g.M);
+      uint4* dst = reinterpret_cast<uint4*>(gather_dst(z, ld, g, row, i, e, rem));
       float amax = 0.0f;
       if (t < 0) {
         for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
@@ -168,7 +181,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         if (lane == 0) rowmax[row] = amax;
       }
     } else {
-      T* dst = z + row * g.M;
+      T* dst = gather_dst(z, ld, g, row, i, e, rem);
       float amax = 0.0f;
       for (int m = lane; m < g.M; m += 32) {
         const T v = t < 0 ? from_f<T>(0.0f) : x[static_cast<size_t>(t) * g.M + m];
@@ -254,7 +267,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     decode_bwd_kernel(SlotGeom g, const T* __restrict__ dy, const int32_t* __restrict__ slot_token,
-                      const float* __restrict__ slot_gate, T* __restrict__ dz, DropZero dzero) {
+                      const float* __restrict__ slot_gate, T* __restrict__ dz, DropZero dzero,
+                      LocalDest ld) {
   pdl_entry();
   zero_dropped_rows(dzero);
   const int lane = threadIdx.x % 32;
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     if constexpr (kVec) {
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
-      uint4* dst = reinterpret_cast<uint4*>(dz + row * g.M);
+      uint4* dst = reinterpret_cast<uint4*>(gather_dst(dz, ld, g, row, i, e, rem));
       if (t < 0) {
         for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
       } else {
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         }
       }
     } else {
-      T* dst = dz + row * g.M;
+      T* dst = gather_dst(dz, ld, g, row, i, e, rem);
       for (int m = lane; m < g.M; m += 32)
         dst[m] = t < 0 ? from_f<T>(0.0f) : from_f<T>(gv * to_f(dy[static_cast<size_t>(t) * g.M + m]));
     }
@@ -415,18 +429,20 @@ bool vec_ok(int dtype, int M) { return (M * (dtype == 1 ? 4 : 2)) % 16 == 0; }
 }  // namespace
 
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax, const DropZero& dzero, unsigned int* reset) {
+                  cudaStream_t st, float* rowmax, const DropZero& dzero, unsigned int* reset,
+                  const LocalDest& local) {
+  if (local.recv && (g.blocks != 1 || local.dE < 1 || local.W * local.dE != g.E)) return -1;
   if (dzero.out && dzero.row_bytes % 16 != 0) return -1;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) launch_k(encode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset);
-    else launch_k(encode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset);
+    if (v) launch_k(encode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset, local);
+    else launch_k(encode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset, local);
   } else {
     using B = __nv_bfloat16;
-    if (v) launch_k(encode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset);
-    else launch_k(encode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset);
+    if (v) launch_k(encode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset, local);
+    else launch_k(encode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset, local);
   }
   return launch_status();
 }
@@ -448,18 +464,19 @@ int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* id
 
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
                            const int32_t* slot_token, const float* slot_gate, void* dz,
-                           cudaStream_t st, const DropZero& dzero) {
+                           cudaStream_t st, const DropZero& dzero, const LocalDest& local) {
+  if (local.recv && (g.blocks != 1 || local.dE < 1 || local.W * local.dE != g.E)) return -1;
   if (dzero.out && dzero.row_bytes % 16 != 0) return -1;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) launch_k(decode_bwd_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
-    else launch_k(decode_bwd_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero);
+    if (v) launch_k(decode_bwd_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero, local);
+    else launch_k(decode_bwd_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(dy), slot_token, slot_gate, static_cast<float*>(dz), dzero, local);
   } else {
     using B = __nv_bfloat16;
-    if (v) launch_k(decode_bwd_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
-    else launch_k(decode_bwd_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero);
+    if (v) launch_k(decode_bwd_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero, local);
+    else launch_k(decode_bwd_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(dy), slot_token, slot_gate, static_cast<B*>(dz), dzero, local);
   }
   return launch_status();
 }

@@ -83,17 +83,26 @@ struct DropZero {
   size_t row_bytes = 0;
 };
 
+// W > 1 peer backend: this rank's own experts' rows go straight into its receive buffer
+// ([chunk][W][dE][cc] layout, source = rank) instead of the send buffer -- the local block of
+// the all-to-all is never copied.
+struct LocalDest {
+  void* recv = nullptr;
+  int W = 1, rank = 0, dE = 0;
+};
+
 // dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rowmax (optional, [z rows]):
 // max_m |z[row][m]| for the ReLU-mask certificate.
 // reset (optional): a counter zeroed by the pass (the ReLU-fixup count; no memset node).
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
                   cudaStream_t st, float* rowmax = nullptr, const DropZero& dzero = DropZero{},
-                  unsigned int* reset = nullptr);
+                  unsigned int* reset = nullptr, const LocalDest& local = LocalDest{});
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
                   const int32_t* locations, const double* gates, void* y, cudaStream_t st);
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
                            const int32_t* slot_token, const float* slot_gate, void* dz,
-                           cudaStream_t st, const DropZero& dzero = DropZero{});
+                           cudaStream_t st, const DropZero& dzero = DropZero{},
+                           const LocalDest& local = LocalDest{});
 // Optional d_gates[t, j] = <Z[e, loc], dy[t]> (dispatch.cpp:143-156); 0 for dropped.
 int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
                                  const int32_t* idxs, const int32_t* locations, double* dgates,

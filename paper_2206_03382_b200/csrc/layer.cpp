@@ -723,10 +723,17 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     yzero.out = y;
     yzero.row_bytes = static_cast<size_t>(M_) * esz_;
   }
+  LocalDest own;  // peer backend: this rank's experts' rows go straight into its receive buffer
+  if (peer_) {
+    own.recv = recv_.p;
+    own.W = W_;
+    own.rank = rank_;
+    own.dE = dE_;
+  }
   prof_mark(kPhEncode, true, st);
   ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st,
                     (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr, yzero,
-                    (cert && W_ == 1) ? static_cast<unsigned int*>(fix_count_.p) : nullptr),
+                    (cert && W_ == 1) ? static_cast<unsigned int*>(fix_count_.p) : nullptr, own),
       "encode");
   prof_mark(kPhEncode, false, st);
   ++launches_;
@@ -799,7 +806,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     peer_->wait_peers_freed(comm_stream_, 0, e0);
     prof_mark(kPhA2aFwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {
-      peer_push(0, z_.p, i, 0, e0, ev_a_[i]);  // ev_a_[i]: my own block of chunk i copied
+      peer_push(0, z_.p, i, 0, e0, nullptr);  // my own block: written into recv by encode
       tl_mark("dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
     // up GEMM over sources [s0, s1) of chunk i; the range's first kernel (the certificate's row
@@ -827,7 +834,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       prof_mark(kPhUp, false, st);
     };
     for (int i = 0; i < degree_; ++i) {
-      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");  // my own block of chunk i is in place
       const FlagWait fw = peer_->ready_wait(0, i, e0);
       down.seg_base = i * W_;
       if (i == 0 && local_first_) {
@@ -970,7 +976,14 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     dxzero.row_bytes = static_cast<size_t>(M_) * esz_;
   }
   prof_mark(kPhDecodeBwd, true, st);
-  ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st, dxzero),
+  LocalDest own;  // peer backend: this rank's experts' dZ rows go straight into drecv
+  if (peer_) {
+    own.recv = drecv_.p;
+    own.W = W_;
+    own.rank = rank_;
+    own.dE = dE_;
+  }
+  ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st, dxzero, own),
       "decode_bwd");
   prof_mark(kPhDecodeBwd, false, st);
   ++launches_;
@@ -1042,11 +1055,10 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     peer_->wait_peers_freed(comm_stream_, 2, e2);
     prof_mark(kPhA2aBwd, true, comm_stream_);
     for (int i = 0; i < degree_; ++i) {  // adjoint of combine
-      peer_push(2, dz_.p, i, 0, e2, ev_a_[i]);
+      peer_push(2, dz_.p, i, 0, e2, nullptr);  // my own block: written into drecv by decode_bwd
       tl_mark("bwd dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
     for (int i = 0; i < degree_; ++i) {
-      ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
       const FlagWait fw = peer_->ready_wait(2, i, e2);
       dg.seg_base = i * W_;
       auto dgm_range = [&](int s0, int s1, bool wait) {

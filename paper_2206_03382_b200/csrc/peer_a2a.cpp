@@ -182,6 +182,7 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
   ck(cudaEventRecord(ev_in_, copy), "event");
   for (int i = 0; i < world_; ++i) {
     const int p = (rank_ + i) % world_;
+    if (p == rank_ && local_done == nullptr) continue;
     cudaStream_t ps = pstreams_[p];
     ck(cudaStreamWaitEvent(ps, ev_in_, 0), "wait");
     char* dst = static_cast<char*>(p == rank_ ? local_bufs_[ch] : peer_bufs_[ch][p]) + ro[rank_] * esz;
@@ -192,7 +193,8 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
     else if (local_done) ck(cudaEventRecord(local_done, ps), "event");
     ck(cudaEventRecord(ev_out_[p], ps), "event");
   }
-  for (int p = 0; p < world_; ++p) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_ || local_done) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
 }
 
 void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch) {

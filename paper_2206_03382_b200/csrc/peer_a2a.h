@@ -41,7 +41,8 @@ class PeerExchange {
   // Copy stream: push block p of `src` (offset so[p]) to peer p's channel buffer at the offset p
   // receives from this rank, ro[rank] (moe_a2a_plan is source-symmetric), then publish
   // ready[ch][me][chunk] = epoch to each peer.
-  // local_done (optional) is recorded right after this rank's own block has been copied.
+  // local_done: recorded right after this rank's own block has been copied; nullptr: the own
+  // block is not copied (the producing kernel wrote it into the receive buffer itself).
   void push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
                   const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch,
                   cudaEvent_t local_done = nullptr);
