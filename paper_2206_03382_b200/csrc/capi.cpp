@@ -131,23 +131,23 @@ unsigned long long* certified_up(int dtype, const void* x, const void* w1, void*
     expert_gemm(moe::kGemmUp, dtype, -1, x, w1, act, up, static_cast<int>(n), st);
     return nullptr;
   }
-  float* colabs = sc.get<float>(static_cast<size_t>(n) * V);
-  float* colabs_blk = sc.get<float>(static_cast<size_t>(n) * (V / 64 + 1));
+  float* colnorm = sc.get<float>(static_cast<size_t>(n) * V);
+  float* colnorm_blk = sc.get<float>(static_cast<size_t>(n) * (V / 64 + 1));
   auto* mask = sc.get<unsigned long long>(static_cast<size_t>(n) * rows * (V / 64 + 1));
   void* w1t = sc.get<char>(static_cast<size_t>(n) * M * V * 2);
-  float* rowmax = sc.get<float>(static_cast<size_t>(n) * rows);
+  float* rownorm = sc.get<float>(static_cast<size_t>(n) * rows);
   const unsigned int cap =
       static_cast<unsigned int>(std::max<int64_t>(1 << 16, n * rows * V / 256));
   auto* list = sc.get<unsigned long long>(cap);
   auto* count = sc.get<unsigned int>(1);
   ckr(moe::weight_stats_device(w1, static_cast<int>(n), static_cast<int>(M), static_cast<int>(V),
-                               colabs, colabs_blk, w1t, st),
+                               colnorm, colnorm_blk, w1t, st),
       "weight stats");
-  ckr(moe::rowmax_device(x, n * rows, static_cast<int>(M), rowmax, st), "rowmax");
+  ckr(moe::rownorm_device(x, n * rows, static_cast<int>(M), rownorm, st), "rownorm");
   ck(cudaMemsetAsync(count, 0, sizeof(unsigned int), st), "memset");
-  up.rowmax = rowmax;
-  up.colabs = colabs;
-  up.colabs_blk = colabs_blk;
+  up.rownorm = rownorm;
+  up.colnorm = colnorm;
+  up.colnorm_blk = colnorm_blk;
   up.relu_mask = mask;
   up.fix_list = list;
   up.fix_count = count;

@@ -128,7 +128,7 @@ __device__ __forceinline__ T* gather_dst(T* z, const LocalDest& ld, const SlotGe
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_kernel(SlotGeom g, const T* __restrict__ x, const int32_t* __restrict__ slot_token,
-                  T* __restrict__ z, float* __restrict__ rowmax, DropZero dzero,
+                  T* __restrict__ z, float* __restrict__ rownorm, DropZero dzero,
                   unsigned int* __restrict__ reset, LocalDest ld) {
   pdl_entry();
   if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0u;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
       uint4* dst = reinterpret_cast<uint4*>(gather_dst(z, ld, g, row, i, e, rem));
-      float amax = 0.0f;
+      float ssq = 0.0f;
       if (t < 0) {
         for (int v = lane; v < nv; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
       } else {
@@ -165,33 +165,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
             const int v = v0 + u * 32 + lane;
             if (v < nv) {
               dst[v] = buf[u];
-              if (rowmax) {
+              if (rownorm) {
                 float f[VN];
                 Vec<T>::to_f32(buf[u], f);
 #pragma unroll
-                for (int q = 0; q < VN; ++q) amax = fmaxf(amax, fabsf(f[q]));
+                for (int q = 0; q < VN; ++q) ssq = fmaf(f[q], f[q], ssq);
               }
             }
           }
         }
       }
-      if (rowmax) {
+      if (rownorm) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        if (lane == 0) rowmax[row] = amax;
+        for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+        if (lane == 0) rownorm[row] = sqrtf(ssq) * 1.001f;  // |x_row|_2, rounded up
       }
     } else {
       T* dst = gather_dst(z, ld, g, row, i, e, rem);
-      float amax = 0.0f;
+      float ssq = 0.0f;
       for (int m = lane; m < g.M; m += 32) {
         const T v = t < 0 ? from_f<T>(0.0f) : x[static_cast<size_t>(t) * g.M + m];
         dst[m] = v;
-        amax = fmaxf(amax, fabsf(to_f(v)));
+        ssq = fmaf(to_f(v), to_f(v), ssq);
       }
-      if (rowmax) {
+      if (rownorm) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        if (lane == 0) rowmax[row] = amax;
+        for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+        if (lane == 0) rownorm[row] = sqrtf(ssq) * 1.001f;  // |x_row|_2, rounded up
       }
     }
   }
@@ -429,7 +429,7 @@ bool vec_ok(int dtype, int M) { return (M * (dtype == 1 ? 4 : 2)) % 16 == 0; }
 }  // namespace
 
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax, const DropZero& dzero, unsigned int* reset,
+                  cudaStream_t st, float* rownorm, const DropZero& dzero, unsigned int* reset,
                   const LocalDest& local) {
   if (local.recv && (g.blocks != 1 || local.dE < 1 || local.W * local.dE != g.E)) return -1;
   if (dzero.out && dzero.row_bytes % 16 != 0) return -1;
@@ -437,12 +437,12 @@ int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* sl
   const int grid = grid_for(rows);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) launch_k(encode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset, local);
-    else launch_k(encode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rowmax, dzero, reset, local);
+    if (v) launch_k(encode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rownorm, dzero, reset, local);
+    else launch_k(encode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(x), slot_token, static_cast<float*>(z), rownorm, dzero, reset, local);
   } else {
     using B = __nv_bfloat16;
-    if (v) launch_k(encode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset, local);
-    else launch_k(encode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rowmax, dzero, reset, local);
+    if (v) launch_k(encode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rownorm, dzero, reset, local);
+    else launch_k(encode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(x), slot_token, static_cast<B*>(z), rownorm, dzero, reset, local);
   }
   return launch_status();
 }

@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(256)
         off = (static_cast<size_t>(g) * a.Mo + m) * a.N + n;
       if (kKind == kGemmUp) {
         if (std::is_same<T, __nv_bfloat16>::value && a.fix_list != nullptr) {
-          const float tau = a.rowmax[static_cast<size_t>(seg) * a.seg_rows + m] * kReluTauScale *
-                            a.colabs[static_cast<size_t>(g) * a.N + n];
+          const float tau = a.rownorm[static_cast<size_t>(seg) * a.seg_rows + m] * kReluTauScale *
+                            a.colnorm[static_cast<size_t>(g) * a.N + n];
           if (fabsf(v) < tau) {
             const unsigned int slot = atomicAdd(a.fix_count, 1u);
             if (slot < a.fix_cap) a.fix_list[slot] = fix_pack(seg, m, n);

@@ -334,10 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool cert = kEpi == kEpiReluBf16 && args.fix_list != nullptr && row_ok;
       if constexpr (kEpi == kEpiReluBf16) {
         if (cert) {
-          rmax = __ldg(args.rowmax + orow) * kReluTauScale;
+          rmax = __ldg(args.rownorm + orow) * kReluTauScale;
 #pragma unroll
           for (uint32_t c = 0; c < kSubs; ++c)
-            tblk[c] = rmax * __ldg(args.colabs_blk + static_cast<size_t>(tc.g) * (args.N / 64) + col0 / 64 + c);
+            tblk[c] = rmax * __ldg(args.colnorm_blk + static_cast<size_t>(tc.g) * (args.N / 64) + col0 / 64 + c);
         }
       }
       unsigned long long mw[kSubs];
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (uint32_t j = 1; j < 32; ++j) m2 = __vminu2(m2, w[j] & 0x7fff7fffu);
               const float mn = __uint_as_float(min(m2 & 0xffffu, m2 >> 16) << 16);
               if (mn < tmax * (1.0f + 1.0f / 128.0f)) {
-                const float* ca = args.colabs + static_cast<size_t>(tc.g) * args.N + cols;
+                const float* ca = args.colnorm + static_cast<size_t>(tc.g) * args.N + cols;
                 for (uint32_t i = 0; i < 64; ++i) {
                   if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
                     const unsigned int slot = atomicAdd(args.fix_count, 1u);

@@ -42,11 +42,11 @@ struct GemmArgs {
   // tcgen05 kGemmUp epilogue (if non-null), read by the tcgen05 kGemmDgradMask epilogue.
   unsigned long long* relu_mask;
   void* d_ptr;        // set by gemm_fwd: output base
-  // kGemmUp ReLU-mask certificate (optional): outputs with |h| < tau = 2^-18 * rowmax[row] *
-  // colabs[g][col] are appended to fix_list for an fp64 sign re-decision (relu_fixup).
-  const float* rowmax;            // [nseg * seg_rows] max_m |X[row, m]|
-  const float* colabs;            // [G][N] sum_m |W1[g][m][col]|
-  const float* colabs_blk;        // [G][N / 64] max of colabs over each 64-column block
+  // kGemmUp ReLU-mask certificate (optional): outputs with |h| < tau = 2^-18 * rownorm[row] *
+  // colnorm[g][col] are appended to fix_list for an fp64 sign re-decision (relu_fixup).
+  const float* rownorm;            // [nseg * seg_rows] |X[row, :]|_2 (rounded up)
+  const float* colnorm;            // [G][N] |W1[g][:, col]|_2 (rounded up)
+  const float* colnorm_blk;        // [G][N / 64] max of colnorm over each 64-column block
   unsigned long long* fix_list;   // packed (seg << 44) | (row << 24) | col
   unsigned int* fix_count;
   unsigned int fix_cap;

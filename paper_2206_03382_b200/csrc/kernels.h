@@ -91,11 +91,11 @@ struct LocalDest {
   int W = 1, rank = 0, dE = 0;
 };
 
-// dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rowmax (optional, [z rows]):
-// max_m |z[row][m]| for the ReLU-mask certificate.
+// dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rownorm (optional, [z rows]):
+// |z[row]|_2 (rounded up) for the ReLU-mask certificate.
 // reset (optional): a counter zeroed by the pass (the ReLU-fixup count; no memset node).
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
-                  cudaStream_t st, float* rowmax = nullptr, const DropZero& dzero = DropZero{},
+                  cudaStream_t st, float* rownorm = nullptr, const DropZero& dzero = DropZero{},
                   unsigned int* reset = nullptr, const LocalDest& local = LocalDest{});
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
                   const int32_t* locations, const double* gates, void* y, cudaStream_t st);
@@ -122,14 +122,14 @@ int fill_uniform_2d_device(void* dst, int dtype, int64_t rows, int64_t cols, int
                            uint64_t seed, uint64_t offset, double lo, double hi, cudaStream_t st);
 
 // ReLU-mask certificate support (relu_fix.cu).
-int weight_stats_device(const void* w1, int G, int M, int V, float* colabs, float* colabs_blk,
+int weight_stats_device(const void* w1, int G, int M, int V, float* colnorm, float* colnorm_blk,
                         void* w1t, cudaStream_t st);
 int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned long long* mask,
                               cudaStream_t st);
 struct FlagWait;
 // wait: optional fused receive wait (peer flags, see peer_flags.cuh); reset: optional counter
 // zeroed by the kernel (the ReLU fixup count)
-int rowmax_device(const void* x, int64_t rows, int M, float* rowmax, cudaStream_t st,
+int rownorm_device(const void* x, int64_t rows, int M, float* rownorm, cudaStream_t st,
                   const FlagWait* wait = nullptr, unsigned int* reset = nullptr);
 int wait_flags_device(const FlagWait& w, cudaStream_t st);
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,

@@ -226,8 +226,8 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   drops_.alloc(4);
   ck(cudaMallocHost(&cap_host_, sizeof(int32_t)), "cudaMallocHost");
   if (cfg.dtype == MOE_DTYPE_BF16) {
-    colabs_.alloc(sizeof(float) * dE_ * V_);
-    colabs_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
+    colnorm_.alloc(sizeof(float) * dE_ * V_);
+    colnorm_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
     w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
     fix_count_.alloc(sizeof(unsigned int));
   }
@@ -261,7 +261,7 @@ void Layer::alloc_capacity(int cap) {
   if (cfg_.dtype == MOE_DTYPE_BF16) {
     const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
     relu_mask_.alloc(sizeof(unsigned long long) * rows_all * (V_ / 64 + 1));
-    rowmax_.alloc(sizeof(float) * rows_all);
+    rownorm_.alloc(sizeof(float) * rows_all);
     fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));
     fix_list_.alloc(sizeof(unsigned long long) * fix_cap_);
   }
@@ -537,9 +537,9 @@ void Layer::set_expert_slices(const double* w1s, const double* w2s) {
 // Enables the ReLU-mask certificate on an up-GEMM launch (bf16 path only).
 void Layer::prepare_up(GemmArgs& up) {
   if (cfg_.dtype != MOE_DTYPE_BF16) return;
-  up.rowmax = static_cast<const float*>(rowmax_.p);
-  up.colabs = static_cast<const float*>(colabs_.p);
-  up.colabs_blk = static_cast<const float*>(colabs_blk_.p);
+  up.rownorm = static_cast<const float*>(rownorm_.p);
+  up.colnorm = static_cast<const float*>(colnorm_.p);
+  up.colnorm_blk = static_cast<const float*>(colnorm_blk_.p);
   up.relu_mask = static_cast<unsigned long long*>(relu_mask_.p);
   up.fix_list = static_cast<unsigned long long*>(fix_list_.p);
   up.fix_count = static_cast<unsigned int*>(fix_count_.p);
@@ -709,8 +709,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
   if (cert && stats_dirty_) {
-    ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colabs_.p),
-                            static_cast<float*>(colabs_blk_.p), w1t_.p, st),
+    ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colnorm_.p),
+                            static_cast<float*>(colnorm_blk_.p), w1t_.p, st),
         "weight stats");
     stats_dirty_ = false;
   }
@@ -732,7 +732,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   prof_mark(kPhEncode, true, st);
   ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st,
-                    (cert && W_ == 1) ? static_cast<float*>(rowmax_.p) : nullptr, yzero,
+                    (cert && W_ == 1) ? static_cast<float*>(rownorm_.p) : nullptr, yzero,
                     (cert && W_ == 1) ? static_cast<unsigned int*>(fix_count_.p) : nullptr, own),
       "encode");
   prof_mark(kPhEncode, false, st);
@@ -818,11 +818,11 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       u.S = static_cast<uint32_t>(s1 - s0);
       if (cert) {
         const size_t r0 = static_cast<size_t>(i * W_ + s0) * dE_ * cc_;
-        ckr(rowmax_device(static_cast<char*>(recv) + r0 * M_ * esz_,
+        ckr(rownorm_device(static_cast<char*>(recv) + r0 * M_ * esz_,
                           static_cast<int64_t>(s1 - s0) * dE_ * cc_, M_,
-                          static_cast<float*>(rowmax_.p) + r0, st, fw,
+                          static_cast<float*>(rownorm_.p) + r0, st, fw,
                           reset ? static_cast<unsigned int*>(fix_count_.p) : nullptr),
-            "rowmax");
+            "rownorm");
         ++launches_;
       } else if (fw) {
         ckr(wait_flags_device(*fw, st), "wait");
@@ -895,10 +895,10 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       down.seg_base = i * W_;
       if (cert) {
         const size_t r0 = static_cast<size_t>(i) * W_ * dE_ * cc_;
-        ckr(rowmax_device(static_cast<char*>(recv) + r0 * M_ * esz_,
+        ckr(rownorm_device(static_cast<char*>(recv) + r0 * M_ * esz_,
                           static_cast<int64_t>(W_) * dE_ * cc_, M_,
-                          static_cast<float*>(rowmax_.p) + r0, st),
-            "rowmax");
+                          static_cast<float*>(rownorm_.p) + r0, st),
+            "rownorm");
         ++launches_;
         ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
       }

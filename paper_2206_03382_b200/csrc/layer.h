@@ -150,7 +150,7 @@ class Layer {
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   void pipe_call(int dir, const void* inh, void* outh, cudaStream_t st);
   // ReLU-mask certificate state (relu_fix.cu)
-  DevMem colabs_, colabs_blk_, w1t_, rowmax_, fix_list_, fix_count_, relu_mask_;
+  DevMem colnorm_, colnorm_blk_, w1t_, rownorm_, fix_list_, fix_count_, relu_mask_;
   unsigned int fix_cap_ = 0;
   bool stats_dirty_ = true;
   void prepare_up(GemmArgs& up);
