@@ -846,11 +846,7 @@ int launch_dmma(const DmmaArgs& da, int gx, int gy, cudaStream_t st) {
     constexpr int NT = decltype(nt_tag)::value;
     using Cf = D2Cfg<TX, NT>;
     auto kern = gate_dmma2_kernel<TX, NT, kMode>;
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-      set = true;
-    }
+    if (!smem_optin(kern, Cf::SMEM)) return -2;
     launch_k(kern, dim3(gx, gy), dim3(kDmWarps * 32), Cf::SMEM, st, da);
     return launch_status();
   };

@@ -548,13 +548,7 @@ int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, 
               const PeerMaps& pm, int num_sms, cudaStream_t stream) {
   using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0>;
   auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK, kCG, kIdx>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) !=
-        cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (!smem_optin(kern, C::SMEM_BYTES)) return -3;
   const uint32_t units = num_tiles<kRowK, C::TM>(args);
   if (units == 0) return 0;
   // persistent: one CTA (pair) per SM (pair of SMs)

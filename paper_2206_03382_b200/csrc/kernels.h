@@ -11,6 +11,14 @@ namespace moe {
 // Launch-error bookkeeping: cudaGetLastError() clears the error, so launch helpers record it
 // here for the caller's message (returns 0 on success, -2 on failure).
 cudaError_t& last_launch_error();
+
+// One-time per-(kernel, device) opt-in to > 48 KiB dynamic shared memory: function attributes
+// are per device, so a process driving several GPUs sets them once on each.
+bool smem_optin_raw(const void* kern, int bytes);
+template <typename F>
+inline bool smem_optin(F* kern, int bytes) {
+  return smem_optin_raw(reinterpret_cast<const void*>(kern), bytes);
+}
 inline int launch_status() {
   const cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) return 0;

@@ -18,6 +18,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <set>
+#include <mutex>
 #include <vector>
 
 #include "gemm_sm100.h"
@@ -46,6 +48,19 @@ void ckn(ncclResult_t r, const char* what) {
 }
 
 }  // namespace
+
+bool smem_optin_raw(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kern, dev})) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return false;
+  done.insert({kern, dev});
+  return true;
+}
 
 cudaError_t& last_launch_error() {
   static thread_local cudaError_t e = cudaSuccess;

@@ -52,3 +52,25 @@ def test_scenario_runner_two_ranks(cuda, tmp_path):
     assert [x.f for x in recs] == [1.0, 2.0, 1.0, 2.0]
     assert recs[0].capacity < recs[1].capacity
     assert all(x.sim_seconds > 0 and x.strategy == "linearx1" for x in recs)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_two_devices_one_process(cuda):
+    """Independent W = 1 handles on two devices of one process (per-device kernel attributes):
+    both produce the oracle's routing and outputs."""
+    import numpy as np
+    import oracle
+    from paper_2206_03382_b200 import LayerState, MoELayerConfig, forward
+    from tests.helpers import layer_inputs
+    E, M, V, T = 8, 256, 512, 1024
+    cfg = MoELayerConfig(global_experts=E, model_dim=M, hidden_dim=V, tokens_per_step=T, top_k=1)
+    inp = layer_inputs(31, 1, T, M, V, E, "bf16")
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], None, 1, 1)
+    for dev in (0, 1):
+        st = LayerState.init(cfg, 31, device=dev)
+        y = forward(st, torch.as_tensor(inp["x"]).to(torch.bfloat16).to(f"cuda:{dev}")).y
+        idxs, loc, _, _ = st.routing()
+        assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
+        assert oracle.max_rel_diff(y.double().cpu().numpy(), ref["y"]) < 2e-2
+        st.close()
