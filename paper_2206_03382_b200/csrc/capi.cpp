@@ -239,8 +239,21 @@ int moe_get_unique_id(uint8_t* id128) {
   });
 }
 
+// A handle's calls run on its device; the caller's current device is restored on return (the
+// layer switches devices internally, a multi-GPU caller must not find its own device changed).
+struct DeviceRestore {
+  int prev = -1;
+  DeviceRestore() {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  }
+  ~DeviceRestore() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 int moe_create(const moe_config* cfg, int32_t rank, const uint8_t* nccl_id128, int32_t device,
                moe_handle** out) {
+  DeviceRestore restore;
   return guard(nullptr, [&] {
     if (!cfg || !out) throw moe::MoeError(MOE_EINVAL, "null argument");
     require_device();
@@ -251,6 +264,7 @@ int moe_create(const moe_config* cfg, int32_t rank, const uint8_t* nccl_id128, i
 }
 
 int moe_destroy(moe_handle* h) {
+  DeviceRestore restore;
   delete h;
   return MOE_OK;
 }
@@ -261,6 +275,7 @@ const char* moe_last_error_global(void) { return g_err.c_str(); }
 #define LAYER_CALL(h, body)                                                 \
   do {                                                                      \
     if (!(h)) return MOE_EINVAL;                                            \
+    DeviceRestore restore_;                                                 \
     return guard(&(h)->err, [&] { body; });                                 \
   } while (0)
 

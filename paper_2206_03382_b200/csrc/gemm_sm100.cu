@@ -57,21 +57,33 @@ constexpr uint32_t BK = 64;   // one 128-byte swizzle atom of bf16 along K
 constexpr uint32_t UK = 16;   // K per tcgen05.mma (bf16)
 constexpr uint32_t kAccStages = 2;
 constexpr uint32_t kTmemCols = kAccStages * BN;  // 512
-constexpr uint32_t kThreads = 384;               // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-11 epilogue
-constexpr uint32_t kEpiThreads = 256;
-constexpr uint32_t kEpiWarps = kEpiThreads / 32;
 constexpr uint32_t EPI_WARP_BYTES = 32 * 128;    // 32 rows x 128 B staging per epilogue warp
 
 // kCG = 1: one CTA computes a 128 x 256 tile. kCG = 2: a CTA pair (cluster of 2, cta_group::2)
 // computes 256 x 256: each CTA holds its 128 A rows and half (128 columns) of B, so B smem per
 // CTA halves and the pipeline gets deeper (6 stages instead of 4).
 // kPeer: the fused-combine kernels store over NVLink, where a bulk store holds its staging
-// buffer longer -- two staging buffers per epilogue warp, one pipeline stage fewer.
-template <int kCG, bool kPeer = false>
-struct Cfg {
+// buffer longer -- two staging buffers per epilogue warp.
+// Epilogue warps per CTA: 4 (one per TMEM lane quadrant, draining all 256 columns) or 8 (two
+// column halves). Measured at TGT: the up GEMM's certificate epilogue needs 8 to keep pace with
+// its K = 1024 mainloop; every other kind is faster with 4 (wgrad -8 %: fewer warps contending
+// with the MMA / TMA issuers).
+template <int kGemmEpiWarps>
+struct EpiCfg {
+  static constexpr uint32_t kEpiWarps = kGemmEpiWarps;
+  static constexpr uint32_t kEpiThreads = kEpiWarps * 32;
+  static constexpr uint32_t kThreads = 128 + kEpiThreads;  // warp0 TMA, warp1 MMA, warp2 TMEM, 4.. epilogue
+  static constexpr uint32_t kEpiCols = BN / (kEpiWarps / 4);  // accumulator columns per epilogue warp
+};
+
+template <int kCG, bool kPeer = false, int kEW = 8>
+struct Cfg : EpiCfg<kEW> {
+  using EpiCfg<kEW>::kEpiWarps;
   static constexpr uint32_t kEpiBufs = kPeer ? 2 : MOE_GEMM_EPI_BUFS;  // staging buffers per warp
+  // peer stores double the staging: with 8 epilogue warps that costs one pipeline stage
   static constexpr uint32_t kStages =
-      (kCG == 1 ? MOE_GEMM_STAGES : MOE_GEMM_STAGES_PAIR) - (kPeer && MOE_GEMM_EPI_BUFS == 1 ? 1 : 0);
+      (kCG == 1 ? MOE_GEMM_STAGES : MOE_GEMM_STAGES_PAIR) -
+      (kPeer && MOE_GEMM_EPI_BUFS == 1 && kEW == 8 ? 1 : 0);
   static constexpr uint32_t TM = BM * kCG;   // tile rows per work unit
   static constexpr uint32_t BNL = BN / kCG;  // B columns loaded per CTA
   static constexpr uint32_t A_BYTES = BM * BK * 2;
@@ -128,13 +140,15 @@ __device__ __forceinline__ uint32_t num_kblocks(const GemmArgs& a) {
     return a.S * ((a.seg_rows + BK - 1) / BK);
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG, uint32_t kIdx>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG, uint32_t kIdx, int kEW>
+__global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmD, const GemmArgs args,
                      const __grid_constant__ PeerMaps pm) {
-  using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0>;
+  using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0, kEW>;
   constexpr uint32_t kStages = C::kStages;
+  constexpr uint32_t kEpiWarps = C::kEpiWarps;
+  constexpr uint32_t kEpiCols = C::kEpiCols;
   constexpr uint32_t kEpiBufs = C::kEpiBufs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -294,10 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the 128 x 256 accumulator; each 128-byte-wide sub-chunk (64 bf16 / 32 fp32 columns) goes
     // registers -> warp-private 128B-swizzled smem -> one TMA bulk store by lane 0.
     const uint32_t q = warp % 4;
-    const uint32_t half = (warp - 4) / 4;
+    const uint32_t half = (warp - 4) / 4;  // column slice of this warp
     const uint32_t row = q * 32 + lane;
     constexpr uint32_t kSub = (kEpi == kEpiF32) ? 32 : 64;  // columns per 128-byte sub-chunk
-    constexpr uint32_t kSubs = (BN / 2) / kSub;
+    constexpr uint32_t kSubs = kEpiCols / kSub;
     constexpr uint32_t kStoreLanes = (kIdx & kIdxScatterD) ? 8 : 1;  // lanes issuing bulk stores
     uint8_t* stage_base = smem + C::SMEM_EPI_OFF + (warp - 4) * EPI_WARP_BYTES * kEpiBufs;
     uint32_t ebuf = 0;
@@ -307,11 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc.m0 += rank * BM;  // this CTA's rows of the pair tile
       const uint32_t acc = iter % kAccStages;
       const uint32_t acc_phase = (iter / kAccStages) & 1;
-      const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16) + half * (BN / 2);
+      const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16) + half * kEpiCols;
       const uint32_t seg = kRowK ? tc.g : (args.seg_base + tc.s) * args.G + tc.g;
       const uint32_t row_in = tc.m0 + row;
       const bool row_ok = kRowK || row_in < args.seg_rows;
-      const uint32_t col0 = tc.n0 + half * (BN / 2);
+      const uint32_t col0 = tc.n0 + half * kEpiCols;
       const size_t orow = static_cast<size_t>(seg) * args.seg_rows + row_in;  // row-M kinds
       const size_t mrow = orow * (args.N / 64);
       // token-indexed epilogue: the row's token (scatter) and gate scale
@@ -543,11 +557,11 @@ int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG, uint32_t kIdx>
+template <bool kAMN, bool kBMN, int kEpi, bool kRowK, int kCG, uint32_t kIdx, int kEW>
 int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const GemmArgs& args,
               const PeerMaps& pm, int num_sms, cudaStream_t stream) {
-  using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0>;
-  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK, kCG, kIdx>;
+  using C = Cfg<kCG, (kIdx & kIdxPeerD) != 0, kEW>;
+  auto kern = gemm_bf16_kernel<kAMN, kBMN, kEpi, kRowK, kCG, kIdx, kEW>;
   if (!smem_optin(kern, C::SMEM_BYTES)) return -3;
   const uint32_t units = num_tiles<kRowK, C::TM>(args);
   if (units == 0) return 0;
@@ -556,7 +570,7 @@ int launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, 
   const uint32_t grid = (units < max_units ? units : max_units) * kCG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -586,9 +600,10 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, con
            int num_sms, cudaStream_t stream, const PeerMaps* pm = nullptr) {
   static const PeerMaps none{};
   const PeerMaps& p = pm ? *pm : none;
+  constexpr int kEW = kEpi == kEpiReluBf16 ? 8 : 4;  // see EpiCfg
   if (gemm_cta_group() == 2)
-    return launch_cg<kAMN, kBMN, kEpi, kRowK, 2, kIdx>(a, b, d, args, p, num_sms, stream);
-  return launch_cg<kAMN, kBMN, kEpi, kRowK, 1, kIdx>(a, b, d, args, p, num_sms, stream);
+    return launch_cg<kAMN, kBMN, kEpi, kRowK, 2, kIdx, kEW>(a, b, d, args, p, num_sms, stream);
+  return launch_cg<kAMN, kBMN, kEpi, kRowK, 1, kIdx, kEW>(a, b, d, args, p, num_sms, stream);
 }
 
 }  // namespace

@@ -364,6 +364,7 @@ void Layer::take_profile(double* ms, int64_t* counts, int n) {
 }
 
 Layer::~Layer() {
+  cudaSetDevice(device_);
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);
   if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& p : pipe_)

@@ -67,10 +67,13 @@ def test_two_devices_one_process(cuda):
     cfg = MoELayerConfig(global_experts=E, model_dim=M, hidden_dim=V, tokens_per_step=T, top_k=1)
     inp = layer_inputs(31, 1, T, M, V, E, "bf16")
     ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], None, 1, 1)
+    torch.cuda.set_device(0)
     for dev in (0, 1):
         st = LayerState.init(cfg, 31, device=dev)
+        assert torch.cuda.current_device() == 0  # the caller's device is restored
         y = forward(st, torch.as_tensor(inp["x"]).to(torch.bfloat16).to(f"cuda:{dev}")).y
         idxs, loc, _, _ = st.routing()
         assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
         assert oracle.max_rel_diff(y.double().cpu().numpy(), ref["y"]) < 2e-2
         st.close()
+    assert torch.cuda.current_device() == 0
