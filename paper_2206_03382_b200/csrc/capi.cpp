@@ -143,7 +143,10 @@ unsigned long long* certified_up(int dtype, const void* x, const void* w1, void*
   ckr(moe::weight_stats_device(w1, static_cast<int>(n), static_cast<int>(M), static_cast<int>(V),
                                colnorm, colnorm_blk, w1t, st),
       "weight stats");
-  ckr(moe::rownorm_device(x, n * rows, static_cast<int>(M), rownorm, st), "rownorm");
+  moe::RowSet all;
+  all.nsegs = 1;
+  all.seg_rows = all.nrows = n * rows;
+  ckr(moe::rownorm_device(x, static_cast<int>(M), rownorm, all, st), "rownorm");
   ck(cudaMemsetAsync(count, 0, sizeof(unsigned int), st), "memset");
   up.rownorm = rownorm;
   up.colnorm = colnorm;

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(256)
 
 template <typename T, typename TD>
 int launch_simt(int kind, const T* A, const T* B, TD* D, const GemmArgs& a, cudaStream_t st) {
+  if (a.row0 || a.nrows || a.skip_seg >= 0 || a.idx_mode) return -1;  // tcgen05-only features
   const bool rowk = kind == kGemmWgrad;
   const int rows = rowk ? a.Mo : a.seg_rows;
   dim3 grid((a.N + TN - 1) / TN, (rows + TM - 1) / TM, rowk ? a.G : a.G * a.S);

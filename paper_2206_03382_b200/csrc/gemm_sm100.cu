@@ -110,10 +110,12 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmArgs& a, uint32_t tile
   c.n0 = (tile % n_tiles) * BN;
   uint32_t rest = tile / n_tiles;
   if constexpr (!kRowK) {
-    const uint32_t mts = (a.seg_rows + TM - 1) / TM;
-    c.m0 = (rest % mts) * TM;
+    const uint32_t nr = a.nrows ? a.nrows : a.seg_rows - a.row0;
+    const uint32_t mts = (nr + TM - 1) / TM;
+    c.m0 = a.row0 + (rest % mts) * TM;
     rest /= mts;
     c.s = rest % a.S;
+    if (a.skip_seg >= 0 && c.s >= static_cast<uint32_t>(a.skip_seg)) ++c.s;
     c.g = rest / a.S;
   } else {
     const uint32_t mts = (a.Mo + TM - 1) / TM;
@@ -127,7 +129,7 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmArgs& a, uint32_t tile
 template <bool kRowK, uint32_t TM>
 __host__ __device__ __forceinline__ uint32_t num_tiles(const GemmArgs& a) {
   if constexpr (!kRowK)
-    return a.G * a.S * ((a.seg_rows + TM - 1) / TM) * (a.N / BN);
+    return a.G * a.S * (((a.nrows ? a.nrows : a.seg_rows - a.row0) + TM - 1) / TM) * (a.N / BN);
   else
     return a.G * ((a.Mo + TM - 1) / TM) * (a.N / BN);
 }
@@ -324,7 +326,8 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
       const uint32_t tmem_row = tmem_base + acc * BN + ((q * 32) << 16) + half * kEpiCols;
       const uint32_t seg = kRowK ? tc.g : (args.seg_base + tc.s) * args.G + tc.g;
       const uint32_t row_in = tc.m0 + row;
-      const bool row_ok = kRowK || row_in < args.seg_rows;
+      const bool row_ok =
+          kRowK || row_in < (args.nrows ? min(args.seg_rows, args.row0 + args.nrows) : args.seg_rows);
       const uint32_t col0 = tc.n0 + half * kEpiCols;
       const size_t orow = static_cast<size_t>(seg) * args.seg_rows + row_in;  // row-M kinds
       const size_t mrow = orow * (args.N / 64);
@@ -610,6 +613,12 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, con
 
 int gemm_validate(const GemmArgs& a, int kind) {
   if (a.G < 1 || a.S < 1 || a.seg_rows < 1 || a.N < 1) return -1;
+  if (kind != kGemmWgrad) {
+    if (a.row0 >= a.seg_rows || a.row0 % 256 || a.row0 + a.nrows > a.seg_rows) return -1;
+    if (a.nrows && a.nrows % 256 && a.row0 + a.nrows != a.seg_rows) return -1;
+  } else if (a.row0 || a.nrows || a.skip_seg >= 0) {
+    return -1;
+  }
   if (a.N % BN != 0) return -1;
   if (kind == kGemmWgrad) {
     if (a.Mo % BM != 0) return -1;

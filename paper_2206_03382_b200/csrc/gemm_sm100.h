@@ -55,6 +55,11 @@ struct GemmArgs {
   uint32_t gather_rows;       // token rows of the scattered tensor
   const int32_t* row_token;   // [nseg * seg_rows]
   const float* row_scale;     // [nseg * seg_rows]
+  // row-M sub-range (pipelined first chunk): rows [row0, row0 + nrows) of every segment (nrows = 0:
+  // all; row0 and nrows multiples of the tile height unless the range ends at seg_rows), and one
+  // segment index of [0, S] skipped (skip_seg < 0: none; S then counts the segments processed)
+  uint32_t row0 = 0, nrows = 0;
+  int32_t skip_seg = -1;
   // kIdxPeerD: destination combine buffer of every rank (this rank's own for src == rank)
   uint32_t peer_world, peer_rank, peer_out_segs;  // out_segs = chunks * E
   void* peer_d[kMaxPeers];

@@ -137,8 +137,14 @@ int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned lon
 struct FlagWait;
 // wait: optional fused receive wait (peer flags, see peer_flags.cuh); reset: optional counter
 // zeroed by the kernel (the ReLU fixup count)
-int rownorm_device(const void* x, int64_t rows, int M, float* rownorm, cudaStream_t st,
-                  const FlagWait* wait = nullptr, unsigned int* reset = nullptr);
+// Rows [row0, row0 + nrows) of segments [seg_begin, seg_begin + nsegs) (seg_rows apart), the
+// segments [skip_begin, skip_begin + skip_count) skipped over (nsegs counts processed segments).
+struct RowSet {
+  int64_t seg_begin = 0, nsegs = 0, seg_rows = 1, row0 = 0, nrows = 0;
+  int64_t skip_begin = 0, skip_count = 0;
+};
+int rownorm_device(const void* x, int M, float* rownorm, const RowSet& rs, cudaStream_t st,
+                   const FlagWait* wait = nullptr, unsigned int* reset = nullptr);
 int wait_flags_device(const FlagWait& w, cudaStream_t st);
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,

@@ -661,6 +661,22 @@ void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
 
 // Copy-engine version of exchange(): push chunk `chunk` of `src` into every peer's channel
 // buffer (same plan), then publish the chunk's ready flag.
+// Rows [row0, row0 + nrows) of every segment of chunk `chunk` to every peer (slot: ready flag).
+void Layer::peer_push_rows(int ch, const void* src, int chunk, int phase, int slot, uint32_t row0,
+                           uint32_t nrows, uint32_t epoch) {
+  std::vector<int64_t> so(W_), ro(W_);
+  int64_t elems = 0;
+  a2a_plan(W_, E_, cc_, M_, chunk, phase, so.data(), ro.data(), &elems);
+  for (int p = 0; p < W_; ++p) {
+    so[p] *= esz_;
+    ro[p] *= esz_;
+  }
+  const size_t row_bytes = static_cast<size_t>(M_) * esz_;
+  peer_->push_rows(comm_stream_, ch, slot, src, so.data(), ro.data(), static_cast<size_t>(dE_),
+                   cc_ * row_bytes, row0 * row_bytes, nrows * row_bytes, epoch);
+  comm_bytes_ += static_cast<double>(dE_) * nrows * row_bytes * (W_ - 1);
+}
+
 // Fused-combine GEMM arguments: segment (chunk, src, g) goes to rank src's channel-ch buffer.
 GemmArgs Layer::peer_args(const GemmArgs& a, int ch) const {
   GemmArgs d = a;
@@ -821,23 +837,46 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[0], 0), "wait");  // my recv buffer consumed
     peer_->wait_peers_freed(comm_stream_, 0, e0);
     prof_mark(kPhA2aFwd, true, comm_stream_);
+    // first chunk in two row halves when the tile shape allows (tcgen05 path): its first rows
+    // land while this rank computes its own segment
+    const bool split0 = local_first_ && fused_combine_ && cc_ % 512 == 0;
+    const uint32_t h0 = static_cast<uint32_t>(cc_ / 2);
     for (int i = 0; i < degree_; ++i) {
+      if (i == 0 && split0) {
+        peer_push_rows(0, z_.p, 0, 0, PeerExchange::kHalfSlot, 0, h0, e0);
+        peer_push_rows(0, z_.p, 0, 0, 0, h0, static_cast<uint32_t>(cc_) - h0, e0);
+        tl_mark("dispatch pushed 0 (2 halves) [comm]", comm_stream_);
+        continue;
+      }
       peer_push(0, z_.p, i, 0, e0, nullptr);  // my own block: written into recv by encode
       tl_mark("dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
-    // up GEMM over sources [s0, s1) of chunk i; the range's first kernel (the certificate's row
-    // max, or a bare wait) polls the peers' ready flags when `fw` is given
-    auto up_range = [&](int i, int s0, int s1, const FlagWait* fw, bool reset) {
-      if (s1 <= s0) return;
+    // up GEMM over sources [s0, s1) of chunk i except `skip` (-1: none), rows [row0, row0 + nrows)
+    // of each segment (nrows 0: to the end); the range's first kernel (the certificate's row
+    // norms, or a bare wait) polls the peers' ready flags when `fw` is given
+    auto up_range = [&](int i, int s0, int s1, int skip, uint32_t row0, uint32_t nrows,
+                        const FlagWait* fw, bool reset) {
+      const int nsrc = (s1 - s0) - (skip >= 0 ? 1 : 0);
+      if (nsrc <= 0) return;
       GemmArgs u = up;
       u.seg_base = static_cast<uint32_t>(i * W_ + s0);
-      u.S = static_cast<uint32_t>(s1 - s0);
+      u.S = static_cast<uint32_t>(nsrc);
+      u.skip_seg = skip >= 0 ? skip - s0 : -1;
+      u.row0 = row0;
+      u.nrows = nrows;
       if (cert) {
-        const size_t r0 = static_cast<size_t>(i * W_ + s0) * dE_ * cc_;
-        ckr(rownorm_device(static_cast<char*>(recv) + r0 * M_ * esz_,
-                          static_cast<int64_t>(s1 - s0) * dE_ * cc_, M_,
-                          static_cast<float*>(rownorm_.p) + r0, st, fw,
-                          reset ? static_cast<unsigned int*>(fix_count_.p) : nullptr),
+        RowSet rs;
+        rs.seg_begin = static_cast<int64_t>(i * W_ + s0) * dE_;
+        rs.nsegs = static_cast<int64_t>(nsrc) * dE_;
+        rs.seg_rows = cc_;
+        rs.row0 = row0;
+        rs.nrows = nrows ? nrows : cc_ - row0;
+        if (skip >= 0) {
+          rs.skip_begin = static_cast<int64_t>(i * W_ + skip) * dE_;
+          rs.skip_count = dE_;
+        }
+        ckr(rownorm_device(recv, M_, static_cast<float*>(rownorm_.p), rs, st, fw,
+                           reset ? static_cast<unsigned int*>(fix_count_.p) : nullptr),
             "rownorm");
         ++launches_;
       } else if (fw) {
@@ -852,13 +891,22 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     for (int i = 0; i < degree_; ++i) {
       const FlagWait fw = peer_->ready_wait(0, i, e0);
       down.seg_base = i * W_;
-      if (i == 0 && local_first_) {
-        // this rank's own source segment first: it hides the first chunk's NVLink transfer
-        up_range(0, rank_, rank_ + 1, nullptr, true);
-        up_range(0, 0, rank_, &fw, false);
-        up_range(0, rank_ + 1, W_, rank_ > 0 ? nullptr : &fw, false);
+      if (i == 0 && split0) {
+        // own rows first, then the peers' first half rows (their own flag), then the rest: each
+        // transfer hides behind the previous GEMM
+        const FlagWait fh = peer_->ready_wait(0, PeerExchange::kHalfSlot, e0);
+        up_range(0, rank_, rank_ + 1, -1, 0, 0, nullptr, true);
+        up_range(0, 0, W_, rank_, 0, h0, &fh, false);
+        up_range(0, 0, W_, rank_, h0, 0, &fw, false);
+      } else if (i == 0 && local_first_ && fused_combine_) {
+        up_range(0, rank_, rank_ + 1, -1, 0, 0, nullptr, true);
+        up_range(0, 0, W_, rank_, 0, 0, &fw, false);
+      } else if (i == 0 && local_first_) {  // SIMT GEMM path: contiguous source ranges only
+        up_range(0, rank_, rank_ + 1, -1, 0, 0, nullptr, true);
+        up_range(0, 0, rank_, -1, 0, 0, &fw, false);
+        up_range(0, rank_ + 1, W_, -1, 0, 0, rank_ > 0 ? nullptr : &fw, false);
       } else {
-        up_range(i, 0, W_, &fw, true);
+        up_range(i, 0, W_, -1, 0, 0, &fw, true);
       }
       fixup(recv);
       prof_mark(kPhDown, true, st);
@@ -910,11 +958,11 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       up.seg_base = i * W_;
       down.seg_base = i * W_;
       if (cert) {
-        const size_t r0 = static_cast<size_t>(i) * W_ * dE_ * cc_;
-        ckr(rownorm_device(static_cast<char*>(recv) + r0 * M_ * esz_,
-                          static_cast<int64_t>(W_) * dE_ * cc_, M_,
-                          static_cast<float*>(rownorm_.p) + r0, st),
-            "rownorm");
+        RowSet rs;  // every source segment of chunk i
+        rs.seg_begin = static_cast<int64_t>(i) * W_ * dE_;
+        rs.nsegs = static_cast<int64_t>(W_) * dE_;
+        rs.seg_rows = rs.nrows = cc_;
+        ckr(rownorm_device(recv, M_, static_cast<float*>(rownorm_.p), rs, st), "rownorm");
         ++launches_;
         ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
       }
@@ -1070,33 +1118,54 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[2], 0), "wait");
     peer_->wait_peers_freed(comm_stream_, 2, e2);
     prof_mark(kPhA2aBwd, true, comm_stream_);
+    const bool split0 = local_first_ && fused_combine_ && cc_ % 512 == 0;  // as in forward
+    const uint32_t h0 = static_cast<uint32_t>(cc_ / 2);
     for (int i = 0; i < degree_; ++i) {  // adjoint of combine
+      if (i == 0 && split0) {
+        peer_push_rows(2, dz_.p, 0, 0, PeerExchange::kHalfSlot, 0, h0, e2);
+        peer_push_rows(2, dz_.p, 0, 0, 0, h0, static_cast<uint32_t>(cc_) - h0, e2);
+        tl_mark("bwd dispatch pushed 0 (2 halves) [comm]", comm_stream_);
+        continue;
+      }
       peer_push(2, dz_.p, i, 0, e2, nullptr);  // my own block: written into drecv by decode_bwd
       tl_mark("bwd dispatch pushed " + std::to_string(i) + " [comm]", comm_stream_);
     }
     for (int i = 0; i < degree_; ++i) {
       const FlagWait fw = peer_->ready_wait(2, i, e2);
       dg.seg_base = i * W_;
-      auto dgm_range = [&](int s0, int s1, bool wait) {
-        if (s1 <= s0) return;
-        if (wait) {
-          ckr(wait_flags_device(fw, st), "wait");
+      // dgrad-mask over sources [s0, s1) except `skip`, rows [row0, row0 + nrows) of each segment
+      auto dgm_range = [&](int s0, int s1, int skip, uint32_t row0, uint32_t nrows, const FlagWait* w) {
+        const int nsrc = (s1 - s0) - (skip >= 0 ? 1 : 0);
+        if (nsrc <= 0) return;
+        if (w) {
+          ckr(wait_flags_device(*w, st), "wait");
           ++launches_;
           tl_mark("bwd dispatch landed " + std::to_string(i), st);
         }
         GemmArgs a = dgm;
         a.seg_base = static_cast<uint32_t>(i * W_ + s0);
-        a.S = static_cast<uint32_t>(s1 - s0);
+        a.S = static_cast<uint32_t>(nsrc);
+        a.skip_seg = skip >= 0 ? skip - s0 : -1;
+        a.row0 = row0;
+        a.nrows = nrows;
         prof_mark(kPhDgradMask, true, st);
         gemm(kGemmDgradMask, drecv, w2_.p, dh_.p, a, nseg, st);
         prof_mark(kPhDgradMask, false, st);
       };
-      if (i == 0 && local_first_) {
-        dgm_range(rank_, rank_ + 1, false);
-        dgm_range(0, rank_, true);
-        dgm_range(rank_ + 1, W_, rank_ == 0);
+      if (i == 0 && split0) {
+        const FlagWait fh = peer_->ready_wait(2, PeerExchange::kHalfSlot, e2);
+        dgm_range(rank_, rank_ + 1, -1, 0, 0, nullptr);
+        dgm_range(0, W_, rank_, 0, h0, &fh);
+        dgm_range(0, W_, rank_, h0, 0, &fw);
+      } else if (i == 0 && local_first_ && fused_combine_) {
+        dgm_range(rank_, rank_ + 1, -1, 0, 0, nullptr);
+        dgm_range(0, W_, rank_, 0, 0, &fw);
+      } else if (i == 0 && local_first_) {  // SIMT GEMM path: contiguous source ranges only
+        dgm_range(rank_, rank_ + 1, -1, 0, 0, nullptr);
+        dgm_range(0, rank_, -1, 0, 0, &fw);
+        dgm_range(rank_ + 1, W_, -1, 0, 0, rank_ == 0 ? &fw : nullptr);
       } else {
-        dgm_range(0, W_, true);
+        dgm_range(0, W_, -1, 0, 0, &fw);
       }
       prof_mark(kPhDgrad, true, st);
       if (fused_combine_) {

@@ -96,6 +96,8 @@ class Layer {
   SlotGeom geom() const;
   void exchange(const void* send, void* recv, int chunk, int phase);
   void peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch, cudaEvent_t local_done);
+  void peer_push_rows(int ch, const void* src, int chunk, int phase, int slot, uint32_t row0,
+                      uint32_t nrows, uint32_t epoch);
   double allreduce_max_host(double v);
   void ensure_io();
   void alloc_capacity(int cap);

@@ -69,7 +69,7 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
   if (!stream_memops_available())
     throw MoeError(MOE_ECUDA, "peer all-to-all: CUDA stream memory operations unavailable");
   for (int c = 0; c < kChannels; ++c) local_bufs_[c] = bufs[c];
-  nflags_ = static_cast<size_t>(kChannels) * world * kMaxChunks + static_cast<size_t>(kChannels) * world +
+  nflags_ = static_cast<size_t>(kChannels) * world * kFlagSlots + static_cast<size_t>(kChannels) * world +
             static_cast<size_t>(kStageSlots) * world;
   ck(cudaMalloc(&flags_, nflags_ * sizeof(uint32_t) + 256), "cudaMalloc flags");
   ck(cudaMemset(flags_, 0, nflags_ * sizeof(uint32_t) + 256), "memset flags");
@@ -131,22 +131,22 @@ PeerExchange::~PeerExchange() {
 
 // Flag block layout (u32): ready[ch][src][chunk] | freed[ch][src] | stage[2*ch + kind]
 uint32_t* PeerExchange::ready_local(int ch, int src, int chunk) const {
-  return static_cast<uint32_t*>(flags_) + (static_cast<size_t>(ch) * world_ + src) * kMaxChunks + chunk;
+  return static_cast<uint32_t*>(flags_) + (static_cast<size_t>(ch) * world_ + src) * kFlagSlots + chunk;
 }
 uint32_t* PeerExchange::freed_local(int ch, int src) const {
-  return static_cast<uint32_t*>(flags_) + static_cast<size_t>(kChannels) * world_ * kMaxChunks +
+  return static_cast<uint32_t*>(flags_) + static_cast<size_t>(kChannels) * world_ * kFlagSlots +
          static_cast<size_t>(ch) * world_ + src;
 }
 uint32_t* PeerExchange::ready_remote(int dst, int ch, int chunk) const {
-  return static_cast<uint32_t*>(peer_flags_[dst]) + (static_cast<size_t>(ch) * world_ + rank_) * kMaxChunks +
+  return static_cast<uint32_t*>(peer_flags_[dst]) + (static_cast<size_t>(ch) * world_ + rank_) * kFlagSlots +
          chunk;
 }
 uint32_t* PeerExchange::freed_remote(int dst, int ch) const {
-  return static_cast<uint32_t*>(peer_flags_[dst]) + static_cast<size_t>(kChannels) * world_ * kMaxChunks +
+  return static_cast<uint32_t*>(peer_flags_[dst]) + static_cast<size_t>(kChannels) * world_ * kFlagSlots +
          static_cast<size_t>(ch) * world_ + rank_;
 }
 uint32_t* PeerExchange::stage(int slot) const {
-  return static_cast<uint32_t*>(flags_) + static_cast<size_t>(kChannels) * world_ * kMaxChunks +
+  return static_cast<uint32_t*>(flags_) + static_cast<size_t>(kChannels) * world_ * kFlagSlots +
          static_cast<size_t>(kChannels) * world_ + slot;
 }
 
@@ -205,10 +205,31 @@ void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch
   }
 }
 
+void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* src, const int64_t* so,
+                             const int64_t* ro, size_t segs, size_t seg_bytes, size_t row0_bytes,
+                             size_t rows_bytes, uint32_t epoch) {
+  if (slot < 0 || slot >= kFlagSlots) throw MoeError(MOE_EINVAL, "peer all-to-all: flag slot");
+  ck(cudaEventRecord(ev_in_, copy), "event");
+  for (int i = 1; i < world_; ++i) {  // own rows are written in place by the producing kernel
+    const int p = (rank_ + i) % world_;
+    cudaStream_t ps = pstreams_[p];
+    ck(cudaStreamWaitEvent(ps, ev_in_, 0), "wait");
+    // segs expert segments of seg_bytes each; rows [row0, row0 + rows) of every segment
+    char* dst = static_cast<char*>(peer_bufs_[ch][p]) + ro[rank_] + row0_bytes;
+    const char* s0 = static_cast<const char*>(src) + so[p] + row0_bytes;
+    ck(cudaMemcpy2DAsync(dst, seg_bytes, s0, seg_bytes, rows_bytes, segs, cudaMemcpyDeviceToDevice, ps),
+       "peer copy (rows)");
+    publish_one(ps, (2 * ch) * world_ + p, epoch, ready_remote(p, ch, slot));
+    ck(cudaEventRecord(ev_out_[p], ps), "event");
+  }
+  for (int p = 0; p < world_; ++p)
+    if (p != rank_) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
+}
+
 FlagWait PeerExchange::ready_wait(int ch, int chunk, uint32_t epoch) const {
   FlagWait w;
   w.base = ready_local(ch, 0, chunk);
-  w.stride = kMaxChunks;
+  w.stride = kFlagSlots;
   w.world = world_;
   w.rank = rank_;
   w.epoch = epoch;

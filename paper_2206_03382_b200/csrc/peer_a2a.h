@@ -29,6 +29,9 @@ class PeerExchange {
  public:
   static constexpr int kChannels = 4;  // fwd dispatch, fwd combine, bwd dispatch, bwd combine
   static constexpr int kMaxChunks = 8;
+  // ready-flag slots per (channel, source): one per chunk + kHalfSlot ("chunk 0, first rows")
+  static constexpr int kHalfSlot = kMaxChunks;
+  static constexpr int kFlagSlots = kMaxChunks + 1;
 
   // bufs[ch]: this rank's receive buffer of channel ch (cudaMalloc base pointers).
   PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels]);
@@ -46,6 +49,13 @@ class PeerExchange {
   void push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
                   const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch,
                   cudaEvent_t local_done = nullptr);
+  // Copy stream: push rows [row0, row0 + rows) of each of `segs` expert segments (seg_bytes apart;
+  // offsets so / ro in BYTES, per destination) to every peer, then publish ready[ch][me][slot].
+  // Used to split the first chunk so its first rows land early (the own rows are written in
+  // place by the producing kernel).
+  void push_rows(cudaStream_t copy, int ch, int slot, const void* src, const int64_t* so,
+                 const int64_t* ro, size_t segs, size_t seg_bytes, size_t row0_bytes,
+                 size_t rows_bytes, uint32_t epoch);
   // Compute stream: wait for every peer's chunk of this epoch (stream memory operations).
   void wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch);
   // The same wait as a device-side poll (fused into the first consuming kernel, or

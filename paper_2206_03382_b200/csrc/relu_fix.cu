@@ -74,8 +74,8 @@ __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, int R, in
 // rownorm[i] = |x[i]|_2 (one warp per row)
 // |x[r]|_2 per row (rounded up). Optionally first waits for the chunk's peer flags (fused
 // receive wait) and resets the fixup counter.
-__global__ void rownorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int M,
-                               float* __restrict__ rownorm, FlagWait fw, unsigned int* reset) {
+__global__ void rownorm_kernel(const __nv_bfloat16* __restrict__ x, int M, float* __restrict__ rownorm,
+                               RowSet rs, FlagWait fw, unsigned int* reset) {
   pdl_entry();
   if (fw.base != nullptr) {
     if (threadIdx.x < 32) wait_flags_warp(fw);
@@ -84,8 +84,12 @@ __global__ void rownorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows
   if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0u;
   const int lane = threadIdx.x % 32;
   const bool vec = (M % 8) == 0;
-  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+  const int64_t total = static_cast<int64_t>(rs.nsegs) * rs.nrows;
+  for (int64_t id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; id < total;
+       id += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    int64_t seg = rs.seg_begin + id / rs.nrows;
+    if (rs.skip_count > 0 && seg >= rs.skip_begin) seg += rs.skip_count;
+    const int64_t r = seg * rs.seg_rows + rs.row0 + id % rs.nrows;
     const __nv_bfloat16* p = x + r * M;
     float s = 0.0f;
     if (vec) {
@@ -222,13 +226,14 @@ int weight_stats_device(const void* w1, int G, int M, int V, float* colnorm, flo
   return launch_status();
 }
 
-int rownorm_device(const void* x, int64_t rows, int M, float* rownorm, cudaStream_t st,
-                  const FlagWait* wait, unsigned int* reset) {
+int rownorm_device(const void* x, int M, float* rownorm, const RowSet& rs, cudaStream_t st,
+                   const FlagWait* wait, unsigned int* reset) {
+  const int64_t rows = static_cast<int64_t>(rs.nsegs) * rs.nrows;
   if (rows <= 0) return 0;
   const int64_t blocks = (rows + 7) / 8;
   const int grid = static_cast<int>(blocks < 148 * 4 ? blocks : 148 * 4);
-  launch_k(rownorm_kernel, grid, 256, 0, st, static_cast<const __nv_bfloat16*>(x), rows, M, rownorm,
-                                      wait ? *wait : FlagWait{}, reset);
+  launch_k(rownorm_kernel, grid, 256, 0, st, static_cast<const __nv_bfloat16*>(x), M, rownorm, rs,
+           wait ? *wait : FlagWait{}, reset);
   return launch_status();
 }
 
