@@ -295,9 +295,10 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # Alg. 1 explores its strategy space (8 forward steps) before exploiting; let that finish
+    # Alg. 1 explores its strategy space (2 forward steps per strategy: the first, cold one is not
+    # recorded) before exploiting; let that finish
     # in the untimed warm-up so the timed steps run the chosen pipelining degree.
-    for _ in range(args.warmup + (10 if adaptive else 0)):
+    for _ in range(args.warmup + (12 if adaptive else 0)):
         step()
     barrier()
     state.take_profile()  # drop warm-up records

@@ -1001,13 +1001,19 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   // all-reduce so every rank records the same time and picks the same strategy), so it runs
   // while the f bucket is still exploring; once every strategy has a time the controller
   // exploits the argmin without stalling the stream.
+  // The first execution of a (f, strategy) pair is not recorded: it pays one-off costs (lazy
+  // loading of the kernel instantiations only that degree uses, first touches) that the
+  // reference's simulated seconds never see, and a single cold sample would decide the argmin.
   if (cfg_.adaptive && !strategy_settled(memo_, f_)) {
-    ck(cudaEventSynchronize(ev_fwd_end_), "event sync");
-    float ms = 0.0f;
-    ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");
-    double sec = ms * 1e-3;
-    if (W_ > 1) sec = allreduce_max_host(sec);
-    optimize_strategy(memo_, f_, strategy_, sec);
+    const auto key = std::make_pair(f_, strategy_index(strategy_));
+    if (!warm_.insert(key).second) {
+      ck(cudaEventSynchronize(ev_fwd_end_), "event sync");
+      float ms = 0.0f;
+      ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");
+      double sec = ms * 1e-3;
+      if (W_ > 1) sec = allreduce_max_host(sec);
+      optimize_strategy(memo_, f_, strategy_, sec);
+    }
   }
 }
 

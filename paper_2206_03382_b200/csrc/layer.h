@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -118,6 +119,7 @@ class Layer {
   double f_ = 1.0;
   Strategy strategy_;
   StrategyMemo memo_;
+  std::set<std::pair<double, int>> warm_;  // (f, strategy) pairs executed once (not recorded)
   bool fwd_done_ = false, metrics_valid_ = false;
   int64_t launches_ = 0, bwd_launches_ = 0;
   double comm_bytes_ = 0.0;
