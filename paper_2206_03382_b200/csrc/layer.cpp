@@ -661,6 +661,16 @@ void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
 
 // Copy-engine version of exchange(): push chunk `chunk` of `src` into every peer's channel
 // buffer (same plan), then publish the chunk's ready flag.
+// Row parts of the first chunk (pipelined in pieces so its first rows land while the own
+// segment is computed): 1/4, 1/4, 1/2 when the quarters are whole 256-row tiles, else halves,
+// else one part. Parts except the last publish kPartSlot0 + i, the last the chunk's slot 0.
+static std::vector<uint32_t> first_chunk_parts(int64_t cc, bool enable) {
+  if (enable && cc % 1024 == 0) return {static_cast<uint32_t>(cc / 4), static_cast<uint32_t>(cc / 4),
+                                        static_cast<uint32_t>(cc / 2)};
+  if (enable && cc % 512 == 0) return {static_cast<uint32_t>(cc / 2), static_cast<uint32_t>(cc / 2)};
+  return {static_cast<uint32_t>(cc)};
+}
+
 // Rows [row0, row0 + nrows) of every segment of chunk `chunk` to every peer (slot: ready flag).
 void Layer::peer_push_rows(int ch, const void* src, int chunk, int phase, int slot, uint32_t row0,
                            uint32_t nrows, uint32_t epoch) {
@@ -837,15 +847,19 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[0], 0), "wait");  // my recv buffer consumed
     peer_->wait_peers_freed(comm_stream_, 0, e0);
     prof_mark(kPhA2aFwd, true, comm_stream_);
-    // first chunk in two row halves when the tile shape allows (tcgen05 path): its first rows
-    // land while this rank computes its own segment
-    const bool split0 = local_first_ && fused_combine_ && cc_ % 512 == 0;
-    const uint32_t h0 = static_cast<uint32_t>(cc_ / 2);
+    // first chunk in row parts when the tile shape allows (tcgen05 path): its first rows land
+    // while this rank computes its own segment
+    const std::vector<uint32_t> parts0 = first_chunk_parts(cc_, local_first_ && fused_combine_);
+    const bool split0 = parts0.size() > 1;
     for (int i = 0; i < degree_; ++i) {
       if (i == 0 && split0) {
-        peer_push_rows(0, z_.p, 0, 0, PeerExchange::kHalfSlot, 0, h0, e0);
-        peer_push_rows(0, z_.p, 0, 0, 0, h0, static_cast<uint32_t>(cc_) - h0, e0);
-        tl_mark("dispatch pushed 0 (2 halves) [comm]", comm_stream_);
+        uint32_t r = 0;
+        for (size_t p = 0; p < parts0.size(); ++p) {
+          const int slot = p + 1 < parts0.size() ? PeerExchange::kPartSlot0 + static_cast<int>(p) : 0;
+          peer_push_rows(0, z_.p, 0, 0, slot, r, parts0[p], e0);
+          r += parts0[p];
+        }
+        tl_mark("dispatch pushed 0 (parts) [comm]", comm_stream_);
         continue;
       }
       peer_push(0, z_.p, i, 0, e0, nullptr);  // my own block: written into recv by encode
@@ -892,12 +906,17 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       const FlagWait fw = peer_->ready_wait(0, i, e0);
       down.seg_base = i * W_;
       if (i == 0 && split0) {
-        // own rows first, then the peers' first half rows (their own flag), then the rest: each
-        // transfer hides behind the previous GEMM
-        const FlagWait fh = peer_->ready_wait(0, PeerExchange::kHalfSlot, e0);
+        // own rows first, then the peers' row parts in arrival order (each under its own flag):
+        // every transfer hides behind the previous GEMM
         up_range(0, rank_, rank_ + 1, -1, 0, 0, nullptr, true);
-        up_range(0, 0, W_, rank_, 0, h0, &fh, false);
-        up_range(0, 0, W_, rank_, h0, 0, &fw, false);
+        uint32_t r = 0;
+        for (size_t p = 0; p < parts0.size(); ++p) {
+          const FlagWait fp = p + 1 < parts0.size()
+                                  ? peer_->ready_wait(0, PeerExchange::kPartSlot0 + static_cast<int>(p), e0)
+                                  : fw;
+          up_range(0, 0, W_, rank_, r, p + 1 < parts0.size() ? parts0[p] : 0, &fp, false);
+          r += parts0[p];
+        }
       } else if (i == 0 && local_first_ && fused_combine_) {
         up_range(0, rank_, rank_ + 1, -1, 0, 0, nullptr, true);
         up_range(0, 0, W_, rank_, 0, 0, &fw, false);
@@ -1124,13 +1143,17 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[2], 0), "wait");
     peer_->wait_peers_freed(comm_stream_, 2, e2);
     prof_mark(kPhA2aBwd, true, comm_stream_);
-    const bool split0 = local_first_ && fused_combine_ && cc_ % 512 == 0;  // as in forward
-    const uint32_t h0 = static_cast<uint32_t>(cc_ / 2);
+    const std::vector<uint32_t> parts0 = first_chunk_parts(cc_, local_first_ && fused_combine_);
+    const bool split0 = parts0.size() > 1;  // as in forward
     for (int i = 0; i < degree_; ++i) {  // adjoint of combine
       if (i == 0 && split0) {
-        peer_push_rows(2, dz_.p, 0, 0, PeerExchange::kHalfSlot, 0, h0, e2);
-        peer_push_rows(2, dz_.p, 0, 0, 0, h0, static_cast<uint32_t>(cc_) - h0, e2);
-        tl_mark("bwd dispatch pushed 0 (2 halves) [comm]", comm_stream_);
+        uint32_t r = 0;
+        for (size_t p = 0; p < parts0.size(); ++p) {
+          const int slot = p + 1 < parts0.size() ? PeerExchange::kPartSlot0 + static_cast<int>(p) : 0;
+          peer_push_rows(2, dz_.p, 0, 0, slot, r, parts0[p], e2);
+          r += parts0[p];
+        }
+        tl_mark("bwd dispatch pushed 0 (parts) [comm]", comm_stream_);
         continue;
       }
       peer_push(2, dz_.p, i, 0, e2, nullptr);  // my own block: written into drecv by decode_bwd
@@ -1159,10 +1182,15 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
         prof_mark(kPhDgradMask, false, st);
       };
       if (i == 0 && split0) {
-        const FlagWait fh = peer_->ready_wait(2, PeerExchange::kHalfSlot, e2);
         dgm_range(rank_, rank_ + 1, -1, 0, 0, nullptr);
-        dgm_range(0, W_, rank_, 0, h0, &fh);
-        dgm_range(0, W_, rank_, h0, 0, &fw);
+        uint32_t r = 0;
+        for (size_t p = 0; p < parts0.size(); ++p) {
+          const FlagWait fp = p + 1 < parts0.size()
+                                  ? peer_->ready_wait(2, PeerExchange::kPartSlot0 + static_cast<int>(p), e2)
+                                  : fw;
+          dgm_range(0, W_, rank_, r, p + 1 < parts0.size() ? parts0[p] : 0, &fp);
+          r += parts0[p];
+        }
       } else if (i == 0 && local_first_ && fused_combine_) {
         dgm_range(rank_, rank_ + 1, -1, 0, 0, nullptr);
         dgm_range(0, W_, rank_, 0, 0, &fw);

@@ -29,9 +29,11 @@ class PeerExchange {
  public:
   static constexpr int kChannels = 4;  // fwd dispatch, fwd combine, bwd dispatch, bwd combine
   static constexpr int kMaxChunks = 8;
-  // ready-flag slots per (channel, source): one per chunk + kHalfSlot ("chunk 0, first rows")
-  static constexpr int kHalfSlot = kMaxChunks;
-  static constexpr int kFlagSlots = kMaxChunks + 1;
+  // ready-flag slots per (channel, source): one per chunk + kPartSlots for the leading row
+  // parts of chunk 0 (its last part publishes the chunk's own slot 0)
+  static constexpr int kPartSlots = 2;
+  static constexpr int kPartSlot0 = kMaxChunks;
+  static constexpr int kFlagSlots = kMaxChunks + kPartSlots;
 
   // bufs[ch]: this rank's receive buffer of channel ch (cudaMalloc base pointers).
   PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels]);

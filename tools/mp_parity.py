@@ -88,8 +88,10 @@ def main():
         (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "nccl"),
         (2, 2, 1.0, 256, 512, 512, True, "bf16", 2, False, "peer", "auto"),
         (2, 1, 1.25, 128, 256, 400, False, "bf16", 4, False, "nccl", "bounded"),
-        # first chunk pushed / computed in two row halves (cc a multiple of 512)
+        # first chunk pushed / computed in row parts (1/4, 1/4, 1/2 when cc % 1024 == 0, halves
+        # when cc % 512 == 0)
         (2, 1, 1.0, 256, 512, 4096, False, "bf16", 1, False, "peer"),
+        (2, 1, 1.0, 256, 512, 8192, False, "bf16", 1, False, "peer"),
         (2, 2, 1.0, 256, 512, 4096, True, "bf16", 2, False, "peer"),
         # test_moe_layer.cpp:62-66: cosine router, auto capacity, base_config(2, 2, 2, T=4, M=3, V=8)
         (2, 1, 1.0, 3, 8, 4, False, "f32", 1, False, "peer", "auto", "cosine"),
