@@ -18,6 +18,7 @@
 
 #include "kernels.h"
 #include "pdl.cuh"
+#include "peer_flags.cuh"
 
 namespace moe {
 
@@ -203,8 +204,12 @@ template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     decode_kernel(SlotGeom g, const T* __restrict__ z, const int32_t* __restrict__ idxs,
                   const int32_t* __restrict__ locations, const double* __restrict__ gates,
-                  T* __restrict__ y) {
+                  T* __restrict__ y, FlagWait fw) {
   pdl_entry();
+  if (fw.base != nullptr) {  // fused receive wait (the peers' combined rows)
+    if (threadIdx.x < 32) wait_flags_warp(fw);
+    __syncthreads();
+  }
   const int lane = threadIdx.x % 32;
   const int ntok = g.blocks * g.T;
   for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
@@ -354,8 +359,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 template <typename T, bool kVec>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
     encode_bwd_kernel(SlotGeom g, const T* __restrict__ dz, const int32_t* __restrict__ idxs,
-                      const int32_t* __restrict__ locations, T* __restrict__ dx) {
+                      const int32_t* __restrict__ locations, T* __restrict__ dx, FlagWait fw) {
   pdl_entry();
+  if (fw.base != nullptr) {  // fused receive wait (the peers' combined dX rows)
+    if (threadIdx.x < 32) wait_flags_warp(fw);
+    __syncthreads();
+  }
   const int lane = threadIdx.x % 32;
   const int ntok = g.blocks * g.T;
   for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
@@ -448,16 +457,18 @@ int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* sl
 }
 
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
-                  const int32_t* locations, const double* gates, void* y, cudaStream_t st) {
+                  const int32_t* locations, const double* gates, void* y, cudaStream_t st,
+                  const FlagWait* wait) {
+  const FlagWait fw = wait ? *wait : FlagWait{};
   const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) launch_k(decode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
-    else launch_k(decode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y));
+    if (v) launch_k(decode_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y), fw);
+    else launch_k(decode_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(z), idxs, locations, gates, static_cast<float*>(y), fw);
   } else {
     using B = __nv_bfloat16;
-    if (v) launch_k(decode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
-    else launch_k(decode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y));
+    if (v) launch_k(decode_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y), fw);
+    else launch_k(decode_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(z), idxs, locations, gates, static_cast<B*>(y), fw);
   }
   return launch_status();
 }
@@ -493,16 +504,18 @@ int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, co
 }
 
 int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
-                           const int32_t* locations, void* dx, cudaStream_t st) {
+                           const int32_t* locations, void* dx, cudaStream_t st,
+                           const FlagWait* wait) {
+  const FlagWait fw = wait ? *wait : FlagWait{};
   const int grid = grid_for(static_cast<size_t>(g.blocks) * g.T);
   const bool v = vec_ok(dtype, g.M);
   if (dtype == 1) {
-    if (v) launch_k(encode_bwd_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
-    else launch_k(encode_bwd_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx));
+    if (v) launch_k(encode_bwd_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx), fw);
+    else launch_k(encode_bwd_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(dz), idxs, locations, static_cast<float*>(dx), fw);
   } else {
     using B = __nv_bfloat16;
-    if (v) launch_k(encode_bwd_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
-    else launch_k(encode_bwd_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx));
+    if (v) launch_k(encode_bwd_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx), fw);
+    else launch_k(encode_bwd_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(dz), idxs, locations, static_cast<B*>(dx), fw);
   }
   return launch_status();
 }

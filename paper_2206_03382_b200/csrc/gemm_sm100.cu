@@ -23,6 +23,7 @@
 #include "gemm_sm100.h"
 #include "kernels.h"
 #include "pdl.cuh"
+#include "peer_flags.cuh"
 #include "ptx.cuh"
 
 #ifndef MOE_GEMM_STAGES
@@ -192,6 +193,14 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
   // programmatic dependent launch: the prologue above overlapped the previous kernel's tail;
   // operands produced by it are read only after this wait
   pdl_entry();
+  if (args.wait.base != nullptr && (warp == 0 || warp >= 4)) {
+    // fused receive wait: the producer warp polls the peers' flags (ld.acquire.sys) before its
+    // first TMA load -- the async proxy must then see what the copy engines wrote before the
+    // flags -- and each epilogue warp acquires them itself before reading peer-written row
+    // norms or storing into peer buffers
+    wait_flags_warp(args.wait);
+    if (warp == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
 
   const uint32_t ntiles = num_tiles<kRowK, C::TM>(args);
   const uint32_t nkb = num_kblocks<kRowK>(args);
@@ -351,7 +360,8 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
       const bool cert = kEpi == kEpiReluBf16 && args.fix_list != nullptr && row_ok;
       if constexpr (kEpi == kEpiReluBf16) {
         if (cert) {
-          rmax = __ldg(args.rownorm + orow) * kReluTauScale;
+          // coherent load: peers' row norms may have landed after this kernel started
+          rmax = __ldcg(args.rownorm + orow) * kReluTauScale;
 #pragma unroll
           for (uint32_t c = 0; c < kSubs; ++c)
             tblk[c] = rmax * __ldg(args.colnorm_blk + static_cast<size_t>(tc.g) * (args.N / 64) + col0 / 64 + c);

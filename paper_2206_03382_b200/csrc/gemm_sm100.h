@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "peer_flags.h"
+
 namespace moe {
 
 enum GemmKind : int {
@@ -60,6 +62,10 @@ struct GemmArgs {
   // segment index of [0, S] skipped (skip_seg < 0: none; S then counts the segments processed)
   uint32_t row0 = 0, nrows = 0;
   int32_t skip_seg = -1;
+  // W > 1: peers' ready (or freed) flags the kernel polls before its first load -- the receive
+  // wait fused into the GEMM (wait.base == nullptr: none). Row norms (certificate) written by the
+  // peers before the flags are then read coherently.
+  FlagWait wait;
   // kIdxPeerD: destination combine buffer of every rank (this rank's own for src == rank)
   uint32_t peer_world, peer_rank, peer_out_segs;  // out_segs = chunks * E
   void* peer_d[kMaxPeers];

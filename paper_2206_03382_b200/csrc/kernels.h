@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "peer_flags.h"
+
 #include <cstdint>
 
 namespace moe {
@@ -105,8 +107,10 @@ struct LocalDest {
 int encode_device(const SlotGeom& g, int dtype, const void* x, const int32_t* slot_token, void* z,
                   cudaStream_t st, float* rownorm = nullptr, const DropZero& dzero = DropZero{},
                   unsigned int* reset = nullptr, const LocalDest& local = LocalDest{});
+// wait (optional): peers' ready flags polled by the kernel before it reads z (fused receive wait)
 int decode_device(const SlotGeom& g, int dtype, const void* z, const int32_t* idxs,
-                  const int32_t* locations, const double* gates, void* y, cudaStream_t st);
+                  const int32_t* locations, const double* gates, void* y, cudaStream_t st,
+                  const FlagWait* wait = nullptr);
 int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
                            const int32_t* slot_token, const float* slot_gate, void* dz,
                            cudaStream_t st, const DropZero& dzero = DropZero{},
@@ -116,7 +120,8 @@ int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, co
                                  const int32_t* idxs, const int32_t* locations, double* dgates,
                                  cudaStream_t st);
 int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
-                           const int32_t* locations, void* dx, cudaStream_t st);
+                           const int32_t* locations, void* dx, cudaStream_t st,
+                           const FlagWait* wait = nullptr);
 
 int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* idxs,
                        const int32_t* locations, const double* gates, int32_t* slot_token,
@@ -134,7 +139,6 @@ int weight_stats_device(const void* w1, int G, int M, int V, float* colnorm, flo
                         void* w1t, cudaStream_t st);
 int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned long long* mask,
                               cudaStream_t st);
-struct FlagWait;
 // wait: optional fused receive wait (peer flags, see peer_flags.cuh); reset: optional counter
 // zeroed by the kernel (the ReLU fixup count)
 // Rows [row0, row0 + nrows) of segments [seg_begin, seg_begin + nsegs) (seg_rows apart), the

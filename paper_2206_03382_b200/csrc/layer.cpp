@@ -805,6 +805,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
 
   void* recv = W_ > 1 ? recv_.p : z_.p;
   void* ycomb = W_ > 1 ? ycomb_.p : yexp_.p;
+  FlagWait combine_wait;  // peer backend: the combined rows' ready flags, polled by decode
   if (fused_) {
     // decode fused into the down GEMM: y[token] = g * (act . W2)[slot], rows scattered by TMA;
     // tokens without a slot get zero rows (the decode's dropped-token case).
@@ -932,11 +933,10 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       if (fused_combine_) {
         // combine fused into the down GEMM: tiles are stored into the source ranks' ycomb over
         // NVLink as they complete; the chunk's ready flags follow the kernel
-        if (i == 0) {
-          ckr(wait_flags_device(peer_->freed_wait(1, e1 - 1), st), "wait");
-          ++launches_;
-        }
         GemmArgs dn = peer_args(down, 1);
+        // before its first store into a peer's ycomb, every peer has consumed it (polled inside
+        // the GEMM by the epilogue warps)
+        if (i == 0) dn.wait = peer_->freed_wait(1, e1 - 1);
         gemm(kGemmDown, act_.p, w2_.p, ycomb, dn, nseg, st);
         peer_->signal_ready(st, 1, i, e1);
         comm_bytes_ += static_cast<double>(dE_) * cc_ * M_ * esz_ * (W_ - 1);
@@ -957,10 +957,9 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       ck(cudaStreamWaitEvent(st, ev_c_[degree_ - 1], 0), "wait");
     }
     prof_mark(kPhA2aFwd, false, comm_stream_);
-    // blocks of one source land in chunk order: the last chunk's flags cover all
-    ckr(wait_flags_device(peer_->ready_wait(1, degree_ - 1, e1), st), "wait");
-    ++launches_;
-    tl_mark("combine landed", st);
+    // blocks of one source land in chunk order: the last chunk's flags cover all -- polled by
+    // the decode kernel itself
+    combine_wait = peer_->ready_wait(1, degree_ - 1, e1);
   } else {
     // Comm stream: all dispatches (chunk order), then all combines (reference FIFO order,
     // pipeline.cpp:180-190); compute stream: per chunk up+down GEMMs.
@@ -1004,7 +1003,9 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   if (!fused_) {
     prof_mark(kPhDecode, true, st);
-    ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st), "decode");
+    ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st,
+                      combine_wait.base ? &combine_wait : nullptr),
+        "decode");
     prof_mark(kPhDecode, false, st);
     ++launches_;
   }
@@ -1105,6 +1106,7 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   void* recv = W_ > 1 ? recv_.p : z_.p;
   void* drecv = W_ > 1 ? drecv_.p : dz_.p;
   void* dxcomb = W_ > 1 ? dxcomb_.p : dxe_.p;
+  FlagWait combine_wait;  // peer backend: polled by encode_bwd
   if (fused_) {
     // encode-backward fused into the dgrad GEMM: dx[token] = (dh . W1^T)[slot], rows scattered
     // by TMA; dropped tokens get zero rows.
@@ -1166,12 +1168,14 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
       auto dgm_range = [&](int s0, int s1, int skip, uint32_t row0, uint32_t nrows, const FlagWait* w) {
         const int nsrc = (s1 - s0) - (skip >= 0 ? 1 : 0);
         if (nsrc <= 0) return;
-        if (w) {
+        GemmArgs a = dgm;
+        if (w && fused_combine_) {
+          a.wait = *w;  // tcgen05 path: the receive wait runs inside the GEMM
+        } else if (w) {
           ckr(wait_flags_device(*w, st), "wait");
           ++launches_;
           tl_mark("bwd dispatch landed " + std::to_string(i), st);
         }
-        GemmArgs a = dgm;
         a.seg_base = static_cast<uint32_t>(i * W_ + s0);
         a.S = static_cast<uint32_t>(nsrc);
         a.skip_seg = skip >= 0 ? skip - s0 : -1;
@@ -1204,11 +1208,8 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
       prof_mark(kPhDgrad, true, st);
       if (fused_combine_) {
         // backward combine fused into the dgrad GEMM (dx blocks straight to the source ranks)
-        if (i == 0) {
-          ckr(wait_flags_device(peer_->freed_wait(3, e3 - 1), st), "wait");
-          ++launches_;
-        }
         GemmArgs d2 = peer_args(dg, 3);
+        if (i == 0) d2.wait = peer_->freed_wait(3, e3 - 1);
         gemm(kGemmDgrad, dh_.p, w1_.p, dxcomb, d2, nseg, st);
         peer_->signal_ready(st, 3, i, e3);
         comm_bytes_ += static_cast<double>(dE_) * cc_ * M_ * esz_ * (W_ - 1);
@@ -1241,9 +1242,7 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     peer_->signal_freed(st, 2, e2);
     ck(cudaEventRecord(ev_freed_[2], st), "event");
     if (!fused_combine_) ck(cudaStreamWaitEvent(st, ev_c_[degree_ - 1], 0), "wait");
-    ckr(wait_flags_device(peer_->ready_wait(3, degree_ - 1, e3), st), "wait");
-    ++launches_;
-    tl_mark("bwd combine landed", st);
+    combine_wait = peer_->ready_wait(3, degree_ - 1, e3);  // polled by the encode_bwd kernel
   } else {
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
@@ -1281,7 +1280,9 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   }
   if (!fused_) {
     prof_mark(kPhEncodeBwd, true, st);
-    ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st), "encode_bwd");
+    ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st,
+                               combine_wait.base ? &combine_wait : nullptr),
+        "encode_bwd");
     prof_mark(kPhEncodeBwd, false, st);
     ++launches_;
   }
