@@ -113,15 +113,23 @@ __device__ __forceinline__ void zero_dropped_rows(const DropZero& d) {
 
 // Destination row of slot-major row `row` = (block b, chunk i, expert e, slot c % cc): the send
 // buffer, or (this rank's experts, LocalDest) the receive buffer's own-source segment.
+__device__ __forceinline__ bool is_own(const LocalDest& ld, int e) {
+  return ld.recv != nullptr && e / ld.dE == ld.rank;
+}
+__device__ __forceinline__ size_t own_row(const LocalDest& ld, const SlotGeom& g, int i, int e, int rem) {
+  return (static_cast<size_t>(i * ld.W + ld.rank) * ld.dE + (e - ld.rank * ld.dE)) * g.cc + rem % g.cc;
+}
 template <typename T>
 __device__ __forceinline__ T* gather_dst(T* z, const LocalDest& ld, const SlotGeom& g, size_t row,
                                          int i, int e, int rem) {
-  if (ld.recv != nullptr && e / ld.dE == ld.rank) {
-    const size_t rrow = (static_cast<size_t>(i * ld.W + ld.rank) * ld.dE + (e - ld.rank * ld.dE)) * g.cc +
-                        rem % g.cc;
-    return static_cast<T*>(ld.recv) + rrow * g.M;
-  }
+  if (is_own(ld, e)) return static_cast<T*>(ld.recv) + own_row(ld, g, i, e, rem) * g.M;
   return z + row * g.M;
+}
+// where the row's norm goes: the receive-side array for own rows (if given), else z order
+__device__ __forceinline__ float* norm_dst(float* rownorm, const LocalDest& ld, const SlotGeom& g,
+                                           size_t row, int i, int e, int rem) {
+  if (is_own(ld, e) && ld.recv_norm != nullptr) return ld.recv_norm + own_row(ld, g, i, e, rem);
+  return rownorm ? rownorm + row : nullptr;
 }
 
 // ------------------------------------------------------------------ encode
@@ -166,7 +174,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
             const int v = v0 + u * 32 + lane;
             if (v < nv) {
               dst[v] = buf[u];
-              if (rownorm) {
+              if (rownorm || (ld.recv_norm && is_own(ld, e))) {
                 float f[VN];
                 Vec<T>::to_f32(buf[u], f);
 #pragma unroll
@@ -176,10 +184,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
           }
         }
       }
-      if (rownorm) {
+      if (rownorm || (ld.recv_norm && is_own(ld, e))) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
-        if (lane == 0) rownorm[row] = sqrtf(ssq) * 1.001f;  // |x_row|_2, rounded up
+        if (lane == 0) {
+          float* nd = norm_dst(rownorm, ld, g, row, i, e, rem);
+          if (nd) *nd = sqrtf(ssq) * 1.001f;  // |x_row|_2, rounded up
+        }
       }
     } else {
       T* dst = gather_dst(z, ld, g, row, i, e, rem);
@@ -189,10 +200,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         dst[m] = v;
         ssq = fmaf(to_f(v), to_f(v), ssq);
       }
-      if (rownorm) {
+      if (rownorm || (ld.recv_norm && is_own(ld, e))) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
-        if (lane == 0) rownorm[row] = sqrtf(ssq) * 1.001f;  // |x_row|_2, rounded up
+        if (lane == 0) {
+          float* nd = norm_dst(rownorm, ld, g, row, i, e, rem);
+          if (nd) *nd = sqrtf(ssq) * 1.001f;  // |x_row|_2, rounded up
+        }
       }
     }
   }

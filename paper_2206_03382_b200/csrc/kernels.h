@@ -99,6 +99,7 @@ struct DropZero {
 struct LocalDest {
   void* recv = nullptr;
   int W = 1, rank = 0, dE = 0;
+  float* recv_norm = nullptr;  // encode: the own rows' norms go here (receive-row index)
 };
 
 // dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rownorm (optional, [z rows]):

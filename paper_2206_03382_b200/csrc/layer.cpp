@@ -244,7 +244,8 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
     colnorm_.alloc(sizeof(float) * dE_ * V_);
     colnorm_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
     w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
-    fix_count_.alloc(sizeof(unsigned int));
+    fix_count_.alloc(3 * sizeof(unsigned int));  // list size, fixup CTAs done, last list size
+    ck(cudaMemset(fix_count_.p, 0, 3 * sizeof(unsigned int)), "memset");
   }
   if (W_ > 1 && cfg.a2a_backend != MOE_A2A_BACKEND_PEER && cfg.a2a_backend != MOE_A2A_BACKEND_NCCL)
     throw MoeError(MOE_EINVAL, "unknown all-to-all backend");
@@ -277,6 +278,7 @@ void Layer::alloc_capacity(int cap) {
     const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
     relu_mask_.alloc(sizeof(unsigned long long) * rows_all * (V_ / 64 + 1));
     rownorm_.alloc(sizeof(float) * rows_all);
+    if (W_ > 1) znorm_.alloc(sizeof(float) * rows_all);
     fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));
     fix_list_.alloc(sizeof(unsigned long long) * fix_cap_);
   }
@@ -287,10 +289,14 @@ void Layer::alloc_capacity(int cap) {
     dxcomb_.alloc(rowsM);
     if (cfg_.a2a_backend == MOE_A2A_BACKEND_PEER) {
       void* bufs[PeerExchange::kChannels] = {recv_.p, ycomb_.p, drecv_.p, dxcomb_.p};
-      peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs);
+      const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
+      peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs, cert ? rownorm_.p : nullptr);
       const char* e = std::getenv("MOE_FUSED_COMBINE");  // =0: copy-engine combine (A/B runs)
       fused_combine_ = !(e && e[0] == '0') && cfg_.dtype == MOE_DTYPE_BF16 && W_ <= kMaxPeers &&
                        M_ % 256 == 0 && V_ % 64 == 0;
+      // certificate row norms computed by the sender and pushed with the rows (tcgen05 path:
+      // the up GEMM then takes the receive wait itself)
+      sender_norms_ = cert && fused_combine_;
       for (auto& e : epoch_) e = 0;  // fresh flag block on every rank
       bwd_pending_ = false;
     }
@@ -682,8 +688,9 @@ void Layer::peer_push_rows(int ch, const void* src, int chunk, int phase, int sl
     ro[p] *= esz_;
   }
   const size_t row_bytes = static_cast<size_t>(M_) * esz_;
+  const float* norms = (ch == 0 && sender_norms_) ? static_cast<const float*>(znorm_.p) : nullptr;
   peer_->push_rows(comm_stream_, ch, slot, src, so.data(), ro.data(), static_cast<size_t>(dE_),
-                   cc_ * row_bytes, row0 * row_bytes, nrows * row_bytes, epoch);
+                   cc_ * row_bytes, row0 * row_bytes, nrows * row_bytes, epoch, norms, row_bytes);
   comm_bytes_ += static_cast<double>(dE_) * nrows * row_bytes * (W_ - 1);
 }
 
@@ -703,8 +710,9 @@ void Layer::peer_push(int ch, const void* src, int chunk, int phase, uint32_t ep
   std::vector<int64_t> so(W_), ro(W_);
   int64_t elems = 0;
   a2a_plan(W_, E_, cc_, M_, chunk, phase, so.data(), ro.data(), &elems);
+  const float* norms = (ch == 0 && sender_norms_) ? static_cast<const float*>(znorm_.p) : nullptr;
   peer_->push_chunk(comm_stream_, ch, chunk, src, so.data(), ro.data(),
-                    static_cast<size_t>(elems) * esz_, esz_, epoch, local_done);
+                    static_cast<size_t>(elems) * esz_, esz_, epoch, local_done, norms, M_);
   comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
 }
 
@@ -771,10 +779,13 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     own.W = W_;
     own.rank = rank_;
     own.dE = dE_;
+    if (sender_norms_) own.recv_norm = static_cast<float*>(rownorm_.p);
   }
+  float* enc_norm = nullptr;  // row norms computed by the encode pass
+  if (cert && W_ == 1) enc_norm = static_cast<float*>(rownorm_.p);
+  if (peer_ && sender_norms_) enc_norm = static_cast<float*>(znorm_.p);
   prof_mark(kPhEncode, true, st);
-  ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st,
-                    (cert && W_ == 1) ? static_cast<float*>(rownorm_.p) : nullptr, yzero,
+  ckr(encode_device(g, cfg_.dtype, x, gb.slot_token, z_.p, st, enc_norm, yzero,
                     (cert && W_ == 1) ? static_cast<unsigned int*>(fix_count_.p) : nullptr, own),
       "encode");
   prof_mark(kPhEncode, false, st);
@@ -879,7 +890,10 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       u.skip_seg = skip >= 0 ? skip - s0 : -1;
       u.row0 = row0;
       u.nrows = nrows;
-      if (cert) {
+      if (sender_norms_) {
+        // norms arrived with the rows; the GEMM polls the flags itself (fixup resets the count)
+        if (fw) u.wait = *fw;
+      } else if (cert) {
         RowSet rs;
         rs.seg_begin = static_cast<int64_t>(i * W_ + s0) * dE_;
         rs.nsegs = static_cast<int64_t>(nsrc) * dE_;
@@ -1443,8 +1457,8 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->fused = (fused_ ? MOE_FUSED_DECODE : 0) | (peer_ && fused_combine_ ? MOE_FUSED_COMBINE : 0);
   m->reserved = 0;
   if (cfg_.dtype == MOE_DTYPE_BF16) {
-    unsigned int nfix = 0;
-    ck(cudaMemcpy(&nfix, fix_count_.p, 4, cudaMemcpyDeviceToHost), "copy");
+    unsigned int nfix = 0;  // the last fixup's list size (relu_fixup_kernel keeps it in [2])
+    ck(cudaMemcpy(&nfix, static_cast<unsigned int*>(fix_count_.p) + 2, 4, cudaMemcpyDeviceToHost), "copy");
     m->relu_fixups = nfix;
     if (nfix > fix_cap_) throw MoeError(MOE_ESTATE, "ReLU-mask certificate list overflowed");
   }

@@ -155,6 +155,10 @@ class Layer {
   void pipe_call(int dir, const void* inh, void* outh, cudaStream_t st);
   // ReLU-mask certificate state (relu_fix.cu)
   DevMem colnorm_, colnorm_blk_, w1t_, rownorm_, fix_list_, fix_count_, relu_mask_;
+  // W > 1 peer backend: row norms of the send buffer (z order); pushed with the rows into the
+  // peers' rownorm_ (receive order), so no receiver-side norm pass is needed
+  DevMem znorm_;
+  bool sender_norms_ = false;
   unsigned int fix_cap_ = 0;
   bool stats_dirty_ = true;
   void prepare_up(GemmArgs& up);

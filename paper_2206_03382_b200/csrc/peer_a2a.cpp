@@ -64,8 +64,9 @@ int stream_wait_geq_u32(cudaStream_t st, const void* addr, uint32_t value) {
              : -2;
 }
 
-PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels])
-    : rank_(rank), world_(world) {
+PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels],
+                           void* norms)
+    : rank_(rank), world_(world), local_norms_(norms) {
   if (!stream_memops_available())
     throw MoeError(MOE_ECUDA, "peer all-to-all: CUDA stream memory operations unavailable");
   for (int c = 0; c < kChannels; ++c) local_bufs_[c] = bufs[c];
@@ -75,10 +76,11 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
   ck(cudaMemset(flags_, 0, nflags_ * sizeof(uint32_t) + 256), "memset flags");
 
   // Exchange IPC handles of {flags, 4 receive buffers} through NCCL.
-  constexpr int kH = 1 + kChannels;
+  constexpr int kH = 2 + kChannels;  // flags, channel buffers, norms (or a placeholder)
   std::vector<cudaIpcMemHandle_t> mine(kH);
   ck(cudaIpcGetMemHandle(&mine[0], flags_), "cudaIpcGetMemHandle");
   for (int c = 0; c < kChannels; ++c) ck(cudaIpcGetMemHandle(&mine[1 + c], bufs[c]), "cudaIpcGetMemHandle");
+  if (norms) ck(cudaIpcGetMemHandle(&mine[1 + kChannels], norms), "cudaIpcGetMemHandle");
   const size_t hb = kH * sizeof(cudaIpcMemHandle_t);
   void* dev = nullptr;
   ck(cudaMalloc(&dev, hb * (world + 1)), "cudaMalloc handles");
@@ -102,6 +104,7 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
   ck(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming), "event");
 
   peer_flags_.assign(world, nullptr);
+  peer_norms_.assign(world, nullptr);
   peer_bufs_.assign(kChannels, std::vector<void*>(world, nullptr));
   for (int p = 0; p < world; ++p) {
     if (p == rank) continue;
@@ -111,6 +114,10 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
       ck(cudaIpcOpenMemHandle(&peer_bufs_[c][p], all[static_cast<size_t>(p) * kH + 1 + c],
                               cudaIpcMemLazyEnablePeerAccess),
          "cudaIpcOpenMemHandle(buffer)");
+    if (norms)  // every rank passes norms or none (same configuration on all ranks)
+      ck(cudaIpcOpenMemHandle(&peer_norms_[p], all[static_cast<size_t>(p) * kH + 1 + kChannels],
+                              cudaIpcMemLazyEnablePeerAccess),
+         "cudaIpcOpenMemHandle(norms)");
   }
 }
 
@@ -120,6 +127,7 @@ PeerExchange::~PeerExchange() {
     if (peer_flags_[p]) cudaIpcCloseMemHandle(peer_flags_[p]);
     for (int c = 0; c < kChannels; ++c)
       if (peer_bufs_[c][p]) cudaIpcCloseMemHandle(peer_bufs_[c][p]);
+    if (peer_norms_[p]) cudaIpcCloseMemHandle(peer_norms_[p]);
   }
   for (auto st : pstreams_)
     if (st) cudaStreamDestroy(st);
@@ -174,7 +182,8 @@ void PeerExchange::wait_peers_freed(cudaStream_t copy, int ch, uint32_t epoch) {
 
 void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
                               const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch,
-                              cudaEvent_t local_done) {
+                              cudaEvent_t local_done, const float* norm_src, int64_t row_len) {
+  if (norm_src && (ch != 0 || !local_norms_)) throw MoeError(MOE_EINVAL, "peer all-to-all: norms");
   if (chunk >= kMaxChunks) throw MoeError(MOE_EINVAL, "peer all-to-all: too many chunks");
   // Push model: peer p receives my block where it receives "from rank_", i.e. at ro[rank_] of
   // the (source-symmetric) plan. One stream per destination: the blocks move concurrently, and
@@ -189,6 +198,12 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
     ck(cudaMemcpyAsync(dst, static_cast<const char*>(src) + so[p] * esz, block_bytes,
                        cudaMemcpyDeviceToDevice, ps),
        "peer copy");
+    if (norm_src) {  // the rows' norms travel with them (before the flag)
+      float* nd = static_cast<float*>(p == rank_ ? local_norms_ : peer_norms_[p]) + ro[rank_] / row_len;
+      ck(cudaMemcpyAsync(nd, norm_src + so[p] / row_len, block_bytes / esz / row_len * sizeof(float),
+                         cudaMemcpyDeviceToDevice, ps),
+         "peer copy (norms)");
+    }
     if (p != rank_) publish_one(ps, (2 * ch) * world_ + p, epoch, ready_remote(p, ch, chunk));
     else if (local_done) ck(cudaEventRecord(local_done, ps), "event");
     ck(cudaEventRecord(ev_out_[p], ps), "event");
@@ -207,7 +222,9 @@ void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch
 
 void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* src, const int64_t* so,
                              const int64_t* ro, size_t segs, size_t seg_bytes, size_t row0_bytes,
-                             size_t rows_bytes, uint32_t epoch) {
+                             size_t rows_bytes, uint32_t epoch, const float* norm_src,
+                             size_t row_bytes) {
+  if (norm_src && (ch != 0 || !local_norms_)) throw MoeError(MOE_EINVAL, "peer all-to-all: norms");
   if (slot < 0 || slot >= kFlagSlots) throw MoeError(MOE_EINVAL, "peer all-to-all: flag slot");
   ck(cudaEventRecord(ev_in_, copy), "event");
   for (int i = 1; i < world_; ++i) {  // own rows are written in place by the producing kernel
@@ -219,6 +236,14 @@ void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* sr
     const char* s0 = static_cast<const char*>(src) + so[p] + row0_bytes;
     ck(cudaMemcpy2DAsync(dst, seg_bytes, s0, seg_bytes, rows_bytes, segs, cudaMemcpyDeviceToDevice, ps),
        "peer copy (rows)");
+    if (norm_src) {  // the rows' norms travel with them (before the flag)
+      const size_t npitch = seg_bytes / row_bytes * sizeof(float);
+      float* nd = static_cast<float*>(peer_norms_[p]) + (ro[rank_] + row0_bytes) / row_bytes;
+      const float* ns = norm_src + (so[p] + row0_bytes) / row_bytes;
+      ck(cudaMemcpy2DAsync(nd, npitch, ns, npitch, rows_bytes / row_bytes * sizeof(float), segs,
+                           cudaMemcpyDeviceToDevice, ps),
+         "peer copy (norms)");
+    }
     publish_one(ps, (2 * ch) * world_ + p, epoch, ready_remote(p, ch, slot));
     ck(cudaEventRecord(ev_out_[p], ps), "event");
   }

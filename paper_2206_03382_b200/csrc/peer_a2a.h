@@ -36,7 +36,10 @@ class PeerExchange {
   static constexpr int kFlagSlots = kMaxChunks + kPartSlots;
 
   // bufs[ch]: this rank's receive buffer of channel ch (cudaMalloc base pointers).
-  PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels]);
+  // norms (optional): this rank's fp32 per-row receive array of channel 0 (the ReLU certificate's
+  // row norms, [rows of recv]); pushes with a norm source copy the rows' norms alongside.
+  PeerExchange(int rank, int world, ncclComm_t comm, void* const bufs[kChannels],
+               void* norms = nullptr);
   ~PeerExchange();
   PeerExchange(const PeerExchange&) = delete;
   PeerExchange& operator=(const PeerExchange&) = delete;
@@ -48,16 +51,19 @@ class PeerExchange {
   // ready[ch][me][chunk] = epoch to each peer.
   // local_done: recorded right after this rank's own block has been copied; nullptr: the own
   // block is not copied (the producing kernel wrote it into the receive buffer itself).
+  // norm_src (optional, channel 0): fp32 norms of src's rows (row_len elements per row).
   void push_chunk(cudaStream_t copy, int ch, int chunk, const void* src, const int64_t* so,
                   const int64_t* ro, size_t block_bytes, size_t esz, uint32_t epoch,
-                  cudaEvent_t local_done = nullptr);
+                  cudaEvent_t local_done = nullptr, const float* norm_src = nullptr,
+                  int64_t row_len = 1);
   // Copy stream: push rows [row0, row0 + rows) of each of `segs` expert segments (seg_bytes apart;
   // offsets so / ro in BYTES, per destination) to every peer, then publish ready[ch][me][slot].
   // Used to split the first chunk so its first rows land early (the own rows are written in
   // place by the producing kernel).
   void push_rows(cudaStream_t copy, int ch, int slot, const void* src, const int64_t* so,
                  const int64_t* ro, size_t segs, size_t seg_bytes, size_t row0_bytes,
-                 size_t rows_bytes, uint32_t epoch);
+                 size_t rows_bytes, uint32_t epoch, const float* norm_src = nullptr,
+                 size_t row_bytes = 1);
   // Compute stream: wait for every peer's chunk of this epoch (stream memory operations).
   void wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch);
   // The same wait as a device-side poll (fused into the first consuming kernel, or
@@ -88,6 +94,8 @@ class PeerExchange {
   std::vector<void*> peer_flags_;               // mapped flag blocks of peers (nullptr for self)
   std::vector<std::vector<void*>> peer_bufs_;   // [ch][peer] mapped receive buffers
   void* local_bufs_[kChannels];
+  void* local_norms_ = nullptr;
+  std::vector<void*> peer_norms_;  // mapped norm arrays of peers
   size_t nflags_ = 0;
   std::vector<cudaStream_t> pstreams_;  // per-destination copy streams
   cudaEvent_t ev_in_ = nullptr;

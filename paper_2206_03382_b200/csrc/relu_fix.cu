@@ -150,7 +150,10 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
     int M, int V, const unsigned long long* __restrict__ list, const unsigned int* __restrict__ count,
     unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
   pdl_entry();
-  const unsigned int n = min(*count, cap);
+  // count[0]: entries listed by the up GEMM; count[1]: CTAs done; count[2]: the last list's size
+  // (metrics). The last CTA to finish resets [0] and [1], so the next chunk's up GEMM starts from
+  // an empty list without a memset or reset kernel.
+  const unsigned int n = min(__ldcg(count), cap);
   const int lane = threadIdx.x % 32;
   const unsigned int nw = gridDim.x * blockDim.x / 32;
   for (unsigned int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n; i += 2 * nw) {
@@ -184,6 +187,16 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
         if (s[j] > 0.0) atomicOr(w, bit);
         else atomicAnd(w, ~bit);
       }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int* c = const_cast<unsigned int*>(count);
+    __threadfence();
+    if (atomicAdd(c + 1, 1u) == gridDim.x - 1) {
+      c[2] = c[0];
+      c[0] = 0u;
+      c[1] = 0u;
     }
   }
 }
