@@ -212,13 +212,6 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
     if (p != rank_ || local_done) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
 }
 
-void PeerExchange::wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch) {
-  for (int p = 0; p < world_; ++p) {
-    if (p == rank_) continue;
-    if (stream_wait_geq_u32(st, ready_local(ch, p, chunk), epoch) != 0)
-      throw MoeError(MOE_ECUDA, "cuStreamWaitValue32 failed");
-  }
-}
 
 void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* src, const int64_t* so,
                              const int64_t* ro, size_t segs, size_t seg_bytes, size_t row0_bytes,

@@ -5,8 +5,8 @@
 // DMA engines at once: the copy engines drive NVLink, so the exchange takes no SMs from the
 // persistent expert GEMMs it overlaps with. Ordering across
 // processes uses 32-bit epoch flags in each receiver's memory:
-//   ready[ch][src][chunk]  -- written (after the data) by src into dst's flags; dst's compute
-//                             stream waits with cuStreamWaitValue32(GEQ epoch).
+//   ready[ch][src][chunk]  -- written (after the data) by src into dst's flags; the kernel on dst
+//                             that first reads the chunk polls it (ld.acquire.sys >= epoch).
 //   freed[ch][src]         -- written by src once it has consumed its channel-ch buffer for an
 //                             epoch; a sender waits on its own copy before overwriting src's buffer
 //                             in the next epoch.
@@ -64,11 +64,9 @@ class PeerExchange {
                  const int64_t* ro, size_t segs, size_t seg_bytes, size_t row0_bytes,
                  size_t rows_bytes, uint32_t epoch, const float* norm_src = nullptr,
                  size_t row_bytes = 1);
-  // Compute stream: wait for every peer's chunk of this epoch (stream memory operations).
-  void wait_chunk(cudaStream_t st, int ch, int chunk, uint32_t epoch);
-  // The same wait as a device-side poll (fused into the first consuming kernel, or
-  // wait_flags_device). Flags of one source arrive in chunk order, so waiting for chunk c also
-  // covers every earlier chunk of the channel.
+  // Wait descriptor for every peer's chunk `chunk` of this epoch: polled on the device by the
+  // first consuming kernel (or wait_flags_device). Flags of one source arrive in chunk order, so
+  // waiting for chunk c also covers every earlier chunk of the channel.
   FlagWait ready_wait(int ch, int chunk, uint32_t epoch) const;
   // Stream st (after the consumers of channel ch's buffer): tell every peer it is free.
   void signal_freed(cudaStream_t st, int ch, uint32_t epoch);
