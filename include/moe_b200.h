@@ -41,8 +41,9 @@ extern "C" {
 #define MOE_A2A_LINEAR 0 /* A2aAlgo::Linear (collectives.hpp:10) */
 #define MOE_A2A_2DH 1    /* A2aAlgo::TwoDH */
 
-/* MoELayerConfig (moe_layer.hpp:22-29) flattened with Dims (core.hpp:32-56). Per-rank placement
- * (ExpertsPerRank{E/W}) only; the linear router only. */
+/* MoELayerConfig (moe_layer.hpp:22-29) flattened with Dims (core.hpp:32-56). The placement
+ * follows from E and W: E >= W is per-rank placement (ExpertsPerRank{E/W}, E = W*x); E < W is
+ * sharded placement (RanksPerExpert{s}, W = E*s): rank r serves expert r/s, slice r%s. */
 typedef struct moe_config {
   int64_t world_size;      /* W */
   int64_t gpus_per_node;   /* m */
@@ -59,7 +60,18 @@ typedef struct moe_config {
   int32_t degree;          /* StrategyControl::fixed.degree (capacity chunks), 1..8 */
   int32_t a2a_backend;     /* MOE_A2A_BACKEND_*: how W > 1 ranks exchange tokens */
   int32_t router;          /* MOE_ROUTER_* (RouterKind, moe_layer.hpp:10) */
+  int32_t parallel;        /* MOE_PARALLEL_* (ParallelControl, moe_layer.hpp:17-20); sharded only */
 } moe_config;
+
+/* ParallelControl / ParallelChoice (parallelism.hpp): the sharded-placement exchange form.
+ * P1 gathers each computed expert's weights and routes every source's tokens to one replica
+ * (moe_layer.cpp:17-57); P2 keeps the weight slices in place, repeats the tokens to all s
+ * shards and sums their partial outputs (moe_layer.cpp:59-108). ADAPTIVE picks the cheaper by
+ * select_parallelism (parallelism.cpp:300-318) every forward. Zero is the reference default
+ * (adaptive = false, fixed = P1). */
+#define MOE_PARALLEL_P1 0
+#define MOE_PARALLEL_P2 1
+#define MOE_PARALLEL_ADAPTIVE 2
 
 /* Router (route_probabilities, moe_layer.cpp:165-169). COSINE: softmax of
  * cos(x . P, C_e) / max(temperature, 0.01) (gate_cosine, gating.cpp:37-56), P (M, 256),
@@ -87,7 +99,7 @@ typedef struct moe_step_metrics {
   int64_t relu_fixups; /* bf16 path: up-GEMM outputs re-decided in fp64 (ReLU-mask certificate,
                           last chunk of the last forward) */
   int32_t fused;       /* MOE_FUSED_* bits: which exchanges ran inside the GEMM epilogues */
-  int32_t reserved;
+  int32_t parallel;    /* MOE_PARALLEL_P1 / _P2: the exchange form used (StepMetrics::parallel) */
 } moe_step_metrics;
 #define MOE_FUSED_DECODE 1  /* W = 1, k = 1: decode / encode-backward = down / dgrad epilogue scatter */
 #define MOE_FUSED_COMBINE 2 /* W > 1 peer backend: combine = down / dgrad epilogue NVLink stores */
@@ -103,8 +115,13 @@ int moe_resolve_capacity(int32_t capacity_kind, double factor, const int64_t* de
 /* capacity_to_factor, core.cpp:61-64. */
 int moe_capacity_to_factor(int64_t capacity, int64_t experts, int64_t top_k, int64_t tokens,
                            double* out);
-/* Dims::validate, core.cpp:8-26 (per-rank placement). */
+/* Dims::validate, core.cpp:8-26 (both placements) + ExpertParams' slice divisibility. */
 int moe_validate_config(const moe_config* cfg);
+/* select_parallelism, parallelism.cpp:288-308: P1 when comm_cost_p1 <= comm_cost_p2 (ties to
+ * the weight gather). local_experts may be fractional (1/s under sharded placement). EINVAL for
+ * n_sharded < 1 (comm_cost_p2's invalid_argument). *out = MOE_PARALLEL_P1 or _P2. */
+int moe_select_parallelism(double local_experts, int64_t gathered_capacity, int64_t model_dim,
+                           double param_bytes, int64_t n_sharded, int32_t* out);
 
 /* Flexible all-to-all plan (flex_all2all, collectives.cpp:116-162, over all2all_linear
  * :48-56) for pipeline chunk `chunk`: element offsets of the block sent to / received from each
@@ -142,13 +159,16 @@ int moe_set_cosine_router(moe_handle* h, const double* proj_host, const double* 
 /* FixedCapacity{f} from the next forward on (the scenario runner's per-step trace,
  * bench.cpp:199-201). Collective when W > 1 (buffers may grow): every rank calls it. */
 int moe_set_capacity_factor(moe_handle* h, double f);
-/* Full weights of local expert `local_e` (global index rank*E/W + local_e); host fp64
- * w1 (M, V), w2 (V, M) -- ExpertParams::assemble layout (parallelism.cpp:80-90). */
+/* Full weights of local expert `local_e` (global index rank*E/W + local_e; sharded placement:
+ * local_e 0 = expert rank/s); host fp64 w1 (M, V), w2 (V, M) -- ExpertParams::assemble layout
+ * (parallelism.cpp:80-90). */
 int moe_set_expert(moe_handle* h, int64_t local_e, const double* w1_host, const double* w2_host);
 /* ZeRO-sliced parameters (ExpertParams, parallelism.hpp:22-37): this rank's slice of every
  * expert (w1 columns / w2 rows [rank*V/W, (rank+1)*V/W)), host fp64, expert-major
  * [E][M][V/W] and [E][V/W][M]. Followed by one grouped exchange that assembles the local
- * experts -- gather_computed_experts, parallelism.cpp:149-206. */
+ * experts -- gather_computed_experts, parallelism.cpp:149-206. Sharded placement: the one slice
+ * rank%s of expert rank/s, [1][M][V/s] and [1][V/s][M], all-gathered within the expert's group
+ * (parallelism.cpp:155-175). */
 int moe_set_expert_slices(moe_handle* h, const double* w1_slices, const double* w2_slices);
 
 /* forward(state, x) (moe_layer.cpp:171-244) for this rank's token block: x, y are device
@@ -174,12 +194,15 @@ int moe_host_sync(moe_handle* h);
 int moe_get_routing(moe_handle* h, int32_t* idxs, int32_t* locations, double* gates,
                     int64_t* capacity);
 int moe_get_metrics(moe_handle* h, moe_step_metrics* out);
-/* Local expert gradients of the last backward, copied to host fp32 (E/W, M, V)+(E/W, V, M). */
+/* Local expert gradients of the last backward, copied to host fp32 (E/W, M, V)+(E/W, V, M).
+ * Sharded placement: the full gradient of expert rank/s (1, M, V)+(1, V, M), already summed over
+ * the expert's s replicas (P1) or assembled from its s slices (P2). */
 int moe_get_expert_grads(moe_handle* h, float* dw1_host, float* dw2_host);
 /* reduce_scatter_grads_p1 (parallelism.cpp:235-286): after a backward, route slice `rank` of
  * every expert's weight gradient (dW1 columns / dW2 rows [rank*V/W, (rank+1)*V/W)) to this rank
  * -- the ZeRO slice layout of moe_set_expert_slices. Device fp32 outputs: w1_slices
- * [E][M][V/W], w2_slices [E][V/W][M]. Collective across ranks (NCCL); synchronizes `stream`. */
+ * [E][M][V/W], w2_slices [E][V/W][M]. Collective across ranks (NCCL); synchronizes `stream`.
+ * Sharded placement: this rank's slice rank%s of expert rank/s, [1][M][V/s] and [1][V/s][M]. */
 int moe_get_expert_grad_slices(moe_handle* h, float* w1_slices, float* w2_slices, void* stream);
 /* Device pointer to local expert weights in the layer dtype: which=1 -> w1, 2 -> w2. */
 int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr);

@@ -37,7 +37,7 @@ struct Tensor {
 enum class CapacityKind { Fixed = MOE_CAP_FIXED, Auto = MOE_CAP_AUTO, Bounded = MOE_CAP_BOUNDED };
 enum class DType { BF16 = MOE_DTYPE_BF16, F32 = MOE_DTYPE_F32 };
 
-struct Dims {  // core.hpp:32-56 (per-rank placement)
+struct Dims {  // core.hpp:32-56 (E >= W: ExpertsPerRank{E/W}; E < W: RanksPerExpert{W/E})
   Index world_size = 1, gpus_per_node = 1, global_experts = 1, model_dim = 1, hidden_dim = 1,
         tokens_per_step = 1, top_k = 1;
 };
@@ -49,6 +49,12 @@ struct StrategyControl {  // moe_layer.hpp:17-20
 };
 
 enum class RouterKind { Linear = MOE_ROUTER_LINEAR, Cosine = MOE_ROUTER_COSINE };  // moe_layer.hpp:10
+enum class ParallelChoice { P1 = MOE_PARALLEL_P1, P2 = MOE_PARALLEL_P2 };  // parallelism.hpp
+
+struct ParallelControl {  // moe_layer.hpp:17-20
+  bool adaptive = false;
+  ParallelChoice fixed = ParallelChoice::P1;
+};
 
 struct MoELayerConfig {  // moe_layer.hpp:22-29
   Dims dims;
@@ -58,6 +64,7 @@ struct MoELayerConfig {  // moe_layer.hpp:22-29
   bool bpr = false;
   DType dtype = DType::BF16;
   StrategyControl strategy;
+  ParallelControl parallel;
 
   moe_config to_c() const {
     moe_config c{};
@@ -76,6 +83,7 @@ struct MoELayerConfig {  // moe_layer.hpp:22-29
     c.degree = strategy.degree;
     c.a2a_backend = strategy.a2a_backend;
     c.router = static_cast<int32_t>(router);
+    c.parallel = parallel.adaptive ? MOE_PARALLEL_ADAPTIVE : static_cast<int32_t>(parallel.fixed);
     return c;
   }
 };
@@ -97,6 +105,7 @@ struct StepMetrics {  // moe_layer.hpp:46-54 (seconds are measured, not simulate
   double seconds = 0.0;
   double comm_bytes = 0.0;
   Index drop_count = 0;
+  ParallelChoice parallel = ParallelChoice::P1;
 };
 
 struct SavedForward {  // handle-owned tensors of the last forward
@@ -206,7 +215,8 @@ inline ForwardResult forward(LayerState& state, const Tensor& x) {
   r.y = detail::unpack(yout, state.config.dtype, x.shape);
   moe_step_metrics m{};
   throw_status(moe_get_metrics(state.handle(), &m), moe_last_error(state.handle()));
-  r.metrics = StepMetrics{m.f, m.capacity, m.degree, m.seconds, m.comm_bytes, m.drop_count};
+  r.metrics = StepMetrics{m.f, m.capacity, m.degree, m.seconds, m.comm_bytes, m.drop_count,
+                          static_cast<ParallelChoice>(m.parallel)};
   r.saved.step = ++state.step;
   return r;
 }

@@ -377,6 +377,25 @@ void orc_flex_combine(const double* in, int64_t W, int64_t E, int64_t dC, int64_
                  in + ((d * dE + e) * (W * dC) + r * dC + c) * M, sizeof(double) * (size_t)M);
 }
 
+/* The exchanges' net effect on the layer under either placement: expert e's computed rows are
+ * (source r, slot c) = z[r][e][c], whichever ranks compute them -- per-rank placement
+ * (flex_all2all above), sharded P1 (one replica per source group, moe_layer.cpp:20-57) and P2
+ * (slices summed back at the source, :61-108) all apply the same full expert to the same rows.
+ * Identical to orc_flex_dispatch / _combine when E % W == 0. */
+static void orc_expert_major(const double* in, int64_t W, int64_t E, int64_t dC, int64_t M,
+                             double* out) {
+  for (int64_t e = 0; e < E; ++e)
+    for (int64_t r = 0; r < W; ++r)
+      memcpy(out + (e * W + r) * dC * M, in + (r * E + e) * dC * M, sizeof(double) * (size_t)(dC * M));
+}
+
+static void orc_expert_major_inv(const double* in, int64_t W, int64_t E, int64_t dC, int64_t M,
+                                 double* out) {
+  for (int64_t e = 0; e < E; ++e)
+    for (int64_t r = 0; r < W; ++r)
+      memcpy(out + (r * E + e) * dC * M, in + (e * W + r) * dC * M, sizeof(double) * (size_t)(dC * M));
+}
+
 /* ------------------------------------------------------------------ dense fp64 GEMMs */
 /* C (m,n) = op(A) . B, row-major; op(A) = A (m,kk) or A^T with A (kk,m). Parallel over
  * (row block, column block) tiles so small per-expert row counts still use every core. */
@@ -511,17 +530,21 @@ int64_t orc_layer_step_probs(const double* x, const double* probs, const double*
   double* ye = (double*)malloc(sizeof(double) * zsz);
   orc_encode(x, W, T, M, E, k, cap, idxs, locations, z);
   /* flex dispatch: expert e's input rows (r, c) = z[r][e][c] (collectives.cpp:123-141) */
-  orc_flex_dispatch(z, W, E, cap, M, xe);
+  if (E % W == 0) orc_flex_dispatch(z, W, E, cap, M, xe);
+  else orc_expert_major(z, W, E, cap, M, xe); /* sharded placement (E < W) */
   orc_expert_ffn(xe, w1, w2, E, rows, M, V, ye);
-  orc_flex_combine(ye, W, E, cap, M, z);
+  if (E % W == 0) orc_flex_combine(ye, W, E, cap, M, z);
+  else orc_expert_major_inv(ye, W, E, cap, M, z);
   orc_decode(z, W, T, M, E, k, cap, idxs, locations, gates, y);
   if (dy) {
     double* dz = (double*)malloc(sizeof(double) * zsz);
     double* dye = (double*)malloc(sizeof(double) * zsz);
     orc_decode_backward(dy, NULL, W, T, M, E, k, cap, idxs, locations, gates, dz, NULL);
-    orc_flex_dispatch(dz, W, E, cap, M, dye);
+    if (E % W == 0) orc_flex_dispatch(dz, W, E, cap, M, dye);
+    else orc_expert_major(dz, W, E, cap, M, dye);
     orc_expert_ffn_backward(xe, w1, w2, dye, E, rows, M, V, ye, dw1, dw2);
-    orc_flex_combine(ye, W, E, cap, M, dz);
+    if (E % W == 0) orc_flex_combine(ye, W, E, cap, M, dz);
+    else orc_expert_major_inv(ye, W, E, cap, M, dz);
     orc_encode_backward(dz, W, T, M, E, k, cap, idxs, locations, dx);
     free(dz);
     free(dye);

@@ -37,7 +37,7 @@ class MoeConfig(C.Structure):
         ("model_dim", C.c_int64), ("hidden_dim", C.c_int64), ("tokens_per_step", C.c_int64),
         ("top_k", C.c_int64), ("capacity_kind", C.c_int32), ("capacity_factor", C.c_double),
         ("bpr", C.c_int32), ("dtype", C.c_int32), ("adaptive", C.c_int32), ("degree", C.c_int32),
-        ("a2a_backend", C.c_int32), ("router", C.c_int32),
+        ("a2a_backend", C.c_int32), ("router", C.c_int32), ("parallel", C.c_int32),
     ]
 
 
@@ -46,7 +46,7 @@ class StepMetrics(C.Structure):
         ("f", C.c_double), ("capacity", C.c_int64), ("a2a_algo", C.c_int32),
         ("degree", C.c_int32), ("seconds", C.c_double), ("comm_bytes", C.c_double),
         ("drop_count", C.c_int64), ("relu_fixups", C.c_int64), ("fused", C.c_int32),
-        ("reserved", C.c_int32),
+        ("parallel", C.c_int32),
     ]
 
 
@@ -60,6 +60,7 @@ SIGNATURES = {
     "moe_resolve_capacity": (I32, [I32, D, PI64, I64, I64, I64, PI64]),
     "moe_capacity_to_factor": (I32, [I64, I64, I64, I64, PD]),
     "moe_validate_config": (I32, [C.POINTER(MoeConfig)]),
+    "moe_select_parallelism": (I32, [D, I64, I64, D, I64, PI32]),
     "moe_a2a_plan": (I32, [I64, I64, I64, I64, I64, I32, PI64, PI64, PI64]),
     "moe_get_unique_id": (I32, [C.c_char_p]),
     "moe_create": (I32, [C.POINTER(MoeConfig), I32, C.c_char_p, I32, C.POINTER(P)]),

@@ -233,6 +233,14 @@ int moe_validate_config(const moe_config* cfg) {
   });
 }
 
+int moe_select_parallelism(double local_experts, int64_t gathered_capacity, int64_t model_dim,
+                           double param_bytes, int64_t n_sharded, int32_t* out) {
+  return guard(nullptr, [&] {
+    if (!out) throw moe::MoeError(MOE_EINVAL, "null output");
+    *out = moe::select_parallelism(local_experts, gathered_capacity, model_dim, param_bytes, n_sharded);
+  });
+}
+
 int moe_get_unique_id(uint8_t* id128) {
   return guard(nullptr, [&] {
     ncclUniqueId id;

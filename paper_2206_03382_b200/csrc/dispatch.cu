@@ -552,6 +552,67 @@ __global__ void build_slots_kernel(int n, int T, int k, int E, int cap,
 }
 }  // namespace
 
+// ------------------------------------------------------------------ sharded P2 combine sum
+namespace {
+// out[b][o] = sum_q part[b][q][o] (combine_sharded_p2, moe_layer.cpp:80-108: the source sums the
+// s shards' partial rows of each expert, q ascending, fp32 accumulate). 16-byte vectors.
+template <typename T>
+__global__ void __launch_bounds__(256) shard_sum_kernel(const T* __restrict__ part, T* __restrict__ out,
+                                                        int64_t nblk, int s, int64_t blk_vecs) {
+  pdl_entry();
+  constexpr int VN = Vec<T>::N;
+  const int64_t n = nblk * blk_vecs;
+  const uint4* p = reinterpret_cast<const uint4*>(part);
+  uint4* o = reinterpret_cast<uint4*>(out);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / blk_vecs, v = i - b * blk_vecs;
+    float acc[VN];
+#pragma unroll
+    for (int j = 0; j < VN; ++j) acc[j] = 0.0f;
+    for (int q = 0; q < s; ++q) {
+      float f[VN];
+      Vec<T>::to_f32(ld_stream(p + (b * s + q) * blk_vecs + v), f);
+#pragma unroll
+      for (int j = 0; j < VN; ++j) acc[j] += f[j];
+    }
+    o[i] = Vec<T>::from_f32(acc);
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) shard_sum_scalar_kernel(const T* __restrict__ part, T* __restrict__ out,
+                                                               int64_t nblk, int s, int64_t blk) {
+  pdl_entry();
+  const int64_t n = nblk * blk;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / blk, e = i - b * blk;
+    float acc = 0.0f;
+    for (int q = 0; q < s; ++q) acc += to_f(part[(b * s + q) * blk + e]);
+    out[i] = from_f<T>(acc);
+  }
+}
+}  // namespace
+
+int shard_sum_device(const void* part, void* out, int64_t nblk, int s, int64_t blk, int dtype,
+                     cudaStream_t st) {
+  if (nblk < 0 || s < 1 || blk < 0) return -1;
+  const int esz = dtype == 1 ? 4 : 2;
+  const bool vec = (blk * esz) % 16 == 0;
+  const int64_t work = vec ? nblk * (blk * esz / 16) : nblk * blk;
+  const int64_t want = (work + 255) / 256;
+  const int grid = static_cast<int>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
+  if (dtype == 1) {
+    if (vec) launch_k(shard_sum_kernel<float>, grid, 256, 0, st, static_cast<const float*>(part), static_cast<float*>(out), nblk, s, blk / 4);
+    else launch_k(shard_sum_scalar_kernel<float>, grid, 256, 0, st, static_cast<const float*>(part), static_cast<float*>(out), nblk, s, blk);
+  } else {
+    using B = __nv_bfloat16;
+    if (vec) launch_k(shard_sum_kernel<B>, grid, 256, 0, st, static_cast<const B*>(part), static_cast<B*>(out), nblk, s, blk / 8);
+    else launch_k(shard_sum_scalar_kernel<B>, grid, 256, 0, st, static_cast<const B*>(part), static_cast<B*>(out), nblk, s, blk);
+  }
+  return launch_status();
+}
+
 // Slot tables (slot -> token, slot -> gate) from an explicit routing plan (DispatchPlan).
 int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* idxs,
                        const int32_t* locations, const double* gates, int32_t* slot_token,

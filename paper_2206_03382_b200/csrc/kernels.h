@@ -123,6 +123,10 @@ int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, co
 int encode_backward_device(const SlotGeom& g, int dtype, const void* dz, const int32_t* idxs,
                            const int32_t* locations, void* dx, cudaStream_t st,
                            const FlagWait* wait = nullptr);
+// Sharded P2 combine: out[b] = sum over q < s of part[b][q] (blocks of blk elements, dtype 0 bf16
+// / 1 f32, fp32 accumulate in q order).
+int shard_sum_device(const void* part, void* out, int64_t nblk, int s, int64_t blk, int dtype,
+                     cudaStream_t st);
 
 int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* idxs,
                        const int32_t* locations, const double* gates, int32_t* slot_token,

@@ -113,10 +113,19 @@ void validate(const moe_config& c) {
   if (c.top_k < 1 || c.top_k > c.global_experts) throw MoeError(MOE_EINVAL, "Dims: need 1 <= k <= E");
   if (c.model_dim < 1 || c.hidden_dim < 1 || c.tokens_per_step < 1)
     throw MoeError(MOE_EINVAL, "Dims: M, V, T must be >= 1");
-  if (c.global_experts % c.world_size != 0)
-    throw MoeError(MOE_EINVAL, "Dims: ExpertsPerRank(x) requires E = W*x");
-  if (c.hidden_dim % c.world_size != 0)
-    throw MoeError(MOE_EINVAL, "ExpertParams: hidden dim must divide into parameter slices");
+  if (c.global_experts < c.world_size) {  // RanksPerExpert{s}: W = E*s
+    if (c.world_size % c.global_experts != 0)
+      throw MoeError(MOE_EINVAL, "Dims: RanksPerExpert(s) requires W = E*s");
+    if (c.hidden_dim % (c.world_size / c.global_experts) != 0)
+      throw MoeError(MOE_EINVAL, "ExpertParams: hidden dim must divide into parameter slices");
+  } else {
+    if (c.global_experts % c.world_size != 0)
+      throw MoeError(MOE_EINVAL, "Dims: ExpertsPerRank(x) requires E = W*x");
+    if (c.hidden_dim % c.world_size != 0)
+      throw MoeError(MOE_EINVAL, "ExpertParams: hidden dim must divide into parameter slices");
+  }
+  if (c.parallel < MOE_PARALLEL_P1 || c.parallel > MOE_PARALLEL_ADAPTIVE)
+    throw MoeError(MOE_EINVAL, "parallel control");
   if (c.top_k > 32) throw MoeError(MOE_EINVAL, "top_k > 32 unsupported");
   if (c.global_experts > 256) throw MoeError(MOE_EINVAL, "E > 256 unsupported by the gate kernel");
   if (c.dtype != MOE_DTYPE_BF16 && c.dtype != MOE_DTYPE_F32) throw MoeError(MOE_EINVAL, "dtype");
@@ -131,6 +140,18 @@ void validate(const moe_config& c) {
     throw MoeError(MOE_EINVAL, "pipelining degree must be 1, 2, 4 or 8");
   if (c.model_dim > (1 << 20) || c.hidden_dim > (1 << 20) || c.tokens_per_step > (1 << 26))
     throw MoeError(MOE_EINVAL, "dims too large");
+}
+
+// comm_cost_p1 / comm_cost_p2 / select_parallelism (parallelism.cpp:288-308), same operation order.
+int32_t select_parallelism(double local_experts, int64_t gathered_capacity, int64_t model_dim,
+                           double param_bytes, int64_t n_sharded) {
+  if (n_sharded < 1) throw MoeError(MOE_EINVAL, "comm_cost_p2: n_sharded must be >= 1");
+  const double p1 = 8.0 * local_experts * static_cast<double>(gathered_capacity) *
+                        static_cast<double>(model_dim) +
+                    param_bytes;
+  const double p2 = 8.0 * static_cast<double>(n_sharded) * local_experts *
+                    static_cast<double>(gathered_capacity) * static_cast<double>(model_dim);
+  return p1 <= p2 ? MOE_PARALLEL_P1 : MOE_PARALLEL_P2;
 }
 
 DevMem::~DevMem() {
@@ -151,6 +172,11 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   W_ = static_cast<int>(cfg.world_size);
   E_ = static_cast<int>(cfg.global_experts);
   dE_ = E_ / W_;
+  sharded_ = E_ < W_;
+  if (sharded_) {
+    s_ = W_ / E_;
+    dE_ = 1;  // the one computed expert, rank / s
+  }
   M_ = static_cast<int>(cfg.model_dim);
   V_ = static_cast<int>(cfg.hidden_dim);
   T_ = static_cast<int>(cfg.tokens_per_step);
@@ -204,6 +230,8 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     ckn(ncclCommInitRank(&comm_, W_, id, rank_), "ncclCommInitRank");
+    if (sharded_)  // the expert's sharing group: dW replica sums (P1) / slice gathers (P2)
+      ckn(ncclCommSplit(comm_, rank_ / s_, rank_ % s_, &group_comm_, nullptr), "ncclCommSplit");
   }
 
   const size_t Tk = static_cast<size_t>(T_) * k_;
@@ -226,6 +254,12 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   ck(cudaMemset(wg_.p, 0, wg_.bytes), "memset");
   ck(cudaMemset(w1_.p, 0, w1_.bytes), "memset");
   ck(cudaMemset(w2_.p, 0, w2_.bytes), "memset");
+  if (sharded_) {
+    const size_t mh = static_cast<size_t>(M_) * (V_ / s_);
+    w1s_.alloc(static_cast<size_t>(esz_) * mh);
+    dws1_.alloc(sizeof(float) * (mh + static_cast<size_t>(M_) * V_));  // slice + gathered slices
+    dws2_.alloc(sizeof(float) * mh);
+  }
 
   idxs_.alloc(4 * Tk);
   gates_.alloc(8 * Tk);
@@ -264,8 +298,10 @@ void Layer::alloc_capacity(int cap) {
   cap_alloc_ = ca;
   slot_token_.alloc(4 * static_cast<size_t>(E_) * cap_alloc_);
   slot_gate_.alloc(4 * static_cast<size_t>(E_) * cap_alloc_);
-  const size_t rowsM = static_cast<size_t>(E_) * cap_alloc_ * M_ * esz_;
-  const size_t rowsV = static_cast<size_t>(E_) * cap_alloc_ * V_ * esz_;
+  // rows in z order are E * cap; the sharded receive order holds up to W * cap rows (P2)
+  const size_t rows_all = static_cast<size_t>(std::max(E_, W_)) * cap_alloc_;
+  const size_t rowsM = rows_all * M_ * esz_;
+  const size_t rowsV = rows_all * V_ * esz_;
   act_.alloc(rowsV);
   dh_.alloc(rowsV);
   z_.alloc(rowsM);
@@ -275,7 +311,6 @@ void Layer::alloc_capacity(int cap) {
     dxe_.alloc(rowsM);
   }
   if (cfg_.dtype == MOE_DTYPE_BF16) {
-    const size_t rows_all = static_cast<size_t>(E_) * cap_alloc_;
     relu_mask_.alloc(sizeof(unsigned long long) * rows_all * (V_ / 64 + 1));
     rownorm_.alloc(sizeof(float) * rows_all);
     if (W_ > 1) znorm_.alloc(sizeof(float) * rows_all);
@@ -287,7 +322,8 @@ void Layer::alloc_capacity(int cap) {
     ycomb_.alloc(rowsM);
     drecv_.alloc(rowsM);
     dxcomb_.alloc(rowsM);
-    if (cfg_.a2a_backend == MOE_A2A_BACKEND_PEER) {
+    if (sharded_) ypart_.alloc(rowsM);  // P2: the s partials of every expert, [chunk][E][s][cc]
+    if (cfg_.a2a_backend == MOE_A2A_BACKEND_PEER && !sharded_) {
       void* bufs[PeerExchange::kChannels] = {recv_.p, ycomb_.p, drecv_.p, dxcomb_.p};
       const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
       peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs, cert ? rownorm_.p : nullptr);
@@ -386,6 +422,7 @@ Layer::~Layer() {
     cudaEventDestroy(r.b);
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  if (group_comm_) ncclCommDestroy(group_comm_);
   if (comm_) ncclCommDestroy(comm_);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
   cudaEventDestroy(ev_fwd_start_);
@@ -411,7 +448,7 @@ void Layer::init_params(uint64_t seed) {
   const int dt = cfg_.dtype == MOE_DTYPE_BF16 ? 0 : 1;
   const size_t mv = static_cast<size_t>(M_) * V_;
   for (int le = 0; le < dE_; ++le) {
-    const uint64_t o = expert_draw_offset(static_cast<int64_t>(rank_) * dE_ + le);
+    const uint64_t o = expert_draw_offset(sharded_ ? rank_ / s_ : static_cast<int64_t>(rank_) * dE_ + le);
     ckr(fill_uniform_device(static_cast<char*>(w1_.p) + le * mv * esz_, dt, mv, seed, o, -0.5, 0.5, 0),
         "init w1");
     ckr(fill_uniform_device(static_cast<char*>(w2_.p) + le * mv * esz_, dt, mv, seed, o + mv, -0.5, 0.5, 0),
@@ -509,6 +546,36 @@ void Layer::set_expert(int64_t le, const double* w1, const double* w2) {
 // destination its experts' slices (w1 slice row-major, then w2 slice), then the owner assembles.
 void Layer::set_expert_slices(const double* w1s, const double* w2s) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (sharded_) {
+    // Sharded placement (parallelism.cpp:155-175): this rank holds slice rank%s of expert rank/s;
+    // the sharing group all-gathers the s slices and every member assembles the full expert.
+    const int h = V_ / s_;
+    const size_t slice = static_cast<size_t>(2) * M_ * h;
+    std::vector<double> packed(slice);
+    std::memcpy(packed.data(), w1s, sizeof(double) * M_ * h);
+    std::memcpy(packed.data() + static_cast<size_t>(M_) * h, w2s, sizeof(double) * h * M_);
+    DevMem send, recv;
+    send.alloc(slice * esz_);
+    recv.alloc(slice * s_ * esz_);
+    upload_weights(send.p, packed.data(), slice);
+    const ncclDataType_t dt = cfg_.dtype == MOE_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
+    ckn(ncclAllGather(send.p, recv.p, slice, dt, group_comm_, comm_stream_), "allgather");
+    ck(cudaStreamSynchronize(comm_stream_), "gather sync");
+    for (int q = 0; q < s_; ++q) {
+      const char* base = static_cast<const char*>(recv.p) + static_cast<size_t>(q) * slice * esz_;
+      ck(cudaMemcpy2D(static_cast<char*>(w1_.p) + static_cast<size_t>(q) * h * esz_,
+                      static_cast<size_t>(V_) * esz_, base, static_cast<size_t>(h) * esz_,
+                      static_cast<size_t>(h) * esz_, M_, cudaMemcpyDeviceToDevice),
+         "assemble w1");
+      ck(cudaMemcpy(static_cast<char*>(w2_.p) + static_cast<size_t>(q) * h * M_ * esz_,
+                    base + static_cast<size_t>(M_) * h * esz_, static_cast<size_t>(h) * M_ * esz_,
+                    cudaMemcpyDeviceToDevice),
+         "assemble w2");
+    }
+    ck(cudaDeviceSynchronize(), "set_expert_slices");
+    stats_dirty_ = true;
+    return;
+  }
   const int h = V_ / W_;
   const size_t slice = static_cast<size_t>(2) * M_ * h;  // elements per (expert, slice)
   // Pack my slices of every expert in destination order (experts are rank-major).
@@ -716,6 +783,220 @@ void Layer::peer_push(int ch, const void* src, int chunk, int phase, uint32_t ep
   comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
 }
 
+// P2's W1 slice (columns [q*h, (q+1)*h) of the computed expert's (M, V) W1) as a contiguous
+// (M, h) operand; W2's slice rows and W1^T's slice rows (certificate) are contiguous in place.
+void Layer::refresh_slices(cudaStream_t st) {
+  const int h = V_ / s_, q = rank_ % s_;
+  ck(cudaMemcpy2DAsync(w1s_.p, static_cast<size_t>(h) * esz_,
+                       static_cast<const char*>(w1_.p) + static_cast<size_t>(q) * h * esz_,
+                       static_cast<size_t>(V_) * esz_, static_cast<size_t>(h) * esz_, M_,
+                       cudaMemcpyDeviceToDevice, st),
+     "W1 slice");
+}
+
+// Sharded-placement exchanges (moe_layer.cpp:17-108) as grouped send/recv on the comm stream.
+// Slabs are (cc, M) blocks: z order [chunk][E][cc], receive order [chunk][nsrc][cc] (P1: the E
+// sources [q*E, (q+1)*E) this replica serves, q = rank % s; P2: all W sources), P2 partials
+// [chunk][E][s][cc].
+void Layer::shard_exchange(const void* send, void* recv, int chunk, int dir, bool p2) {
+  const ncclDataType_t dt = cfg_.dtype == MOE_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
+  const int64_t blk = static_cast<int64_t>(cc_) * M_;
+  const int nsrc = p2 ? W_ : E_;
+  const int q_src = rank_ / E_;  // P1: the replica index serving my tokens
+  const int q_mine = rank_ % s_;
+  const char* sb = static_cast<const char*>(send);
+  char* rb = static_cast<char*>(recv);
+  auto zslab = [&](int e) { return (static_cast<int64_t>(chunk) * E_ + e) * blk * esz_; };
+  auto rslab = [&](int j) { return (static_cast<int64_t>(chunk) * nsrc + j) * blk * esz_; };
+  auto pslab = [&](int e, int q) { return ((static_cast<int64_t>(chunk) * E_ + e) * s_ + q) * blk * esz_; };
+  int sent = 0;
+  auto snd = [&](const char* p, int peer) {
+    ckn(ncclSend(p, blk, dt, peer, comm_, comm_stream_), "ncclSend");
+    sent += peer != rank_;
+  };
+  auto rcv = [&](char* p, int peer) { ckn(ncclRecv(p, blk, dt, peer, comm_, comm_stream_), "ncclRecv"); };
+  ckn(ncclGroupStart(), "ncclGroupStart");
+  if (dir == 0) {
+    // dispatch_sharded_p1 (:20-39): slab e -> the replica e*s + r/E; p2 (:61-78): -> all s shards
+    for (int e = 0; e < E_; ++e) {
+      if (!p2) {
+        snd(sb + zslab(e), e * s_ + q_src);
+      } else {
+        for (int q = 0; q < s_; ++q) snd(sb + zslab(e), e * s_ + q);
+      }
+    }
+    for (int j = 0; j < nsrc; ++j) rcv(rb + rslab(j), p2 ? j : q_mine * E_ + j);
+  } else {
+    // combine_sharded_p1 (:42-57): source slabs back; p2 (:82-108): every shard's partials
+    for (int j = 0; j < nsrc; ++j) snd(sb + rslab(j), p2 ? j : q_mine * E_ + j);
+    for (int e = 0; e < E_; ++e) {
+      if (!p2) {
+        rcv(rb + zslab(e), e * s_ + q_src);
+      } else {
+        for (int q = 0; q < s_; ++q) rcv(rb + pslab(e, q), e * s_ + q);
+      }
+    }
+  }
+  ckn(ncclGroupEnd(), "ncclGroupEnd");
+  comm_bytes_ += static_cast<double>(sent) * blk * esz_;
+}
+
+// Forward expert section under sharded placement: the computed expert is the full expert
+// rank/s (P1) or its slice rank%s (P2, hidden width h = V/s; partial outputs summed at the
+// source). Comm stream: all dispatches, then all combines; compute stream: per chunk up + down.
+void Layer::sharded_forward(GemmArgs up, GemmArgs down, bool cert, cudaStream_t st) {
+  const bool p2 = parallel_ == MOE_PARALLEL_P2;
+  const int nsrc = p2 ? W_ : E_;
+  const int h = p2 ? V_ / s_ : V_;
+  const size_t qoff = p2 ? static_cast<size_t>(rank_ % s_) * h : 0;  // first hidden column held
+  const void* w1 = p2 ? w1s_.p : w1_.p;
+  const void* w2 = static_cast<const char*>(w2_.p) + qoff * M_ * esz_;
+  const int nseg = degree_ * nsrc;
+  up.G = 1;
+  up.S = nsrc;
+  up.seg_rows = cc_;
+  up.N = h;
+  up.K = M_;
+  down.G = 1;
+  down.S = nsrc;
+  down.seg_rows = cc_;
+  down.N = M_;
+  down.K = h;
+  if (cert) {
+    up.colnorm += qoff;
+    up.colnorm_blk += qoff / 64;
+  }
+  ck(cudaEventRecord(ev_sync_, st), "event");
+  ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+  prof_mark(kPhA2aFwd, true, comm_stream_);
+  for (int i = 0; i < degree_; ++i) {
+    shard_exchange(z_.p, recv_.p, i, 0, p2);
+    ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+  }
+  for (int i = 0; i < degree_; ++i) {
+    ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
+    up.seg_base = down.seg_base = static_cast<uint32_t>(i * nsrc);
+    if (cert) {
+      RowSet rs;
+      rs.seg_begin = static_cast<int64_t>(i) * nsrc;
+      rs.nsegs = nsrc;
+      rs.seg_rows = rs.nrows = cc_;
+      ckr(rownorm_device(recv_.p, M_, static_cast<float*>(rownorm_.p), rs, st), "rownorm");
+      ++launches_;
+      ck(cudaMemsetAsync(fix_count_.p, 0, sizeof(unsigned int), st), "memset");
+    }
+    prof_mark(kPhUp, true, st);
+    gemm(kGemmUp, recv_.p, w1, act_.p, up, nseg, st);
+    prof_mark(kPhUp, false, st);
+    if (cert) {
+      prof_mark(kPhReluFix, true, st);
+      ckr(relu_fixup_device(recv_.p, static_cast<const char*>(w1t_.p) + qoff * M_ * esz_, 1, cc_, M_, h,
+                            static_cast<const unsigned long long*>(fix_list_.p),
+                            static_cast<const unsigned int*>(fix_count_.p), fix_cap_, act_.p,
+                            static_cast<unsigned long long*>(relu_mask_.p), st),
+          "relu_fixup");
+      prof_mark(kPhReluFix, false, st);
+      ++launches_;
+    }
+    prof_mark(kPhDown, true, st);
+    gemm(kGemmDown, act_.p, w2, yexp_.p, down, nseg, st);
+    prof_mark(kPhDown, false, st);
+    ck(cudaEventRecord(ev_b_[i], st), "event");
+  }
+  for (int i = 0; i < degree_; ++i) {
+    ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+    shard_exchange(yexp_.p, p2 ? ypart_.p : ycomb_.p, i, 1, p2);
+  }
+  prof_mark(kPhA2aFwd, false, comm_stream_);
+  ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
+  ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
+  if (p2) {
+    ckr(shard_sum_device(ypart_.p, ycomb_.p, static_cast<int64_t>(degree_) * E_, s_,
+                         static_cast<int64_t>(cc_) * M_, cfg_.dtype, st),
+        "shard_sum");
+    ++launches_;
+  }
+}
+
+// Backward expert section under sharded placement (moe_layer.cpp:246-319 with make_exchange's
+// sharded ops): dY rows go out with the dispatch op, dX comes back with the combine op. The
+// weight gradient of the computed expert is summed over its s replicas (P1,
+// reduce_scatter_grads_p1 :247-262) or assembled from the s complete slice gradients (P2), so
+// every member of the group returns the full expert gradient.
+void Layer::sharded_backward(GemmArgs dgm, GemmArgs dg, GemmArgs wg1, GemmArgs wg2, float* gw1,
+                             float* gw2, cudaStream_t st) {
+  const bool p2 = parallel_ == MOE_PARALLEL_P2;
+  const int nsrc = p2 ? W_ : E_;
+  const int h = p2 ? V_ / s_ : V_;
+  const size_t qoff = p2 ? static_cast<size_t>(rank_ % s_) * h : 0;
+  const void* w1 = p2 ? w1s_.p : w1_.p;
+  const void* w2 = static_cast<const char*>(w2_.p) + qoff * M_ * esz_;
+  const int nseg = degree_ * nsrc;
+  dgm.G = dg.G = wg1.G = wg2.G = 1;
+  dgm.S = dg.S = nsrc;
+  dgm.N = h;
+  dgm.K = M_;
+  dg.N = M_;
+  dg.K = h;
+  wg1.S = wg2.S = degree_ * nsrc;
+  wg1.N = h;
+  wg1.Mo = M_;
+  wg2.N = M_;
+  wg2.Mo = h;
+  float* o1 = p2 ? static_cast<float*>(dws1_.p) : gw1;
+  float* o2 = p2 ? static_cast<float*>(dws2_.p) : gw2;
+  ck(cudaEventRecord(ev_sync_, st), "event");
+  ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
+  prof_mark(kPhA2aBwd, true, comm_stream_);
+  for (int i = 0; i < degree_; ++i) {  // adjoint of combine
+    shard_exchange(dz_.p, drecv_.p, i, 0, p2);
+    ck(cudaEventRecord(ev_a_[i], comm_stream_), "event");
+  }
+  for (int i = 0; i < degree_; ++i) {
+    ck(cudaStreamWaitEvent(st, ev_a_[i], 0), "wait");
+    dgm.seg_base = dg.seg_base = static_cast<uint32_t>(i * nsrc);
+    prof_mark(kPhDgradMask, true, st);
+    gemm(kGemmDgradMask, drecv_.p, w2, dh_.p, dgm, nseg, st);
+    prof_mark(kPhDgradMask, false, st);
+    prof_mark(kPhDgrad, true, st);
+    gemm(kGemmDgrad, dh_.p, w1, dxe_.p, dg, nseg, st);
+    prof_mark(kPhDgrad, false, st);
+    ck(cudaEventRecord(ev_b_[i], st), "event");
+  }
+  for (int i = 0; i < degree_; ++i) {  // adjoint of dispatch
+    ck(cudaStreamWaitEvent(comm_stream_, ev_b_[i], 0), "wait");
+    shard_exchange(dxe_.p, p2 ? ypart_.p : dxcomb_.p, i, 1, p2);
+  }
+  prof_mark(kPhA2aBwd, false, comm_stream_);
+  ck(cudaEventRecord(ev_comm_done_, comm_stream_), "event");
+  prof_mark(kPhWgrad1, true, st);
+  gemm(kGemmWgrad, recv_.p, dh_.p, o1, wg1, nseg, st);
+  prof_mark(kPhWgrad1, false, st);
+  prof_mark(kPhWgrad2, true, st);
+  gemm(kGemmWgrad, act_.p, drecv_.p, o2, wg2, nseg, st);
+  prof_mark(kPhWgrad2, false, st);
+  // group collectives after the data exchanges (two communicators never interleave)
+  ck(cudaStreamWaitEvent(st, ev_comm_done_, 0), "wait");
+  const size_t mv = static_cast<size_t>(M_) * V_;
+  if (p2) {
+    const size_t mh = static_cast<size_t>(M_) * h;
+    float* g1 = static_cast<float*>(dws1_.p) + mh;  // [q][M][h]
+    ckn(ncclAllGather(o1, g1, mh, ncclFloat32, group_comm_, st), "allgather dW1");
+    ckn(ncclAllGather(o2, gw2, mh, ncclFloat32, group_comm_, st), "allgather dW2");  // [q][h][M] = (V, M)
+    for (int q = 0; q < s_; ++q)
+      ck(cudaMemcpy2DAsync(gw1 + static_cast<size_t>(q) * h, sizeof(float) * V_, g1 + q * mh,
+                           sizeof(float) * h, sizeof(float) * h, M_, cudaMemcpyDeviceToDevice, st),
+         "assemble dW1");
+    ckr(shard_sum_device(ypart_.p, dxcomb_.p, static_cast<int64_t>(degree_) * E_, s_,
+                         static_cast<int64_t>(cc_) * M_, cfg_.dtype, st),
+        "shard_sum");
+    ++launches_;
+  } else {
+    ckn(ncclAllReduce(gw1, gw1, mv, ncclFloat32, ncclSum, group_comm_, st), "allreduce dW1");
+    ckn(ncclAllReduce(gw2, gw2, mv, ncclFloat32, ncclSum, group_comm_, st), "allreduce dW2");
+  }
+}
+
 void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   launches_ = 0;
@@ -758,12 +1039,22 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   launches_ += 4 + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
-  if (cert && stats_dirty_) {
-    ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colnorm_.p),
-                            static_cast<float*>(colnorm_blk_.p), w1t_.p, st),
-        "weight stats");
+  if (stats_dirty_) {
+    if (cert)
+      ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colnorm_.p),
+                              static_cast<float*>(colnorm_blk_.p), w1t_.p, st),
+          "weight stats");
+    if (sharded_) refresh_slices(st);
     stats_dirty_ = false;
   }
+  // ParallelControl (moe_layer.cpp:185-186): sharded placement picks P1 / P2 by the cost model
+  // over the gathered capacity W * dC; per-rank placement admits only P1.
+  parallel_ = MOE_PARALLEL_P1;
+  if (sharded_)
+    parallel_ = cfg_.parallel == MOE_PARALLEL_ADAPTIVE
+                    ? select_parallelism(1.0 / static_cast<double>(s_), static_cast<int64_t>(W_) * cap_,
+                                         M_, 8.0 * 2.0 * M_ * V_, s_)
+                    : cfg_.parallel;
   const SlotGeom g = geom();
   DropZero yzero;  // fused decode: the encode pass also zeroes the dropped tokens' y rows
   if (fused_) {
@@ -843,6 +1134,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     prof_mark(kPhDown, true, st);
     gemm(kGemmDown, act_.p, w2_.p, yexp_.p, down, nseg, st);
     prof_mark(kPhDown, false, st);
+  } else if (sharded_) {
+    sharded_forward(up, down, cert, st);
   } else if (peer_) {
     if (bwd_pending_) {
       // The previous forward was not followed by a backward (inference): its saved expert
@@ -1152,6 +1445,8 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     prof_mark(kPhWgrad2, true, st);
     gemm(kGemmWgrad, act_.p, drecv, gw2, wg2, nseg, st);
     prof_mark(kPhWgrad2, false, st);
+  } else if (sharded_) {
+    sharded_backward(dgm, dg, wg1, wg2, gw1, gw2, st);
   } else if (peer_) {
     const uint32_t e2 = ++epoch_[2], e3 = ++epoch_[3];
     ck(cudaEventRecord(ev_sync_, st), "event");
@@ -1317,6 +1612,19 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
 void Layer::grad_slices(float* w1s, float* w2s, cudaStream_t st) {
   if (!last_dw1_) throw MoeError(MOE_ESTATE, "grad_slices: no backward yet");
   ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (sharded_) {
+    // reduce_scatter_grads_p1, sharded (parallelism.cpp:247-262): the summed gradient of slice
+    // rank%s of expert rank/s -- already reduced over the group by backward.
+    const int h = V_ / s_, q = rank_ % s_;
+    ck(cudaMemcpy2DAsync(w1s, sizeof(float) * h, last_dw1_ + static_cast<size_t>(q) * h,
+                         sizeof(float) * V_, sizeof(float) * h, M_, cudaMemcpyDeviceToDevice, st),
+       "dW1 slice");
+    ck(cudaMemcpyAsync(w2s, last_dw2_ + static_cast<size_t>(q) * h * M_, sizeof(float) * h * M_,
+                       cudaMemcpyDeviceToDevice, st),
+       "dW2 slice");
+    ck(cudaStreamSynchronize(st), "sync");
+    return;
+  }
   const int h = V_ / W_;
   const size_t blk1 = static_cast<size_t>(dE_) * M_ * h;  // floats per (dst) block, each of w1/w2
   DevMem pack;
@@ -1455,7 +1763,7 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->drop_count = drops;
   m->relu_fixups = 0;
   m->fused = (fused_ ? MOE_FUSED_DECODE : 0) | (peer_ && fused_combine_ ? MOE_FUSED_COMBINE : 0);
-  m->reserved = 0;
+  m->parallel = parallel_;
   if (cfg_.dtype == MOE_DTYPE_BF16) {
     unsigned int nfix = 0;  // the last fixup's list size (relu_fixup_kernel keeps it in [2])
     ck(cudaMemcpy(&nfix, static_cast<unsigned int*>(fix_count_.p) + 2, 4, cudaMemcpyDeviceToHost), "copy");

@@ -44,6 +44,9 @@ void a2a_plan(int64_t W, int64_t E, int64_t cc, int64_t M, int64_t chunk, int ph
               int64_t* send_off, int64_t* recv_off, int64_t* elems);
 int64_t expert_capacity(int64_t k, double f, int64_t tokens, int64_t experts);
 void validate(const moe_config& c);
+// select_parallelism (parallelism.cpp:288-308): MOE_PARALLEL_P1 iff comm_cost_p1 <= comm_cost_p2.
+int32_t select_parallelism(double local_experts, int64_t gathered_capacity, int64_t model_dim,
+                           double param_bytes, int64_t n_sharded);
 
 // Phases timed with CUDA events on the compute stream when profiling is on (Timeline tracing,
 // pipeline.hpp:36-46 / pipeline.cpp:68-76, with measured instead of simulated intervals).
@@ -100,6 +103,14 @@ class Layer {
   void peer_push_rows(int ch, const void* src, int chunk, int phase, int slot, uint32_t row0,
                       uint32_t nrows, uint32_t epoch);
   double allreduce_max_host(double v);
+  // Sharded placement (W = E*s, moe_layer.cpp:17-108): grouped NCCL exchanges of chunk `chunk`,
+  // dir 0 = dispatch (z order -> [chunk][nsrc][cc] receive order), dir 1 = combine (inverse; P2
+  // lands the s partials in [chunk][E][s][cc] order for shard_sum).
+  void shard_exchange(const void* send, void* recv, int chunk, int dir, bool p2);
+  void sharded_forward(GemmArgs up, GemmArgs down, bool cert, cudaStream_t st);
+  void sharded_backward(GemmArgs dgm, GemmArgs dg, GemmArgs wg1, GemmArgs wg2, float* gw1,
+                        float* gw2, cudaStream_t st);
+  void refresh_slices(cudaStream_t st);
   void ensure_io();
   void alloc_capacity(int cap);
   void prof_mark(int phase, bool begin, cudaStream_t st);
@@ -112,6 +123,13 @@ class Layer {
   moe_config cfg_;
   int rank_, device_;
   int W_, E_, dE_, M_, V_, T_, k_, esz_;
+  // sharded placement: s_ ranks per expert; this rank computes expert rank/s_ and holds slice
+  // rank%s_ (h = V/s_ hidden columns); parallel_ is the last forward's ParallelChoice
+  bool sharded_ = false;
+  int s_ = 1;
+  int parallel_ = MOE_PARALLEL_P1;
+  ncclComm_t group_comm_ = nullptr;  // the s_ ranks sharing this rank's expert
+  DevMem w1s_, ypart_, dws1_, dws2_;  // P2: W1 slice (M, h), partial outputs, slice grads
   int cap_, cap_alloc_ = 0, cap_formula_ = 0;
   int32_t* cap_host_ = nullptr;
   int degree_ = 1, cc_ = 1;

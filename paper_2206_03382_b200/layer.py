@@ -24,7 +24,8 @@ _CAP = {"fixed": _lib.CAP_FIXED, "auto": _lib.CAP_AUTO, "bounded": _lib.CAP_BOUN
 
 @dataclass
 class MoELayerConfig:
-    """MoELayerConfig + Dims (moe_layer.hpp:22-29, core.hpp:32-56), per-rank placement."""
+    """MoELayerConfig + Dims (moe_layer.hpp:22-29, core.hpp:32-56). E >= W: per-rank placement
+    (E/W experts per rank); E < W: sharded placement (W = E*s, rank r serves expert r/s)."""
     world_size: int = 1
     gpus_per_node: int = 1
     global_experts: int = 1
@@ -40,6 +41,7 @@ class MoELayerConfig:
     degree: int = 1
     a2a_backend: str = "peer"   # "peer" (copy engines over NVLink) or "nccl"
     router: str = "linear"      # RouterKind (moe_layer.hpp:10): "linear" or "cosine"
+    parallel: str = "p1"        # ParallelControl (sharded placement): "p1", "p2" or "adaptive"
 
     def to_c(self) -> MoeConfig:
         return MoeConfig(self.world_size, self.gpus_per_node, self.global_experts, self.model_dim,
@@ -47,11 +49,18 @@ class MoELayerConfig:
                          float(self.capacity_factor), int(self.bpr), _DT[self.dtype],
                          int(self.adaptive), int(self.degree),
                          {"peer": 0, "nccl": 1}[self.a2a_backend],
-                         {"linear": 0, "cosine": 1}[self.router])
+                         {"linear": 0, "cosine": 1}[self.router],
+                         {"p1": 0, "p2": 1, "adaptive": 2}[self.parallel])
 
     @property
     def local_experts(self) -> int:
-        return self.global_experts // self.world_size
+        """Experts this rank computes: E/W, or 1 under sharded placement."""
+        return max(1, self.global_experts // self.world_size)
+
+    @property
+    def n_sharded(self) -> int:
+        """s of RanksPerExpert{s} (W = E*s); 1 under per-rank placement."""
+        return self.world_size // self.global_experts if self.global_experts < self.world_size else 1
 
     @property
     def torch_dtype(self) -> torch.dtype:
@@ -73,6 +82,7 @@ class StepMetricsPy:
     drop_count: int
     relu_fixups: int = 0
     fused: int = 0  # MOE_FUSED_DECODE (1) | MOE_FUSED_COMBINE (2)
+    parallel: str = "p1"  # StepMetrics::parallel
 
 
 @dataclass
@@ -209,15 +219,19 @@ class LayerState:
         m = StepMetrics()
         check(lib().moe_get_metrics(self._h, C.byref(m)), self._h)
         return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
-                             m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups, m.fused)
+                             m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups, m.fused,
+                             "p2" if m.parallel == 1 else "p1")
 
     def grad_slices(self):
         """reduce_scatter_grads_p1: this rank's slice of every expert's dW1 / dW2 (fp32 device),
-        shapes (E, M, V/W) and (E, V/W, M). Collective across ranks."""
+        shapes (E, M, V/W) and (E, V/W, M); under sharded placement the summed slice r%s of expert
+        r/s, shapes (1, M, V/s) and (1, V/s, M). Collective across ranks."""
         cfg = self.config
-        h = cfg.hidden_dim // cfg.world_size
-        w1s = torch.empty(cfg.global_experts, cfg.model_dim, h, dtype=torch.float32, device=self.device)
-        w2s = torch.empty(cfg.global_experts, h, cfg.model_dim, dtype=torch.float32, device=self.device)
+        s = cfg.n_sharded
+        ne = 1 if s > 1 else cfg.global_experts
+        h = cfg.hidden_dim // (s if s > 1 else cfg.world_size)
+        w1s = torch.empty(ne, cfg.model_dim, h, dtype=torch.float32, device=self.device)
+        w2s = torch.empty(ne, h, cfg.model_dim, dtype=torch.float32, device=self.device)
         check(lib().moe_get_expert_grad_slices(self._h, _ptr(w1s), _ptr(w2s), _stream(self.device)),
               self._h)
         return w1s, w2s

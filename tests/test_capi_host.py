@@ -67,6 +67,49 @@ def test_validate_config_mirrors_dims_validate():
     assert b"E = W*x" in lib().moe_last_error_global() or True
 
 
+def test_validate_config_sharded_placement():
+    """RanksPerExpert{s} (core.cpp:17-23): E < W needs W = E*s; slices need V % s == 0."""
+    v = lambda c: lib().moe_validate_config(C.byref(c))  # noqa: E731
+    assert v(cfg(world_size=4, global_experts=2, top_k=1)) == 0             # s = 2
+    assert v(cfg(world_size=4, global_experts=1, top_k=1)) == 0             # s = 4
+    assert v(cfg(world_size=4, global_experts=3, top_k=1)) == _lib.MOE_EINVAL  # W != E*s
+    assert v(cfg(world_size=4, global_experts=2, top_k=1, hidden_dim=3)) == _lib.MOE_EINVAL
+    assert v(cfg(world_size=4, global_experts=2, top_k=1, parallel=3)) == _lib.MOE_EINVAL
+    for p in (0, 1, 2):
+        assert v(cfg(world_size=4, global_experts=2, top_k=1, parallel=p)) == 0
+
+
+def select(dE, C_, M, pb, s):
+    out = C.c_int32(-1)
+    rc = lib().moe_select_parallelism(dE, C_, M, pb, s, C.byref(out))
+    return rc, out.value
+
+
+def test_select_parallelism_kats():
+    """comm_cost_p1/p2 and select_parallelism (test_parallelism.cpp:255-279, acceptance.cpp:360-404)."""
+    P1, P2 = 0, 1
+    # exact tie -> P1 (weight gather): p1 = 8*1*8*2 + 384 = 512 = p2 = 8*4*1*8*2
+    assert select(1.0, 8, 2, 384.0, 4) == (0, P1)
+    assert select(1.0, 8, 2, 384.0 + 1e-9, 4) == (0, P2)
+    assert select(1.0, 8, 2, 0.0, 0)[0] == _lib.MOE_EINVAL  # comm_cost_p2: n_sharded >= 1
+    rng = __import__("random").Random(208)
+    for _ in range(200):
+        dE, C_, M = rng.uniform(0.1, 4.0), rng.randint(1, 1 << 14), rng.randint(1, 1024)
+        pb, s = rng.uniform(0.0, 1e8), rng.randint(1, 8)
+        p1 = 8.0 * dE * float(C_) * float(M) + pb
+        p2 = 8.0 * float(s) * dE * float(C_) * float(M)
+        assert select(dE, C_, M, pb, s) == (0, P1 if p1 <= p2 else P2)
+    # the published large-model shape: 2 experts over 8 ranks, 4-way shards; one crossover P2 -> P1
+    # as the capacity factor grows (acceptance.cpp:377-404)
+    picks = []
+    for f in (1.0, 2.0, 4.0, 8.0, 16.0):
+        cap = C.c_int64()
+        assert lib().moe_expert_capacity(1, f, 2048, 2, C.byref(cap)) == 0
+        picks.append(select(1.0 / 4, 8 * cap.value, 2048, 8.0 * 2.0 * 2048 * 8192, 4)[1])
+    assert picks[0] == P2 and picks[-1] == P1
+    assert sum(a != b for a, b in zip(picks, picks[1:])) == 1
+
+
 def test_a2a_plan_is_the_flex_interleave():
     """Send/recv blocks of the flexible all-to-all (collectives.cpp:123-160)."""
     W, E, cc, M = 4, 8, 3, 5

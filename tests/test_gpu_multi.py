@@ -1,6 +1,7 @@
 """Expert parallelism on >= 2 GPUs (skipped on a 1-GPU box): tools/mp_parity.py under torchrun
 checks every rank's routing, y, dx and local dW against the fp64 oracle of the whole layer for
-pipelining degrees 1/2/4/8, an fp32 case and the adaptive Alg. 1 controller."""
+pipelining degrees 1/2/4/8, an fp32 case and the adaptive Alg. 1 controller, plus sharded placement
+(E < W: P1 / P2 / adaptive parallel control, weights loaded through the slice gather)."""
 import socket
 import subprocess
 import sys

@@ -254,3 +254,25 @@ def test_cosine_gate_kat():
     x[1] = 0.0
     with pytest.raises(ValueError):
         oracle.gate_cosine(x, proj, experts, 1.0)
+
+
+def test_layer_step_sharded_placement_matches_frozen_plan():
+    """E < W (RanksPerExpert): the oracle's layer equals the per-token frozen plan
+    (frozen_plan_forward, moe_layer.cpp:321-335) -- placement changes who computes, not what."""
+    import numpy as np
+    import oracle
+    from tests.helpers import layer_inputs
+    for W, E, k in ((4, 2, 1), (4, 2, 2), (2, 1, 1)):
+        T, M, V = 16, 8, 16
+        inp = layer_inputs(402, W, T, M, V, E, "f32")
+        ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, 0, 1.0, False)
+        y = np.zeros_like(inp["x"])
+        for t in range(W * T):
+            for j in range(k):
+                if ref["locations"][t, j] < 0:
+                    continue
+                e = ref["idxs"][t, j]
+                h = np.maximum(inp["x"][t] @ inp["w1"][e], 0.0)
+                y[t] += ref["gates"][t, j] * (h @ inp["w2"][e])
+        assert oracle.max_rel_diff(y, ref["y"]) < 1e-12
+        assert np.abs(ref["dw1"]).max() > 0 and np.abs(ref["dx"]).max() > 0

@@ -69,6 +69,76 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     return ok and t.item() == 0, errs, m
 
 
+def run_sharded(rank, W, dev, s, k, f, M, V, T, bpr, dt, degree, parallel, slices, seed=402):
+    """Sharded placement (W = E*s, moe_layer.cpp:17-108): P1 / P2 / adaptive exchange forms.
+    Every rank returns the full gradient of expert rank//s; `slices` loads the weights through
+    moe_set_expert_slices (the group all-gathers its slices) after a differently seeded init."""
+    E = W // s
+    cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
+                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f, bpr=bpr,
+                         dtype=dt, degree=degree, a2a_backend="nccl", parallel=parallel)
+    obj = [LayerState.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    inp = layer_inputs(seed, W, T, M, V, E, dt)
+    e, q, h = rank // s, rank % s, V // s
+    st = LayerState.init(cfg, seed + 1 if slices else seed, rank=rank, device=dev.index, nccl_id=obj[0])
+    if slices:
+        st.set_router(inp["wg"])
+        st.set_expert_slices(inp["w1"][e:e + 1, :, q * h:(q + 1) * h], inp["w2"][e:e + 1, q * h:(q + 1) * h, :])
+    tdt = cfg.torch_dtype
+    xs = torch.as_tensor(inp["x"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
+    dys = torch.as_tensor(inp["dy"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
+    for it in range(2):
+        res = forward(st, xs)
+        if it == 0:
+            res = forward(st, xs)
+        g = backward(st, res.saved, dys)
+    torch.cuda.synchronize()
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, 0, f, bpr)
+    sl = slice(rank * T, (rank + 1) * T)
+    idxs, loc, gates, cap = st.routing()
+    tol = 1e-5 if dt == "f32" else 2e-2
+    m = st.metrics()
+    want = parallel
+    if parallel == "adaptive":  # select_parallelism(dims, W * dC) (moe_layer.cpp:185-186)
+        p1 = 8.0 * (1.0 / s) * float(W * cap) * float(M) + 8.0 * 2.0 * M * V
+        p2 = 8.0 * float(s) * (1.0 / s) * float(W * cap) * float(M)
+        want = "p1" if p1 <= p2 else "p2"
+    errs = dict(
+        routing=int(not (np.array_equal(idxs, ref["idxs"][sl]) and np.array_equal(loc, ref["locations"][sl]))),
+        cap=int(cap != ref["capacity"]),
+        parallel=int(m.parallel != want),
+        y=oracle.max_rel_diff(res.y.double().cpu().numpy(), ref["y"][sl]),
+        dx=oracle.max_rel_diff(g.dx.double().cpu().numpy(), ref["dx"][sl]),
+        dw1=oracle.max_rel_diff(g.dw1.double().cpu().numpy(), ref["dw1"][e:e + 1]),
+        dw2=oracle.max_rel_diff(g.dw2.double().cpu().numpy(), ref["dw2"][e:e + 1]),
+    )
+    w1s, w2s = st.grad_slices()
+    errs["dw1_slice"] = oracle.max_rel_diff(w1s.double().cpu().numpy(), ref["dw1"][e:e + 1, :, q * h:(q + 1) * h])
+    errs["dw2_slice"] = oracle.max_rel_diff(w2s.double().cpu().numpy(), ref["dw2"][e:e + 1, q * h:(q + 1) * h, :])
+    ok = errs["routing"] == 0 and errs["cap"] == 0 and errs["parallel"] == 0 and all(
+        errs[n] < tol for n in ("y", "dx", "dw1", "dw2", "dw1_slice", "dw2_slice"))
+    t = torch.tensor([0.0 if ok else 1.0], device=dev)
+    dist.all_reduce(t)
+    st.close()
+    return ok and t.item() == 0, errs, m
+
+
+SHARDED_CASES = [
+    # s, k, f, M, V, T, bpr, dtype, degree, parallel, load through set_expert_slices
+    (2, 1, 1.0, 256, 512, 512, False, "bf16", 1, "p1", False),
+    (2, 1, 1.0, 256, 512, 512, False, "bf16", 2, "p2", False),
+    (2, 1, 1.25, 256, 512, 512, False, "bf16", 1, "adaptive", True),
+    (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, "p2", False),
+    (2, 2, 1.0, 256, 512, 512, True, "bf16", 2, "p1", True),
+    (2, 1, 1.0, 64, 128, 200, False, "f32", 2, "p1", False),
+    (2, 1, 0.5, 64, 128, 200, False, "f32", 2, "p2", True),
+    (4, 1, 1.0, 256, 1024, 512, False, "bf16", 2, "p2", False),
+    (4, 1, 1.0, 128, 256, 300, False, "bf16", 4, "p1", False),
+    (2, 1, 1.0, 256, 512, 4096, False, "bf16", 1, "adaptive", False),  # tokens dominate: P1
+]
+
+
 def main():
     rank, W, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     dev = torch.device("cuda", local)
@@ -98,6 +168,19 @@ def main():
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer", "fixed", "cosine"),
     ]
     all_ok = True
+    only_sharded = os.environ.get("MP_SHARDED_ONLY") == "1"
+    for c in SHARDED_CASES:
+        s, k = c[0], c[1]
+        if W % s != 0 or W // s < k:
+            continue
+        ok, errs, m = run_sharded(rank, W, dev, *c)
+        all_ok &= ok
+        if rank == 0:
+            print(("PASS" if ok else "FAIL"), "sharded", c,
+                  {n: (round(v, 7) if isinstance(v, float) else v) for n, v in errs.items()},
+                  f"parallel={m.parallel} degree={m.degree} comm_bytes={m.comm_bytes:.0f}", flush=True)
+    if only_sharded:
+        cases = []
     for c in cases:
         ok, errs, m = run(rank, W, dev, *c)
         all_ok &= ok
