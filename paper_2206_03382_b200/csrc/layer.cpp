@@ -1047,14 +1047,16 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     if (sharded_) refresh_slices(st);
     stats_dirty_ = false;
   }
-  // ParallelControl (moe_layer.cpp:185-186): sharded placement picks P1 / P2 by the cost model
-  // over the gathered capacity W * dC; per-rank placement admits only P1.
-  parallel_ = MOE_PARALLEL_P1;
-  if (sharded_)
-    parallel_ = cfg_.parallel == MOE_PARALLEL_ADAPTIVE
-                    ? select_parallelism(1.0 / static_cast<double>(s_), static_cast<int64_t>(W_) * cap_,
-                                         M_, 8.0 * 2.0 * M_ * V_, s_)
-                    : cfg_.parallel;
+  // ParallelControl (moe_layer.cpp:184-186): adaptive picks P1 / P2 by the cost model over the
+  // gathered capacity W * dC under sharded placement and P1 otherwise; a fixed choice is
+  // reported as configured (per-rank placement runs the flex exchange either way, :112-118).
+  if (cfg_.parallel != MOE_PARALLEL_ADAPTIVE)
+    parallel_ = cfg_.parallel;
+  else if (sharded_)
+    parallel_ = select_parallelism(1.0 / static_cast<double>(s_), static_cast<int64_t>(W_) * cap_, M_,
+                                   8.0 * 2.0 * M_ * V_, s_);
+  else
+    parallel_ = MOE_PARALLEL_P1;
   const SlotGeom g = geom();
   DropZero yzero;  // fused decode: the encode pass also zeroes the dropped tokens' y rows
   if (fused_) {

@@ -11,8 +11,8 @@ Differences, by design:
   * `sim_seconds` holds the *measured* forward time on the B200s (CUDA events, max over ranks).
   * The payload-free path (bench.cpp:222-248) evaluates the reference's fabric cost model, which is
     out of scope here; settings that cannot run on the launched GPUs (W larger than the process
-    count or than `ranks_materialize_max`), sharded placement (experts_per_rank < 1) and P2 are
-    skipped with a note on stderr.
+    count or than `ranks_materialize_max`) are skipped with a note on stderr. Sharded placement
+    (experts_per_rank < 1) and the parallel control (adaptive | p1 | p2) run on the GPUs.
   * The layer runs in `dtype` (bf16 or f32); x is drawn in fp64 by the reference Rng and rounded.
 
 Usage (one process per GPU; W-rank settings use ranks 0..W-1):
@@ -314,8 +314,6 @@ def runnable(d: Dims, parallel: str, world: int, ranks_materialize_max: int):
         return "payload-free path (fabric cost model) is out of scope"
     if d.world_size > world:
         return f"needs {d.world_size} GPU processes, {world} launched"
-    if d.is_sharded or parallel == "p2":
-        return "sharded placement / P2 is out of scope"
     return None
 
 
@@ -345,7 +343,8 @@ def run_scenario(sc: Scenario, ranks_materialize_max: int = 64, dtype: str = "f3
                              global_experts=d.global_experts, model_dim=M,
                              hidden_dim=d.hidden_dim, tokens_per_step=T, top_k=d.top_k,
                              capacity="fixed", capacity_factor=trace[0], dtype=dtype,
-                             adaptive=sc.adaptive, degree=sc.degree if not sc.adaptive else 1)
+                             adaptive=sc.adaptive, degree=sc.degree if not sc.adaptive else 1,
+                             parallel=sc.parallel)
         nid = None
         if W > 1:
             obj = [LayerState.unique_id() if rank == 0 else None]
@@ -365,7 +364,7 @@ def run_scenario(sc: Scenario, ranks_materialize_max: int = 64, dtype: str = "f3
                 forward(st, x)
                 m = st.metrics()
                 recs.append([step, m.f, m.capacity, m.degree, m.a2a_algo, m.seconds, m.comm_bytes,
-                             m.drop_count])
+                             m.drop_count, m.parallel])
             torch.cuda.synchronize()
             st.close()
         if W > 1:
@@ -379,17 +378,17 @@ def run_scenario(sc: Scenario, ranks_materialize_max: int = 64, dtype: str = "f3
             tsum = t[:, 1:].clone()
             dist.all_reduce(tsum)
             if not active:
-                recs = [[s_, 0.0, 0, 0, "linear", 0.0, 0.0, 0] for s_ in range(sc.steps)]
+                recs = [[s_, 0.0, 0, 0, "linear", 0.0, 0.0, 0, "p1"] for s_ in range(sc.steps)]
                 meta = [None]
             else:
-                meta = [[(r[1], r[2], r[3], r[4]) for r in recs]] if rank == 0 else [None]
+                meta = [[(r[1], r[2], r[3], r[4], r[8]) for r in recs]] if rank == 0 else [None]
             dist.broadcast_object_list(meta, src=0)
             for s_ in range(sc.steps):
-                f, cap, deg, algo = meta[0][s_]
+                f, cap, deg, algo, par = meta[0][s_]
                 recs[s_] = [s_, f, cap, deg, algo, float(tmax[s_]), float(tsum[s_, 0]),
-                            int(round(float(tsum[s_, 1])))]
-        for step, f, cap, deg, algo, secs, cbytes, drops in recs:
-            records.append(StepRecord(setting.id, step, f, cap, f"{algo}x{deg}", "p1", secs,
+                            int(round(float(tsum[s_, 1]))), par]
+        for step, f, cap, deg, algo, secs, cbytes, drops, par in recs:
+            records.append(StepRecord(setting.id, step, f, cap, f"{algo}x{deg}", par, secs,
                                       cbytes, drops))
     return records
 

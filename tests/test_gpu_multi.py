@@ -57,6 +57,25 @@ def test_scenario_runner_two_ranks(cuda, tmp_path):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
+def test_scenario_runner_sharded_adaptive_parallel(cuda, tmp_path):
+    """A sharded setting (experts_per_rank 1/2: E = 1 over W = 2) with adaptive parallel control:
+    select_parallelism picks P2 at f = 0.125 (C = 16 < 4V) and P1 at f = 1 (C = 128)."""
+    from paper_2206_03382_b200 import scenario as S
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "-m",
+           "paper_2206_03382_b200.scenario", "run", str(ROOT / "tests" / "golden" / "scenario_sharded.json"),
+           "--out", str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    recs = S.parse_records_csv((tmp_path / "records.csv").read_text())
+    assert [x.capacity for x in recs] == [8, 64, 8, 64]
+    assert [x.parallel for x in recs] == ["p2", "p1", "p2", "p1"]
+    assert all(x.sim_seconds > 0 for x in recs)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
 def test_two_devices_one_process(cuda):
     """Independent W = 1 handles on two devices of one process (per-device kernel attributes):
     both produce the oracle's routing and outputs."""
