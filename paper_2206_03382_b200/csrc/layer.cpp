@@ -205,6 +205,12 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
     tl_on_ = t && t[0] == '1';
   }
   {
+    const char* pt = std::getenv("MOE_PIPE_TIMELINE");
+    pipe_tl_on_ = pt && pt[0] == '1';
+    const char* hc = std::getenv("MOE_HOST_CHUNK_MB");
+    host_chunk_ = hc ? static_cast<size_t>(std::atol(hc)) << 20 : 0;
+  }
+  {
     const char* lf = std::getenv("MOE_LOCAL_FIRST");  // =0: chunk 0 waits for every source
     local_first_ = !(lf && lf[0] == '0');
     const char* e = std::getenv("MOE_FUSED");  // MOE_FUSED=0: unfused single-rank path (A/B runs)
@@ -1691,6 +1697,17 @@ void Layer::backward_host(const void* dyh, void* dxh, cudaStream_t st) {
   ck(cudaStreamSynchronize(st), "sync");
 }
 
+// Host <-> device staging copy, issued in pieces of host_chunk_ bytes (MOE_HOST_CHUNK_MB; 0 =
+// one copy) so that latency-critical peer pushes sharing a copy engine wait for one piece at
+// most, not for a whole multi-MiB step input.
+void Layer::host_copy(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t st) {
+  const size_t piece = host_chunk_ ? host_chunk_ : n;
+  for (size_t o = 0; o < n; o += piece)
+    ck(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                       std::min(piece, n - o), kind, st),
+       "host copy");
+}
+
 void Layer::pipe_call(int dir, const void* inh, void* outh, cudaStream_t st) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   const size_t n = static_cast<size_t>(T_) * M_ * esz_;
@@ -1711,19 +1728,36 @@ void Layer::pipe_call(int dir, const void* inh, void* outh, cudaStream_t st) {
   p.slot ^= 1;
   // upload once the call that last read this staging buffer is done with it
   ck(cudaStreamWaitEvent(h2d_, p.in_free[s], 0), "wait");
-  ck(cudaMemcpyAsync(p.in[s].p, inh, n, cudaMemcpyHostToDevice, h2d_), "h2d");
+  const char* tag = dir == 0 ? "fwd" : "bwd";
+  pipe_mark(std::string(tag) + " h2d >", h2d_);
+  host_copy(p.in[s].p, inh, n, cudaMemcpyHostToDevice, h2d_);
+  pipe_mark(std::string(tag) + " h2d <", h2d_);
   ck(cudaEventRecord(p.in_ready[s], h2d_), "event");
   ck(cudaStreamWaitEvent(st, p.in_ready[s], 0), "wait");
   ck(cudaStreamWaitEvent(st, p.out_free[s], 0), "wait");
+  pipe_mark(std::string(tag) + " compute >", st);
   if (dir == 0)
     forward(p.in[s].p, p.out[s].p, st);
   else
     backward(p.in[s].p, p.out[s].p, nullptr, nullptr, st);
+  pipe_mark(std::string(tag) + " compute <", st);
   ck(cudaEventRecord(p.in_free[s], st), "event");
   ck(cudaEventRecord(p.out_ready[s], st), "event");
   ck(cudaStreamWaitEvent(d2h_, p.out_ready[s], 0), "wait");
-  ck(cudaMemcpyAsync(outh, p.out[s].p, n, cudaMemcpyDeviceToHost, d2h_), "d2h");
+  pipe_mark(std::string(tag) + " d2h >", d2h_);
+  host_copy(outh, p.out[s].p, n, cudaMemcpyDeviceToHost, d2h_);
+  pipe_mark(std::string(tag) + " d2h <", d2h_);
   ck(cudaEventRecord(p.out_free[s], d2h_), "event");
+}
+
+// MOE_PIPE_TIMELINE=1 (debug): events on the staging-copy and compute streams of the pipelined
+// host calls, printed (ms from the first) by host_sync -- no synchronisation in between.
+void Layer::pipe_mark(const std::string& name, cudaStream_t st) {
+  if (!pipe_tl_on_) return;
+  cudaEvent_t e;
+  ck(cudaEventCreateWithFlags(&e, cudaEventDefault), "event");
+  ck(cudaEventRecord(e, st), "event");
+  pipe_tl_.emplace_back(name, e);
 }
 
 void Layer::forward_host_async(const void* xh, void* yh, cudaStream_t st) { pipe_call(0, xh, yh, st); }
@@ -1733,6 +1767,16 @@ void Layer::host_sync() {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   if (d2h_) ck(cudaStreamSynchronize(d2h_), "sync");
   if (h2d_) ck(cudaStreamSynchronize(h2d_), "sync");
+  if (!pipe_tl_.empty()) {
+    ck(cudaDeviceSynchronize(), "sync");
+    for (auto& [nm, e] : pipe_tl_) {
+      float t = 0.0f;
+      ck(cudaEventElapsedTime(&t, pipe_tl_.front().second, e), "elapsed");
+      std::fprintf(stderr, "[pipe r%d] %9.3f ms  %s\n", rank_, t, nm.c_str());
+    }
+    for (auto& pe : pipe_tl_) cudaEventDestroy(pe.second);
+    pipe_tl_.clear();
+  }
 }
 
 void Layer::get_routing(int32_t* idxs, int32_t* locs, double* gates, int64_t* capacity) {

@@ -171,6 +171,11 @@ class Layer {
   HostPipe pipe_[2];  // [forward, backward]
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
   void pipe_call(int dir, const void* inh, void* outh, cudaStream_t st);
+  void host_copy(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t st);
+  size_t host_chunk_ = 0;
+  void pipe_mark(const std::string& name, cudaStream_t st);
+  bool pipe_tl_on_ = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> pipe_tl_;
   // ReLU-mask certificate state (relu_fix.cu)
   DevMem colnorm_, colnorm_blk_, w1t_, rownorm_, fix_list_, fix_count_, relu_mask_;
   // W > 1 peer backend: row norms of the send buffer (z order); pushed with the rows into the
