@@ -39,7 +39,10 @@ extern "C" {
 #define MOE_CAP_BOUNDED 2 /* BoundedCapacity{max_factor} core.hpp:29-31 */
 
 #define MOE_A2A_LINEAR 0 /* A2aAlgo::Linear (collectives.hpp:10) */
-#define MOE_A2A_2DH 1    /* A2aAlgo::TwoDH */
+#define MOE_A2A_2DH 1    /* A2aAlgo::TwoDH (all2all_2dh, collectives.cpp:58-88): intra-node exchange
+                            of node-aligned blocks, then inter-node exchange between same-local
+                            GPUs. Run as two NCCL phases when gpus_per_node < W on the NCCL
+                            transport; the peer transport and m == W run it as linear. */
 
 /* MoELayerConfig (moe_layer.hpp:22-29) flattened with Dims (core.hpp:32-56). The placement
  * follows from E and W: E >= W is per-rank placement (ExpertsPerRank{E/W}, E = W*x); E < W is
@@ -61,6 +64,7 @@ typedef struct moe_config {
   int32_t a2a_backend;     /* MOE_A2A_BACKEND_*: how W > 1 ranks exchange tokens */
   int32_t router;          /* MOE_ROUTER_* (RouterKind, moe_layer.hpp:10) */
   int32_t parallel;        /* MOE_PARALLEL_* (ParallelControl, moe_layer.hpp:17-20); sharded only */
+  int32_t a2a_algo;        /* StrategyControl::fixed.algo: MOE_A2A_LINEAR or MOE_A2A_2DH */
 } moe_config;
 
 /* ParallelControl / ParallelChoice (parallelism.hpp): the sharded-placement exchange form.

@@ -44,6 +44,7 @@ struct Dims {  // core.hpp:32-56 (E >= W: ExpertsPerRank{E/W}; E < W: RanksPerEx
 
 struct StrategyControl {  // moe_layer.hpp:17-20
   bool adaptive = false;
+  int algo = MOE_A2A_LINEAR;  // fixed.algo
   int degree = 1;
   int a2a_backend = MOE_A2A_BACKEND_PEER;
 };
@@ -84,6 +85,7 @@ struct MoELayerConfig {  // moe_layer.hpp:22-29
     c.a2a_backend = strategy.a2a_backend;
     c.router = static_cast<int32_t>(router);
     c.parallel = parallel.adaptive ? MOE_PARALLEL_ADAPTIVE : static_cast<int32_t>(parallel.fixed);
+    c.a2a_algo = strategy.algo;
     return c;
   }
 };

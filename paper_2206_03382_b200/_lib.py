@@ -38,6 +38,7 @@ class MoeConfig(C.Structure):
         ("top_k", C.c_int64), ("capacity_kind", C.c_int32), ("capacity_factor", C.c_double),
         ("bpr", C.c_int32), ("dtype", C.c_int32), ("adaptive", C.c_int32), ("degree", C.c_int32),
         ("a2a_backend", C.c_int32), ("router", C.c_int32), ("parallel", C.c_int32),
+        ("a2a_algo", C.c_int32),
     ]
 
 

@@ -126,6 +126,8 @@ void validate(const moe_config& c) {
   }
   if (c.parallel < MOE_PARALLEL_P1 || c.parallel > MOE_PARALLEL_ADAPTIVE)
     throw MoeError(MOE_EINVAL, "parallel control");
+  if (c.a2a_algo != MOE_A2A_LINEAR && c.a2a_algo != MOE_A2A_2DH)
+    throw MoeError(MOE_EINVAL, "all-to-all algorithm");
   if (c.top_k > 32) throw MoeError(MOE_EINVAL, "top_k > 32 unsupported");
   if (c.global_experts > 256) throw MoeError(MOE_EINVAL, "E > 256 unsupported by the gate kernel");
   if (c.dtype != MOE_DTYPE_BF16 && c.dtype != MOE_DTYPE_F32) throw MoeError(MOE_EINVAL, "dtype");
@@ -727,6 +729,13 @@ void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
   std::vector<int64_t> so(W_), ro(W_);
   int64_t elems = 0;
   a2a_plan(W_, E_, cc_, M_, chunk, phase, so.data(), ro.data(), &elems);
+  const int m = static_cast<int>(cfg_.gpus_per_node);
+  if (strategy_.algo == MOE_A2A_2DH && m < W_) {
+    // the W blocks of either side are contiguous in rank order (a2a_plan's offsets)
+    exchange_2dh(static_cast<const char*>(send) + so[0] * esz_, static_cast<char*>(recv) + ro[0] * esz_,
+                 static_cast<size_t>(elems) * esz_, dt, elems);
+    return;
+  }
   ckn(ncclGroupStart(), "ncclGroupStart");
   for (int p = 0; p < W_; ++p) {
     ckn(ncclSend(static_cast<const char*>(send) + so[p] * esz_, elems, dt, p, comm_, comm_stream_),
@@ -736,6 +745,43 @@ void Layer::exchange(const void* send, void* recv, int chunk, int phase) {
   }
   ckn(ncclGroupEnd(), "ncclGroupEnd");
   comm_bytes_ += static_cast<double>(elems) * esz_ * (W_ - 1);
+}
+
+// all2all_2dh (collectives.cpp:58-88) on the comm stream: block p of `send` goes to rank p and
+// block p of `recv` comes from rank p, as the linear exchange, but in two NCCL phases over
+// n = W/m nodes of m GPUs. (1) Reorder the blocks so those for local GPU g are contiguous
+// ([g][node]); (2) intra-node exchange of n blocks with each local GPU; (3) reorder to
+// [node][source local]; (4) inter-node exchange of m blocks with the same-local GPU of every
+// node, landing in source-rank order. The reorders are strided 2-D copies of whole blocks.
+void Layer::exchange_2dh(const char* send, char* recv, size_t B, ncclDataType_t dt, int64_t elems) {
+  const int m = static_cast<int>(cfg_.gpus_per_node), n = W_ / m;
+  const int node = rank_ / m, local = rank_ % m;
+  a2a_tmp_.alloc(2 * static_cast<size_t>(W_) * B);
+  char* ta = static_cast<char*>(a2a_tmp_.p);
+  char* tb = ta + static_cast<size_t>(W_) * B;
+  for (int g = 0; g < m; ++g)  // ta[g][nd] = send[nd * m + g]
+    ck(cudaMemcpy2DAsync(ta + static_cast<size_t>(g) * n * B, B, send + static_cast<size_t>(g) * B,
+                         static_cast<size_t>(m) * B, B, n, cudaMemcpyDeviceToDevice, comm_stream_),
+       "2dh align");
+  ckn(ncclGroupStart(), "ncclGroupStart");
+  for (int g = 0; g < m; ++g) {
+    const int peer = node * m + g;
+    ckn(ncclSend(ta + static_cast<size_t>(g) * n * B, n * elems, dt, peer, comm_, comm_stream_), "ncclSend");
+    ckn(ncclRecv(tb + static_cast<size_t>(g) * n * B, n * elems, dt, peer, comm_, comm_stream_), "ncclRecv");
+  }
+  ckn(ncclGroupEnd(), "ncclGroupEnd");
+  for (int nd = 0; nd < n; ++nd)  // ta[nd][g] = tb[g][nd]
+    ck(cudaMemcpy2DAsync(ta + static_cast<size_t>(nd) * m * B, B, tb + static_cast<size_t>(nd) * B,
+                         static_cast<size_t>(n) * B, B, m, cudaMemcpyDeviceToDevice, comm_stream_),
+       "2dh align");
+  ckn(ncclGroupStart(), "ncclGroupStart");
+  for (int nd = 0; nd < n; ++nd) {
+    const int peer = local + nd * m;
+    ckn(ncclSend(ta + static_cast<size_t>(nd) * m * B, m * elems, dt, peer, comm_, comm_stream_), "ncclSend");
+    ckn(ncclRecv(recv + static_cast<size_t>(nd) * m * B, m * elems, dt, peer, comm_, comm_stream_), "ncclRecv");
+  }
+  ckn(ncclGroupEnd(), "ncclGroupEnd");
+  comm_bytes_ += static_cast<double>(B) * (static_cast<double>(n) * (m - 1) + static_cast<double>(m) * (n - 1));
 }
 
 // Copy-engine version of exchange(): push chunk `chunk` of `src` into every peer's channel
@@ -1033,7 +1079,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   prof_mark(kPhGate, false, st);
   f_ = static_cast<double>(cap_) * E_ / (static_cast<double>(k_) * T_);  // capacity_to_factor
-  strategy_ = cfg_.adaptive ? get_strategy(memo_, f_) : Strategy{0, cfg_.degree};
+  strategy_ = cfg_.adaptive ? get_strategy(memo_, f_) : Strategy{cfg_.a2a_algo, cfg_.degree};
   // 2DH degenerates to the linear algorithm inside one NVSwitch domain (collectives.cpp:58-88
   // with m == W); it is executed as linear and reported as chosen.
   degree_ = W_ == 1 ? 1 : strategy_.degree;

@@ -99,6 +99,8 @@ class Layer {
   GatingBuffers gating_buffers();
   SlotGeom geom() const;
   void exchange(const void* send, void* recv, int chunk, int phase);
+  void exchange_2dh(const char* send, char* recv, size_t block_bytes, ncclDataType_t dt, int64_t elems);
+  DevMem a2a_tmp_;  // 2DH staging (two W-block buffers)
   void peer_push(int ch, const void* src, int chunk, int phase, uint32_t epoch, cudaEvent_t local_done);
   void peer_push_rows(int ch, const void* src, int chunk, int phase, int slot, uint32_t row0,
                       uint32_t nrows, uint32_t epoch);

@@ -42,6 +42,7 @@ class MoELayerConfig:
     a2a_backend: str = "peer"   # "peer" (copy engines over NVLink) or "nccl"
     router: str = "linear"      # RouterKind (moe_layer.hpp:10): "linear" or "cosine"
     parallel: str = "p1"        # ParallelControl (sharded placement): "p1", "p2" or "adaptive"
+    a2a_algo: str = "linear"    # StrategyControl::fixed.algo: "linear" or "2dh"
 
     def to_c(self) -> MoeConfig:
         return MoeConfig(self.world_size, self.gpus_per_node, self.global_experts, self.model_dim,
@@ -50,7 +51,8 @@ class MoELayerConfig:
                          int(self.adaptive), int(self.degree),
                          {"peer": 0, "nccl": 1}[self.a2a_backend],
                          {"linear": 0, "cosine": 1}[self.router],
-                         {"p1": 0, "p2": 1, "adaptive": 2}[self.parallel])
+                         {"p1": 0, "p2": 1, "adaptive": 2}[self.parallel],
+                         {"linear": 0, "2dh": 1}[self.a2a_algo])
 
     @property
     def local_experts(self) -> int:

@@ -77,6 +77,9 @@ def test_validate_config_sharded_placement():
     assert v(cfg(world_size=4, global_experts=2, top_k=1, parallel=3)) == _lib.MOE_EINVAL
     for p in (0, 1, 2):
         assert v(cfg(world_size=4, global_experts=2, top_k=1, parallel=p)) == 0
+    # StrategyControl::fixed.algo: linear or 2DH
+    assert v(cfg(a2a_algo=1)) == 0
+    assert v(cfg(a2a_algo=2)) == _lib.MOE_EINVAL
 
 
 def select(dE, C_, M, pb, s):

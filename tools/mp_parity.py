@@ -15,16 +15,16 @@ from tests.helpers import layer_inputs  # noqa: E402
 
 
 def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, cap="fixed",
-        router="linear", seed=402):
+        router="linear", seed=402, m=None, algo="linear"):
     E = E_per * W
     ce = backend == "peer-ce"  # peer backend with the copy-engine combine (fused combine off)
     if ce:
         backend = "peer"
         os.environ["MOE_FUSED_COMBINE"] = "0"
-    cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
+    cfg = MoELayerConfig(world_size=W, gpus_per_node=m or W, global_experts=E, model_dim=M,
                          hidden_dim=V, tokens_per_step=T, top_k=k, capacity=cap,
                          capacity_factor=f, bpr=bpr, dtype=dt, degree=degree, adaptive=adaptive,
-                         a2a_backend=backend, router=router)
+                         a2a_backend=backend, router=router, a2a_algo=algo)
     obj = [LayerState.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
@@ -179,6 +179,18 @@ def main():
             print(("PASS" if ok else "FAIL"), "sharded", c,
                   {n: (round(v, 7) if isinstance(v, float) else v) for n, v in errs.items()},
                   f"parallel={m.parallel} degree={m.degree} comm_bytes={m.comm_bytes:.0f}", flush=True)
+    # 2DH (all2all_2dh, collectives.cpp:58-88) over W/m "nodes" of m GPUs on the NCCL transport,
+    # fixed and under Alg. 1 (which then explores linear and 2DH x {1,2,4,8})
+    for m_, algo, degree, adaptive in ((W // 2, "2dh", 2, False), (1, "2dh", 1, False), (W // 2, "linear", 1, True)):
+        if only_sharded:
+            break
+        c = (2, 2, 1.25, 256, 512, 512, True, "bf16", degree, adaptive, "nccl")
+        ok, errs, mt = run(rank, W, dev, *c, m=m_, algo=algo)
+        all_ok &= ok
+        if rank == 0:
+            print(("PASS" if ok else "FAIL"), f"m={m_} algo={algo}", c,
+                  {n: (round(v, 7) if isinstance(v, float) else v) for n, v in errs.items()},
+                  f"a2a={mt.a2a_algo} degree={mt.degree} comm_bytes={mt.comm_bytes:.0f}", flush=True)
     if only_sharded:
         cases = []
     for c in cases:
