@@ -344,7 +344,7 @@ def run_scenario(sc: Scenario, ranks_materialize_max: int = 64, dtype: str = "f3
                              hidden_dim=d.hidden_dim, tokens_per_step=T, top_k=d.top_k,
                              capacity="fixed", capacity_factor=trace[0], dtype=dtype,
                              adaptive=sc.adaptive, degree=sc.degree if not sc.adaptive else 1,
-                             parallel=sc.parallel)
+                             parallel=sc.parallel, a2a_algo=sc.algo if not sc.adaptive else "linear")
         nid = None
         if W > 1:
             obj = [LayerState.unique_id() if rank == 0 else None]
