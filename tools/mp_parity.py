@@ -69,14 +69,15 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     return ok and t.item() == 0, errs, m
 
 
-def run_sharded(rank, W, dev, s, k, f, M, V, T, bpr, dt, degree, parallel, slices, seed=402):
+def run_sharded(rank, W, dev, s, k, f, M, V, T, bpr, dt, degree, parallel, slices, cap="fixed",
+                seed=402):
     """Sharded placement (W = E*s, moe_layer.cpp:17-108): P1 / P2 / adaptive exchange forms.
     Every rank returns the full gradient of expert rank//s; `slices` loads the weights through
     moe_set_expert_slices (the group all-gathers its slices) after a differently seeded init."""
     E = W // s
     cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
-                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f, bpr=bpr,
-                         dtype=dt, degree=degree, a2a_backend="nccl", parallel=parallel)
+                         hidden_dim=V, tokens_per_step=T, top_k=k, capacity=cap, capacity_factor=f,
+                         bpr=bpr, dtype=dt, degree=degree, a2a_backend="nccl", parallel=parallel)
     obj = [LayerState.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     inp = layer_inputs(seed, W, T, M, V, E, dt)
@@ -94,7 +95,8 @@ def run_sharded(rank, W, dev, s, k, f, M, V, T, bpr, dt, degree, parallel, slice
             res = forward(st, xs)
         g = backward(st, res.saved, dys)
     torch.cuda.synchronize()
-    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, 0, f, bpr)
+    kind = {"fixed": 0, "auto": 1, "bounded": 2}[cap]
+    ref = oracle.layer_step(inp["x"], inp["wg"], inp["w1"], inp["w2"], inp["dy"], W, k, kind, f, bpr)
     sl = slice(rank * T, (rank + 1) * T)
     idxs, loc, gates, cap = st.routing()
     tol = 1e-5 if dt == "f32" else 2e-2
@@ -136,6 +138,8 @@ SHARDED_CASES = [
     (4, 1, 1.0, 256, 1024, 512, False, "bf16", 2, "p2", False),
     (4, 1, 1.0, 128, 256, 300, False, "bf16", 4, "p1", False),
     (2, 1, 1.0, 256, 512, 4096, False, "bf16", 1, "adaptive", False),  # tokens dominate: P1
+    (2, 2, 1.0, 256, 512, 512, True, "bf16", 2, "p2", False, "auto"),   # Auto capacity (all-reduce max)
+    (2, 1, 1.25, 128, 256, 300, False, "bf16", 2, "p1", False, "bounded"),
 ]
 
 
