@@ -234,7 +234,9 @@ inline LayerGrads backward(LayerState& state, const SavedForward& saved, const T
                moe_last_error(state.handle()));
   LayerGrads g;
   g.dx = detail::unpack(dxout, state.config.dtype, dy.shape);
-  const Index nE = d.global_experts / d.world_size, M = d.model_dim, V = d.hidden_dim;
+  // computed experts: E/W, or the one expert rank/s under sharded placement (E < W)
+  const Index nE = d.global_experts < d.world_size ? 1 : d.global_experts / d.world_size;
+  const Index M = d.model_dim, V = d.hidden_dim;
   std::vector<float> w1(static_cast<size_t>(nE * M * V)), w2(static_cast<size_t>(nE * V * M));
   throw_status(moe_get_expert_grads(state.handle(), w1.data(), w2.data()),
                moe_last_error(state.handle()));
