@@ -57,27 +57,85 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: an NVML thread polling every
+    2 ms (nvidia_ml_py), else `nvidia-smi -lms 50` (few samples in a sub-second region)."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
-        self.device = device
+        self.device = self.smi_id(device)
         self.proc = None
+        self.thread = None
+        self.sm, self.mx, self.reasons, self.lines = [], 0.0, set(), []
+
+    @staticmethod
+    def smi_id(local: int) -> str:
+        """nvidia-smi's id of CUDA device `local`: its UUID (robust to CUDA_VISIBLE_DEVICES
+        remapping), else the CUDA_VISIBLE_DEVICES entry, else the index itself."""
+        try:
+            import torch
+            u = str(torch.cuda.get_device_properties(local).uuid)
+            if u:
+                return u if u.startswith("GPU-") else "GPU-" + u
+        except Exception:
+            pass
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if local < len(ids):
+            return ids[local]
+        return str(local)
+
+    def _nvml_start(self) -> bool:
+        try:
+            import threading
+            import pynvml as N
+            N.nvmlInit()
+            h = (N.nvmlDeviceGetHandleByUUID(self.device) if self.device.startswith("GPU-")
+                 else N.nvmlDeviceGetHandleByIndex(int(self.device)))
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons",
+                                  getattr(N, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+            bits = [getattr(N, "nvmlClocksEventReason" + n, getattr(N, "nvmlClocksThrottleReason" + n, 0))
+                    for n in ("HwSlowdown", "HwThermalSlowdown", "SwThermalSlowdown", "SwPowerCap")]
+            self.stop = threading.Event()
+
+            def loop():
+                while not self.stop.is_set():
+                    try:
+                        self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                        r = get_reasons(h) if get_reasons else 0
+                        for name, b in zip(self.NAMES, bits):
+                            if b and r & b:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    self.stop.wait(0.002)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return True
+        except Exception:
+            return False
 
     def __enter__(self):
+        if self._nvml_start():
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50", "-i", str(self.device)],
+                 "-lms", "50", "-i", self.device],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            return
         if self.proc is not None:
             time.sleep(0.06)
             self.proc.terminate()
@@ -87,24 +145,23 @@ class ClockSampler:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            for ln in self.lines:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx = max(self.mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for n, v in zip(self.NAMES, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(n)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.mx or None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 def dist_env():
