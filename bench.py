@@ -439,6 +439,25 @@ def run_gpu(args):
         dispatch_stats.update({"decode_gbs": gbs(dec_bytes, dec_ms), "encode_bwd_gbs": gbs(dec_bytes, ebwd_ms),
                                "decode_frac": (gbs(dec_bytes, dec_ms) or 0) / peaks["hbm"]})
     phases_ms = {n: round(prof[n][0] / args.steps, 4) for n in prof}
+    a2a_stats = None
+    if world > 1:
+        # dispatch (x rows forward, g*dy rows backward) = copy-engine pushes over NVLink: bytes this
+        # rank sends off-GPU per step / the summed spans of its pushes (first block start -> last
+        # block landed, CUDA events on the copy stream, phase pass)
+        cc = -(-cap // max(1, metrics.degree))
+        disp_bytes = 2.0 * (world - 1) * cfg.local_experts * metrics.degree * cc * M * esz
+        xfer_ms = prof["xfer_dispatch"][0] / args.steps
+        a2a_stats = {
+            "transport": args.a2a, "dispatch_bytes_per_step": disp_bytes,
+            "dispatch_xfer_ms_per_step": xfer_ms,
+            "dispatch_gbs": gbs(disp_bytes, xfer_ms) if args.a2a == "peer" else None,
+            "nvlink_peak_gbs": 900.0, "peak_source": "nominal NVLink 5 per direction per GPU",
+            "combine": "fused into the down / dgrad GEMM epilogues (NVLink TMA stores)"
+                       if metrics.fused & 2 else "copy-engine pushes",
+            "note": "dispatch spans overlap the previous part's GEMM; a2a_fwd / a2a_bwd phases are "
+                    "comm-stream spans incl. waits"}
+        if a2a_stats["dispatch_gbs"]:
+            a2a_stats["frac"] = a2a_stats["dispatch_gbs"] / 900.0
 
     # end to end through the host-buffer C ABI (H2D of x, dy and D2H of y, dx every step)
     e2e = None
@@ -502,6 +521,7 @@ def run_gpu(args):
                          "timing": "CUDA events around every GEMM launch over a second K-step "
                                    "pass (the headline value comes from an event-free pass)"},
             "dispatch": dispatch_stats,
+            "a2a": a2a_stats,
             "phases_ms": phases_ms,
             "cpu_baseline": cpu,
             "e2e": e2e,

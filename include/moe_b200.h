@@ -215,8 +215,10 @@ int64_t moe_kernel_launches(const moe_handle* h);
 /* Measured timeline (replaces the simulated Timeline of pipeline.hpp:36-46): when on, every
  * phase is bracketed by CUDA events on the stream it runs on. Phases, in order: gate, encode,
  * gemm_up, gemm_down, decode, decode_bwd, gemm_dgrad_mask, gemm_dgrad, gemm_wgrad1,
- * gemm_wgrad2, encode_bwd, a2a_fwd, a2a_bwd, assign, relu_fixup (MOE_NUM_PHASES). */
-#define MOE_NUM_PHASES 15
+ * gemm_wgrad2, encode_bwd, a2a_fwd, a2a_bwd, assign, relu_fixup, xfer_dispatch, xfer_combine
+ * (MOE_NUM_PHASES). a2a_* span the comm stream's enqueue and waits; xfer_* span only the
+ * copy-engine pushes over NVLink (peer transport), from the push's start to its last block landing. */
+#define MOE_NUM_PHASES 17
 int moe_set_profiling(moe_handle* h, int32_t on);
 /* Per-phase summed milliseconds and interval counts since the last call (synchronizes). */
 int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n);

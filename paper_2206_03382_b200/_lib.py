@@ -20,7 +20,7 @@ CAP_FIXED, CAP_AUTO, CAP_BOUNDED = 0, 1, 2
 
 PHASES = ["gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd", "gemm_dgrad_mask",
           "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2", "encode_bwd", "a2a_fwd", "a2a_bwd",
-          "assign", "relu_fixup"]
+          "assign", "relu_fixup", "xfer_dispatch", "xfer_combine"]
 
 _ERRNAMES = {1: "EINVAL", 2: "ECUDA", 3: "ECOMM", 4: "ESTATE", 5: "ENOMEM"}
 

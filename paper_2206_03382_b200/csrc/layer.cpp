@@ -335,6 +335,10 @@ void Layer::alloc_capacity(int cap) {
       void* bufs[PeerExchange::kChannels] = {recv_.p, ycomb_.p, drecv_.p, dxcomb_.p};
       const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
       peer_ = std::make_unique<PeerExchange>(rank_, W_, comm_, bufs, cert ? rownorm_.p : nullptr);
+      // copy-engine transfer spans (channels 0 / 2 dispatch, 1 / 3 combine) for the profile
+      peer_->probe = [this](int ch, cudaStream_t s, bool begin) {
+        if (prof_ || tl_on_) prof_mark(ch % 2 == 0 ? kPhXferDispatch : kPhXferCombine, begin, s);
+      };
       const char* e = std::getenv("MOE_FUSED_COMBINE");  // =0: copy-engine combine (A/B runs)
       fused_combine_ = !(e && e[0] == '0') && cfg_.dtype == MOE_DTYPE_BF16 && W_ <= kMaxPeers &&
                        M_ % 256 == 0 && V_ % 64 == 0;
@@ -372,8 +376,9 @@ void Layer::prof_mark(int phase, bool begin, cudaStream_t st) {
   if (tl_on_) {
     static const char* names[] = {"gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd",
                                   "gemm_dgrad_mask", "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2",
-                                  "encode_bwd", "a2a_fwd", "a2a_bwd", "assign", "relu_fixup"};
-    tl_mark(std::string(phase < 15 ? names[phase] : "?") + (begin ? " >" : " <") +
+                                  "encode_bwd", "a2a_fwd", "a2a_bwd", "assign", "relu_fixup",
+                                  "xfer_dispatch", "xfer_combine"};
+    tl_mark(std::string(phase < kNumPhases ? names[phase] : "?") + (begin ? " >" : " <") +
                 (st == comm_stream_ ? " [comm]" : ""),
             st);
   }

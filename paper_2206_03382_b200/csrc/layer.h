@@ -52,7 +52,8 @@ int32_t select_parallelism(double local_experts, int64_t gathered_capacity, int6
 // pipeline.hpp:36-46 / pipeline.cpp:68-76, with measured instead of simulated intervals).
 enum Phase : int {
   kPhGate = 0, kPhEncode, kPhUp, kPhDown, kPhDecode, kPhDecodeBwd, kPhDgradMask, kPhDgrad,
-  kPhWgrad1, kPhWgrad2, kPhEncodeBwd, kPhA2aFwd, kPhA2aBwd, kPhAssign, kPhReluFix, kNumPhases
+  kPhWgrad1, kPhWgrad2, kPhEncodeBwd, kPhA2aFwd, kPhA2aBwd, kPhAssign, kPhReluFix,
+  kPhXferDispatch, kPhXferCombine, kNumPhases
 };
 
 class Layer {

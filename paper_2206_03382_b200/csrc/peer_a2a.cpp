@@ -189,6 +189,7 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
   // the (source-symmetric) plan. One stream per destination: the blocks move concurrently, and
   // each peer's ready flag follows its own block.
   ck(cudaEventRecord(ev_in_, copy), "event");
+  if (probe) probe(ch, copy, true);
   for (int i = 0; i < world_; ++i) {
     const int p = (rank_ + i) % world_;
     if (p == rank_ && local_done == nullptr) continue;
@@ -210,6 +211,7 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
   }
   for (int p = 0; p < world_; ++p)
     if (p != rank_ || local_done) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
+  if (probe) probe(ch, copy, false);
 }
 
 
@@ -220,6 +222,7 @@ void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* sr
   if (norm_src && (ch != 0 || !local_norms_)) throw MoeError(MOE_EINVAL, "peer all-to-all: norms");
   if (slot < 0 || slot >= kFlagSlots) throw MoeError(MOE_EINVAL, "peer all-to-all: flag slot");
   ck(cudaEventRecord(ev_in_, copy), "event");
+  if (probe) probe(ch, copy, true);
   for (int i = 1; i < world_; ++i) {  // own rows are written in place by the producing kernel
     const int p = (rank_ + i) % world_;
     cudaStream_t ps = pstreams_[p];
@@ -242,6 +245,7 @@ void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* sr
   }
   for (int p = 0; p < world_; ++p)
     if (p != rank_) ck(cudaStreamWaitEvent(copy, ev_out_[p], 0), "wait");
+  if (probe) probe(ch, copy, false);
 }
 
 FlagWait PeerExchange::ready_wait(int ch, int chunk, uint32_t epoch) const {

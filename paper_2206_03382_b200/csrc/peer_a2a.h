@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "peer_flags.h"
@@ -34,6 +35,9 @@ class PeerExchange {
   static constexpr int kPartSlots = 2;
   static constexpr int kPartSlot0 = kMaxChunks;
   static constexpr int kFlagSlots = kMaxChunks + kPartSlots;
+  // optional profiling hook: called on the copy stream at the start (begin) and end of each
+  // push, so the span covers exactly the concurrent per-destination copies
+  std::function<void(int ch, cudaStream_t copy, bool begin)> probe;
 
   // bufs[ch]: this rank's receive buffer of channel ch (cudaMalloc base pointers).
   // norms (optional): this rank's fp32 per-row receive array of channel 0 (the ReLU certificate's
