@@ -229,7 +229,10 @@ def run_reference(args):
         return 0
     wl = pick_workload(args, world)
     d = layer_dims(wl, world)
-    sample = max(256, d["T"] // 16)
+    # bounded per-step sample so a --steps 50 run stays within a few minutes: 2 048 tokens
+    # (~2.4 s/step at N=1 TGT on 16 host cores); at N=8 (C4, E=64) the per-step cost is dominated
+    # by the E full-size fp64 dW the reference's backward writes (4.3 GB), so 1 024 tokens there
+    sample = 2048 if world < 8 else 1024
     run, threads = prepare_cpu(d, sample)
     for _ in range(args.warmup):
         run()
