@@ -56,6 +56,26 @@ def load_peaks() -> dict:
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="fallback (B200_PROFILING.md)")
 
 
+def fp64_gemm_peak(dev) -> float:
+    """fp64 GEMM TF/s of this GPU (cuBLAS DGEMM, 8192^3, best of 5): the fp32 layer's roofline."""
+    import torch
+    n = 8192
+    a = torch.rand(n, n, dtype=torch.float64, device=dev)
+    b = torch.rand(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region: an NVML thread polling every
     2 ms (nvidia_ml_py), else `nvidia-smi -lms 50` (few samples in a sub-second region)."""
@@ -401,6 +421,15 @@ def run_gpu(args):
 
     # roofline: expert GEMMs (tensor-bound) -- 12 * rows * M * V per step over capacity rows
     peaks = load_peaks()
+    gemm_peak, gemm_bound = peaks["bf16_sus"], "tensor"
+    gemm_peak_src = peaks["source"] + " bf16_tflops_sustained"
+    gemm_kernel = "gemm_bf16_kernel (tcgen05 expert GEMMs, 6 launches/step)"
+    if d["dtype"] == "f32":
+        # fp32 layer: SIMT GEMMs with fp64 accumulation (fp32 products are exact in fp64) -- the
+        # denominator is the fp64 GEMM rate of this GPU, measured here with cuBLAS DGEMM
+        gemm_peak, gemm_bound = fp64_gemm_peak(dev), "fp64"
+        gemm_peak_src = "measured in this run: cuBLAS DGEMM 8192^3, best of 5"
+        gemm_kernel = "gemm_simt_kernel<float> (DFMA expert GEMMs)"
     cap = metrics.capacity
     rows = cfg.local_experts * world * cap  # capacity rows per GPU: dE * (W * dC)
     gemm_flops = 12.0 * rows * M * V
@@ -513,14 +542,14 @@ def run_gpu(args):
                        "a2a": args.a2a if world > 1 else None,
                        "degree": metrics.degree, "adaptive": adaptive,
                        "l2": "per-step working set >1 GiB/GPU >> 126 MB L2 (no flush needed)"},
-            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["bf16_sus"],
+            "roofline": {"bound": gemm_bound, "achieved": achieved_tf, "peak": gemm_peak,
                          "unit": "TFLOP/s",
-                         "frac": achieved_tf / peaks["bf16_sus"] if achieved_tf else None,
+                         "frac": achieved_tf / gemm_peak if achieved_tf else None,
                          "traffic": traffic, "traffic_unit": "bytes per step (6 GEMM launches, ncu)",
-                         "kernel": "gemm_bf16_kernel (tcgen05 expert GEMMs, 6 launches/step)",
+                         "kernel": gemm_kernel,
                          "algorithmic": f"12*rows*M*V per step, rows={rows} capacity rows/GPU",
                          "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,
-                         "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                         "peak_source": gemm_peak_src,
                          "timing": "CUDA events around every GEMM launch over a second K-step "
                                    "pass (the headline value comes from an event-free pass)"},
             "dispatch": dispatch_stats,

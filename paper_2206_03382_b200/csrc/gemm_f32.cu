@@ -9,6 +9,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "gemm_sm100.h"
@@ -130,6 +131,142 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// fp32 layer (C1): the same five kinds on the FP64 tensor cores. fp32 operands are widened to
+// fp64 once, when staged in shared memory, and mma.sync.m8n8k4.f64 (DMMA) accumulates in fp64:
+// products are exact and the sums are fp64, as in gemm_simt_kernel<float>, at the DMMA rate
+// instead of DFMA + per-use F2F conversions. CTA tile 64 x 64 x 16, 8 warps of 32 x 16 (4 m8 x
+// 2 n8 tiles). Global loads run along each operand's contiguous dimension (K for row-major A and
+// K-major B, M / N otherwise). Fragment layout (m8n8k4 .f64): A[r][c] r = lane/4, c = lane%4;
+// B[r][c] r = lane%4, c = lane/4; D[r][2*(lane%4) + i] r = lane/4. Shared rows are padded to
+// 68 doubles: a half-warp's 16 8-byte fragment loads then hit 16 distinct bank pairs.
+constexpr int DM_TM = 64, DM_TN = 64, DM_TK = 16, DM_S = 68;
+
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int kKind>
+__global__ void __launch_bounds__(256)
+    gemm_dmma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                         float* __restrict__ D, GemmArgs a) {
+  __shared__ double As[DM_TK][DM_S];
+  __shared__ double Bs[DM_TK][DM_S];
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const int wm = warp % 2, wn = warp / 2;  // warp tile rows [wm*32, +32), cols [wn*16, +16)
+  const bool rowk = kKind == kGemmWgrad;
+  const int n0 = blockIdx.x * DM_TN;
+  const int m0 = blockIdx.y * DM_TM;
+  int g, seg, rows;
+  if (!rowk) {
+    g = blockIdx.z / a.S;
+    const int s = blockIdx.z % a.S;
+    seg = (a.seg_base + s) * a.G + g;
+    rows = a.seg_rows;
+  } else {
+    g = blockIdx.z;
+    seg = 0;
+    rows = a.Mo;
+  }
+  if (m0 >= rows) return;
+  const int K = rowk ? a.S * a.seg_rows : a.K;
+  const int N = static_cast<int>(a.N);
+  constexpr bool kBk = kKind == kGemmDgradMask || kKind == kGemmDgrad;  // B is [N][K]
+  double acc[4][2][2] = {};
+  for (int k0 = 0; k0 < K; k0 += DM_TK) {
+    for (int i = threadIdx.x; i < DM_TK * DM_TM; i += 256) {
+      int kk, mm;
+      if (!rowk) { kk = i % DM_TK; mm = i / DM_TK; }  // A [rows][K]: K contiguous
+      else { kk = i / DM_TM; mm = i % DM_TM; }        // A [K][Mo]: M contiguous
+      const int k = k0 + kk, m = m0 + mm;
+      float v = 0.0f;
+      if (k < K && m < rows) {
+        if (!rowk) {
+          v = A[(static_cast<size_t>(seg) * a.seg_rows + m) * a.K + k];
+        } else {
+          const int s = k / a.seg_rows, r = k % a.seg_rows;
+          const size_t sg = static_cast<size_t>(a.seg_base + s) * a.G + g;
+          v = A[(sg * a.seg_rows + r) * a.Mo + m];
+        }
+      }
+      As[kk][mm] = static_cast<double>(v);
+    }
+    for (int i = threadIdx.x; i < DM_TK * DM_TN; i += 256) {
+      int kk, nn;
+      if (kBk) { kk = i % DM_TK; nn = i / DM_TK; }
+      else { kk = i / DM_TN; nn = i % DM_TN; }
+      const int k = k0 + kk, n = n0 + nn;
+      float v = 0.0f;
+      if (k < K && n < N) {
+        if (kKind == kGemmUp || kKind == kGemmDown) {
+          v = B[(static_cast<size_t>(g) * a.K + k) * a.N + n];
+        } else if (kBk) {
+          v = B[(static_cast<size_t>(g) * a.N + n) * a.K + k];
+        } else {
+          const int s = k / a.seg_rows, r = k % a.seg_rows;
+          const size_t sg = static_cast<size_t>(a.seg_base + s) * a.G + g;
+          v = B[(sg * a.seg_rows + r) * a.N + n];
+        }
+      }
+      Bs[kk][nn] = static_cast<double>(v);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < DM_TK; k4 += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[k4 + lane % 4][wm * 32 + i * 8 + lane / 4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[k4 + lane % 4][wn * 16 + j * 8 + lane / 4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm * 32 + i * 8 + lane / 4;
+    if (m >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn * 16 + j * 8 + 2 * (lane % 4) + h;
+        if (n >= N) continue;
+        float v = static_cast<float>(acc[i][j][h]);
+        size_t off;
+        if (!rowk)
+          off = (static_cast<size_t>(seg) * a.seg_rows + m) * a.N + n;
+        else
+          off = (static_cast<size_t>(g) * a.Mo + m) * a.N + n;
+        if (kKind == kGemmUp) v = fmaxf(v, 0.0f);
+        if (kKind == kGemmDgradMask) v = static_cast<const float*>(a.aux)[off] > 0.0f ? v : 0.0f;
+        D[off] = v;
+      }
+    }
+  }
+}
+
+int launch_dmma_f32(int kind, const float* A, const float* B, float* D, const GemmArgs& a,
+                    cudaStream_t st) {
+  if (a.row0 || a.nrows || a.skip_seg >= 0 || a.idx_mode) return -1;  // tcgen05-only features
+  const bool rowk = kind == kGemmWgrad;
+  const int rows = rowk ? a.Mo : a.seg_rows;
+  dim3 grid((a.N + DM_TN - 1) / DM_TN, (rows + DM_TM - 1) / DM_TM, rowk ? a.G : a.G * a.S);
+  switch (kind) {
+    case kGemmUp: gemm_dmma_f32_kernel<kGemmUp><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmDown: gemm_dmma_f32_kernel<kGemmDown><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmDgradMask: gemm_dmma_f32_kernel<kGemmDgradMask><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmDgrad: gemm_dmma_f32_kernel<kGemmDgrad><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    case kGemmWgrad: gemm_dmma_f32_kernel<kGemmWgrad><<<grid, 256, 0, st>>>(A, B, D, a); break;
+    default: return -1;
+  }
+  return launch_status();
+}
+
 template <typename T, typename TD>
 int launch_simt(int kind, const T* A, const T* B, TD* D, const GemmArgs& a, cudaStream_t st) {
   if (a.row0 || a.nrows || a.skip_seg >= 0 || a.idx_mode) return -1;  // tcgen05-only features
@@ -151,7 +288,12 @@ int launch_simt(int kind, const T* A, const T* B, TD* D, const GemmArgs& a, cuda
 
 int gemm_f32(int kind, const float* A, const float* B, float* D, const GemmArgs& a,
              cudaStream_t st) {
-  return launch_simt<float, float>(kind, A, B, D, a, st);
+  static const bool simt = [] {
+    const char* e = std::getenv("MOE_F32_SIMT");  // A/B: the DFMA SIMT kernel
+    return e != nullptr && e[0] == '1';
+  }();
+  if (simt) return launch_simt<float, float>(kind, A, B, D, a, st);
+  return launch_dmma_f32(kind, A, B, D, a, st);
 }
 
 // bf16 operands, fp32 accumulation; bf16 output except wgrad (fp32).
