@@ -148,7 +148,7 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
 }
 
 template <int kKind>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     gemm_dmma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B,
                          float* __restrict__ D, GemmArgs a) {
   __shared__ double As[DM_TK][DM_S];
@@ -174,8 +174,13 @@ __global__ void __launch_bounds__(256)
   const int N = static_cast<int>(a.N);
   constexpr bool kBk = kKind == kGemmDgradMask || kKind == kGemmDgrad;  // B is [N][K]
   double acc[4][2][2] = {};
-  for (int k0 = 0; k0 < K; k0 += DM_TK) {
-    for (int i = threadIdx.x; i < DM_TK * DM_TM; i += 256) {
+  // register prefetch: stage k0 + DM_TK is loaded from global while stage k0 runs its DMMAs
+  constexpr int kPer = DM_TK * DM_TM / 256;  // operand elements per thread per stage (4)
+  float ra[kPer], rb[kPer];
+  auto load_stage = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = threadIdx.x + u * 256;
       int kk, mm;
       if (!rowk) { kk = i % DM_TK; mm = i / DM_TK; }  // A [rows][K]: K contiguous
       else { kk = i / DM_TM; mm = i % DM_TM; }        // A [K][Mo]: M contiguous
@@ -183,16 +188,18 @@ __global__ void __launch_bounds__(256)
       float v = 0.0f;
       if (k < K && m < rows) {
         if (!rowk) {
-          v = A[(static_cast<size_t>(seg) * a.seg_rows + m) * a.K + k];
+          v = __ldg(A + (static_cast<size_t>(seg) * a.seg_rows + m) * a.K + k);
         } else {
           const int s = k / a.seg_rows, r = k % a.seg_rows;
           const size_t sg = static_cast<size_t>(a.seg_base + s) * a.G + g;
-          v = A[(sg * a.seg_rows + r) * a.Mo + m];
+          v = __ldg(A + (sg * a.seg_rows + r) * a.Mo + m);
         }
       }
-      As[kk][mm] = static_cast<double>(v);
+      ra[u] = v;
     }
-    for (int i = threadIdx.x; i < DM_TK * DM_TN; i += 256) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = threadIdx.x + u * 256;
       int kk, nn;
       if (kBk) { kk = i % DM_TK; nn = i / DM_TK; }
       else { kk = i / DM_TN; nn = i % DM_TN; }
@@ -200,18 +207,30 @@ __global__ void __launch_bounds__(256)
       float v = 0.0f;
       if (k < K && n < N) {
         if (kKind == kGemmUp || kKind == kGemmDown) {
-          v = B[(static_cast<size_t>(g) * a.K + k) * a.N + n];
+          v = __ldg(B + (static_cast<size_t>(g) * a.K + k) * a.N + n);
         } else if (kBk) {
-          v = B[(static_cast<size_t>(g) * a.N + n) * a.K + k];
+          v = __ldg(B + (static_cast<size_t>(g) * a.N + n) * a.K + k);
         } else {
           const int s = k / a.seg_rows, r = k % a.seg_rows;
           const size_t sg = static_cast<size_t>(a.seg_base + s) * a.G + g;
-          v = B[(sg * a.seg_rows + r) * a.N + n];
+          v = __ldg(B + (sg * a.seg_rows + r) * a.N + n);
         }
       }
-      Bs[kk][nn] = static_cast<double>(v);
+      rb[u] = v;
+    }
+  };
+  load_stage(0);
+  for (int k0 = 0; k0 < K; k0 += DM_TK) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = threadIdx.x + u * 256;
+      if (!rowk) As[i % DM_TK][i / DM_TK] = static_cast<double>(ra[u]);
+      else As[i / DM_TM][i % DM_TM] = static_cast<double>(ra[u]);
+      if (kBk) Bs[i % DM_TK][i / DM_TK] = static_cast<double>(rb[u]);
+      else Bs[i / DM_TN][i % DM_TN] = static_cast<double>(rb[u]);
     }
     __syncthreads();
+    if (k0 + DM_TK < K) load_stage(k0 + DM_TK);
 #pragma unroll
     for (int k4 = 0; k4 < DM_TK; k4 += 4) {
       double af[4], bf[2];
