@@ -134,12 +134,12 @@ __global__ void __launch_bounds__(256)
 // fp32 layer (C1): the same five kinds on the FP64 tensor cores. fp32 operands are widened to
 // fp64 once, when staged in shared memory, and mma.sync.m8n8k4.f64 (DMMA) accumulates in fp64:
 // products are exact and the sums are fp64, as in gemm_simt_kernel<float>, at the DMMA rate
-// instead of DFMA + per-use F2F conversions. CTA tile 64 x 64 x 16, 8 warps of 32 x 16 (4 m8 x
+// instead of DFMA + per-use F2F conversions. CTA tile 64 x 64 x 32, 8 warps of 32 x 16 (4 m8 x
 // 2 n8 tiles). Global loads run along each operand's contiguous dimension (K for row-major A and
 // K-major B, M / N otherwise). Fragment layout (m8n8k4 .f64): A[r][c] r = lane/4, c = lane%4;
 // B[r][c] r = lane%4, c = lane/4; D[r][2*(lane%4) + i] r = lane/4. Shared rows are padded to
 // 68 doubles: a half-warp's 16 8-byte fragment loads then hit 16 distinct bank pairs.
-constexpr int DM_TM = 64, DM_TN = 64, DM_TK = 16, DM_S = 68;
+constexpr int DM_TM = 64, DM_TN = 64, DM_TK = 32, DM_S = 68;
 
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
