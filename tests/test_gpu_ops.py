@@ -106,6 +106,8 @@ GATING_CASES = [
     (1, 32768, 1024, 32, 1, "fixed", 1.0, False, "bf16"),  # TGT routing
     (1, 32768, 1024, 32, 2, "fixed", 1.25, True, "bf16"),  # C3 routing (top-2 + BPR)
     (1, 7, 5, 3, 3, "fixed", 1.0, True, "f32"),           # k = E, tiny, ragged
+    (2, 4096, 32, 2, 2, "fixed", 0.5, True, "f32"),       # BPR lists of exactly 4096 (sort width)
+    (1, 20000, 32, 2, 1, "fixed", 0.8, True, "f32"),      # BPR lists > 8192: pairwise fallback
 ]
 
 
