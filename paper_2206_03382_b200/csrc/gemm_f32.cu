@@ -134,12 +134,30 @@ __global__ void __launch_bounds__(256)
 // fp32 layer (C1): the same five kinds on the FP64 tensor cores. fp32 operands are widened to
 // fp64 once, when staged in shared memory, and mma.sync.m8n8k4.f64 (DMMA) accumulates in fp64:
 // products are exact and the sums are fp64, as in gemm_simt_kernel<float>, at the DMMA rate
-// instead of DFMA + per-use F2F conversions. CTA tile 64 x 64 x 32, 8 warps of 32 x 16 (4 m8 x
+// instead of DFMA + per-use F2F conversions. CTA tile 64 x 64 x 16, 8 warps of 32 x 16 (4 m8 x
 // 2 n8 tiles). Global loads run along each operand's contiguous dimension (K for row-major A and
 // K-major B, M / N otherwise). Fragment layout (m8n8k4 .f64): A[r][c] r = lane/4, c = lane%4;
 // B[r][c] r = lane%4, c = lane/4; D[r][2*(lane%4) + i] r = lane/4. Shared rows are padded to
 // 68 doubles: a half-warp's 16 8-byte fragment loads then hit 16 distinct bank pairs.
-constexpr int DM_TM = 64, DM_TN = 64, DM_TK = 32, DM_S = 68;
+// Tile sweep at C1 (ms/step): 64x64x16, 3 CTAs/SM 2.43; 64x64x32, 2/SM 2.52-2.55; 64x64x32 3/SM
+// 2.52; 32x64x32 4/SM 2.67; 64x128x16 1/SM 2.95; 128x128x16 1/SM 2.73 -- occupancy hides the
+// DMMA / shared-memory latencies better than per-warp operand reuse.
+#ifndef MOE_F32_WMT
+#define MOE_F32_WMT 4  // m8 tiles per warp (warps are 2 along M x 4 along N)
+#endif
+#ifndef MOE_F32_WNT
+#define MOE_F32_WNT 2  // n8 tiles per warp
+#endif
+#ifndef MOE_F32_TK
+#define MOE_F32_TK 16
+#endif
+#ifndef MOE_F32_MINB
+#define MOE_F32_MINB 3
+#endif
+constexpr int DM_WMT = MOE_F32_WMT, DM_WNT = MOE_F32_WNT;
+constexpr int DM_TM = 2 * 8 * DM_WMT, DM_TN = 4 * 8 * DM_WNT, DM_TK = MOE_F32_TK;
+constexpr int DM_SA = DM_TM + 4, DM_SB = DM_TN + 4;  // padded rows: == 4 (mod 16) doubles
+static_assert(DM_TK * DM_TM % 256 == 0 && DM_TK * DM_TN % 256 == 0, "stage / thread split");
 
 __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -148,13 +166,13 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
 }
 
 template <int kKind>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, MOE_F32_MINB)
     gemm_dmma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B,
                          float* __restrict__ D, GemmArgs a) {
-  __shared__ double As[DM_TK][DM_S];
-  __shared__ double Bs[DM_TK][DM_S];
+  __shared__ double As[DM_TK][DM_SA];
+  __shared__ double Bs[DM_TK][DM_SB];
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  const int wm = warp % 2, wn = warp / 2;  // warp tile rows [wm*32, +32), cols [wn*16, +16)
+  const int wm = warp % 2, wn = warp / 2;  // warp tile rows [wm*8*WMT, +8*WMT), cols [wn*8*WNT, ...)
   const bool rowk = kKind == kGemmWgrad;
   const int n0 = blockIdx.x * DM_TN;
   const int m0 = blockIdx.y * DM_TM;
@@ -173,10 +191,10 @@ __global__ void __launch_bounds__(256, 2)
   const int K = rowk ? a.S * a.seg_rows : a.K;
   const int N = static_cast<int>(a.N);
   constexpr bool kBk = kKind == kGemmDgradMask || kKind == kGemmDgrad;  // B is [N][K]
-  double acc[4][2][2] = {};
+  double acc[DM_WMT][DM_WNT][2] = {};
   // register prefetch: stage k0 + DM_TK is loaded from global while stage k0 runs its DMMAs
-  constexpr int kPer = DM_TK * DM_TM / 256;  // operand elements per thread per stage (4)
-  float ra[kPer], rb[kPer];
+  constexpr int kPer = DM_TK * DM_TM / 256, kPerB = DM_TK * DM_TN / 256;  // per thread per stage
+  float ra[kPer], rb[kPerB];
   auto load_stage = [&](int k0) {
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -198,7 +216,7 @@ __global__ void __launch_bounds__(256, 2)
       ra[u] = v;
     }
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
+    for (int u = 0; u < kPerB; ++u) {
       const int i = threadIdx.x + u * 256;
       int kk, nn;
       if (kBk) { kk = i % DM_TK; nn = i / DM_TK; }
@@ -226,6 +244,10 @@ __global__ void __launch_bounds__(256, 2)
       const int i = threadIdx.x + u * 256;
       if (!rowk) As[i % DM_TK][i / DM_TK] = static_cast<double>(ra[u]);
       else As[i / DM_TM][i % DM_TM] = static_cast<double>(ra[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kPerB; ++u) {
+      const int i = threadIdx.x + u * 256;
       if (kBk) Bs[i % DM_TK][i / DM_TK] = static_cast<double>(rb[u]);
       else Bs[i / DM_TN][i % DM_TN] = static_cast<double>(rb[u]);
     }
@@ -233,27 +255,27 @@ __global__ void __launch_bounds__(256, 2)
     if (k0 + DM_TK < K) load_stage(k0 + DM_TK);
 #pragma unroll
     for (int k4 = 0; k4 < DM_TK; k4 += 4) {
-      double af[4], bf[2];
+      double af[DM_WMT], bf[DM_WNT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[k4 + lane % 4][wm * 32 + i * 8 + lane / 4];
+      for (int i = 0; i < DM_WMT; ++i) af[i] = As[k4 + lane % 4][wm * 8 * DM_WMT + i * 8 + lane / 4];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[k4 + lane % 4][wn * 16 + j * 8 + lane / 4];
+      for (int j = 0; j < DM_WNT; ++j) bf[j] = Bs[k4 + lane % 4][wn * 8 * DM_WNT + j * 8 + lane / 4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < DM_WMT; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < DM_WNT; ++j) dmma_f64(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + wm * 32 + i * 8 + lane / 4;
+  for (int i = 0; i < DM_WMT; ++i) {
+    const int m = m0 + wm * 8 * DM_WMT + i * 8 + lane / 4;
     if (m >= rows) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < DM_WNT; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int n = n0 + wn * 16 + j * 8 + 2 * (lane % 4) + h;
+        const int n = n0 + wn * 8 * DM_WNT + j * 8 + 2 * (lane % 4) + h;
         if (n >= N) continue;
         float v = static_cast<float>(acc[i][j][h]);
         size_t off;
