@@ -225,6 +225,9 @@ def prepare_cpu(d: dict, sample_tokens: int):
     x = rng.round_dtype(rng.uniform(SEED, off["x"], T * M), d["dtype"]).reshape(T, M)
     dy = rng.round_dtype(rng.uniform(SEED, off["x"] + T * M, T * M), d["dtype"]).reshape(T, M)
 
+    # every host core: torchrun sets OMP_NUM_THREADS=1 per rank, but only rank 0 runs this leg
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
+
     def run():
         oracle.layer_step(x, wg, w1, w2, dy, 1, k, 0, f, d["bpr"])
     return run, oracle.num_threads()

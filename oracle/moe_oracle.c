@@ -570,3 +570,7 @@ int64_t orc_layer_step(const double* x, const double* wg, const double* w1, cons
 }
 
 int32_t orc_num_threads(void) { return (int32_t)omp_get_max_threads(); }
+
+/* bench.py's reference arm runs on rank 0 only; torchrun exports OMP_NUM_THREADS=1 to every
+   rank, so the arm raises the pool back to the host's cores here. */
+void orc_set_num_threads(int32_t n) { if (n > 0) omp_set_num_threads(n); }

@@ -117,6 +117,7 @@ int64_t orc_layer_step(const double* x, const double* wg, const double* w1, cons
 
 /* Number of OpenMP threads the oracle uses (for the CPU-baseline "cores" field). */
 int32_t orc_num_threads(void);
+void orc_set_num_threads(int32_t n);
 
 #ifdef __cplusplus
 }

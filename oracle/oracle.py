@@ -72,6 +72,10 @@ def num_threads() -> int:
     return int(lib().orc_num_threads())
 
 
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(C.c_int32(n))
+
+
 def fill_uniform(seed: int, offset: int, n: int, lo: float, hi: float) -> np.ndarray:
     out = np.empty(n, np.float64)
     lib().orc_fill_uniform(C.c_uint64(seed), C.c_uint64(offset), I64(n), D(lo), D(hi), _p(out))
