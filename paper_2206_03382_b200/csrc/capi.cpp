@@ -19,7 +19,7 @@ struct moe_handle {
 };
 
 struct moe_memo {
-  moe::StrategyMemo memo;
+  moe::StrategySearch search;
 };
 
 namespace {
@@ -628,7 +628,7 @@ int moe_op_fill_uniform(void* dst, int32_t dtype, int64_t n, uint64_t seed, uint
 int moe_memo_create(double bucket_length, moe_memo** out) {
   return guard(nullptr, [&] {
     auto m = std::make_unique<moe_memo>();
-    m->memo.bucket_length = bucket_length;
+    m->search = moe::StrategySearch(bucket_length);
     *out = m.release();
   });
 }
@@ -637,46 +637,32 @@ int moe_memo_destroy(moe_memo* m) {
   return MOE_OK;
 }
 int moe_memo_get_strategy(moe_memo* m, double f, int32_t* s) {
-  return guard(nullptr, [&] { *s = moe::strategy_index(moe::get_strategy(m->memo, f)); });
+  return guard(nullptr, [&] { *s = m->search.choose(f); });
 }
 int moe_memo_optimize_strategy(moe_memo* m, double f, int32_t s, double seconds) {
-  return guard(nullptr, [&] {
-    const auto& sp = moe::strategy_space();
-    if (s < 0 || s >= static_cast<int32_t>(sp.size())) throw moe::MoeError(MOE_EINVAL, "strategy");
-    moe::optimize_strategy(m->memo, f, sp[s], seconds);
-  });
+  return guard(nullptr, [&] { m->search.record(f, s, seconds); });
 }
 int moe_memo_recompute_buckets(moe_memo* m, double f) {
-  return guard(nullptr, [&] { moe::recompute_buckets(m->memo, f); });
+  return guard(nullptr, [&] { m->search.rebucket(f); });
 }
 int moe_memo_num_buckets(moe_memo* m, int64_t* n) {
-  return guard(nullptr, [&] { *n = static_cast<int64_t>(m->memo.buckets.size()); });
+  return guard(nullptr, [&] { *n = m->search.num_buckets(); });
 }
 int moe_memo_bucket(moe_memo* m, int64_t i, double* start, int64_t* n_members, double* members,
                     int64_t max_members, double* table8) {
   return guard(nullptr, [&] {
-    if (i < 0 || i >= static_cast<int64_t>(m->memo.buckets.size()))
-      throw moe::MoeError(MOE_EINVAL, "bucket index");
-    const auto& b = m->memo.buckets[i];
-    *start = b.start;
-    *n_members = static_cast<int64_t>(b.members.size());
-    for (int64_t j = 0; j < *n_members && j < max_members; ++j) members[j] = b.members[j];
-    for (int s = 0; s < 8; ++s) {
-      auto it = b.table.find(s);
-      table8[s] = it == b.table.end() ? std::numeric_limits<double>::quiet_NaN() : it->second;
-    }
+    if (i < 0 || i >= m->search.num_buckets()) throw moe::MoeError(MOE_EINVAL, "bucket index");
+    const int b = static_cast<int>(i);
+    *start = m->search.bucket_start(b);
+    const auto mem = m->search.bucket_members(b);
+    *n_members = static_cast<int64_t>(mem.size());
+    for (int64_t j = 0; j < *n_members && j < max_members; ++j) members[j] = mem[j];
+    const double* t = m->search.bucket_times(b);
+    for (int s = 0; s < moe::kNumStrategies; ++s) table8[s] = t[s];
   });
 }
 int moe_memo_lookup(moe_memo* m, double f, int32_t s, double* seconds, int32_t* present) {
-  return guard(nullptr, [&] {
-    *present = 0;
-    auto it = m->memo.per_f.find(f);
-    if (it == m->memo.per_f.end()) return;
-    auto jt = it->second.find(s);
-    if (jt == it->second.end()) return;
-    *present = 1;
-    *seconds = jt->second;
-  });
+  return guard(nullptr, [&] { *present = m->search.lookup(f, s, seconds) ? 1 : 0; });
 }
 
 }  // extern "C"

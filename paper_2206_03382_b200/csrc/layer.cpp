@@ -185,7 +185,7 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   k_ = static_cast<int>(cfg.top_k);
   esz_ = cfg.dtype == MOE_DTYPE_BF16 ? 2 : 4;
   if (rank < 0 || rank >= W_) throw MoeError(MOE_EINVAL, "rank out of range");
-  if (cfg.gpus_per_node == cfg.world_size) memo_.allowed = {0, 1, 2, 3};  // linear x {1,2,4,8}
+  if (cfg.gpus_per_node == cfg.world_size) search_.restrict_to({0, 1, 2, 3});  // linear x {1,2,4,8}
   // Fixed: the formula; Bounded: its formula at max_factor bounds every step; Auto: start at the
   // f = 1 capacity and grow (collectively) when a step's max demand exceeds the allocation.
   if (cfg.capacity_kind == MOE_CAP_AUTO)
@@ -1084,7 +1084,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   prof_mark(kPhGate, false, st);
   f_ = static_cast<double>(cap_) * E_ / (static_cast<double>(k_) * T_);  // capacity_to_factor
-  strategy_ = cfg_.adaptive ? get_strategy(memo_, f_) : Strategy{cfg_.a2a_algo, cfg_.degree};
+  strategy_ = cfg_.adaptive ? strategy_at(search_.choose(f_)) : Strategy{cfg_.a2a_algo, cfg_.degree};
   // 2DH degenerates to the linear algorithm inside one NVSwitch domain (collectives.cpp:58-88
   // with m == W); it is executed as linear and reported as chosen.
   degree_ = W_ == 1 ? 1 : strategy_.degree;
@@ -1390,15 +1390,15 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   // The first execution of a (f, strategy) pair is not recorded: it pays one-off costs (lazy
   // loading of the kernel instantiations only that degree uses, first touches) that the
   // reference's simulated seconds never see, and a single cold sample would decide the argmin.
-  if (cfg_.adaptive && !strategy_settled(memo_, f_)) {
-    const auto key = std::make_pair(f_, strategy_index(strategy_));
+  if (cfg_.adaptive && !search_.settled(f_)) {
+    const auto key = std::make_pair(f_, strategy_id(strategy_));
     if (!warm_.insert(key).second) {
       ck(cudaEventSynchronize(ev_fwd_end_), "event sync");
       float ms = 0.0f;
       ck(cudaEventElapsedTime(&ms, ev_fwd_start_, ev_fwd_end_), "elapsed");
       double sec = ms * 1e-3;
       if (W_ > 1) sec = allreduce_max_host(sec);
-      optimize_strategy(memo_, f_, strategy_, sec);
+      search_.record(f_, strategy_id(strategy_), sec);
     }
   }
 }

@@ -139,7 +139,7 @@ class Layer {
   int num_sms_ = 148;
   double f_ = 1.0;
   Strategy strategy_;
-  StrategyMemo memo_;
+  StrategySearch search_;
   std::set<std::pair<double, int>> warm_;  // (f, strategy) pairs executed once (not recorded)
   bool fwd_done_ = false, metrics_valid_ = false;
   int64_t launches_ = 0, bwd_launches_ = 0;
