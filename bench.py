@@ -424,15 +424,19 @@ def run_gpu(args):
 
     # roofline: expert GEMMs (tensor-bound) -- 12 * rows * M * V per step over capacity rows
     peaks = load_peaks()
-    gemm_peak, gemm_bound = peaks["bf16_sus"], "tensor"
-    gemm_peak_src = peaks["source"] + " bf16_tflops_sustained"
+    # event-timed ~0.2 ms kernels: the burst peak is the denominator (B200_PROFILING.md); the
+    # sustained-peak fraction is reported beside it
+    gemm_peak, gemm_bound = peaks["bf16"], "tensor"
+    gemm_peak_sus = peaks["bf16_sus"]
+    gemm_peak_src = peaks["source"] + " bf16_tflops (burst); frac_sustained uses bf16_tflops_sustained"
     gemm_kernel = "gemm_bf16_kernel (tcgen05 expert GEMMs, 6 launches/step)"
     if d["dtype"] == "f32":
         # fp32 layer: SIMT GEMMs with fp64 accumulation (fp32 products are exact in fp64) -- the
         # denominator is the fp64 GEMM rate of this GPU, measured here with cuBLAS DGEMM
         gemm_peak, gemm_bound = fp64_gemm_peak(dev), "fp64"
+        gemm_peak_sus = gemm_peak
         gemm_peak_src = "measured in this run: cuBLAS DGEMM 8192^3, best of 5"
-        gemm_kernel = "gemm_simt_kernel<float> (DFMA expert GEMMs)"
+        gemm_kernel = "gemm_dmma_f32_kernel (DMMA fp64-accumulated fp32 expert GEMMs)"
     cap = metrics.capacity
     rows = cfg.local_experts * world * cap  # capacity rows per GPU: dE * (W * dC)
     gemm_flops = 12.0 * rows * M * V
@@ -441,6 +445,9 @@ def run_gpu(args):
     gemm_ms = sum(prof[n][0] for n in gemm_names) / args.steps
     gemm_launches = sum(prof[n][1] for n in gemm_names) / args.steps
     achieved_tf = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    # algorithmic GEMM operand bytes per step: each of the 6 GEMMs reads its two operands and
+    # writes its output once (rows x M / rows x V activations in the layer dtype, weights, fp32 dW)
+    alg_bytes = float(rows * (M + V) * esz * 6 + cfg.local_experts * M * V * (esz * 4 + 4 * 2))
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
@@ -548,7 +555,14 @@ def run_gpu(args):
             "roofline": {"bound": gemm_bound, "achieved": achieved_tf, "peak": gemm_peak,
                          "unit": "TFLOP/s",
                          "frac": achieved_tf / gemm_peak if achieved_tf else None,
-                         "traffic": traffic, "traffic_unit": "bytes per step (6 GEMM launches, ncu)",
+                         "frac_sustained": achieved_tf / gemm_peak_sus if achieved_tf else None,
+                         "traffic": traffic / 6.0 if traffic else None,
+                         "traffic_unit": "DRAM bytes per GEMM launch (mean of the 6 launches of a step)",
+                         "traffic_per_step": traffic,
+                         "traffic_source": "static: profiles/ncu_traffic.json (dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum from one ncu --set full capture of "
+                                           "this workload; not re-measured in this run)" if traffic else None,
+                         "algorithmic_bytes_per_step": alg_bytes,
                          "kernel": gemm_kernel,
                          "algorithmic": f"12*rows*M*V per step, rows={rows} capacity rows/GPU",
                          "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_launches,

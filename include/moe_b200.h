@@ -208,8 +208,16 @@ int moe_get_expert_grads(moe_handle* h, float* dw1_host, float* dw2_host);
  * [E][M][V/W], w2_slices [E][V/W][M]. Collective across ranks (NCCL); synchronizes `stream`.
  * Sharded placement: this rank's slice rank%s of expert rank/s, [1][M][V/s] and [1][V/s][M]. */
 int moe_get_expert_grad_slices(moe_handle* h, float* w1_slices, float* w2_slices, void* stream);
-/* Device pointer to local expert weights in the layer dtype: which=1 -> w1, 2 -> w2. */
+/* Device pointer to local expert weights in the layer dtype: which=1 -> w1, 2 -> w2 (layouts
+ * [E/W][M][V] / [E/W][V][M]). The pointer is writable (an on-device optimizer step updates the
+ * weights in place): handing it out marks the layer's derived weight state (the ReLU
+ * certificate's W1^T copy and column norms, the sharded W1 slice) stale, and a caller that keeps
+ * the pointer and writes through it later must call moe_weights_updated before the next
+ * forward. Writes must be ordered before that forward's stream work. */
 int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr);
+/* Declare that the resident expert weights changed (in place, through moe_get_weights_device):
+ * the next forward rebuilds the state derived from them. Cheap; no device work until then. */
+int moe_weights_updated(moe_handle* h);
 /* Number of kernels launched by the last forward + backward (benchmark bookkeeping). */
 int64_t moe_kernel_launches(const moe_handle* h);
 /* Measured timeline (replaces the simulated Timeline of pipeline.hpp:36-46): when on, every

@@ -514,6 +514,87 @@ void orc_frozen_plan_forward(const double* x, int64_t Ttot, int64_t M, int64_t V
   }
 }
 
+/* The backward of the frozen plan, token by token (moe_layer.cpp:246-319 restricted to the listed
+ * tokens): dz = g[t,j] * dy[t] (fast_decode_backward, dispatch.cpp:136-157), the expert's
+ * dX row = ((dz . W2^T) * [x W1 > 0]) . W1^T (expert_ffn_backward, parallelism.cpp:123-147),
+ * summed over kept j (fast_encode_backward, dispatch.cpp:117-128). Rows are independent, so
+ * a token subset of a large layer is checked exactly. */
+void orc_frozen_plan_backward_rows(const double* x, const double* dy, int64_t Tsel, int64_t M,
+                                   int64_t V, int64_t k, const int64_t* idxs,
+                                   const int64_t* locations, const double* gates, const double* w1,
+                                   const double* w2, double* dx) {
+#pragma omp parallel
+  {
+    double* hid = (double*)malloc(sizeof(double) * (size_t)V);
+    double* dh = (double*)malloc(sizeof(double) * (size_t)V);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t t = 0; t < Tsel; ++t) {
+      double* dr = dx + t * M;
+      for (int64_t m = 0; m < M; ++m) dr[m] = 0.0;
+      for (int64_t j = 0; j < k; ++j) {
+        if (locations[t * k + j] < 0) continue;
+        const int64_t e = idxs[t * k + j];
+        const double* W1 = w1 + e * M * V;
+        const double* W2 = w2 + e * V * M;
+        const double g = gates[t * k + j];
+        for (int64_t v = 0; v < V; ++v) hid[v] = 0.0;
+        for (int64_t m = 0; m < M; ++m) {
+          const double xv = x[t * M + m];
+          for (int64_t v = 0; v < V; ++v) hid[v] += xv * W1[m * V + v];
+        }
+        for (int64_t v = 0; v < V; ++v) {
+          double a = 0.0;
+          if (hid[v] > 0.0)
+            for (int64_t m = 0; m < M; ++m) a += g * dy[t * M + m] * W2[v * M + m];
+          dh[v] = a;
+        }
+        for (int64_t m = 0; m < M; ++m) {
+          double a = 0.0;
+          for (int64_t v = 0; v < V; ++v) a += dh[v] * W1[m * V + v];
+          dr[m] += a;
+        }
+      }
+    }
+    free(hid);
+    free(dh);
+  }
+}
+
+/* Selected hidden units of one expert's weight gradient (expert_ffn_backward,
+ * parallelism.cpp:123-147): with h = X W1, dh = (dZ W2^T) * [h > 0], column v of dW1 = X^T dh
+ * and row v of dW2 = relu(h)^T dZ need only column v of h and dh, so a few units of a large
+ * expert are exact. X, dZ: the expert's (rows, M) inputs and output gradients (gate-scaled,
+ * all source ranks, empty capacity slots omitted -- they contribute zero).
+ * Outputs dw1c (M, ncols) = dW1[:, cols], dw2r (ncols, M) = dW2[cols, :]. */
+void orc_expert_backward_columns(const double* X, const double* dZ, int64_t rows, int64_t M,
+                                 int64_t V, const double* w1, const double* w2, int64_t ncols,
+                                 const int64_t* cols, double* dw1c, double* dw2r) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t c = 0; c < ncols; ++c) {
+    const int64_t v = cols[c];
+    double* a1 = (double*)calloc((size_t)M, sizeof(double));
+    double* a2 = (double*)calloc((size_t)M, sizeof(double));
+    for (int64_t r = 0; r < rows; ++r) {
+      const double* xr = X + r * M;
+      const double* dr = dZ + r * M;
+      double h = 0.0, da = 0.0;
+      for (int64_t m = 0; m < M; ++m) h += xr[m] * w1[m * V + v];
+      if (!(h > 0.0)) continue; /* a = 0 and dh = 0: the row adds nothing */
+      for (int64_t m = 0; m < M; ++m) da += dr[m] * w2[v * M + m];
+      for (int64_t m = 0; m < M; ++m) {
+        a1[m] += xr[m] * da;
+        a2[m] += h * dr[m];
+      }
+    }
+    for (int64_t m = 0; m < M; ++m) {
+      dw1c[m * ncols + c] = a1[m];
+      dw2r[c * M + m] = a2[m];
+    }
+    free(a1);
+    free(a2);
+  }
+}
+
 /* ------------------------------------------------------------------ moe_layer.cpp:171-319 */
 /* moe_layer.cpp:171-319 from the router's probabilities (route_probabilities, :165-169). */
 int64_t orc_layer_step_probs(const double* x, const double* probs, const double* w1,

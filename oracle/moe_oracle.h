@@ -100,6 +100,16 @@ void orc_frozen_plan_forward(const double* x, int64_t Ttot, int64_t M, int64_t V
                              const int64_t* idxs, const int64_t* locations, const double* gates,
                              const double* w1, const double* w2, double* y);
 
+/* Frozen-plan backward of selected tokens (moe_layer.cpp:246-319): dx rows (Tsel, M). */
+void orc_frozen_plan_backward_rows(const double* x, const double* dy, int64_t Tsel, int64_t M,
+                                   int64_t V, int64_t k, const int64_t* idxs,
+                                   const int64_t* locations, const double* gates, const double* w1,
+                                   const double* w2, double* dx);
+/* Selected hidden units of one expert's dW1 columns / dW2 rows (parallelism.cpp:123-147). */
+void orc_expert_backward_columns(const double* X, const double* dZ, int64_t rows, int64_t M,
+                                 int64_t V, const double* w1, const double* w2, int64_t ncols,
+                                 const int64_t* cols, double* dw1c, double* dw2r);
+
 /* Whole layer for W source blocks on one host (moe_layer.cpp:171-319, per-rank placement,
  * linear router): gate -> encode -> per-expert FFN over the gathered capacity rows -> decode,
  * and the reverse pass (gates frozen; d_gates discarded). w1 (E,M,V), w2 (E,V,M).

@@ -273,6 +273,32 @@ def frozen_plan_forward(x, k, idxs, locations, gates, w1, w2):
     return y
 
 
+def frozen_plan_backward_rows(x, dy, k, idxs, locations, gates, w1, w2):
+    """dx of the listed tokens under a frozen plan (moe_layer.cpp:246-319); rows independent."""
+    x, dy, w1, w2 = _f64(x), _f64(dy), _f64(w1), _f64(w2)
+    T, M = x.shape
+    V = w1.shape[2]
+    dx = np.empty_like(x)
+    lib().orc_frozen_plan_backward_rows(_p(x), _p(dy), I64(T), I64(M), I64(V), I64(k),
+                                        _p(_i64(idxs)), _p(_i64(locations)), _p(_f64(gates)),
+                                        _p(w1), _p(w2), _p(dx))
+    return dx
+
+
+def expert_backward_columns(X, dZ, w1, w2, cols):
+    """dW1[:, cols] (M, n) and dW2[cols, :] (n, M) of one expert from its rows (X, dZ)."""
+    X, dZ, w1, w2 = _f64(X), _f64(dZ), _f64(w1), _f64(w2)
+    rows, M = X.shape
+    V = w1.shape[1]
+    cols = _i64(cols)
+    n = cols.shape[0]
+    dw1c = np.empty((M, n), np.float64)
+    dw2r = np.empty((n, M), np.float64)
+    lib().orc_expert_backward_columns(_p(X), _p(dZ), I64(rows), I64(M), I64(V), _p(w1), _p(w2),
+                                      I64(n), _p(cols), _p(dw1c), _p(dw2r))
+    return dw1c, dw2r
+
+
 def layer_step(x, wg, w1, w2, dy, W, k, cap_kind=0, factor=1.0, bpr=False, cosine=None):
     """Whole layer over W source blocks; returns dict of y, routing and (if dy) dx, dw1, dw2.
     cosine = (proj (M, D), experts (E, D), temperature) selects RouterKind::Cosine."""

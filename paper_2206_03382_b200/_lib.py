@@ -85,6 +85,7 @@ SIGNATURES = {
     "moe_get_metrics": (I32, [P, C.POINTER(StepMetrics)]),
     "moe_get_expert_grads": (I32, [P, P, P]),
     "moe_get_weights_device": (I32, [P, I32, C.POINTER(P)]),
+    "moe_weights_updated": (I32, [P]),
     "moe_get_expert_grad_slices": (I32, [P, P, P, P]),
     "moe_kernel_launches": (I64, [P]),
     "moe_set_profiling": (I32, [P, I32]),

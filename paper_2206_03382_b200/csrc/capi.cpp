@@ -336,8 +336,10 @@ int moe_get_weights_device(moe_handle* h, int32_t which, void** ptr) {
     if (which == 1) *ptr = h->layer->w1();
     else if (which == 2) *ptr = h->layer->w2();
     else throw moe::MoeError(MOE_EINVAL, "which must be 1 or 2");
+    h->layer->weights_updated();  // the caller may write through it
   });
 }
+int moe_weights_updated(moe_handle* h) { LAYER_CALL(h, h->layer->weights_updated()); }
 int64_t moe_kernel_launches(const moe_handle* h) { return h ? h->layer->launches() : 0; }
 int moe_set_profiling(moe_handle* h, int32_t on) { LAYER_CALL(h, h->layer->set_profiling(on != 0)); }
 int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n) {

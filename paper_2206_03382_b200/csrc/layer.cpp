@@ -286,8 +286,9 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
     colnorm_.alloc(sizeof(float) * dE_ * V_);
     colnorm_blk_.alloc(sizeof(float) * dE_ * (V_ / 64 + 1));
     w1t_.alloc(static_cast<size_t>(esz_) * dE_ * M_ * V_);
-    fix_count_.alloc(3 * sizeof(unsigned int));  // list size, fixup CTAs done, last list size
-    ck(cudaMemset(fix_count_.p, 0, 3 * sizeof(unsigned int)), "memset");
+    // list size, fixup CTAs done, last list size, largest list since the last metrics read
+    fix_count_.alloc(4 * sizeof(unsigned int));
+    ck(cudaMemset(fix_count_.p, 0, 4 * sizeof(unsigned int)), "memset");
   }
   if (W_ > 1 && cfg.a2a_backend != MOE_A2A_BACKEND_PEER && cfg.a2a_backend != MOE_A2A_BACKEND_NCCL)
     throw MoeError(MOE_EINVAL, "unknown all-to-all backend");
@@ -1862,19 +1863,24 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->fused = (fused_ ? MOE_FUSED_DECODE : 0) | (peer_ && fused_combine_ ? MOE_FUSED_COMBINE : 0);
   m->parallel = parallel_;
   if (cfg_.dtype == MOE_DTYPE_BF16) {
-    unsigned int nfix = 0;  // the last fixup's list size (relu_fixup_kernel keeps it in [2])
-    ck(cudaMemcpy(&nfix, static_cast<unsigned int*>(fix_count_.p) + 2, 4, cudaMemcpyDeviceToHost), "copy");
-    m->relu_fixups = nfix;
-    if (nfix > fix_cap_) throw MoeError(MOE_ESTATE, "ReLU-mask certificate list overflowed");
+    // [2]: the last fixup's list size; [3]: the largest list of any fixup since the last read
+    // (an overflow in an earlier chunk or source range must not be masked by a later one)
+    unsigned int c[2] = {0u, 0u};
+    ck(cudaMemcpy(c, static_cast<unsigned int*>(fix_count_.p) + 2, 8, cudaMemcpyDeviceToHost), "copy");
+    ck(cudaMemset(static_cast<unsigned int*>(fix_count_.p) + 3, 0, 4), "memset");
+    m->relu_fixups = c[0];
+    if (c[1] > fix_cap_) throw MoeError(MOE_ESTATE, "ReLU-mask certificate list overflowed");
   }
 }
 
 void Layer::get_grads(float* dw1, float* dw2) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (!last_dw1_ || !last_dw2_) throw MoeError(MOE_ESTATE, "expert grads: no backward yet");
   ck(cudaDeviceSynchronize(), "sync");
   const size_t n = static_cast<size_t>(dE_) * M_ * V_;
-  if (dw1) ck(cudaMemcpy(dw1, dw1_.p, 4 * n, cudaMemcpyDeviceToHost), "copy");
-  if (dw2) ck(cudaMemcpy(dw2, dw2_.p, 4 * n, cudaMemcpyDeviceToHost), "copy");
+  // the last backward's gradients, wherever they went (internal or caller-supplied buffers)
+  if (dw1) ck(cudaMemcpy(dw1, last_dw1_, 4 * n, cudaMemcpyDeviceToHost), "copy");
+  if (dw2) ck(cudaMemcpy(dw2, last_dw2_, 4 * n, cudaMemcpyDeviceToHost), "copy");
 }
 
 }  // namespace moe

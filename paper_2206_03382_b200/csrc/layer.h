@@ -83,6 +83,8 @@ class Layer {
   void grad_slices(float* w1s, float* w2s, cudaStream_t st);
   void* w1() { return w1_.p; }
   void* w2() { return w2_.p; }
+  // resident weights changed in place: rebuild the derived state (W1^T, column norms, W1 slice)
+  void weights_updated() { stats_dirty_ = true; }
   int64_t launches() const { return launches_; }
   void set_profiling(bool on) { prof_ = on; }
   // Sums (ms) and counts per phase since the last call; synchronizes.

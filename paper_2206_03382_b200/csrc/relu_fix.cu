@@ -71,6 +71,66 @@ __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, int R, in
   }
 }
 
+// One pass over W1 for the certificate's weight statistics (M % 64 == 0, V % 64 == 0): a CTA owns
+// the 64-column strip [64 b, 64 b + 64) of expert g, walks M in 64-row tiles (16-byte loads, two
+// per thread), writes the transposed tile to w1t with 16-byte stores, and accumulates the
+// columns' sums of squares in fp64. It then writes colnorm for its 64 columns and their max
+// (colnorm_blk). Algorithmic traffic: read G*M*V*2 B + write G*M*V*2 B.
+__global__ void __launch_bounds__(256) weight_stats_kernel(const __nv_bfloat16* __restrict__ w1,
+                                                           int M, int V, float* __restrict__ colnorm,
+                                                           float* __restrict__ blk,
+                                                           __nv_bfloat16* __restrict__ w1t) {
+  pdl_entry();
+  __shared__ __align__(16) __nv_bfloat16 tile[64][64 + 8];
+  __shared__ double part[4][64];
+  __shared__ float wmax[2];
+  const int nb = V / 64;
+  const int g = blockIdx.x / nb, b = blockIdx.x % nb;
+  const int t = threadIdx.x;
+  const __nv_bfloat16* src = w1 + static_cast<size_t>(g) * M * V + 64 * b;
+  __nv_bfloat16* dst = w1t + (static_cast<size_t>(g) * V + 64 * b) * M;
+  const int lr = t / 8, lc = (t % 8) * 8;  // load: rows lr, lr + 32; 8 columns at lc
+  const int c = t % 64, qq = t / 64;       // transpose: column c, row groups qq and qq + 4
+  double acc = 0.0;
+  uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(lr) * V + lc));
+  uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(lr + 32) * V + lc));
+  for (int m0 = 0; m0 < M; m0 += 64) {
+    *reinterpret_cast<uint4*>(&tile[lr][lc]) = v0;
+    *reinterpret_cast<uint4*>(&tile[lr + 32][lc]) = v1;
+    __syncthreads();
+    if (m0 + 64 < M) {  // the next tile's loads fly while this one is transposed
+      v0 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(m0 + 64 + lr) * V + lc));
+      v1 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(m0 + 96 + lr) * V + lc));
+    }
+    // w1t row 64 b + c, elements [m0 + 8 q, m0 + 8 q + 8); a warp reads 32 adjacent columns
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = qq + 4 * h;
+      __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j] = tile[8 * q + j][c];
+        const double w = __bfloat162float(o[j]);
+        acc = fma(w, w, acc);
+      }
+      __stcs(reinterpret_cast<uint4*>(dst + static_cast<size_t>(c) * M + m0 + 8 * q),
+             *reinterpret_cast<const uint4*>(o));
+    }
+    __syncthreads();
+  }
+  part[qq][c] = acc;
+  __syncthreads();
+  if (t < 64) {
+    const double s = part[0][t] + part[1][t] + part[2][t] + part[3][t];
+    float n = static_cast<float>(sqrt(s)) * 1.0001f;  // |W1[:, col]|_2, rounded up
+    colnorm[static_cast<size_t>(g) * V + 64 * b + t] = n;
+    for (int o = 16; o > 0; o >>= 1) n = fmaxf(n, __shfl_xor_sync(0xffffffffu, n, o));
+    if (t % 32 == 0) wmax[t / 32] = n;
+  }
+  __syncthreads();
+  if (t == 0 && blk) blk[static_cast<size_t>(g) * nb + b] = fmaxf(wmax[0], wmax[1]);
+}
+
 // rownorm[i] = |x[i]|_2 (one warp per row)
 // |x[r]|_2 per row (rounded up). Optionally first waits for the chunk's peer flags (fused
 // receive wait) and resets the fixup counter.
@@ -151,7 +211,7 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
     unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
   pdl_entry();
   // count[0]: entries listed by the up GEMM; count[1]: CTAs done; count[2]: the last list's size
-  // (metrics). The last CTA to finish resets [0] and [1], so the next chunk's up GEMM starts from
+  // (metrics); count[3]: the largest list since the host last read it (overflow check). The last CTA to finish resets [0] and [1], so the next chunk's up GEMM starts from
   // an empty list without a memset or reset kernel.
   const unsigned int n = min(__ldcg(count), cap);
   const int lane = threadIdx.x % 32;
@@ -195,6 +255,7 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
     __threadfence();
     if (atomicAdd(c + 1, 1u) == gridDim.x - 1) {
       c[2] = c[0];
+      c[3] = max(c[3], c[0]);  // sticky: the largest list since the last metrics read
       c[0] = 0u;
       c[1] = 0u;
     }
@@ -228,6 +289,11 @@ int relu_mask_from_act_device(const void* act, int64_t rows, int V, unsigned lon
 
 int weight_stats_device(const void* w1, int G, int M, int V, float* colnorm, float* colnorm_blk,
                         void* w1t, cudaStream_t st) {
+  if (M % 64 == 0 && V % 64 == 0) {
+    launch_k(weight_stats_kernel, G * (V / 64), 256, 0, st, static_cast<const __nv_bfloat16*>(w1), M,
+             V, colnorm, colnorm_blk, static_cast<__nv_bfloat16*>(w1t));
+    return launch_status();
+  }
   const int n = G * V;
   launch_k(colnorm_kernel, (n + 255) / 256, 256, 0, st, static_cast<const __nv_bfloat16*>(w1), G, M, V,
                                                  colnorm);

@@ -190,7 +190,9 @@ class LayerState:
                                           b.ctypes.data_as(C.c_void_p)), self._h)
 
     def weights(self):
-        """Device views (E/W, M, V) / (E/W, V, M) of the resident local expert weights."""
+        """Device views (E/W, M, V) / (E/W, V, M) of the resident local expert weights. Writable:
+        fetching them marks the derived weight state stale; after writing through views kept
+        from an earlier call, call weights_updated() before the next forward."""
         cfg = self.config
         out = []
         for which, shape in ((1, (cfg.local_experts, cfg.model_dim, cfg.hidden_dim)),
@@ -201,6 +203,22 @@ class LayerState:
             esz = 2 if cfg.dtype == "bf16" else 4
             out.append(_from_ptr(p.value, n * esz, cfg.torch_dtype, shape, self.device))
         return out
+
+    def expert_grads(self):
+        """Host fp32 copies of the last backward's local expert gradients (moe_get_expert_grads),
+        wherever backward wrote them; MoeError before any backward."""
+        import numpy as np
+        cfg = self.config
+        n_e = cfg.local_experts
+        w1 = np.empty((n_e, cfg.model_dim, cfg.hidden_dim), np.float32)
+        w2 = np.empty((n_e, cfg.hidden_dim, cfg.model_dim), np.float32)
+        check(lib().moe_get_expert_grads(self._h, w1.ctypes.data_as(C.c_void_p),
+                                         w2.ctypes.data_as(C.c_void_p)), self._h)
+        return w1, w2
+
+    def weights_updated(self) -> None:
+        """The resident weights were changed in place (moe_weights_updated)."""
+        check(lib().moe_weights_updated(self._h), self._h)
 
     # -- results
     def routing(self):

@@ -1,4 +1,4 @@
-"""Multi-rank host logic on CPU (world_size 2, gloo): the flexible all-to-all plan the layer's
+"""Multi-rank host logic on CPU (world_size 2, 4 and 8, gloo): the flexible all-to-all plan the layer's
 NCCL exchanges use (moe_a2a_plan) moves exactly the blocks of the reference flex_all2all
 (collectives.cpp:123-160) for every pipeline chunk, and the per-rank token blocks / gating
 blocks compose to the reference's blocked layer (moe_layer.cpp:171-244)."""
@@ -41,7 +41,7 @@ def _worker(rank, W, port, q):
         dist.init_process_group("gloo", rank=rank, world_size=W)
         import oracle
         from paper_2206_03382_b200._lib import lib
-        E, dC, M, degree = 4, 5, 3, 2
+        E, dC, M, degree = 8, 5, 3, 2
         cc = -(-dC // degree)
         dE = E // W
         rs = np.random.RandomState(100)
@@ -80,6 +80,32 @@ def _worker(rank, W, port, q):
         assert cap == lcap
         assert np.array_equal(li, gi[rank * T:(rank + 1) * T])
         assert np.array_equal(ll, gl[rank * T:(rank + 1) * T])
+        # Auto capacity across ranks (gating.cpp:141-147): per-rank demand, all-reduce MAX (the
+        # layer's ncclAllReduce), resolve, assign my block == the reference's blocked gating
+        for kind, fac in ((1, 1.0), (2, 1.25), (2, 0.5)):
+            gi, gg, gl, cap = oracle.run_gating_blocked(probs, W, k, kind, fac, True)
+            dem = torch.from_numpy(np.bincount(li.ravel(), minlength=Ex).astype(np.int64))
+            dist.all_reduce(dem, op=dist.ReduceOp.MAX)
+            lcap = oracle.resolve_capacity(kind, fac, dem.numpy(), Ex, k, T)
+            assert lcap == cap
+            assert np.array_equal(oracle.assign_locations(li, lg, lcap, True), gl[rank * T:(rank + 1) * T])
+        # Alg. 1 consensus: each rank measures its own seconds, the layer all-reduces the max
+        # before recording, so every rank's memo explores and exploits the same strategies
+        memo = C.c_void_p()
+        assert lib().moe_memo_create(C.c_double(0.5), C.byref(memo)) == 0
+        picks = []
+        s = C.c_int32()
+        for step in range(14):
+            f = (1.0, 1.2, 2.0)[step % 3]
+            assert lib().moe_memo_get_strategy(memo, C.c_double(f), C.byref(s)) == 0
+            picks.append(s.value)
+            t = torch.tensor([float(rs.uniform(1, 2)) * (1 + rank) + s.value * 0.01])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            assert lib().moe_memo_optimize_strategy(memo, C.c_double(f), s, C.c_double(t.item())) == 0
+        lib().moe_memo_destroy(memo)
+        allp = [None] * W
+        dist.all_gather_object(allp, picks)
+        assert all(p == picks for p in allp)
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
@@ -88,8 +114,8 @@ def _worker(rank, W, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-def test_flex_all2all_plan_world2_gloo():
-    W = 2
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_flex_all2all_plan_gloo(W):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -114,6 +114,46 @@ def test_layer_slices_gather_single_rank(cuda):
     assert np.array_equal(w2.double().cpu().numpy(), inp["w2"])
 
 
+@pytest.mark.parametrize("keep_views", [False, True])
+def test_in_place_weight_update(cuda, keep_views):
+    """An on-device SGD step written through the exported weight pointers: the next
+    forward must rebuild the ReLU certificate's W1^T copy and column norms, so y, dx and dW match
+    the oracle run on the updated weights. keep_views: views fetched before the step, then
+    moe_weights_updated; else views fetched after the step (the fetch marks the state stale)."""
+    E, k, f, M, V, T = 8, 1, 1.0, 512, 1024, 4096
+    st, res, g, _, inp = run_case(E, k, f, M, V, T, False, "bf16")
+    dw1, dw2 = st.expert_grads()  # the buffers backward() wrote (caller-supplied), not internal
+    assert np.array_equal(dw1, g.dw1.cpu().numpy()) and np.array_equal(dw2, g.dw2.cpu().numpy())
+    views = st.weights() if keep_views else None
+    forward(st, torch.as_tensor(inp["x"]).to(torch.bfloat16).cuda())  # stats now clean
+    w1, w2 = views if keep_views else st.weights()
+    lr = 0.5 / float(g.dw1.abs().max())  # a step large enough to flip many ReLU signs
+    w1 -= (lr * g.dw1).to(torch.bfloat16)
+    w2 -= (lr * g.dw2).to(torch.bfloat16)
+    if keep_views:
+        st.weights_updated()
+    x = torch.as_tensor(inp["x"]).to(torch.bfloat16).cuda()
+    dy = torch.as_tensor(inp["dy"]).to(torch.bfloat16).cuda()
+    res = forward(st, x)
+    g2 = backward(st, res.saved, dy)
+    torch.cuda.synchronize()
+    nw1, nw2 = w1.double().cpu().numpy(), w2.double().cpu().numpy()
+    assert not np.array_equal(nw1, inp["w1"])
+    ref = oracle.layer_step(inp["x"], inp["wg"], nw1, nw2, inp["dy"], 1, k, 0, f, False)
+    idxs, loc, _, _ = st.routing()
+    assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
+    for name, got in (("y", res.y), ("dx", g2.dx), ("dw1", g2.dw1), ("dw2", g2.dw2)):
+        assert oracle.max_rel_diff(got.double().cpu().numpy(), ref[name]) < 2e-2, name
+    assert st.metrics().relu_fixups > 0
+
+
+def test_expert_grads_before_backward_fails(cuda):
+    from paper_2206_03382_b200 import MoeError
+    cfg = MoELayerConfig(global_experts=2, model_dim=64, hidden_dim=64, tokens_per_step=16)
+    with pytest.raises(MoeError):
+        LayerState.init(cfg, 1).expert_grads()
+
+
 def test_grad_slices_single_rank(cuda):
     """reduce_scatter_grads_p1 at W = 1: the slice is the whole gradient."""
     st, res, g, ref, _ = run_case(4, 1, 1.0, 64, 256, 256, False, "f32")

@@ -276,3 +276,26 @@ def test_layer_step_sharded_placement_matches_frozen_plan():
                 y[t] += ref["gates"][t, j] * (h @ inp["w2"][e])
         assert oracle.max_rel_diff(y, ref["y"]) < 1e-12
         assert np.abs(ref["dw1"]).max() > 0 and np.abs(ref["dx"]).max() > 0
+
+
+@pytest.mark.parametrize("W,k,f,bpr", [(2, 1, 1.0, False), (2, 2, 0.75, True)])
+def test_sampled_oracle_matches_whole_layer(W, k, f, bpr):
+    """The sampled checkers used at full C4 size (frozen-plan backward rows; an expert's dW1
+    columns / dW2 rows from its gathered rows) equal the whole-layer oracle on a small layer."""
+    E, M, V, T = 4 * W, 24, 40, 64
+    x = rng.uniform(7, 0, W * T * M).reshape(W * T, M)
+    dy = rng.uniform(7, 10**6, W * T * M).reshape(W * T, M)
+    wg, w1, w2 = rng.layer_params(7, M, E, V)
+    ref = oracle.layer_step(x, wg, w1, w2, dy, W, k, 0, f, bpr)
+    idxs, loc, gates = ref["idxs"], ref["locations"], ref["gates"]
+    sel = np.array([0, 3, 17, T + 5, W * T - 1])
+    dx = oracle.frozen_plan_backward_rows(x[sel], dy[sel], k, idxs[sel], loc[sel], gates[sel], w1, w2)
+    assert oracle.max_rel_diff(dx, ref["dx"][sel]) < 1e-12
+    cols = np.array([0, 7, V - 1])
+    for e in range(E):
+        t, j = np.nonzero((idxs == e) & (loc >= 0))
+        X = x[t]
+        dZ = gates[t, j][:, None] * dy[t]
+        d1, d2 = oracle.expert_backward_columns(X, dZ, w1[e], w2[e], cols)
+        assert oracle.max_rel_diff(d1, ref["dw1"][e][:, cols]) < 1e-12
+        assert oracle.max_rel_diff(d2, ref["dw2"][e][cols, :]) < 1e-12
