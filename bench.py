@@ -316,6 +316,10 @@ def main():
                     help="W>1 all-to-all: copy engines over NVLink peer memory, or NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--update-weights", action="store_true",
+                    help="training-loop variant: declare the expert weights changed every step "
+                         "(moe_weights_updated, as after an on-device optimizer step), so every "
+                         "forward rebuilds the ReLU certificate's W1^T copy and column norms")
     ap.add_argument("--no-phase-events", action="store_true",
                     help="A/B: time the steps without the per-phase CUDA events (no roofline)")
     args = ap.parse_args()
@@ -371,6 +375,8 @@ def run_gpu(args):
     def step():
         res = forward(state, x, y)
         backward(state, res.saved, dy, dx, dw1, dw2)
+        if args.update_weights:
+            state.weights_updated()
 
     def barrier():
         torch.cuda.synchronize()
@@ -551,6 +557,7 @@ def run_gpu(args):
                        "capacity": cap, "parallelism": f"ep{world}",
                        "a2a": args.a2a if world > 1 else None,
                        "degree": metrics.degree, "adaptive": adaptive,
+                       "update_weights": bool(args.update_weights),
                        "l2": "per-step working set >1 GiB/GPU >> 126 MB L2 (no flush needed)"},
             "roofline": {"bound": gemm_bound, "achieved": achieved_tf, "peak": gemm_peak,
                          "unit": "TFLOP/s",

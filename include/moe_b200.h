@@ -65,7 +65,18 @@ typedef struct moe_config {
   int32_t router;          /* MOE_ROUTER_* (RouterKind, moe_layer.hpp:10) */
   int32_t parallel;        /* MOE_PARALLEL_* (ParallelControl, moe_layer.hpp:17-20); sharded only */
   int32_t a2a_algo;        /* StrategyControl::fixed.algo: MOE_A2A_LINEAR or MOE_A2A_2DH */
+  int32_t gate_precision;  /* MOE_GATE_*: how the router logits are computed */
 } moe_config;
+
+/* Router GEMM precision. AUTO (0, the default): the bf16 layer with the linear router and FIFO
+ * routing (E % 8 == 0, E <= 64, M % 64 == 0, k <= 8) runs the certified tensor-core gate --
+ * logits from bf16 MMAs with a proven error bound, every token whose top-k order the bound
+ * cannot prove re-decided from fp64 logits, so expert ids, slots and drops stay bit-exact;
+ * gate values of certified tokens carry the bound's error (relative ~1e-6 typical, well inside
+ * the bf16 output tolerance). Every other layer, and FP64, runs the fp64 DMMA gate (gate values
+ * equal to the fp64 reference's up to summation order). */
+#define MOE_GATE_AUTO 0
+#define MOE_GATE_FP64 1
 
 /* ParallelControl / ParallelChoice (parallelism.hpp): the sharded-placement exchange form.
  * P1 gathers each computed expert's weights and routes every source's tokens to one replica
@@ -104,6 +115,8 @@ typedef struct moe_step_metrics {
                           last chunk of the last forward) */
   int32_t fused;       /* MOE_FUSED_* bits: which exchanges ran inside the GEMM epilogues */
   int32_t parallel;    /* MOE_PARALLEL_P1 / _P2: the exchange form used (StepMetrics::parallel) */
+  int64_t gate_fixups; /* certified gate: tokens re-decided from fp64 logits since the last
+                          moe_get_metrics (0 with the fp64 gate) */
 } moe_step_metrics;
 #define MOE_FUSED_DECODE 1  /* W = 1, k = 1: decode / encode-backward = down / dgrad epilogue scatter */
 #define MOE_FUSED_COMBINE 2 /* W > 1 peer backend: combine = down / dgrad epilogue NVLink stores */
@@ -223,10 +236,11 @@ int64_t moe_kernel_launches(const moe_handle* h);
 /* Measured timeline (replaces the simulated Timeline of pipeline.hpp:36-46): when on, every
  * phase is bracketed by CUDA events on the stream it runs on. Phases, in order: gate, encode,
  * gemm_up, gemm_down, decode, decode_bwd, gemm_dgrad_mask, gemm_dgrad, gemm_wgrad1,
- * gemm_wgrad2, encode_bwd, a2a_fwd, a2a_bwd, assign, relu_fixup, xfer_dispatch, xfer_combine
- * (MOE_NUM_PHASES). a2a_* span the comm stream's enqueue and waits; xfer_* span only the
+ * gemm_wgrad2, encode_bwd, a2a_fwd, a2a_bwd, assign, relu_fixup, xfer_dispatch, xfer_combine,
+ * weight_stats (MOE_NUM_PHASES; weight_stats = rebuilding the ReLU certificate's W1^T and column
+ * norms after the weights changed). a2a_* span the comm stream's enqueue and waits; xfer_* span only the
  * copy-engine pushes over NVLink (peer transport), from the push's start to its last block landing. */
-#define MOE_NUM_PHASES 17
+#define MOE_NUM_PHASES 18
 int moe_set_profiling(moe_handle* h, int32_t on);
 /* Per-phase summed milliseconds and interval counts since the last call (synchronizes). */
 int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n);

@@ -20,7 +20,7 @@ CAP_FIXED, CAP_AUTO, CAP_BOUNDED = 0, 1, 2
 
 PHASES = ["gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd", "gemm_dgrad_mask",
           "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2", "encode_bwd", "a2a_fwd", "a2a_bwd",
-          "assign", "relu_fixup", "xfer_dispatch", "xfer_combine"]
+          "assign", "relu_fixup", "xfer_dispatch", "xfer_combine", "weight_stats"]
 
 _ERRNAMES = {1: "EINVAL", 2: "ECUDA", 3: "ECOMM", 4: "ESTATE", 5: "ENOMEM"}
 
@@ -38,7 +38,7 @@ class MoeConfig(C.Structure):
         ("top_k", C.c_int64), ("capacity_kind", C.c_int32), ("capacity_factor", C.c_double),
         ("bpr", C.c_int32), ("dtype", C.c_int32), ("adaptive", C.c_int32), ("degree", C.c_int32),
         ("a2a_backend", C.c_int32), ("router", C.c_int32), ("parallel", C.c_int32),
-        ("a2a_algo", C.c_int32),
+        ("a2a_algo", C.c_int32), ("gate_precision", C.c_int32),
     ]
 
 
@@ -47,7 +47,7 @@ class StepMetrics(C.Structure):
         ("f", C.c_double), ("capacity", C.c_int64), ("a2a_algo", C.c_int32),
         ("degree", C.c_int32), ("seconds", C.c_double), ("comm_bytes", C.c_double),
         ("drop_count", C.c_int64), ("relu_fixups", C.c_int64), ("fused", C.c_int32),
-        ("parallel", C.c_int32),
+        ("parallel", C.c_int32), ("gate_fixups", C.c_int64),
     ]
 
 

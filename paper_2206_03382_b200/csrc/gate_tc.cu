@@ -1,0 +1,486 @@
+// Certified tensor-core router GEMM for the bf16 layer (linear router, FIFO routing).
+//
+// The reference routes in fp64 (gate_linear + softmax_rows + topk_select, gating.cpp:19-78).
+// Its expert choice depends only on the ORDER of a token's logits, so the logits need fp64
+// accuracy only where two of the top-(k+1) are close. This kernel computes them on the tensor
+// cores and proves each token's top-k order from an error bound; tokens it cannot prove are
+// re-decided from fp64 logits inside the same CTA:
+//
+//   Wg = hi + lo with hi = bf16(Wg), lo = bf16(Wg - hi)   (|Wg - hi - lo| <= 2^-18 |Wg|)
+//   L~[t][e] = sum over 64-wide K chunks of fp64(HMMA_fp32(x, hi) + HMMA_fp32(x, lo))
+//   |L~ - L| <= eps_t = 2^-14 * |x_t|_2 * max_e |Wg[:, e]|_2
+// x is bf16, so every product is exact. Each K chunk starts from a zero fp32 accumulator (4
+// m16n8k16 steps) and is added into an fp64 running sum, so the fp32 error never scales with the
+// whole row: assuming a step truncates each of its 17 aligned addends (16 products + C) to the
+// largest one's 24-bit grid, a chunk errs by <= 4 * 18 * 2^-23 * 2 * sum_chunk|x w| ~ 2^-15.8 *
+// sum_chunk|x w|; with the split residual the total is <= 2^-15.5 * sum|x w| <= 2^-15.5 |x|_2
+// |w|_2 (Cauchy-Schwarz). eps_t keeps a 2.8x margin on that pessimistic model (measured errors
+// are ~100x smaller). A token is certified when each of its first k sorted logits beats the next
+// by more than 2 eps_t; then its idxs are the fp64 reference's (exactly equal logits never
+// certify). Uncertified tokens go to a list that gate_fixup_kernel re-decides from fp64 logits
+// (products of bf16 x with fp64 Wg are exact; only the summation order differs from Eigen) with
+// the fp64 softmax / top-k of the DMMA gate, patching idxs / gates / the CTA histograms before
+// the capacity scan reads them.
+// Gate VALUES of certified tokens come from the softmax of L~ (relative error ~1e-6 typical,
+// bounded by ~4 eps_t); they scale expert outputs, which the north star holds to 2e-2 (bf16).
+// BPR needs fp64-accurate cross-token keys, so BPR layers keep the DMMA gate.
+//
+// Work: 2*T*M*(2E) bf16 MACs on mma.sync.m16n8k16 (HMMA) -- the kernel is HBM-bound on reading
+// x once (T*M*2 bytes; 64 MiB at TGT ~ 10 us at 6.5 TB/s), so the tensor pipe stays mostly idle.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "kernels.h"
+#include "pdl.cuh"
+
+namespace moe {
+
+namespace {
+
+constexpr int kTcWarps = 4;              // 4 warps x 16 tokens = the 64-token gate block
+constexpr int kTcTok = kTcWarps * 16;
+constexpr int kTcKC = 64;                // K per stage (one 128-byte row chunk)
+constexpr int kTcStages = 4;
+constexpr double kTcEpsScale = 1.0 / 16384.0;  // 2^-14
+constexpr int kFixWarps = 8;                   // fixup CTA: warps split M
+constexpr int kTcMaxK = 8;
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(pred ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(addr));
+}
+__device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+// 128-byte smem rows, 16-byte chunks XOR-swizzled by row % 8 (conflict-free cp.async / ldmatrix)
+__device__ __forceinline__ uint32_t sw(uint32_t base, int row, int chunk) {
+  return base + row * 128 + ((chunk ^ (row & 7)) << 4);
+}
+
+template <int NT>
+struct TcCfg {
+  static constexpr int E = 8 * NT;
+  static constexpr int XB = kTcTok * 128;     // x stage bytes
+  static constexpr int WB = 2 * E * 128;      // hi + lo pieces, E rows each
+  static constexpr int STAGE = XB + WB;
+  static constexpr int SMEM = kTcStages * STAGE;
+};
+
+struct TcArgs {
+  const __nv_bfloat16* x;       // [blocks*T][M]
+  const __nv_bfloat16* pieces;  // [2][E][M]: hi, lo
+  const double* wg;             // [M][E] fp64 (re-decision)
+  const float* wn_max;          // max_e |Wg[:, e]|_2, rounded up
+  int T, M, E, k, cpb;
+  int32_t* idxs;
+  double* gates;
+  int32_t* hist;
+  int32_t* fixups;              // += tokens re-decided in fp64 (metrics; may be null)
+  int32_t* flag_list;           // [blocks*T] uncertified token indices
+  int32_t* flag_count;          // [0] list size, [1] fixup CTAs done (reset by the fixup kernel)
+};
+
+template <int NT>
+__global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
+  using Cf = TcCfg<NT>;
+  constexpr int E = Cf::E;
+  constexpr int NTH = kTcWarps * 32;
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ int32_t sh_hist[E];
+  pdl_entry();
+  const int M = a.M;
+  const int b = blockIdx.x / a.cpb, c = blockIdx.x % a.cpb;
+  const int t_begin = b * a.T + c * kTcTok;
+  const int ntok = min(b * a.T + a.T, t_begin + kTcTok) - t_begin;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int e = threadIdx.x; e < E; e += NTH) sh_hist[e] = 0;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+
+  auto issue = [&](int ch) {
+    const int k0 = ch * kTcKC;
+    const uint32_t st = sbase + (ch % kTcStages) * Cf::STAGE;
+    for (int i = threadIdx.x; i < kTcTok * 8; i += NTH) {
+      const int r = i / 8, q = i % 8;
+      const bool ok = r < ntok;
+      const __nv_bfloat16* src = a.x + (ok ? static_cast<size_t>(t_begin + r) * M + k0 + q * 8 : 0);
+      cp16(sw(st, r, q), src, ok);
+    }
+    for (int i = threadIdx.x; i < 2 * E * 8; i += NTH) {
+      const int r = i / 8, q = i % 8;  // r = piece * E + e
+      cp16(sw(st + Cf::XB, r, q), a.pieces + static_cast<size_t>(r) * M + k0 + q * 8, true);
+    }
+  };
+
+  double tot[NT][4];  // fp64 running sums of the per-chunk fp32 accumulators (hi + lo)
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tot[j][i] = 0.0;
+  float ss0 = 0.0f, ss1 = 0.0f;  // sum of squares of this lane's A elements, rows g and g + 8
+
+  const int nch = M / kTcKC;
+#pragma unroll
+  for (int s = 0; s < kTcStages - 1; ++s) {
+    if (s < nch) issue(s);
+    cp_commit();
+  }
+  // ldmatrix lane roles: A x4 = (rows 0-7 | 8-15) x (k 0-7 | 8-15); B x2 = 8 experts x (k 0-7 | 8-15)
+  const int a_row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+  const int a_kc = lane >> 4;
+  const int b_row = lane & 7;
+  const int b_kc = (lane >> 3) & 1;
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_wait<kTcStages - 2>();
+    __syncthreads();
+    if (ch + kTcStages - 1 < nch) issue(ch + kTcStages - 1);
+    cp_commit();
+    const uint32_t st = sbase + (ch % kTcStages) * Cf::STAGE;
+    float acc[2][NT][4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[p][j][i] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < kTcKC / 16; ++ks) {
+      uint32_t af[4];
+      ldsm_x4(sw(st, a_row, ks * 2 + a_kc), af[0], af[1], af[2], af[3]);
+      ss0 = fmaf(bf_lo(af[0]), bf_lo(af[0]), ss0);
+      ss0 = fmaf(bf_hi(af[0]), bf_hi(af[0]), ss0);
+      ss0 = fmaf(bf_lo(af[2]), bf_lo(af[2]), ss0);
+      ss0 = fmaf(bf_hi(af[2]), bf_hi(af[2]), ss0);
+      ss1 = fmaf(bf_lo(af[1]), bf_lo(af[1]), ss1);
+      ss1 = fmaf(bf_hi(af[1]), bf_hi(af[1]), ss1);
+      ss1 = fmaf(bf_lo(af[3]), bf_lo(af[3]), ss1);
+      ss1 = fmaf(bf_hi(af[3]), bf_hi(af[3]), ss1);
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          uint32_t b0, b1;
+          ldsm_x2(sw(st + Cf::XB, p * E + j * 8 + b_row, ks * 2 + b_kc), b0, b1);
+          hmma(acc[p][j], af, b0, b1);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        tot[j][i] += static_cast<double>(acc[0][j][i]) + static_cast<double>(acc[1][j][i]);
+  }
+  cp_wait<0>();
+
+  // ---- epilogue: lane (g = lane / 4, c = lane % 4) holds rows g and g + 8, columns 8j + 2c + i
+  const int g = lane >> 2, cq = lane & 3;
+  ss0 += __shfl_xor_sync(0xffffffffu, ss0, 1);
+  ss0 += __shfl_xor_sync(0xffffffffu, ss0, 2);
+  ss1 += __shfl_xor_sync(0xffffffffu, ss1, 1);
+  ss1 += __shfl_xor_sync(0xffffffffu, ss1, 2);
+  const double wn = static_cast<double>(__ldg(a.wn_max));
+  const int k = a.k;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int tt = warp * 16 + g + 8 * h;
+    const bool tok_ok = tt < ntok;
+    const int t = t_begin + tt;
+    double L[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        L[j][i] = tot[j][2 * h + i];
+    // |x_t|_2 rounded up (fp32 sum of squares of exact bf16 values: relative error < 2^-14)
+    const double xn = sqrt(static_cast<double>(h ? ss1 : ss0)) * (1.0 + 1.0 / 4096.0);
+    const double eps = kTcEpsScale * xn * wn;
+    double mx = -DBL_MAX;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mx = fmax(mx, fmax(L[j][0], L[j][1]));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) s += exp(L[j][i] - mx);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    // top-(k + 1) by (logit desc, expert asc); the (k + 1)-th only bounds the k-th's margin
+    unsigned taken = 0;
+    bool certified = true;
+    double prev = 0.0;
+    int sel[kTcMaxK];
+    double selv[kTcMaxK];
+    const int kk = k < E ? k + 1 : k;
+    for (int r = 0; r < kk; ++r) {
+      double bv = -DBL_MAX;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int e = j * 8 + cq * 2 + i;
+          if (!(taken & (1u << (j * 2 + i))) && (L[j][i] > bv || (L[j][i] == bv && e < bi))) {
+            bv = L[j][i];
+            bi = e;
+          }
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (((bi & 7) >> 1) == cq) taken |= 1u << ((bi >> 3) * 2 + (bi & 1));
+      if (r > 0 && !(prev - bv > 2.0 * eps)) certified = false;
+      // the reference orders fp64 PROBABILITIES (ties -> lower id): below exp's normal range
+      // distinct logits can give equal (denormal / zero) probabilities, so a selected expert
+      // that deep under the max is never certified from logits
+      if (r < k && bv - mx < -690.0) certified = false;
+      prev = bv;
+      if (r < k) {
+        sel[r] = bi;
+        selv[r] = bv;
+      }
+    }
+    if (cq == 0 && tok_ok) {
+      if (certified) {
+        for (int r = 0; r < k; ++r) {
+          a.idxs[static_cast<size_t>(t) * k + r] = sel[r];
+          a.gates[static_cast<size_t>(t) * k + r] = exp(selv[r] - mx) / s;
+          atomicAdd(&sh_hist[sel[r]], 1);
+        }
+      } else {
+        a.flag_list[atomicAdd(a.flag_count, 1)] = t;
+      }
+    }
+  }
+  __syncthreads();
+
+  for (int e = threadIdx.x; e < E; e += NTH) a.hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
+}
+
+// fp64 re-decision of the tokens gate_tc_kernel could not certify: one token per CTA at a time,
+// warps split M, lanes own experts (lane, lane + 32); warp 0 runs the fp64 softmax + top-k
+// (prob desc, expert asc; gating.cpp:19-78) and patches idxs / gates / the token's CTA histogram
+// row. The last CTA to finish resets the list and adds its size to the metrics counter.
+__global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a) {
+  __shared__ double red[kFixWarps][64];
+  pdl_entry();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = *reinterpret_cast<volatile int32_t*>(a.flag_count);
+  const int M = a.M, E = a.E, k = a.k;
+  const int mlen = (M + kFixWarps - 1) / kFixWarps;
+  for (int f = blockIdx.x; f < n; f += gridDim.x) {
+    const int t = a.flag_list[f];
+    const __nv_bfloat16* __restrict__ xr = a.x + static_cast<size_t>(t) * M;
+    const double* __restrict__ wg = a.wg;
+    const int m0 = warp * mlen, m1 = min(M, m0 + mlen);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = lane + 32 * i;
+      double p[4] = {0.0, 0.0, 0.0, 0.0};
+      if (e < E) {
+        // 32 independent loads in flight per thread (the loop is L2-latency bound)
+        int m = m0;
+        for (; m + 32 <= m1; m += 32) {
+          double xv[32], wv[32];
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            xv[u] = static_cast<double>(__bfloat162float(__ldg(xr + m + u)));
+            wv[u] = __ldg(wg + static_cast<size_t>(m + u) * E + e);
+          }
+#pragma unroll
+          for (int u = 0; u < 32; ++u) p[u & 3] = fma(xv[u], wv[u], p[u & 3]);
+        }
+        for (; m < m1; ++m)
+          p[0] = fma(static_cast<double>(__bfloat162float(xr[m])), __ldg(a.wg + static_cast<size_t>(m) * E + e), p[0]);
+      }
+      red[warp][e] = (p[0] + p[1]) + (p[2] + p[3]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double l[2], pv[2];
+      double mx = -DBL_MAX;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int e = lane + 32 * i;
+        l[i] = -DBL_MAX;
+        if (e < E) {
+          double v = 0.0;
+          for (int q = 0; q < kFixWarps; ++q) v += red[q][e];
+          l[i] = v;
+          mx = fmax(mx, v);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        pv[i] = (lane + 32 * i < E) ? exp(l[i] - mx) : 0.0;
+        s += pv[i];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) pv[i] = (lane + 32 * i < E) ? pv[i] / s : -1.0;
+      const int cta = (t / a.T) * a.cpb + (t % a.T) / kTcTok;
+      unsigned taken = 0;
+      for (int r = 0; r < k; ++r) {
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int e = lane + 32 * i;
+          if (e < E && !(taken & (1u << i)) && (pv[i] > bv || (pv[i] == bv && e < bi))) {
+            bv = pv[i];
+            bi = e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == 0) {
+          a.idxs[static_cast<size_t>(t) * k + r] = bi;
+          a.gates[static_cast<size_t>(t) * k + r] = bv;
+          atomicAdd(a.hist + static_cast<size_t>(cta) * E + bi, 1);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.flag_count + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      if (a.fixups) atomicAdd(a.fixups, n);
+      a.flag_count[0] = 0;
+      a.flag_count[1] = 0;
+    }
+  }
+}
+
+// hi / lo bf16 split of Wg ([M][E] fp64 -> [2][E][M]) and max_e |Wg[:, e]|_2 (rounded up).
+// One CTA of 32 warps; warp w handles experts w, w + 32.
+__global__ void __launch_bounds__(1024) wg_split_kernel(const double* __restrict__ wg, int M, int E,
+                                                        __nv_bfloat16* __restrict__ pieces,
+                                                        float* __restrict__ wn_max) {
+  pdl_entry();
+  __shared__ float wmax[32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float nmax = 0.0f;
+  for (int e = warp; e < E; e += 32) {
+    double ss = 0.0;
+    for (int m = lane; m < M; m += 32) {
+      const double w = wg[static_cast<size_t>(m) * E + e];
+      const __nv_bfloat16 hi = __double2bfloat16(w);
+      const __nv_bfloat16 lo = __double2bfloat16(w - static_cast<double>(__bfloat162float(hi)));
+      pieces[static_cast<size_t>(e) * M + m] = hi;
+      pieces[static_cast<size_t>(E + e) * M + m] = lo;
+      ss = fma(w, w, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    nmax = fmaxf(nmax, static_cast<float>(sqrt(ss)) * 1.0001f);
+  }
+  if (lane == 0) wmax[warp] = nmax;
+  __syncthreads();
+  if (warp == 0) {
+    float v = wmax[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) *wn_max = v;
+  }
+}
+
+}  // namespace
+
+bool gate_tc_supported(int M, int E, int k) {
+  return E % 8 == 0 && E >= 8 && E <= 64 && M % kTcKC == 0 && M > 0 && k <= E && k <= kTcMaxK;
+}
+
+int gate_tc_prepare_device(const double* wg, int M, int E, void* pieces, float* wn_max,
+                           cudaStream_t st) {
+  launch_k(wg_split_kernel, 1, 1024, 0, st, wg, M, E,
+           static_cast<__nv_bfloat16*>(pieces), wn_max);
+  return launch_status();
+}
+
+int gate_tc_device(const void* x, const void* pieces, const double* wg, const float* wn_max,
+                   int blocks, int T, int M, int E, int k, int32_t* idxs, double* gates,
+                   int32_t* hist, int32_t* fixups, int32_t* flag_list, int32_t* flag_count,
+                   cudaStream_t st) {
+  if (!gate_tc_supported(M, E, k) || (reinterpret_cast<uintptr_t>(x) % 16) != 0) return -1;
+  TcArgs a{};
+  a.x = static_cast<const __nv_bfloat16*>(x);
+  a.pieces = static_cast<const __nv_bfloat16*>(pieces);
+  a.wg = wg;
+  a.wn_max = wn_max;
+  a.T = T;
+  a.M = M;
+  a.E = E;
+  a.k = k;
+  a.cpb = (T + kTcTok - 1) / kTcTok;
+  a.idxs = idxs;
+  a.gates = gates;
+  a.hist = hist;
+  a.fixups = fixups;
+  a.flag_list = flag_list;
+  a.flag_count = flag_count;
+  auto go = [&](auto nt_tag) -> int {
+    constexpr int NT = decltype(nt_tag)::value;
+    auto kern = gate_tc_kernel<NT>;
+    if (!smem_optin(kern, TcCfg<NT>::SMEM)) return -2;
+    launch_k(kern, dim3(blocks * a.cpb), dim3(kTcWarps * 32), TcCfg<NT>::SMEM, st, a);
+    if (launch_status() != 0) return -2;
+    launch_k(gate_fixup_kernel, dim3(148 * 4), dim3(kFixWarps * 32), 0, st, a);
+    return launch_status();
+  };
+  switch (E / 8) {
+    case 1: return go(std::integral_constant<int, 1>{});
+    case 2: return go(std::integral_constant<int, 2>{});
+    case 3: return go(std::integral_constant<int, 3>{});
+    case 4: return go(std::integral_constant<int, 4>{});
+    case 5: return go(std::integral_constant<int, 5>{});
+    case 6: return go(std::integral_constant<int, 6>{});
+    case 7: return go(std::integral_constant<int, 7>{});
+    default: return go(std::integral_constant<int, 8>{});
+  }
+}
+
+}  // namespace moe

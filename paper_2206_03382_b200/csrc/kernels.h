@@ -45,7 +45,22 @@ struct GatingArgs {
   int cos_dim;             // D
   double* cos_buf;         // [blocks*T][D] fp64 scratch: x . P
   int32_t* err;            // set to 1 on a zero-norm projected token
+  // Certified tensor-core gate (gate_tc.cu; linear router, bf16 x): set -> used when the shape
+  // allows it and no probs are requested; null -> the fp64 DMMA gate
+  const void* wg_pieces = nullptr;    // [2][E][M] bf16 hi / lo split of wg
+  const float* wg_norm_max = nullptr; // max_e |wg[:, e]|_2
+  int32_t* gate_fixups = nullptr;     // += tokens re-decided in fp64
+  int32_t* gate_flags = nullptr;      // [blocks*T] scratch: uncertified tokens
+  int32_t* gate_flag_count = nullptr; // [2], zero at rest (the fixup kernel resets it)
 };
+
+bool gate_tc_supported(int M, int E, int k);
+int gate_tc_prepare_device(const double* wg, int M, int E, void* pieces, float* wn_max,
+                           cudaStream_t st);
+int gate_tc_device(const void* x, const void* pieces, const double* wg, const float* wn_max,
+                   int blocks, int T, int M, int E, int k, int32_t* idxs, double* gates,
+                   int32_t* hist, int32_t* fixups, int32_t* flag_list, int32_t* flag_count,
+                   cudaStream_t st);
 
 // Cosine router weights: ct = C^T, en[e] = |C_e|; err = 2 if an expert row has zero norm.
 int cosine_prep_device(const double* ce, int E, int D, double* ct, double* en, int32_t* err,

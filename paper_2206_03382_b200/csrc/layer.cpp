@@ -9,6 +9,9 @@
 // nothing updates weights between steps, so this is numerically identical.
 #include "layer.h"
 
+#include <chrono>
+#include <thread>
+
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -126,6 +129,8 @@ void validate(const moe_config& c) {
   }
   if (c.parallel < MOE_PARALLEL_P1 || c.parallel > MOE_PARALLEL_ADAPTIVE)
     throw MoeError(MOE_EINVAL, "parallel control");
+  if (c.gate_precision != MOE_GATE_AUTO && c.gate_precision != MOE_GATE_FP64)
+    throw MoeError(MOE_EINVAL, "gate_precision must be MOE_GATE_AUTO or MOE_GATE_FP64");
   if (c.a2a_algo != MOE_A2A_LINEAR && c.a2a_algo != MOE_A2A_2DH)
     throw MoeError(MOE_EINVAL, "all-to-all algorithm");
   if (c.top_k > 32) throw MoeError(MOE_EINVAL, "top_k > 32 unsupported");
@@ -245,6 +250,15 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   const size_t Tk = static_cast<size_t>(T_) * k_;
   const size_t cpb = gate_cta_per_block(T_);
   wg_.alloc(sizeof(double) * M_ * E_);
+  gate_tc_ = cfg_.gate_precision != MOE_GATE_FP64 && cfg_.dtype == MOE_DTYPE_BF16 &&
+             cfg_.router == MOE_ROUTER_LINEAR && !cfg_.bpr && gate_tc_supported(M_, E_, k_);
+  if (gate_tc_) {
+    wg_pieces_.alloc(static_cast<size_t>(2) * E_ * M_ * 2);
+    wg_nmax_.alloc(sizeof(float));
+    gate_fix_.alloc(3 * sizeof(int32_t));  // [0] metrics counter, [1..2] flag list size / CTAs done
+    ck(cudaMemset(gate_fix_.p, 0, 3 * sizeof(int32_t)), "memset");
+    gate_flags_.alloc(sizeof(int32_t) * static_cast<size_t>(T_));
+  }
   gate_err_.alloc(sizeof(int32_t));
   ck(cudaMemset(gate_err_.p, 0, sizeof(int32_t)), "memset");
   if (cfg_.router == MOE_ROUTER_COSINE) {
@@ -378,7 +392,7 @@ void Layer::prof_mark(int phase, bool begin, cudaStream_t st) {
     static const char* names[] = {"gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd",
                                   "gemm_dgrad_mask", "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2",
                                   "encode_bwd", "a2a_fwd", "a2a_bwd", "assign", "relu_fixup",
-                                  "xfer_dispatch", "xfer_combine"};
+                                  "xfer_dispatch", "xfer_combine", "weight_stats"};
     tl_mark(std::string(phase < kNumPhases ? names[phase] : "?") + (begin ? " >" : " <") +
                 (st == comm_stream_ ? " [comm]" : ""),
             st);
@@ -459,6 +473,7 @@ void Layer::init_params(uint64_t seed) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ckr(fill_uniform_device(wg_.p, MOE_DTYPE_F64, static_cast<int64_t>(M_) * E_, seed, 0, -1.0, 1.0, 0),
       "init router");
+  wg_dirty_ = true;
   const int dt = cfg_.dtype == MOE_DTYPE_BF16 ? 0 : 1;
   const size_t mv = static_cast<size_t>(M_) * V_;
   for (int le = 0; le < dE_; ++le) {
@@ -532,6 +547,7 @@ void Layer::check_gate_error() {
 void Layer::set_router(const double* wg) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ck(cudaMemcpy(wg_.p, wg, sizeof(double) * M_ * E_, cudaMemcpyHostToDevice), "set_router");
+  wg_dirty_ = true;
 }
 
 void Layer::upload_weights(void* dst, const double* src, size_t n) {
@@ -574,7 +590,7 @@ void Layer::set_expert_slices(const double* w1s, const double* w2s) {
     upload_weights(send.p, packed.data(), slice);
     const ncclDataType_t dt = cfg_.dtype == MOE_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32;
     ckn(ncclAllGather(send.p, recv.p, slice, dt, group_comm_, comm_stream_), "allgather");
-    ck(cudaStreamSynchronize(comm_stream_), "gather sync");
+    sync_comm(comm_stream_, "gather sync");
     for (int q = 0; q < s_; ++q) {
       const char* base = static_cast<const char*>(recv.p) + static_cast<size_t>(q) * slice * esz_;
       ck(cudaMemcpy2D(static_cast<char*>(w1_.p) + static_cast<size_t>(q) * h * esz_,
@@ -614,7 +630,7 @@ void Layer::set_expert_slices(const double* w1s, const double* w2s) {
       ckn(ncclRecv(static_cast<char*>(recv.p) + p * per_peer * esz_, per_peer, dt, p, comm_, comm_stream_), "recv");
     }
     ckn(ncclGroupEnd(), "group");
-    ck(cudaStreamSynchronize(comm_stream_), "gather sync");
+    sync_comm(comm_stream_, "gather sync");
   }
   // recv block q = slice q of my dE experts -> full weights (strided 2-D copies).
   const size_t mv = static_cast<size_t>(M_) * V_;
@@ -693,6 +709,13 @@ GatingArgs Layer::gating_args(const void* x) const {
     g.cos_buf = static_cast<double*>(cos_buf_.p);
   }
   g.err = static_cast<int32_t*>(gate_err_.p);
+  if (gate_tc_) {
+    g.wg_pieces = wg_pieces_.p;
+    g.wg_norm_max = static_cast<const float*>(wg_nmax_.p);
+    g.gate_fixups = static_cast<int32_t*>(gate_fix_.p);
+    g.gate_flags = static_cast<int32_t*>(gate_flags_.p);
+    g.gate_flag_count = static_cast<int32_t*>(gate_fix_.p) + 1;
+  }
   return g;
 }
 
@@ -1057,6 +1080,8 @@ void Layer::sharded_backward(GemmArgs dgm, GemmArgs dg, GemmArgs wg1, GemmArgs w
 
 void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (W_ > 1 && comm_ == nullptr) throw MoeError(MOE_ECOMM, "forward: communicator aborted after an earlier failure");
+  check_comm("forward");
   launches_ = 0;
   comm_bytes_ = 0.0;
   ck(cudaEventRecord(ev_fwd_start_, st), "event");
@@ -1065,6 +1090,13 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   // --- gating: router GEMM + softmax + top-k + capacity + slots (per source block)
   GatingArgs ga = gating_args(x);
   GatingBuffers gb = gating_buffers();
+  if (gate_tc_ && wg_dirty_) {  // router weights changed: refresh the bf16 split + norm bound
+    ckr(gate_tc_prepare_device(wg_.p == nullptr ? nullptr : static_cast<const double*>(wg_.p), M_, E_,
+                               wg_pieces_.p, static_cast<float*>(wg_nmax_.p), st),
+        "gate split");
+    ++launches_;
+    wg_dirty_ = false;
+  }
   prof_mark(kPhGate, true, st);
   ckr(run_gating_device(ga, gb, st), "gating");
   if (cfg_.capacity_kind != MOE_CAP_FIXED) {
@@ -1078,7 +1110,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     }
     ckr(resolve_capacity_device(dmax, E_, cfg_.capacity_kind, cap_formula_, gb.cap, st), "capacity");
     ck(cudaMemcpyAsync(cap_host_, gb.cap, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
-    ck(cudaStreamSynchronize(st), "sync");
+    sync_comm(st, "sync");
     cap_ = *cap_host_;
     alloc_capacity(cap_);  // collective growth when needed
     gb = gating_buffers();
@@ -1094,15 +1126,17 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
   prof_mark(kPhAssign, false, st);
   // gate + column scan + capacity finalize, assign (+ BPR rank), (+ resolve_capacity)
-  launches_ += 4 + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
+  launches_ += 4 + (gate_tc_ ? 1 : 0) + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
   if (stats_dirty_) {
+    prof_mark(kPhWeightStats, true, st);
     if (cert)
       ckr(weight_stats_device(w1_.p, dE_, M_, V_, static_cast<float*>(colnorm_.p),
                               static_cast<float*>(colnorm_blk_.p), w1t_.p, st),
           "weight stats");
     if (sharded_) refresh_slices(st);
+    prof_mark(kPhWeightStats, false, st);
     stats_dirty_ = false;
   }
   // ParallelControl (moe_layer.cpp:184-186): adaptive picks P1 / P2 by the cost model over the
@@ -1404,12 +1438,60 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
 }
 
+// Host wait on a stream whose work includes collectives or peer-flag waits (W > 1). Instead of
+// blocking in cudaStreamSynchronize -- which never returns if a peer died mid-exchange -- poll
+// the stream and the communicator's asynchronous error state (the analogue of the reference
+// fabric's rank-id failure reporting, fabric.cpp:142-160), with a timeout (MOE_COMM_TIMEOUT_S,
+// default 300 s). On an NCCL error or the timeout the communicator is aborted and MOE_ECOMM
+// names this rank.
+void Layer::sync_comm(cudaStream_t s, const char* what) {
+  if (W_ == 1 || comm_ == nullptr) {
+    ck(cudaStreamSynchronize(s), what);
+    return;
+  }
+  static const double limit_s = [] {
+    const char* e = std::getenv("MOE_COMM_TIMEOUT_S");
+    return e ? std::atof(e) : 300.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) ck(q, what);
+    check_comm(what);
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit_s) {
+      ncclCommAbort(comm_);
+      comm_ = nullptr;
+      throw MoeError(MOE_ECOMM, "rank " + std::to_string(rank_) + ": " + what + ": timed out after " +
+                                    std::to_string(static_cast<int>(limit_s)) + " s waiting for peers");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+void Layer::check_comm(const char* what) {
+  if (comm_ == nullptr) return;
+  for (ncclComm_t c : {comm_, group_comm_}) {
+    if (c == nullptr) continue;
+    ncclResult_t r = ncclSuccess;
+    ncclCommGetAsyncError(c, &r);
+    if (r != ncclSuccess && r != ncclInProgress) {
+      if (group_comm_) ncclCommAbort(group_comm_);
+      ncclCommAbort(comm_);
+      comm_ = nullptr;
+      group_comm_ = nullptr;
+      throw MoeError(MOE_ECOMM, "rank " + std::to_string(rank_) + ": " + what +
+                                    ": NCCL asynchronous error: " + ncclGetErrorString(r));
+    }
+  }
+}
+
 double Layer::allreduce_max_host(double v) {
   DevMem d;
   d.alloc(sizeof(double));
   ck(cudaMemcpy(d.p, &v, sizeof(double), cudaMemcpyHostToDevice), "copy");
   ckn(ncclAllReduce(d.p, d.p, 1, ncclFloat64, ncclMax, comm_, comm_stream_), "allreduce");
-  ck(cudaStreamSynchronize(comm_stream_), "sync");
+  sync_comm(comm_stream_, "sync");
   ck(cudaMemcpy(&v, d.p, sizeof(double), cudaMemcpyDeviceToHost), "copy");
   return v;
 }
@@ -1417,6 +1499,8 @@ double Layer::allreduce_max_host(double v) {
 void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStream_t st) {
   if (!fwd_done_) throw MoeError(MOE_ESTATE, "backward: no saved forward");
   ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (W_ > 1 && comm_ == nullptr) throw MoeError(MOE_ECOMM, "backward: communicator aborted after an earlier failure");
+  check_comm("backward");
   const SlotGeom g = geom();
   GatingBuffers gb = gating_buffers();
   float* gw1 = dw1 ? dw1 : static_cast<float*>(dw1_.p);
@@ -1682,7 +1766,7 @@ void Layer::grad_slices(float* w1s, float* w2s, cudaStream_t st) {
     ck(cudaMemcpyAsync(w2s, last_dw2_ + static_cast<size_t>(q) * h * M_, sizeof(float) * h * M_,
                        cudaMemcpyDeviceToDevice, st),
        "dW2 slice");
-    ck(cudaStreamSynchronize(st), "sync");
+    sync_comm(st, "sync");
     return;
   }
   const int h = V_ / W_;
@@ -1718,7 +1802,7 @@ void Layer::grad_slices(float* w1s, float* w2s, cudaStream_t st) {
     }
     ckn(ncclGroupEnd(), "group");
   }
-  ck(cudaStreamSynchronize(st), "sync");  // the pack buffer is freed on return
+  sync_comm(st, "sync");  // the pack buffer is freed on return
 }
 
 void Layer::ensure_io() {
@@ -1736,7 +1820,7 @@ void Layer::forward_host(const void* xh, void* yh, cudaStream_t st) {
   ck(cudaMemcpyAsync(io_x_.p, xh, n, cudaMemcpyHostToDevice, st), "h2d x");
   forward(io_x_.p, io_y_.p, st);
   ck(cudaMemcpyAsync(yh, io_y_.p, n, cudaMemcpyDeviceToHost, st), "d2h y");
-  ck(cudaStreamSynchronize(st), "sync");
+  sync_comm(st, "sync");
 }
 
 void Layer::backward_host(const void* dyh, void* dxh, cudaStream_t st) {
@@ -1746,7 +1830,7 @@ void Layer::backward_host(const void* dyh, void* dxh, cudaStream_t st) {
   ck(cudaMemcpyAsync(io_dy_.p, dyh, n, cudaMemcpyHostToDevice, st), "h2d dy");
   backward(io_dy_.p, io_dx_.p, nullptr, nullptr, st);
   ck(cudaMemcpyAsync(dxh, io_dx_.p, n, cudaMemcpyDeviceToHost, st), "d2h dx");
-  ck(cudaStreamSynchronize(st), "sync");
+  sync_comm(st, "sync");
 }
 
 // Host <-> device staging copy, issued in pieces of host_chunk_ bytes (MOE_HOST_CHUNK_MB; 0 =
@@ -1862,6 +1946,13 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->relu_fixups = 0;
   m->fused = (fused_ ? MOE_FUSED_DECODE : 0) | (peer_ && fused_combine_ ? MOE_FUSED_COMBINE : 0);
   m->parallel = parallel_;
+  m->gate_fixups = 0;
+  if (gate_tc_) {
+    int32_t nf = 0;
+    ck(cudaMemcpy(&nf, gate_fix_.p, 4, cudaMemcpyDeviceToHost), "copy");
+    ck(cudaMemset(gate_fix_.p, 0, 4), "memset");
+    m->gate_fixups = nf;
+  }
   if (cfg_.dtype == MOE_DTYPE_BF16) {
     // [2]: the last fixup's list size; [3]: the largest list of any fixup since the last read
     // (an overflow in an earlier chunk or source range must not be masked by a later one)

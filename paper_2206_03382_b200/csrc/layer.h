@@ -53,7 +53,7 @@ int32_t select_parallelism(double local_experts, int64_t gathered_capacity, int6
 enum Phase : int {
   kPhGate = 0, kPhEncode, kPhUp, kPhDown, kPhDecode, kPhDecodeBwd, kPhDgradMask, kPhDgrad,
   kPhWgrad1, kPhWgrad2, kPhEncodeBwd, kPhA2aFwd, kPhA2aBwd, kPhAssign, kPhReluFix,
-  kPhXferDispatch, kPhXferCombine, kNumPhases
+  kPhXferDispatch, kPhXferCombine, kPhWeightStats, kNumPhases
 };
 
 class Layer {
@@ -108,6 +108,8 @@ class Layer {
   void peer_push_rows(int ch, const void* src, int chunk, int phase, int slot, uint32_t row0,
                       uint32_t nrows, uint32_t epoch);
   double allreduce_max_host(double v);
+  void sync_comm(cudaStream_t s, const char* what);  // polls NCCL async errors, times out
+  void check_comm(const char* what);                 // throws MOE_ECOMM on an NCCL async error
   // Sharded placement (W = E*s, moe_layer.cpp:17-108): grouped NCCL exchanges of chunk `chunk`,
   // dir 0 = dispatch (z order -> [chunk][nsrc][cc] receive order), dir 1 = combine (inverse; P2
   // lands the s partials in [chunk][E][s][cc] order for shard_sum).
@@ -159,6 +161,9 @@ class Layer {
   bool bwd_pending_ = false;  // last forward's receive buffer still held for a backward
 
   DevMem wg_, w1_, w2_, dw1_, dw2_;
+  // certified tensor-core gate: bf16 hi/lo split of Wg, max column norm, re-decision counter
+  DevMem wg_pieces_, wg_nmax_, gate_fix_, gate_flags_;
+  bool gate_tc_ = false, wg_dirty_ = true;
   // cosine router (RouterParams, gating.hpp:25-30): P [M][256], C [E][256], C^T, |C_e|, x . P
   DevMem cos_p_, cos_ce_, cos_ct_, cos_en_, cos_buf_, gate_err_;
   double cos_tau_ = 1.0;

@@ -43,6 +43,7 @@ class MoELayerConfig:
     router: str = "linear"      # RouterKind (moe_layer.hpp:10): "linear" or "cosine"
     parallel: str = "p1"        # ParallelControl (sharded placement): "p1", "p2" or "adaptive"
     a2a_algo: str = "linear"    # StrategyControl::fixed.algo: "linear" or "2dh"
+    gate_precision: str = "auto"  # "auto" (certified tensor-core gate where it applies) or "fp64"
 
     def to_c(self) -> MoeConfig:
         return MoeConfig(self.world_size, self.gpus_per_node, self.global_experts, self.model_dim,
@@ -52,7 +53,8 @@ class MoELayerConfig:
                          {"peer": 0, "nccl": 1}[self.a2a_backend],
                          {"linear": 0, "cosine": 1}[self.router],
                          {"p1": 0, "p2": 1, "adaptive": 2}[self.parallel],
-                         {"linear": 0, "2dh": 1}[self.a2a_algo])
+                         {"linear": 0, "2dh": 1}[self.a2a_algo],
+                         {"auto": 0, "fp64": 1}[self.gate_precision])
 
     @property
     def local_experts(self) -> int:
@@ -85,6 +87,7 @@ class StepMetricsPy:
     relu_fixups: int = 0
     fused: int = 0  # MOE_FUSED_DECODE (1) | MOE_FUSED_COMBINE (2)
     parallel: str = "p1"  # StepMetrics::parallel
+    gate_fixups: int = 0  # certified gate: tokens re-decided in fp64 since the last read
 
 
 @dataclass
@@ -240,7 +243,7 @@ class LayerState:
         check(lib().moe_get_metrics(self._h, C.byref(m)), self._h)
         return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
                              m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups, m.fused,
-                             "p2" if m.parallel == 1 else "p1")
+                             "p2" if m.parallel == 1 else "p1", m.gate_fixups)
 
     def grad_slices(self):
         """reduce_scatter_grads_p1: this rank's slice of every expert's dW1 / dW2 (fp32 device),

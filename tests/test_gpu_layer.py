@@ -49,7 +49,10 @@ def test_layer_forward_backward(cuda, case):
     assert cap == ref["capacity"]
     assert np.array_equal(idxs, ref["idxs"])
     assert np.array_equal(loc, ref["locations"])
-    np.testing.assert_allclose(gates, ref["gates"], rtol=1e-12, atol=0)
+    # gate values: fp64 DMMA gate (f32 / BPR layers) up to summation order; the certified
+    # tensor-core gate (bf16 FIFO) carries its logit error -- ~1e-6 typical, checked at 1e-4
+    certified = dt == "bf16" and not bpr and E % 8 == 0 and M % 64 == 0
+    np.testing.assert_allclose(gates, ref["gates"], rtol=1e-4 if certified else 1e-12, atol=0)
     tol = 1e-5 if dt == "f32" else 2e-2
     y = res.y.double().cpu().numpy()
     assert oracle.max_rel_diff(y, ref["y"]) < tol
@@ -257,7 +260,10 @@ def test_layer_cosine_router(cuda, E, k, f, M, V, T, bpr, dt, cap):
     idxs, loc, gates, capv = st.routing()
     assert capv == ref["capacity"]
     assert np.array_equal(idxs, ref["idxs"]) and np.array_equal(loc, ref["locations"])
-    np.testing.assert_allclose(gates, ref["gates"], rtol=1e-12, atol=0)
+    # gate values: fp64 DMMA gate (f32 / BPR layers) up to summation order; the certified
+    # tensor-core gate (bf16 FIFO) carries its logit error -- ~1e-6 typical, checked at 1e-4
+    certified = dt == "bf16" and not bpr and E % 8 == 0 and M % 64 == 0
+    np.testing.assert_allclose(gates, ref["gates"], rtol=1e-4 if certified else 1e-12, atol=0)
     tol = 1e-5 if dt == "f32" else 2e-2
     for name, got in (("y", res.y), ("dx", g.dx), ("dw1", g.dw1), ("dw2", g.dw2)):
         assert oracle.max_rel_diff(got.double().cpu().numpy(), ref[name]) < tol, name
