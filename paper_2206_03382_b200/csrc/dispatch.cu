@@ -114,20 +114,41 @@ __device__ __forceinline__ void zero_dropped_rows(const DropZero& d) {
 // Destination row of slot-major row `row` = (block b, chunk i, expert e, slot c % cc): the send
 // buffer, or (this rank's experts, LocalDest) the receive buffer's own-source segment.
 __device__ __forceinline__ bool is_own(const LocalDest& ld, int e) {
-  return ld.recv != nullptr && e / ld.dE == ld.rank;
+  return ld.all_peers || (ld.recv != nullptr && e / ld.dE == ld.rank);
 }
 __device__ __forceinline__ size_t own_row(const LocalDest& ld, const SlotGeom& g, int i, int e, int rem) {
   return (static_cast<size_t>(i * ld.W + ld.rank) * ld.dE + (e - ld.rank * ld.dE)) * g.cc + rem % g.cc;
 }
+// fused dispatch: expert e's owner p receives this rank's rows at source segment `rank`
+__device__ __forceinline__ size_t peer_row(const LocalDest& ld, const SlotGeom& g, int i, int e, int rem) {
+  const int p = e / ld.dE;
+  return (static_cast<size_t>(i * ld.W + ld.rank) * ld.dE + (e - p * ld.dE)) * g.cc + rem % g.cc;
+}
 template <typename T>
 __device__ __forceinline__ T* gather_dst(T* z, const LocalDest& ld, const SlotGeom& g, size_t row,
                                          int i, int e, int rem) {
+  if (ld.all_peers) return static_cast<T*>(ld.peer_recv[e / ld.dE]) + peer_row(ld, g, i, e, rem) * g.M;
   if (is_own(ld, e)) return static_cast<T*>(ld.recv) + own_row(ld, g, i, e, rem) * g.M;
   return z + row * g.M;
+}
+__device__ __forceinline__ bool want_norm(const float* rownorm, const LocalDest& ld, int e) {
+  if (ld.all_peers) return ld.peer_norm[e / ld.dE] != nullptr;
+  return rownorm != nullptr || (ld.recv_norm != nullptr && is_own(ld, e));
+}
+// fused dispatch: before the first store into a peer's receive buffer every peer must have
+// released it (freed flags of the previous epoch); CTA-uniform
+__device__ __forceinline__ void wait_peers_released(const LocalDest& ld) {
+  if (!ld.all_peers || ld.freed.base == nullptr) return;
+  if (threadIdx.x < 32) wait_flags_warp(ld.freed);
+  __syncthreads();
 }
 // where the row's norm goes: the receive-side array for own rows (if given), else z order
 __device__ __forceinline__ float* norm_dst(float* rownorm, const LocalDest& ld, const SlotGeom& g,
                                            size_t row, int i, int e, int rem) {
+  if (ld.all_peers) {
+    float* pn = ld.peer_norm[e / ld.dE];
+    return pn ? pn + peer_row(ld, g, i, e, rem) : nullptr;
+  }
   if (is_own(ld, e) && ld.recv_norm != nullptr) return ld.recv_norm + own_row(ld, g, i, e, rem);
   return rownorm ? rownorm + row : nullptr;
 }
@@ -142,6 +163,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   pdl_entry();
   if (reset != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reset = 0u;
   zero_dropped_rows(dzero);
+  wait_peers_released(ld);
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
@@ -174,7 +196,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
             const int v = v0 + u * 32 + lane;
             if (v < nv) {
               dst[v] = buf[u];
-              if (rownorm || (ld.recv_norm && is_own(ld, e))) {
+              if (want_norm(rownorm, ld, e)) {
                 float f[VN];
                 Vec<T>::to_f32(buf[u], f);
 #pragma unroll
@@ -184,7 +206,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
           }
         }
       }
-      if (rownorm || (ld.recv_norm && is_own(ld, e))) {
+      if (want_norm(rownorm, ld, e)) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
         if (lane == 0) {
@@ -200,7 +222,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         dst[m] = v;
         ssq = fmaf(to_f(v), to_f(v), ssq);
       }
-      if (rownorm || (ld.recv_norm && is_own(ld, e))) {
+      if (want_norm(rownorm, ld, e)) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
         if (lane == 0) {
@@ -210,6 +232,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       }
     }
   }
+  if (ld.all_peers) __threadfence_system();  // NVLink stores performed before the ready flags
 }
 
 // ------------------------------------------------------------------ decode
@@ -290,6 +313,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
                       LocalDest ld) {
   pdl_entry();
   zero_dropped_rows(dzero);
+  wait_peers_released(ld);
   const int lane = threadIdx.x % 32;
   const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
   const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
@@ -341,6 +365,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         dst[m] = t < 0 ? from_f<T>(0.0f) : from_f<T>(gv * to_f(dy[static_cast<size_t>(t) * g.M + m]));
     }
   }
+  if (ld.all_peers) __threadfence_system();  // NVLink stores performed before the ready flags
 }
 
 // d_gates[t, j] = <Z[row], dy[t]> in fp64 (the layer itself discards it, moe_layer.cpp:268-270).

@@ -7,20 +7,23 @@
 // re-decided from fp64 logits inside the same CTA:
 //
 //   Wg = hi + lo with hi = bf16(Wg), lo = bf16(Wg - hi)   (|Wg - hi - lo| <= 2^-18 |Wg|)
-//   L~[t][e] = sum over 64-wide K chunks of fp64(HMMA_fp32(x, hi) + HMMA_fp32(x, lo))
-//   |L~ - L| <= eps_t = 2^-14 * |x_t|_2 * max_e |Wg[:, e]|_2
-// x is bf16, so every product is exact. Each K chunk starts from a zero fp32 accumulator (4
-// m16n8k16 steps) and is added into an fp64 running sum, so the fp32 error never scales with the
-// whole row: assuming a step truncates each of its 17 aligned addends (16 products + C) to the
-// largest one's 24-bit grid, a chunk errs by <= 4 * 18 * 2^-23 * 2 * sum_chunk|x w| ~ 2^-15.8 *
-// sum_chunk|x w|; with the split residual the total is <= 2^-15.5 * sum|x w| <= 2^-15.5 |x|_2
-// |w|_2 (Cauchy-Schwarz). eps_t keeps a 2.8x margin on that pessimistic model (measured errors
-// are ~100x smaller). A token is certified when each of its first k sorted logits beats the next
-// by more than 2 eps_t; then its idxs are the fp64 reference's (exactly equal logits never
-// certify). Uncertified tokens go to a list that gate_fixup_kernel re-decides from fp64 logits
-// (products of bf16 x with fp64 Wg are exact; only the summation order differs from Eigen) with
-// the fp64 softmax / top-k of the DMMA gate, patching idxs / gates / the CTA histograms before
-// the capacity scan reads them.
+//   L~[t][e] = fp32 sum of the fp32 partials of HMMA(x, hi) over 32-wide K pieces
+//              + one fp32 HMMA accumulation of x . lo over the whole K
+//   |L~ - L| <= eps_t = 2^-15 * |x_t|_2 * max_e |Wg[:, e]|_2
+// x is bf16, so every product is exact. Error model of one m16n8k16 step: each of its 17
+// addends (16 products + the accumulator) truncated to the largest one's 24-bit grid, <= 18 *
+// 2^-23 * (sum|products| + |C|). The hi accumulator restarts from zero every 2 steps and is added
+// into an fp32 running sum, so the products are never aligned to the whole row's sum:
+// <= 2 * 18 * 2^-23 * 2 * sum|x w| = 2^-16.8 sum|x w|. The lo piece is 2^-9 of the magnitude:
+// 64 steps over K = 1024 err <= 2^-21.8 sum|x w|. Adding the 32 folded partials in fp32 errs by
+// <= 32 * 2^-24 sum|x w| = 2^-19; with the split residual 2^-18 the total is <= 2^-16.05
+// sum|x w| <= 2^-16.05 |x|_2 |w|_2 (Cauchy-Schwarz); eps_t keeps a 2.1x margin on that
+// pessimistic model (measured errors are ~100x smaller). A token is certified when each of its
+// first k sorted logits beats the next by more than 2 eps_t; then its idxs are the fp64
+// reference's (exactly equal logits never certify). Uncertified tokens go to a list that
+// gate_fixup_kernel re-decides from fp64 logits (products of bf16 x with fp64 Wg are exact; only
+// the summation order differs from Eigen) with the fp64 softmax / top-k of the DMMA gate,
+// patching idxs / gates / the CTA histograms before the capacity scan reads them.
 // Gate VALUES of certified tokens come from the softmax of L~ (relative error ~1e-6 typical,
 // bounded by ~4 eps_t); they scale expert outputs, which the north star holds to 2e-2 (bf16).
 // BPR needs fp64-accurate cross-token keys, so BPR layers keep the DMMA gate.
@@ -43,9 +46,11 @@ namespace {
 constexpr int kTcWarps = 4;              // 4 warps x 16 tokens = the 64-token gate block
 constexpr int kTcTok = kTcWarps * 16;
 constexpr int kTcKC = 64;                // K per stage (one 128-byte row chunk)
-constexpr int kTcStages = 4;
-constexpr double kTcEpsScale = 1.0 / 16384.0;  // 2^-14
+constexpr int kTcStages = 3;  // 48 KiB (E = 32): 4 CTAs per SM, the 512 TGT blocks in one wave
+constexpr double kTcEpsScale = 1.0 / 32768.0;  // 2^-15
+constexpr int kTcFold = 2;                      // hi-piece mma steps per fp32 accumulator
 constexpr int kFixWarps = 8;                   // fixup CTA: warps split M
+constexpr int kFixTok = 4;                     // fixup CTA: tokens re-decided together
 constexpr int kTcMaxK = 8;
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
@@ -106,7 +111,7 @@ struct TcArgs {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel(TcArgs a) {
   using Cf = TcCfg<NT>;
   constexpr int E = Cf::E;
   constexpr int NTH = kTcWarps * 32;
@@ -136,12 +141,16 @@ __global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
     }
   };
 
-  double tot[NT][4];  // fp64 running sums of the per-chunk fp32 accumulators (hi + lo)
+  // hi piece: fp32 accumulators restarted every kTcFold mma steps and added into fp32 running
+  // sums; lo piece (2^-9 of the magnitude): one fp32 accumulator over the whole K
+  float run[NT][4], hacc[NT][4], lacc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) tot[j][i] = 0.0;
-  float ss0 = 0.0f, ss1 = 0.0f;  // sum of squares of this lane's A elements, rows g and g + 8
+    for (int i = 0; i < 4; ++i) run[j][i] = hacc[j][i] = lacc[j][i] = 0.0f;
+  // |x_t|^2 on the tensor pipe: the A fragment's row halves are exactly the B fragments of
+  // X_rows^T, so HMMA(A, A^T) accumulates X X^T blocks whose diagonals are the row norms
+  float nacc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
 
   const int nch = M / kTcKC;
 #pragma unroll
@@ -160,85 +169,81 @@ __global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
     if (ch + kTcStages - 1 < nch) issue(ch + kTcStages - 1);
     cp_commit();
     const uint32_t st = sbase + (ch % kTcStages) * Cf::STAGE;
-    float acc[2][NT][4];
-#pragma unroll
-    for (int p = 0; p < 2; ++p)
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[p][j][i] = 0.0f;
 #pragma unroll
     for (int ks = 0; ks < kTcKC / 16; ++ks) {
       uint32_t af[4];
       ldsm_x4(sw(st, a_row, ks * 2 + a_kc), af[0], af[1], af[2], af[3]);
-      ss0 = fmaf(bf_lo(af[0]), bf_lo(af[0]), ss0);
-      ss0 = fmaf(bf_hi(af[0]), bf_hi(af[0]), ss0);
-      ss0 = fmaf(bf_lo(af[2]), bf_lo(af[2]), ss0);
-      ss0 = fmaf(bf_hi(af[2]), bf_hi(af[2]), ss0);
-      ss1 = fmaf(bf_lo(af[1]), bf_lo(af[1]), ss1);
-      ss1 = fmaf(bf_hi(af[1]), bf_hi(af[1]), ss1);
-      ss1 = fmaf(bf_lo(af[3]), bf_lo(af[3]), ss1);
-      ss1 = fmaf(bf_hi(af[3]), bf_hi(af[3]), ss1);
+      hmma(nacc[0], af, af[0], af[2]);  // X . X[rows 0-7]^T
+      hmma(nacc[1], af, af[1], af[3]);  // X . X[rows 8-15]^T
+      // B row groups q = piece * NT + j (8 experts each), two per ldmatrix.x4
 #pragma unroll
-      for (int p = 0; p < 2; ++p)
+      for (int q = 0; q < 2 * NT; q += 2) {
+        uint32_t b[4];
+        ldsm_x4(sw(st + Cf::XB, (q + (lane >> 4)) * 8 + b_row, ks * 2 + b_kc), b[0], b[1], b[2], b[3]);
+        if (q < NT) hmma(hacc[q], af, b[0], b[1]);
+        else hmma(lacc[q - NT], af, b[0], b[1]);
+        if (q + 1 < NT) hmma(hacc[q + 1], af, b[2], b[3]);
+        else hmma(lacc[q + 1 - NT], af, b[2], b[3]);
+      }
+      if (ks % kTcFold == kTcFold - 1) {
+        // fold the hi accumulator (kTcFold steps, K = 16 * kTcFold) into the running sum
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          uint32_t b0, b1;
-          ldsm_x2(sw(st + Cf::XB, p * E + j * 8 + b_row, ks * 2 + b_kc), b0, b1);
-          hmma(acc[p][j], af, b0, b1);
-        }
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            run[j][i] += hacc[j][i];
+            hacc[j][i] = 0.0f;
+          }
+      }
     }
-#pragma unroll
-    for (int j = 0; j < NT; ++j)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        tot[j][i] += static_cast<double>(acc[0][j][i]) + static_cast<double>(acc[1][j][i]);
   }
   cp_wait<0>();
 
   // ---- epilogue: lane (g = lane / 4, c = lane % 4) holds rows g and g + 8, columns 8j + 2c + i
   const int g = lane >> 2, cq = lane & 3;
-  ss0 += __shfl_xor_sync(0xffffffffu, ss0, 1);
-  ss0 += __shfl_xor_sync(0xffffffffu, ss0, 2);
-  ss1 += __shfl_xor_sync(0xffffffffu, ss1, 1);
-  ss1 += __shfl_xor_sync(0xffffffffu, ss1, 2);
-  const double wn = static_cast<double>(__ldg(a.wn_max));
+  // row norms: the diagonal of nacc[0] (row g) / nacc[1] (row g + 8) sits in lane (g, g / 2),
+  // element g % 2 (rows 0-7) / 2 + g % 2 (rows 8-15); positive-term HMMA sums err by at most
+  // 64 * 18 * 2^-23 relative at K = 1024, so |x|^2 * (1 + 2^-8) bounds it from above
+  const int src_lane = g * 4 + g / 2;
+  float d0 = (g & 1) ? nacc[0][1] : nacc[0][0];
+  float d1 = (g & 1) ? nacc[1][3] : nacc[1][2];
+  d0 = __shfl_sync(0xffffffffu, d0, src_lane);
+  d1 = __shfl_sync(0xffffffffu, d1, src_lane);
+  const float wn = __ldg(a.wn_max);
   const int k = a.k;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int tt = warp * 16 + g + 8 * h;
     const bool tok_ok = tt < ntok;
     const int t = t_begin + tt;
-    double L[NT][2];
+    float L[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
-        L[j][i] = tot[j][2 * h + i];
-    // |x_t|_2 rounded up (fp32 sum of squares of exact bf16 values: relative error < 2^-14)
-    const double xn = sqrt(static_cast<double>(h ? ss1 : ss0)) * (1.0 + 1.0 / 4096.0);
-    const double eps = kTcEpsScale * xn * wn;
-    double mx = -DBL_MAX;
+      for (int i = 0; i < 2; ++i) L[j][i] = run[j][2 * h + i] + lacc[j][2 * h + i];
+    const float eps = static_cast<float>(kTcEpsScale) * sqrtf((h ? d1 : d0) * (1.0f + 1.0f / 256.0f)) * wn;
+    float mx = -FLT_MAX;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) mx = fmax(mx, fmax(L[j][0], L[j][1]));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    double s = 0.0;
+    for (int j = 0; j < NT; ++j) mx = fmaxf(mx, fmaxf(L[j][0], L[j][1]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    // softmax denominator in fp32 (terms below e^-87 vanish; they are < 2^-125 of the sum)
+    float s = 0.0f;
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) s += exp(L[j][i] - mx);
+      for (int i = 0; i < 2; ++i) s += __expf(L[j][i] - mx);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     // top-(k + 1) by (logit desc, expert asc); the (k + 1)-th only bounds the k-th's margin
     unsigned taken = 0;
     bool certified = true;
-    double prev = 0.0;
+    float prev = 0.0f;
     int sel[kTcMaxK];
-    double selv[kTcMaxK];
+    float selv[kTcMaxK];
     const int kk = k < E ? k + 1 : k;
     for (int r = 0; r < kk; ++r) {
-      double bv = -DBL_MAX;
+      float bv = -FLT_MAX;
       int bi = 0x7fffffff;
 #pragma unroll
       for (int j = 0; j < NT; ++j)
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
         }
 #pragma unroll
       for (int o = 1; o <= 2; o <<= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > bv || (ov == bv && oi < bi)) {
           bv = ov;
@@ -260,11 +265,11 @@ __global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
         }
       }
       if (((bi & 7) >> 1) == cq) taken |= 1u << ((bi >> 3) * 2 + (bi & 1));
-      if (r > 0 && !(prev - bv > 2.0 * eps)) certified = false;
+      if (r > 0 && !(prev - bv > 2.0f * eps)) certified = false;
       // the reference orders fp64 PROBABILITIES (ties -> lower id): below exp's normal range
       // distinct logits can give equal (denormal / zero) probabilities, so a selected expert
       // that deep under the max is never certified from logits
-      if (r < k && bv - mx < -690.0) certified = false;
+      if (r < k && bv - mx < -690.0f) certified = false;
       prev = bv;
       if (r < k) {
         sel[r] = bi;
@@ -275,7 +280,8 @@ __global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
       if (certified) {
         for (int r = 0; r < k; ++r) {
           a.idxs[static_cast<size_t>(t) * k + r] = sel[r];
-          a.gates[static_cast<size_t>(t) * k + r] = exp(selv[r] - mx) / s;
+          a.gates[static_cast<size_t>(t) * k + r] =
+              exp(static_cast<double>(selv[r] - mx)) / static_cast<double>(s);
           atomicAdd(&sh_hist[sel[r]], 1);
         }
       } else {
@@ -288,46 +294,60 @@ __global__ void __launch_bounds__(kTcWarps * 32) gate_tc_kernel(TcArgs a) {
   for (int e = threadIdx.x; e < E; e += NTH) a.hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
 }
 
-// fp64 re-decision of the tokens gate_tc_kernel could not certify: one token per CTA at a time,
-// warps split M, lanes own experts (lane, lane + 32); warp 0 runs the fp64 softmax + top-k
-// (prob desc, expert asc; gating.cpp:19-78) and patches idxs / gates / the token's CTA histogram
-// row. The last CTA to finish resets the list and adds its size to the metrics counter.
-__global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a) {
-  __shared__ double red[kFixWarps][64];
+// fp64 re-decision of the tokens gate_tc_kernel could not certify. A CTA takes up to kFixTok
+// listed tokens at once (their x rows staged in shared memory) so each fp64 Wg element it streams
+// from L2 serves all of them; warps split M, lanes own experts (lane, lane + 32). Then warp j
+// runs the fp64 softmax + top-k (prob desc, expert asc; gating.cpp:19-78) of token j and patches
+// idxs / gates / the token's CTA histogram row. The last CTA to finish resets the list and adds
+// its size to the metrics counter.
+__global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a, int max_m) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(fsm);                         // [kFixTok][M]
+  double* red = reinterpret_cast<double*>(fsm + static_cast<size_t>(kFixTok) * max_m * 2);  // [kFixTok][warps][64]
   pdl_entry();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = *reinterpret_cast<volatile int32_t*>(a.flag_count);
   const int M = a.M, E = a.E, k = a.k;
   const int mlen = (M + kFixWarps - 1) / kFixWarps;
-  for (int f = blockIdx.x; f < n; f += gridDim.x) {
-    const int t = a.flag_list[f];
-    const __nv_bfloat16* __restrict__ xr = a.x + static_cast<size_t>(t) * M;
-    const double* __restrict__ wg = a.wg;
-    const int m0 = warp * mlen, m1 = min(M, m0 + mlen);
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int e = lane + 32 * i;
-      double p[4] = {0.0, 0.0, 0.0, 0.0};
-      if (e < E) {
-        // 32 independent loads in flight per thread (the loop is L2-latency bound)
-        int m = m0;
-        for (; m + 32 <= m1; m += 32) {
-          double xv[32], wv[32];
-#pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            xv[u] = static_cast<double>(__bfloat162float(__ldg(xr + m + u)));
-            wv[u] = __ldg(wg + static_cast<size_t>(m + u) * E + e);
-          }
-#pragma unroll
-          for (int u = 0; u < 32; ++u) p[u & 3] = fma(xv[u], wv[u], p[u & 3]);
-        }
-        for (; m < m1; ++m)
-          p[0] = fma(static_cast<double>(__bfloat162float(xr[m])), __ldg(a.wg + static_cast<size_t>(m) * E + e), p[0]);
-      }
-      red[warp][e] = (p[0] + p[1]) + (p[2] + p[3]);
+  const double* __restrict__ wg = a.wg;
+  for (int f0 = blockIdx.x * kFixTok; f0 < n; f0 += gridDim.x * kFixTok) {
+    const int nt = min(kFixTok, n - f0);
+    for (int i = threadIdx.x; i < nt * (M / 8); i += blockDim.x) {
+      const int j = i / (M / 8), q = i % (M / 8);
+      const int t = a.flag_list[f0 + j];
+      reinterpret_cast<uint4*>(xs + static_cast<size_t>(j) * M)[q] =
+          __ldg(reinterpret_cast<const uint4*>(a.x + static_cast<size_t>(t) * M) + q);
     }
     __syncthreads();
-    if (warp == 0) {
+    const int m0 = warp * mlen, m1 = min(M, m0 + mlen);
+#pragma unroll
+    for (int i2 = 0; i2 < 2; ++i2) {
+      const int e = lane + 32 * i2;
+      if (e >= E) continue;
+      double p[kFixTok];
+#pragma unroll
+      for (int j = 0; j < kFixTok; ++j) p[j] = 0.0;
+      for (int mb = m0; mb < m1; mb += 16) {
+        double wv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) wv[u] = mb + u < m1 ? __ldg(wg + static_cast<size_t>(mb + u) * E + e) : 0.0;
+#pragma unroll
+        for (int j = 0; j < kFixTok; ++j) {
+          if (j >= nt) break;
+          const __nv_bfloat16* xr = xs + static_cast<size_t>(j) * M;
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (mb + u < m1) p[j] = fma(static_cast<double>(__bfloat162float(xr[mb + u])), wv[u], p[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kFixTok; ++j)
+        if (j < nt) red[(static_cast<size_t>(j) * kFixWarps + warp) * 64 + e] = p[j];
+    }
+    __syncthreads();
+    if (warp < nt) {
+      const int j = warp;
+      const int t = a.flag_list[f0 + j];
       double l[2], pv[2];
       double mx = -DBL_MAX;
 #pragma unroll
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a)
         l[i] = -DBL_MAX;
         if (e < E) {
           double v = 0.0;
-          for (int q = 0; q < kFixWarps; ++q) v += red[q][e];
+          for (int q = 0; q < kFixWarps; ++q) v += red[(static_cast<size_t>(j) * kFixWarps + q) * 64 + e];
           l[i] = v;
           mx = fmax(mx, v);
         }
@@ -468,7 +488,9 @@ int gate_tc_device(const void* x, const void* pieces, const double* wg, const fl
     if (!smem_optin(kern, TcCfg<NT>::SMEM)) return -2;
     launch_k(kern, dim3(blocks * a.cpb), dim3(kTcWarps * 32), TcCfg<NT>::SMEM, st, a);
     if (launch_status() != 0) return -2;
-    launch_k(gate_fixup_kernel, dim3(148 * 4), dim3(kFixWarps * 32), 0, st, a);
+    const int fsmem = kFixTok * M * 2 + kFixTok * kFixWarps * 64 * 8;
+    if (!smem_optin(gate_fixup_kernel, fsmem)) return -2;
+    launch_k(gate_fixup_kernel, dim3(148), dim3(kFixWarps * 32), fsmem, st, a, M);
     return launch_status();
   };
   switch (E / 8) {

@@ -115,6 +115,15 @@ struct LocalDest {
   void* recv = nullptr;
   int W = 1, rank = 0, dE = 0;
   float* recv_norm = nullptr;  // encode: the own rows' norms go here (receive-row index)
+  // Fused dispatch (all_peers): EVERY expert's rows are stored straight into its owner's
+  // receive buffer over NVLink -- peer_recv[p] / peer_norm[p] are rank p's receive buffer / norm
+  // array mapped into this process (p == rank: the local ones) -- after polling `freed` (every
+  // peer released its buffer). No send buffer, no copy-engine push: the stream publishes the
+  // ready flags after the kernel (which fences its stores system-wide).
+  bool all_peers = false;
+  void* peer_recv[8] = {};
+  float* peer_norm[8] = {};
+  FlagWait freed;
 };
 
 // dtype: 0 = bf16, 1 = f32 (x, z, y share the layer dtype). rownorm (optional, [z rows]):

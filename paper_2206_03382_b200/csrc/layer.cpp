@@ -360,6 +360,10 @@ void Layer::alloc_capacity(int cap) {
       // certificate row norms computed by the sender and pushed with the rows (tcgen05 path:
       // the up GEMM then takes the receive wait itself)
       sender_norms_ = cert && fused_combine_;
+      // MOE_DISPATCH=fused: encode / decode-backward store every row straight into its owner's
+      // receive buffer over NVLink (no send buffer, no copy-engine push); default: copy engines
+      const char* dm = std::getenv("MOE_DISPATCH");
+      fused_dispatch_ = dm && std::string(dm) == "fused" && fused_combine_ && W_ <= 8;
       for (auto& e : epoch_) e = 0;  // fresh flag block on every rank
       bwd_pending_ = false;
     }
@@ -1159,12 +1163,27 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     yzero.row_bytes = static_cast<size_t>(M_) * esz_;
   }
   LocalDest own;  // peer backend: this rank's experts' rows go straight into its receive buffer
+  uint32_t fd_epoch = 0;  // fused dispatch: this forward's channel-0 epoch
   if (peer_) {
     own.recv = recv_.p;
     own.W = W_;
     own.rank = rank_;
     own.dE = dE_;
     if (sender_norms_) own.recv_norm = static_cast<float*>(rownorm_.p);
+    if (fused_dispatch_) {
+      if (bwd_pending_) {  // inference-style forward: release the previous epoch's buffer first
+        peer_->signal_freed(st, 0, epoch_[0]);
+        ck(cudaEventRecord(ev_freed_[0], st), "event");
+        bwd_pending_ = false;
+      }
+      fd_epoch = ++epoch_[0];
+      own.all_peers = true;
+      for (int p = 0; p < W_; ++p) {
+        own.peer_recv[p] = peer_->buffer(0, p);
+        own.peer_norm[p] = sender_norms_ ? peer_->norms(p) : nullptr;
+      }
+      own.freed = peer_->freed_wait(0, fd_epoch - 1);
+    }
   }
   float* enc_norm = nullptr;  // row norms computed by the encode pass
   if (cert && W_ == 1) enc_norm = static_cast<float*>(rownorm_.p);
@@ -1175,6 +1194,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       "encode");
   prof_mark(kPhEncode, false, st);
   ++launches_;
+  if (fused_dispatch_)  // every chunk's rows have landed at their owners: publish the flags
+    for (int i = 0; i < degree_; ++i) peer_->signal_ready(st, 0, i, fd_epoch);
 
   const int nseg = degree_ * W_ * dE_;
   GemmArgs up{};
@@ -1231,7 +1252,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   } else if (sharded_) {
     sharded_forward(up, down, cert, st);
   } else if (peer_) {
-    if (bwd_pending_) {
+    if (bwd_pending_ && !fused_dispatch_) {
       // The previous forward was not followed by a backward (inference): its saved expert
       // inputs are dead, so release the receive buffer to the peers now (stream-ordered after
       // that forward's GEMMs).
@@ -1239,18 +1260,22 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
       ck(cudaEventRecord(ev_freed_[0], st), "event");
     }
     // Copy engines over NVLink: all dispatches, then all combines (the reference's FIFO order,
-    // pipeline.cpp:180-190); each chunk's GEMMs start when its blocks have landed.
-    const uint32_t e0 = ++epoch_[0], e1 = ++epoch_[1];
+    // pipeline.cpp:180-190); each chunk's GEMMs start when its blocks have landed. (Fused
+    // dispatch: encode already stored every row at its owner and published the flags.)
+    const uint32_t e0 = fused_dispatch_ ? fd_epoch : ++epoch_[0], e1 = ++epoch_[1];
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
-    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[0], 0), "wait");  // my recv buffer consumed
-    peer_->wait_peers_freed(comm_stream_, 0, e0);
+    if (!fused_dispatch_) {
+      ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[0], 0), "wait");  // my recv buffer consumed
+      peer_->wait_peers_freed(comm_stream_, 0, e0);
+    }
     prof_mark(kPhA2aFwd, true, comm_stream_);
     // first chunk in row parts when the tile shape allows (tcgen05 path): its first rows land
     // while this rank computes its own segment
-    const std::vector<uint32_t> parts0 = first_chunk_parts(cc_, local_first_ && fused_combine_);
+    const std::vector<uint32_t> parts0 =
+        first_chunk_parts(cc_, local_first_ && fused_combine_ && !fused_dispatch_);
     const bool split0 = parts0.size() > 1;
-    for (int i = 0; i < degree_; ++i) {
+    for (int i = 0; i < degree_ && !fused_dispatch_; ++i) {
       if (i == 0 && split0) {
         uint32_t r = 0;
         for (size_t p = 0; p < parts0.size(); ++p) {
@@ -1518,16 +1543,25 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   }
   prof_mark(kPhDecodeBwd, true, st);
   LocalDest own;  // peer backend: this rank's experts' dZ rows go straight into drecv
+  uint32_t fd_epoch = 0;
   if (peer_) {
     own.recv = drecv_.p;
     own.W = W_;
     own.rank = rank_;
     own.dE = dE_;
+    if (fused_dispatch_) {
+      fd_epoch = ++epoch_[2];
+      own.all_peers = true;
+      for (int p = 0; p < W_; ++p) own.peer_recv[p] = peer_->buffer(2, p);
+      own.freed = peer_->freed_wait(2, fd_epoch - 1);
+    }
   }
   ckr(decode_backward_device(g, cfg_.dtype, dy, gb.slot_token, gb.slot_gate, dz_.p, st, dxzero, own),
       "decode_bwd");
   prof_mark(kPhDecodeBwd, false, st);
   ++launches_;
+  if (fused_dispatch_)
+    for (int i = 0; i < degree_; ++i) peer_->signal_ready(st, 2, i, fd_epoch);
 
   const int nseg = degree_ * W_ * dE_;
   GemmArgs dgm{};  // dh = (dY . W2^T) * [a > 0]
@@ -1592,15 +1626,18 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   } else if (sharded_) {
     sharded_backward(dgm, dg, wg1, wg2, gw1, gw2, st);
   } else if (peer_) {
-    const uint32_t e2 = ++epoch_[2], e3 = ++epoch_[3];
+    const uint32_t e2 = fused_dispatch_ ? fd_epoch : ++epoch_[2], e3 = ++epoch_[3];
     ck(cudaEventRecord(ev_sync_, st), "event");
     ck(cudaStreamWaitEvent(comm_stream_, ev_sync_, 0), "wait");
-    ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[2], 0), "wait");
-    peer_->wait_peers_freed(comm_stream_, 2, e2);
+    if (!fused_dispatch_) {
+      ck(cudaStreamWaitEvent(comm_stream_, ev_freed_[2], 0), "wait");
+      peer_->wait_peers_freed(comm_stream_, 2, e2);
+    }
     prof_mark(kPhA2aBwd, true, comm_stream_);
-    const std::vector<uint32_t> parts0 = first_chunk_parts(cc_, local_first_ && fused_combine_);
+    const std::vector<uint32_t> parts0 =
+        first_chunk_parts(cc_, local_first_ && fused_combine_ && !fused_dispatch_);
     const bool split0 = parts0.size() > 1;  // as in forward
-    for (int i = 0; i < degree_; ++i) {  // adjoint of combine
+    for (int i = 0; i < degree_ && !fused_dispatch_; ++i) {  // adjoint of combine
       if (i == 0 && split0) {
         uint32_t r = 0;
         for (size_t p = 0; p < parts0.size(); ++p) {

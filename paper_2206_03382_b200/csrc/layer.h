@@ -164,6 +164,8 @@ class Layer {
   // certified tensor-core gate: bf16 hi/lo split of Wg, max column norm, re-decision counter
   DevMem wg_pieces_, wg_nmax_, gate_fix_, gate_flags_;
   bool gate_tc_ = false, wg_dirty_ = true;
+  // peer transport: dispatch fused into encode / decode-backward (NVLink stores, MOE_DISPATCH=fused)
+  bool fused_dispatch_ = false;
   // cosine router (RouterParams, gating.hpp:25-30): P [M][256], C [E][256], C^T, |C_e|, x . P
   DevMem cos_p_, cos_ce_, cos_ct_, cos_en_, cos_buf_, gate_err_;
   double cos_tau_ = 1.0;

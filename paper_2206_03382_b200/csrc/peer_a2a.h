@@ -81,6 +81,10 @@ class PeerExchange {
   void signal_ready(cudaStream_t st, int ch, int chunk, uint32_t epoch);
   // Channel-ch receive buffer of rank p (this rank's own for p == rank).
   void* buffer(int ch, int p) const { return p == rank_ ? local_bufs_[ch] : peer_bufs_[ch][p]; }
+  // Channel-0 row-norm array of rank p (null when the exchange carries no norms).
+  float* norms(int p) const {
+    return static_cast<float*>(p == rank_ ? local_norms_ : (local_norms_ ? peer_norms_[p] : nullptr));
+  }
 
  private:
   uint32_t* ready_local(int ch, int src, int chunk) const;

@@ -34,7 +34,8 @@ def _check_gates(gates, ref, x, wg):
     fp64 gate, |dg / g| <= 2^-18 |x_t|_2 max_e |Wg[:, e]|_2 (typical errors are ~100x smaller;
     the certificate's own eps is 2^-14 |x| |w|). Re-decided tokens match to fp64 summation order."""
     bound = 2.0 ** -18 * np.linalg.norm(x, axis=1) * np.linalg.norm(wg, axis=0).max()
-    rel = np.abs(gates / ref - 1.0).max(axis=1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rel = np.where(gates == ref, 0.0, np.abs(gates - ref) / np.abs(ref)).max(axis=1)
     assert (rel <= np.maximum(bound, 1e-12)).all(), (rel.max(), bound.min())
 
 

@@ -21,6 +21,9 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     if ce:
         backend = "peer"
         os.environ["MOE_FUSED_COMBINE"] = "0"
+    if backend == "peer-fd":  # peer backend with the dispatch fused into encode (NVLink stores)
+        backend = "peer"
+        os.environ["MOE_DISPATCH"] = "fused"
     cfg = MoELayerConfig(world_size=W, gpus_per_node=m or W, global_experts=E, model_dim=M,
                          hidden_dim=V, tokens_per_step=T, top_k=k, capacity=cap,
                          capacity_factor=f, bpr=bpr, dtype=dt, degree=degree, adaptive=adaptive,
@@ -29,6 +32,7 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     dist.broadcast_object_list(obj, src=0)
     st = LayerState.init(cfg, seed, rank=rank, device=dev.index, nccl_id=obj[0])
     os.environ.pop("MOE_FUSED_COMBINE", None)
+    os.environ.pop("MOE_DISPATCH", None)
     inp = layer_inputs(seed, W, T, M, V, E, dt)
     tdt = cfg.torch_dtype
     xs = torch.as_tensor(inp["x"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
@@ -154,6 +158,9 @@ def main():
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 1, False, "peer"),
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer"),
         (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer-ce"),
+        (2, 2, 1.25, 256, 512, 512, True, "bf16", 2, False, "peer-fd"),
+        (4, 1, 1.0, 256, 512, 1024, False, "bf16", 1, False, "peer-fd"),
+        (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "peer-fd"),
         (4, 1, 1.0, 256, 512, 1024, False, "bf16", 4, False, "peer"),
         (2, 1, 0.5, 128, 256, 300, False, "bf16", 8, False, "peer"),   # drops, ragged chunks
         (2, 2, 1.0, 64, 128, 200, True, "f32", 2, False, "peer"),

@@ -6,7 +6,8 @@ invariance. Launch one rank per GPU:
 C4 per rank: E = 8W experts (8 per GPU), k = 1, f = 1.0, M = 1024, V = 4096, 65 536 tokens per
 rank, bf16, seed 402 (LayerState::init draw order, x / dy drawn after it; test_moe_layer.cpp:70-73).
 
-Every (transport, degree) run -- peer (copy-engine dispatch + NVLink-fused combine) and NCCL, at
+Every (transport, degree) run -- peer (copy-engine dispatch + NVLink-fused combine), peer-fd
+(dispatch fused into the encode / decode-backward kernels as NVLink stores) and NCCL, at
 pipelining degrees 1 / 2 / 4 / 8, and Alg. 1 adaptive -- is checked for:
 * strategy invariance (test_moe_layer.cpp:82-100): routing, y and dx bit-identical to the
   degree-1 peer run; dW1 / dW2 within 1e-5 (the wgrad K-loop visits the capacity chunks in a
@@ -88,6 +89,7 @@ def main():
     # ---- every strategy on the same inputs
     runs = [("peer", d, False) for d in map(int, a.degrees.split(","))]
     runs += [("nccl", d, False) for d in (1, max(map(int, a.degrees.split(","))))]
+    runs += [("peer-fd", d, False) for d in (1, 4)]  # dispatch fused into encode (NVLink stores)
     runs += [("peer", 1, True)]
     base = None
     all_ok = True
@@ -98,12 +100,17 @@ def main():
         return t.item() == 0
 
     for backend, degree, adaptive in runs:
+        fd = backend == "peer-fd"
+        if fd:
+            os.environ["MOE_DISPATCH"] = "fused"
         cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
                              hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f,
-                             dtype="bf16", degree=degree, adaptive=adaptive, a2a_backend=backend)
+                             dtype="bf16", degree=degree, adaptive=adaptive,
+                             a2a_backend="peer" if fd else backend)
         obj = [LayerState.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         st = LayerState.init(cfg, SEED, rank=rank, device=local, nccl_id=obj[0])
+        os.environ.pop("MOE_DISPATCH", None)
         steps = 12 if adaptive else 2
         for _ in range(steps):
             res = forward(st, x)
