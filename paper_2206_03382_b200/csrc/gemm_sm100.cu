@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j) w[j] = ptx::pack_bf16x2(f[2 * j], f[2 * j + 1]);
           if constexpr (kEpi == kEpiReluBf16) {
+#ifndef MOE_EXP_NO_CERT  // timing experiments only (tools/gemm_exp.sh): drops the certificate
             if (cert) {
               // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64
               // re-decision. Prefilter: min |bf16(h)| over the 64 columns (magnitude order ==
@@ -445,6 +446,8 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
                 }
               }
             }
+#endif
+#ifndef MOE_EXP_NO_MASK  // timing experiments only: drops the ReLU bitmask
             // [h > 0] bits from the fp32 values (exact zeros stay 0), relu on the pairs
             uint32_t lo = 0u, hi = 0u;
 #pragma unroll
@@ -454,6 +457,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
             }
             if (args.relu_mask != nullptr && row_ok)
               args.relu_mask[mrow + cols / 64] = (static_cast<unsigned long long>(hi) << 32) | lo;
+#endif
 #pragma unroll
             for (uint32_t j = 0; j < 32; ++j) w[j] = __vmaxs2(w[j], 0u);  // int16 max == bf16 relu
           }
@@ -613,7 +617,13 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, con
            int num_sms, cudaStream_t stream, const PeerMaps* pm = nullptr) {
   static const PeerMaps none{};
   const PeerMaps& p = pm ? *pm : none;
-  constexpr int kEW = kEpi == kEpiReluBf16 ? 8 : 4;  // see EpiCfg
+#ifndef MOE_UP_EPI_WARPS
+#define MOE_UP_EPI_WARPS 8
+#endif
+#ifndef MOE_EPI_WARPS
+#define MOE_EPI_WARPS 4
+#endif
+  constexpr int kEW = kEpi == kEpiReluBf16 ? MOE_UP_EPI_WARPS : MOE_EPI_WARPS;  // see EpiCfg
   if (gemm_cta_group() == 2)
     return launch_cg<kAMN, kBMN, kEpi, kRowK, 2, kIdx, kEW>(a, b, d, args, p, num_sms, stream);
   return launch_cg<kAMN, kBMN, kEpi, kRowK, 1, kIdx, kEW>(a, b, d, args, p, num_sms, stream);
