@@ -303,6 +303,13 @@ int moe_op_gemm(int32_t kind, int32_t dtype, int32_t use_tc, const void* A, cons
                 int64_t seg_base, int64_t N, int64_t K, int64_t Mo, int64_t nseg_total,
                 void* stream);
 
+/* The ReLU certificate's weight statistics (bf16 path; no reference counterpart -- the fp64
+ * reference needs no certificate): for n experts' w1 [n][M][V] bf16, colnorm [n][V] =
+ * |w1[:, v]|_2 rounded up, colnorm_blk [n][V/64] = max over each 64-column block, w1t [n][V][M] =
+ * w1 transposed. One pass over w1 when M % 64 == 0 and V % 64 == 0. */
+int moe_op_weight_stats(const void* w1, int64_t n, int64_t M, int64_t V, float* colnorm,
+                        float* colnorm_blk, void* w1t, void* stream);
+
 /* Rng stream (core.cpp:66-83) on the device: dst[i] = lo + (hi-lo)*uniform(draw offset+i). */
 int moe_op_fill_uniform(void* dst, int32_t dtype, int64_t n, uint64_t seed, uint64_t offset,
                         double lo, double hi, void* stream);

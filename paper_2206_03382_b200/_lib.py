@@ -101,6 +101,7 @@ SIGNATURES = {
     "moe_op_encode_backward": (I32, [P, I32, I64, I64, I64, I64, I64, I64, I64, P, P, P, P]),
     "moe_op_expert_ffn": (I32, [P, P, P, P, P, I32, I64, I64, I64, I64, P]),
     "moe_op_expert_ffn_backward": (I32, [P, P, P, P, P, P, P, I32, I64, I64, I64, I64, P]),
+    "moe_op_weight_stats": (I32, [P, I64, I64, I64, PF, PF, P, P]),
     "moe_op_gemm": (I32, [I32, I32, I32, P, P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, P]),
     "moe_op_fill_uniform": (I32, [P, I32, I64, U64, U64, D, D, P]),
     "moe_memo_create": (I32, [D, C.POINTER(P)]),

@@ -139,7 +139,7 @@ unsigned long long* certified_up(int dtype, const void* x, const void* w1, void*
   const unsigned int cap =
       static_cast<unsigned int>(std::max<int64_t>(1 << 16, n * rows * V / 256));
   auto* list = sc.get<unsigned long long>(cap);
-  auto* count = sc.get<unsigned int>(3);  // list size, fixup CTAs done, last list size
+  auto* count = sc.get<unsigned int>(4);  // list size, fixup CTAs done, last / largest list size
   ckr(moe::weight_stats_device(w1, static_cast<int>(n), static_cast<int>(M), static_cast<int>(V),
                                colnorm, colnorm_blk, w1t, st),
       "weight stats");
@@ -147,7 +147,7 @@ unsigned long long* certified_up(int dtype, const void* x, const void* w1, void*
   all.nsegs = 1;
   all.seg_rows = all.nrows = n * rows;
   ckr(moe::rownorm_device(x, static_cast<int>(M), rownorm, all, st), "rownorm");
-  ck(cudaMemsetAsync(count, 0, 3 * sizeof(unsigned int), st), "memset");
+  ck(cudaMemsetAsync(count, 0, 4 * sizeof(unsigned int), st), "memset");
   up.rownorm = rownorm;
   up.colnorm = colnorm;
   up.colnorm_blk = colnorm_blk;
@@ -585,6 +585,17 @@ int moe_op_expert_ffn_backward(const void* x, const void* w1, const void* w2, co
     wg.N = M;
     wg.Mo = V;
     expert_gemm(moe::kGemmWgrad, dtype, -1, a, dy, dw2, wg, nseg, st);
+  });
+}
+
+int moe_op_weight_stats(const void* w1, int64_t n, int64_t M, int64_t V, float* colnorm,
+                        float* colnorm_blk, void* w1t, void* stream) {
+  return guard(nullptr, [&] {
+    require_device();
+    if (n < 1 || M < 1 || V < 1) throw moe::MoeError(MOE_EINVAL, "weight_stats: empty shape");
+    ckr(moe::weight_stats_device(w1, static_cast<int>(n), static_cast<int>(M), static_cast<int>(V),
+                                 colnorm, colnorm_blk, w1t, S(stream)),
+        "weight stats");
   });
 }
 

@@ -22,6 +22,7 @@
 #include <stdexcept>
 #include <string>
 #include <set>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -53,15 +54,18 @@ void ckn(ncclResult_t r, const char* what) {
 }  // namespace
 
 bool smem_optin_raw(const void* kern, int bytes) {
+  // per (kernel, device): the largest dynamic shared memory size set so far (a later, larger
+  // request -- e.g. a second layer with a larger M -- raises it again)
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, int> done;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count({kern, dev})) return true;
+  auto it = done.find({kern, dev});
+  if (it != done.end() && it->second >= bytes) return true;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
     return false;
-  done.insert({kern, dev});
+  done[{kern, dev}] = bytes;
   return true;
 }
 

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) weight_stats_kernel(const __nv_bfloat16* 
                                                            __nv_bfloat16* __restrict__ w1t) {
   pdl_entry();
   __shared__ __align__(16) __nv_bfloat16 tile[64][64 + 8];
-  __shared__ double part[4][64];
+  __shared__ double part[8][64];
   __shared__ float wmax[2];
   const int nb = V / 64;
   const int g = blockIdx.x / nb, b = blockIdx.x % nb;
@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(256) weight_stats_kernel(const __nv_bfloat16* 
   const __nv_bfloat16* src = w1 + static_cast<size_t>(g) * M * V + 64 * b;
   __nv_bfloat16* dst = w1t + (static_cast<size_t>(g) * V + 64 * b) * M;
   const int lr = t / 8, lc = (t % 8) * 8;  // load: rows lr, lr + 32; 8 columns at lc
-  const int c = t % 64, qq = t / 64;       // transpose: column c, row groups qq and qq + 4
-  double acc = 0.0;
+  const int cp = t % 32, rg = t / 32;      // transpose: columns 2cp, 2cp + 1; rows [8 rg, 8 rg + 8)
+  double acc0 = 0.0, acc1 = 0.0;
   uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(lr) * V + lc));
   uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(lr + 32) * V + lc));
   for (int m0 = 0; m0 < M; m0 += 64) {
@@ -102,26 +102,32 @@ __global__ void __launch_bounds__(256) weight_stats_kernel(const __nv_bfloat16* 
       v0 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(m0 + 64 + lr) * V + lc));
       v1 = __ldcs(reinterpret_cast<const uint4*>(src + static_cast<size_t>(m0 + 96 + lr) * V + lc));
     }
-    // w1t row 64 b + c, elements [m0 + 8 q, m0 + 8 q + 8); a warp reads 32 adjacent columns
+    // 8 rows x the column pair as 32-bit words; low halves -> column 2cp, high -> 2cp + 1
+    uint32_t wv[8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = qq + 4 * h;
-      __align__(16) __nv_bfloat16 o[8];
+    for (int j = 0; j < 8; ++j) wv[j] = *reinterpret_cast<const uint32_t*>(&tile[8 * rg + j][2 * cp]);
+    uint4 o0, o1;
+    o0.x = __byte_perm(wv[0], wv[1], 0x5410); o1.x = __byte_perm(wv[0], wv[1], 0x7632);
+    o0.y = __byte_perm(wv[2], wv[3], 0x5410); o1.y = __byte_perm(wv[2], wv[3], 0x7632);
+    o0.z = __byte_perm(wv[4], wv[5], 0x5410); o1.z = __byte_perm(wv[4], wv[5], 0x7632);
+    o0.w = __byte_perm(wv[6], wv[7], 0x5410); o1.w = __byte_perm(wv[6], wv[7], 0x7632);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        o[j] = tile[8 * q + j][c];
-        const double w = __bfloat162float(o[j]);
-        acc = fma(w, w, acc);
-      }
-      __stcs(reinterpret_cast<uint4*>(dst + static_cast<size_t>(c) * M + m0 + 8 * q),
-             *reinterpret_cast<const uint4*>(o));
+    for (int j = 0; j < 8; ++j) {
+      const double lo = __uint_as_float(wv[j] << 16), hi = __uint_as_float(wv[j] & 0xffff0000u);
+      acc0 = fma(lo, lo, acc0);
+      acc1 = fma(hi, hi, acc1);
     }
+    __stcs(reinterpret_cast<uint4*>(dst + static_cast<size_t>(2 * cp) * M + m0 + 8 * rg), o0);
+    __stcs(reinterpret_cast<uint4*>(dst + static_cast<size_t>(2 * cp + 1) * M + m0 + 8 * rg), o1);
     __syncthreads();
   }
-  part[qq][c] = acc;
+  part[rg][2 * cp] = acc0;
+  part[rg][2 * cp + 1] = acc1;
   __syncthreads();
   if (t < 64) {
-    const double s = part[0][t] + part[1][t] + part[2][t] + part[3][t];
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += part[q][t];
     float n = static_cast<float>(sqrt(s)) * 1.0001f;  // |W1[:, col]|_2, rounded up
     colnorm[static_cast<size_t>(g) * V + 64 * b + t] = n;
     for (int o = 16; o > 0; o >>= 1) n = fmaxf(n, __shfl_xor_sync(0xffffffffu, n, o));

@@ -154,3 +154,16 @@ def fill_uniform(out: torch.Tensor, seed: int, offset: int, lo: float = -1.0, hi
     check(lib().moe_op_fill_uniform(_p(out), _DT[out.dtype], out.numel(), C.c_uint64(seed),
                                     C.c_uint64(offset), float(lo), float(hi), _st(out)))
     return out
+
+
+def weight_stats(w1: torch.Tensor):
+    """ReLU-certificate weight statistics of w1 [n][M][V] bf16 -> (colnorm [n][V] fp32,
+    colnorm_blk [n][V/64] fp32, w1t [n][V][M] bf16)."""
+    _need(w1, "w1")
+    n, M, V = w1.shape
+    colnorm = torch.empty(n, V, dtype=torch.float32, device=w1.device)
+    blk = torch.empty(n, V // 64 + 1, dtype=torch.float32, device=w1.device)
+    w1t = torch.empty(n, V, M, dtype=w1.dtype, device=w1.device)
+    check(lib().moe_op_weight_stats(_p(w1), n, M, V, C.cast(_p(colnorm), _lib.PF),
+                                    C.cast(_p(blk), _lib.PF), _p(w1t), _st(w1)))
+    return colnorm, blk[:, :V // 64], w1t

@@ -260,3 +260,19 @@ def test_cosine_gating_rejects_zero_norms(cuda):
     x[5] = 0.0
     with pytest.raises(MoeError):
         ops.gating_cosine(x, proj, experts, 1, 1)
+
+
+@pytest.mark.parametrize("n,M,V", [(2, 1024, 4096), (3, 64, 192), (1, 40, 72)])
+def test_weight_stats_matches_torch(cuda, n, M, V):
+    """The ReLU certificate's weight statistics (one-pass kernel for M, V multiples of 64; the
+    generic kernels otherwise): W1^T bit-exact, column norms >= the fp64 norm and within 2e-4."""
+    from paper_2206_03382_b200 import ops
+    w1 = (torch.rand(n, M, V, device="cuda", dtype=torch.float64) - 0.5).to(torch.bfloat16)
+    colnorm, blk, w1t = ops.weight_stats(w1)
+    torch.cuda.synchronize()
+    assert torch.equal(w1t, w1.transpose(1, 2).contiguous())
+    ref = w1.double().pow(2).sum(dim=1).sqrt()
+    cn = colnorm.double()
+    assert (cn >= ref * (1 - 1e-7)).all() and ((cn - ref) / ref).abs().max() < 2e-4
+    if V % 64 == 0:
+        assert torch.equal(blk, colnorm.view(n, V // 64, 64).amax(dim=2))
