@@ -394,6 +394,10 @@ int op_gating(const void* x, int32_t x_dtype, const double* wg, const CosineOp* 
     g.list_base = sc.get<int32_t>(blocks * E);
     g.fill = sc.get<int32_t>(blocks * E);
     g.list = sc.get<int32_t>(Tk);
+    if (bpr) {
+      g.bpr_keys = sc.get<unsigned long long>(Tk);
+      g.bpr_pos = sc.get<int32_t>(Tk);
+    }
     g.cap = sc.get<int32_t>(1);
     g.drops = sc.get<int32_t>(1);
     int32_t* err = nullptr;

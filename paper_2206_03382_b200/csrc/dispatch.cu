@@ -256,6 +256,43 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
       uint4* dst = reinterpret_cast<uint4*>(y + static_cast<size_t>(t) * g.M);
+      if (g.k == 2) {
+        // top-2: both rows' loads in flight before any math; same j-ascending fma order
+        const int2 loc = *reinterpret_cast<const int2*>(locations + static_cast<size_t>(t) * 2);
+        const int2 ex = *reinterpret_cast<const int2*>(idxs + static_cast<size_t>(t) * 2);
+        const double2 gt = *reinterpret_cast<const double2*>(gates + static_cast<size_t>(t) * 2);
+        const uint4* s0 = loc.x >= 0 ? reinterpret_cast<const uint4*>(z + slot_row(g, b, ex.x, loc.x) * g.M) : nullptr;
+        const uint4* s1 = loc.y >= 0 ? reinterpret_cast<const uint4*>(z + slot_row(g, b, ex.y, loc.y) * g.M) : nullptr;
+        const float g0 = static_cast<float>(gt.x), g1 = static_cast<float>(gt.y);
+        for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+          uint4 b0[kUnroll], b1[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv && s0) b0[u] = ld_stream(s0 + v);
+            if (v < nv && s1) b1[u] = ld_stream(s1 + v);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            float acc[VN], f[VN];
+#pragma unroll
+            for (int q = 0; q < VN; ++q) acc[q] = 0.0f;
+            if (s0) {
+              Vec<T>::to_f32(b0[u], f);
+#pragma unroll
+              for (int q = 0; q < VN; ++q) acc[q] = fmaf(g0, f[q], acc[q]);
+            }
+            if (s1) {
+              Vec<T>::to_f32(b1[u], f);
+#pragma unroll
+              for (int q = 0; q < VN; ++q) acc[q] = fmaf(g1, f[q], acc[q]);
+            }
+            if (v < nv) dst[v] = Vec<T>::from_f32(acc);
+          }
+        }
+        continue;
+      }
       for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
         float acc[kUnroll][VN];
 #pragma unroll
@@ -413,6 +450,41 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
       uint4* dst = reinterpret_cast<uint4*>(dx + static_cast<size_t>(t) * g.M);
+      if (g.k == 2) {
+        // top-2: both rows' loads in flight before any math; same j-ascending sum order
+        const int2 loc = *reinterpret_cast<const int2*>(locations + static_cast<size_t>(t) * 2);
+        const int2 ex = *reinterpret_cast<const int2*>(idxs + static_cast<size_t>(t) * 2);
+        const uint4* s0 = loc.x >= 0 ? reinterpret_cast<const uint4*>(dz + slot_row(g, b, ex.x, loc.x) * g.M) : nullptr;
+        const uint4* s1 = loc.y >= 0 ? reinterpret_cast<const uint4*>(dz + slot_row(g, b, ex.y, loc.y) * g.M) : nullptr;
+        for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+          uint4 b0[kUnroll], b1[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nv && s0) b0[u] = ld_stream(s0 + v);
+            if (v < nv && s1) b1[u] = ld_stream(s1 + v);
+          }
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = v0 + u * 32 + lane;
+            float acc[VN], f[VN];
+#pragma unroll
+            for (int q = 0; q < VN; ++q) acc[q] = 0.0f;
+            if (s0) {
+              Vec<T>::to_f32(b0[u], f);
+#pragma unroll
+              for (int q = 0; q < VN; ++q) acc[q] += f[q];
+            }
+            if (s1) {
+              Vec<T>::to_f32(b1[u], f);
+#pragma unroll
+              for (int q = 0; q < VN; ++q) acc[q] += f[q];
+            }
+            if (v < nv) dst[v] = Vec<T>::from_f32(acc);
+          }
+        }
+        continue;
+      }
       for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
         float acc[kUnroll][VN];
 #pragma unroll

@@ -7,17 +7,17 @@
 // re-decided from fp64 logits inside the same CTA:
 //
 //   Wg = hi + lo with hi = bf16(Wg), lo = bf16(Wg - hi)   (|Wg - hi - lo| <= 2^-18 |Wg|)
-//   L~[t][e] = fp32 sum of the fp32 partials of HMMA(x, hi) over 32-wide K pieces
-//              + one fp32 HMMA accumulation of x . lo over the whole K
+//   L~[t][e] = fp32 sum of fp32 partials HMMA(x, hi) + HMMA(x, lo) over 32-wide K pieces
 //   |L~ - L| <= eps_t = 2^-15 * |x_t|_2 * max_e |Wg[:, e]|_2
 // x is bf16, so every product is exact. Error model of one m16n8k16 step: each of its 17
 // addends (16 products + the accumulator) truncated to the largest one's 24-bit grid, <= 18 *
-// 2^-23 * (sum|products| + |C|). The hi accumulator restarts from zero every 2 steps and is added
-// into an fp32 running sum, so the products are never aligned to the whole row's sum:
-// <= 2 * 18 * 2^-23 * 2 * sum|x w| = 2^-16.8 sum|x w|. The lo piece is 2^-9 of the magnitude:
-// 64 steps over K = 1024 err <= 2^-21.8 sum|x w|. Adding the 32 folded partials in fp32 errs by
-// <= 32 * 2^-24 sum|x w| = 2^-19; with the split residual 2^-18 the total is <= 2^-16.05
-// sum|x w| <= 2^-16.05 |x|_2 |w|_2 (Cauchy-Schwarz); eps_t keeps a 2.1x margin on that
+// 2^-23 * (sum|products| + |C|), and within one accumulator window that is <= 18 * 2^-23 times
+// the window's sum|x (|hi| + |lo|)|. The accumulator restarts from zero every 2 K16 steps (4 mma:
+// hi and lo pieces) and is added into an fp32 running sum, so products are never aligned to the
+// whole row's sum: <= 4 * 18 * 2^-23 = 2^-16.8 of each window's sum, 2^-16.8 sum|x w| in all.
+// Adding the 32 partials in fp32 errs by <= 32 * 2^-24 sum|x w| = 2^-19; with the
+// split residual 2^-18 the total is <= 2^-16.05 sum|x w| <= 2^-16.05 |x|_2 |w|_2
+// (Cauchy-Schwarz); eps_t keeps a 2.1x margin on that
 // pessimistic model (measured errors are ~100x smaller). A token is certified when each of its
 // first k sorted logits beats the next by more than 2 eps_t; then its idxs are the fp64
 // reference's (exactly equal logits never certify). Uncertified tokens go to a list that
@@ -49,7 +49,7 @@ constexpr int kTcKC = 64;                // K per stage (one 128-byte row chunk)
 constexpr int kTcStages = 3;  // 48 KiB (E = 32): 4 CTAs per SM, the 512 TGT blocks in one wave
 constexpr double kTcEpsScale = 1.0 / 32768.0;  // 2^-15
 constexpr int kTcFold = 2;                      // hi-piece mma steps per fp32 accumulator
-constexpr int kFixWarps = 8;                   // fixup CTA: warps split M
+constexpr int kFixWarps = 32;                  // fixup CTA: warps split M
 constexpr int kFixTok = 4;                     // fixup CTA: tokens re-decided together
 constexpr int kTcMaxK = 8;
 
@@ -141,13 +141,13 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
     }
   };
 
-  // hi piece: fp32 accumulators restarted every kTcFold mma steps and added into fp32 running
-  // sums; lo piece (2^-9 of the magnitude): one fp32 accumulator over the whole K
-  float run[NT][4], hacc[NT][4], lacc[NT][4];
+  // fp32 accumulators of x.hi + x.lo restarted every kTcFold mma steps and added into fp32
+  // running sums
+  float run[NT][4], hacc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) run[j][i] = hacc[j][i] = lacc[j][i] = 0.0f;
+    for (int i = 0; i < 4; ++i) run[j][i] = hacc[j][i] = 0.0f;
   // |x_t|^2 on the tensor pipe: the A fragment's row halves are exactly the B fragments of
   // X_rows^T, so HMMA(A, A^T) accumulates X X^T blocks whose diagonals are the row norms
   float nacc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
@@ -180,10 +180,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
       for (int q = 0; q < 2 * NT; q += 2) {
         uint32_t b[4];
         ldsm_x4(sw(st + Cf::XB, (q + (lane >> 4)) * 8 + b_row, ks * 2 + b_kc), b[0], b[1], b[2], b[3]);
-        if (q < NT) hmma(hacc[q], af, b[0], b[1]);
-        else hmma(lacc[q - NT], af, b[0], b[1]);
-        if (q + 1 < NT) hmma(hacc[q + 1], af, b[2], b[3]);
-        else hmma(lacc[q + 1 - NT], af, b[2], b[3]);
+        hmma(hacc[q % NT], af, b[0], b[1]);
+        hmma(hacc[(q + 1) % NT], af, b[2], b[3]);
       }
       if (ks % kTcFold == kTcFold - 1) {
         // fold the hi accumulator (kTcFold steps, K = 16 * kTcFold) into the running sum
@@ -220,7 +218,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) L[j][i] = run[j][2 * h + i] + lacc[j][2 * h + i];
+      for (int i = 0; i < 2; ++i) L[j][i] = run[j][2 * h + i];
     const float eps = static_cast<float>(kTcEpsScale) * sqrtf((h ? d1 : d0) * (1.0f + 1.0f / 256.0f)) * wn;
     float mx = -FLT_MAX;
 #pragma unroll
@@ -301,6 +299,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
 // idxs / gates / the token's CTA histogram row. The last CTA to finish resets the list and adds
 // its size to the metrics counter.
 __global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a, int max_m) {
+  static_assert(kFixTok <= kFixWarps, "one finalising warp per token");
   extern __shared__ __align__(16) uint8_t fsm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(fsm);                         // [kFixTok][M]
   double* red = reinterpret_cast<double*>(fsm + static_cast<size_t>(kFixTok) * max_m * 2);  // [kFixTok][warps][64]

@@ -873,6 +873,114 @@ __global__ void __launch_bounds__(kBprSortThreads)
     bpr_write(lst[pos[r]], r, k, b, E, e, cap, gates, locations, slot_token, slot_gate, drops);
 }
 
+// BPR ranking in chunks (C3: one 2-5 K list per expert). Phase 1: CTA (list, chunk) bitonic-sorts
+// kBprChunk members of one list by (key desc, list position asc) -- key = the member token's max
+// gate as u64 bits (positive fp64 orders like its bit pattern, ties stay exact) -- and writes
+// the sorted chunk to scratch. Phase 2: each member's rank = its position in its own sorted
+// chunk + for every other chunk the number of members ordered before it (binary search).
+// Same ranks as bpr_sort_kernel / bpr_rank_kernel; ~100 CTAs instead of E, no O(n^2) work.
+constexpr int kBprChunk = 512;
+
+__device__ __forceinline__ bool bpr_before(unsigned long long ka, int pa, unsigned long long kb, int pb) {
+  return ka > kb || (ka == kb && pa < pb);
+}
+
+__global__ void __launch_bounds__(256)
+    bpr_chunk_sort_kernel(const double* __restrict__ gates, int k, int nchunk_max,
+                          const int32_t* __restrict__ demand, const int32_t* __restrict__ list_base,
+                          const int32_t* __restrict__ list, unsigned long long* __restrict__ skeys,
+                          int32_t* __restrict__ spos) {
+  pdl_entry();
+  __shared__ unsigned long long keys[kBprChunk];
+  __shared__ int32_t pos[kBprChunk];
+  const int be = blockIdx.x / nchunk_max, ch = blockIdx.x % nchunk_max;
+  const int n = demand[be];
+  const int c0 = ch * kBprChunk;
+  if (c0 >= n) return;  // CTA-uniform
+  const int cn = min(kBprChunk, n - c0);
+  const int32_t* lst = list + list_base[be];
+  for (int j = threadIdx.x; j < kBprChunk; j += blockDim.x) {
+    keys[j] = j < cn ? static_cast<unsigned long long>(
+                           __double_as_longlong(gates[static_cast<size_t>(lst[c0 + j] / k) * k]))
+                     : 0ull;                        // padding: key 0 sorts last
+    pos[j] = j < cn ? c0 + j : 0x7fffffff;
+  }
+  __syncthreads();
+  for (int size = 2; size <= kBprChunk; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int t = threadIdx.x;  // kBprChunk / 2 == blockDim.x
+      const int lo = 2 * t - (t & (stride - 1));
+      const int hi = lo + stride;
+      const bool up = (lo & size) == 0;
+      const unsigned long long kl = keys[lo], kh = keys[hi];
+      const int pl = pos[lo], ph = pos[hi];
+      if (bpr_before(kh, ph, kl, pl) == up) {
+        keys[lo] = kh; keys[hi] = kl;
+        pos[lo] = ph; pos[hi] = pl;
+      }
+      __syncthreads();
+    }
+  }
+  const size_t base = static_cast<size_t>(list_base[be]) + c0;
+  for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+    skeys[base + j] = keys[j];
+    spos[base + j] = pos[j];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    bpr_chunk_rank_kernel(const double* __restrict__ gates, int k, int E, int nchunk_max,
+                          const int32_t* __restrict__ demand, const int32_t* __restrict__ list_base,
+                          const int32_t* __restrict__ list, const unsigned long long* __restrict__ skeys,
+                          const int32_t* __restrict__ spos, const int32_t* __restrict__ cap_ptr,
+                          int32_t* __restrict__ locations, int32_t* __restrict__ slot_token,
+                          float* __restrict__ slot_gate, int32_t* __restrict__ drops) {
+  pdl_entry();
+  const int be = blockIdx.x / nchunk_max, ch = blockIdx.x % nchunk_max;
+  const int b = be / E, e = be % E;
+  const int n = demand[be];
+  const int c0 = ch * kBprChunk;
+  if (c0 >= n) return;  // CTA-uniform
+  const int cn = min(kBprChunk, n - c0);
+  const int nch = (n + kBprChunk - 1) / kBprChunk;
+  const size_t lb = static_cast<size_t>(list_base[be]);
+  const int cap = *cap_ptr;
+  const int32_t* lst = list + lb;
+  const int lane = threadIdx.x % 32;
+  for (int j0 = 0; j0 < kBprChunk; j0 += blockDim.x) {  // warp-uniform trip count
+    const int j = j0 + threadIdx.x;
+    const bool active = j < cn;
+    int loc = 0, f = 0;
+    if (active) {
+      const unsigned long long kj = skeys[lb + c0 + j];
+      const int pj = spos[lb + c0 + j];
+      int rank = j;  // members of its own chunk ordered before it
+      for (int oc = 0; oc < nch; ++oc) {
+        if (oc == ch) continue;
+        const int o0 = oc * kBprChunk, on = min(kBprChunk, n - o0);
+        // first index of chunk oc NOT ordered before (kj, pj)
+        int lo = 0, hi = on;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (bpr_before(skeys[lb + o0 + mid], spos[lb + o0 + mid], kj, pj)) lo = mid + 1;
+          else hi = mid;
+        }
+        rank += lo;
+      }
+      f = lst[pj];
+      loc = rank < cap ? rank : -1;
+      locations[f] = loc;
+      if (loc >= 0) {
+        const size_t slot = static_cast<size_t>(b * E + e) * cap + loc;
+        slot_token[slot] = f / k;
+        slot_gate[slot] = static_cast<float>(gates[f]);
+      }
+    }
+    const unsigned dropped = __ballot_sync(0xffffffffu, active && loc < 0);
+    if (lane == 0 && dropped) atomicAdd(drops, __popc(dropped));
+  }
+}
+
 // BPR: rank of each member of expert e's list by (max gate desc, token asc).
 // gridDim.x = blocks * E, gridDim.y = ceil(max list length / 256).
 __global__ void __launch_bounds__(256)
@@ -1156,7 +1264,16 @@ int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound
       const char* e = std::getenv("MOE_BPR_PAIRWISE");  // A/B: the O(n^2) pairwise-count kernel
       return e != nullptr && e[0] == '1';
     }();
-    if (!pairwise && smem_optin(bpr_sort_kernel, kBprSortSmem)) {
+    if (!pairwise && g.bpr_keys != nullptr && g.bpr_pos != nullptr) {
+      const int nchunk_max = (a.T * a.k + kBprChunk - 1) / kBprChunk;
+      const dim3 grid(a.blocks * a.E * nchunk_max);
+      launch_k(bpr_chunk_sort_kernel, grid, kBprChunk / 2, 0, st, g.gates, a.k, nchunk_max, g.demand,
+               g.list_base, g.list, g.bpr_keys, g.bpr_pos);
+      if (launch_status() != 0) return -2;
+      launch_k(bpr_chunk_rank_kernel, grid, 256, 0, st, g.gates, a.k, a.E, nchunk_max, g.demand,
+               g.list_base, g.list, g.bpr_keys, g.bpr_pos, g.cap, g.locations, g.slot_token,
+               g.slot_gate, g.drops);
+    } else if (!pairwise && smem_optin(bpr_sort_kernel, kBprSortSmem)) {
       launch_k(bpr_sort_kernel, dim3(a.blocks * a.E), kBprSortThreads, kBprSortSmem, st, g.gates, a.k,
                a.E, g.demand, g.list_base, g.list, g.cap, g.locations, g.slot_token, g.slot_gate,
                g.drops);

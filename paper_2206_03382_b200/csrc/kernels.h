@@ -81,6 +81,9 @@ struct GatingBuffers {
   int32_t* slot_token;  // [blocks, E, cap]
   float* slot_gate;     // [blocks, E, cap]
   double* probs;        // optional [blocks*T, E]
+  // BPR chunked ranking scratch ([blocks*T*k] each); null: the one-CTA-per-list sort
+  unsigned long long* bpr_keys = nullptr;
+  int32_t* bpr_pos = nullptr;
 };
 
 int gate_cta_per_block(int T);

@@ -297,6 +297,10 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   list_base_.alloc(4 * E_);
   fill_.alloc(4 * E_);
   list_.alloc(4 * Tk);
+  if (cfg.bpr) {  // chunked BPR ranking scratch
+    bpr_keys_.alloc(8 * Tk);
+    bpr_pos_.alloc(4 * Tk);
+  }
   capd_.alloc(4);
   drops_.alloc(4);
   ck(cudaMallocHost(&cap_host_, sizeof(int32_t)), "cudaMallocHost");
@@ -743,6 +747,10 @@ GatingBuffers Layer::gating_buffers() {
   b.slot_token = static_cast<int32_t*>(slot_token_.p);
   b.slot_gate = static_cast<float*>(slot_gate_.p);
   b.probs = nullptr;
+  if (cfg_.bpr) {
+    b.bpr_keys = static_cast<unsigned long long*>(bpr_keys_.p);
+    b.bpr_pos = static_cast<int32_t*>(bpr_pos_.p);
+  }
   return b;
 }
 

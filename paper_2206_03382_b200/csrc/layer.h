@@ -163,6 +163,7 @@ class Layer {
   DevMem wg_, w1_, w2_, dw1_, dw2_;
   // certified tensor-core gate: bf16 hi/lo split of Wg, max column norm, re-decision counter
   DevMem wg_pieces_, wg_nmax_, gate_fix_, gate_flags_;
+  DevMem bpr_keys_, bpr_pos_;  // chunked BPR ranking scratch
   bool gate_tc_ = false, wg_dirty_ = true;
   // peer transport: dispatch fused into encode / decode-backward (NVLink stores, MOE_DISPATCH=fused)
   bool fused_dispatch_ = false;

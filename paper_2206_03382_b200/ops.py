@@ -162,8 +162,8 @@ def weight_stats(w1: torch.Tensor):
     _need(w1, "w1")
     n, M, V = w1.shape
     colnorm = torch.empty(n, V, dtype=torch.float32, device=w1.device)
-    blk = torch.empty(n, V // 64 + 1, dtype=torch.float32, device=w1.device)
+    blk = torch.empty(n * (V // 64) + 1, dtype=torch.float32, device=w1.device)  # [n][V/64]
     w1t = torch.empty(n, V, M, dtype=w1.dtype, device=w1.device)
     check(lib().moe_op_weight_stats(_p(w1), n, M, V, C.cast(_p(colnorm), _lib.PF),
                                     C.cast(_p(blk), _lib.PF), _p(w1t), _st(w1)))
-    return colnorm, blk[:, :V // 64], w1t
+    return colnorm, blk[:n * (V // 64)].view(n, V // 64), w1t
