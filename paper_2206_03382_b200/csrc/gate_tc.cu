@@ -50,7 +50,10 @@ constexpr int kTcStages = 3;  // 48 KiB (E = 32): 4 CTAs per SM, the 512 TGT blo
 constexpr double kTcEpsScale = 1.0 / 32768.0;  // 2^-15
 constexpr int kTcFold = 2;                      // hi-piece mma steps per fp32 accumulator
 constexpr int kFixWarps = 32;                  // fixup CTA: warps split M
-constexpr int kFixTok = 4;                     // fixup CTA: tokens re-decided together
+#ifndef MOE_FIX_TOK
+#define MOE_FIX_TOK 1  // measured: one token per CTA beats sharing Wg reads across 4 (shorter critical path)
+#endif
+constexpr int kFixTok = MOE_FIX_TOK;           // fixup CTA: tokens re-decided together
 constexpr int kTcMaxK = 8;
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
@@ -144,6 +147,13 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
   // fp32 accumulators of x.hi + x.lo restarted every kTcFold mma steps and added into fp32
   // running sums
   float run[NT][4], hacc[NT][4];
+#ifdef MOE_GATE_SPLIT_ACC  // experiment: x.lo in its own whole-K accumulator (shorter mma chains)
+  float lacc[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lacc[j][i] = 0.0f;
+#endif
 #pragma unroll
   for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -180,8 +190,15 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
       for (int q = 0; q < 2 * NT; q += 2) {
         uint32_t b[4];
         ldsm_x4(sw(st + Cf::XB, (q + (lane >> 4)) * 8 + b_row, ks * 2 + b_kc), b[0], b[1], b[2], b[3]);
+#ifdef MOE_GATE_SPLIT_ACC
+        if (q < NT) hmma(hacc[q], af, b[0], b[1]);
+        else hmma(lacc[q - NT], af, b[0], b[1]);
+        if (q + 1 < NT) hmma(hacc[q + 1], af, b[2], b[3]);
+        else hmma(lacc[q + 1 - NT], af, b[2], b[3]);
+#else
         hmma(hacc[q % NT], af, b[0], b[1]);
         hmma(hacc[(q + 1) % NT], af, b[2], b[3]);
+#endif
       }
       if (ks % kTcFold == kTcFold - 1) {
         // fold the hi accumulator (kTcFold steps, K = 16 * kTcFold) into the running sum
@@ -218,7 +235,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) L[j][i] = run[j][2 * h + i];
+      for (int i = 0; i < 2; ++i) {
+        L[j][i] = run[j][2 * h + i];
+#ifdef MOE_GATE_SPLIT_ACC
+        L[j][i] += lacc[j][2 * h + i];
+#endif
+      }
     const float eps = static_cast<float>(kTcEpsScale) * sqrtf((h ? d1 : d0) * (1.0f + 1.0f / 256.0f)) * wn;
     float mx = -FLT_MAX;
 #pragma unroll

@@ -886,88 +886,108 @@ __device__ __forceinline__ bool bpr_before(unsigned long long ka, int pa, unsign
 }
 
 __global__ void __launch_bounds__(256)
-    bpr_chunk_sort_kernel(const double* __restrict__ gates, int k, int nchunk_max,
+    bpr_chunk_sort_kernel(const double* __restrict__ gates, int k,
                           const int32_t* __restrict__ demand, const int32_t* __restrict__ list_base,
                           const int32_t* __restrict__ list, unsigned long long* __restrict__ skeys,
                           int32_t* __restrict__ spos) {
   pdl_entry();
   __shared__ unsigned long long keys[kBprChunk];
   __shared__ int32_t pos[kBprChunk];
-  const int be = blockIdx.x / nchunk_max, ch = blockIdx.x % nchunk_max;
+  const int be = blockIdx.x;
   const int n = demand[be];
-  const int c0 = ch * kBprChunk;
-  if (c0 >= n) return;  // CTA-uniform
-  const int cn = min(kBprChunk, n - c0);
   const int32_t* lst = list + list_base[be];
-  for (int j = threadIdx.x; j < kBprChunk; j += blockDim.x) {
-    keys[j] = j < cn ? static_cast<unsigned long long>(
-                           __double_as_longlong(gates[static_cast<size_t>(lst[c0 + j] / k) * k]))
-                     : 0ull;                        // padding: key 0 sorts last
-    pos[j] = j < cn ? c0 + j : 0x7fffffff;
-  }
-  __syncthreads();
-  for (int size = 2; size <= kBprChunk; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const int t = threadIdx.x;  // kBprChunk / 2 == blockDim.x
-      const int lo = 2 * t - (t & (stride - 1));
-      const int hi = lo + stride;
-      const bool up = (lo & size) == 0;
-      const unsigned long long kl = keys[lo], kh = keys[hi];
-      const int pl = pos[lo], ph = pos[hi];
-      if (bpr_before(kh, ph, kl, pl) == up) {
-        keys[lo] = kh; keys[hi] = kl;
-        pos[lo] = ph; pos[hi] = pl;
-      }
-      __syncthreads();
+  const size_t lb = static_cast<size_t>(list_base[be]);
+  for (int c0 = blockIdx.y * kBprChunk; c0 < n; c0 += gridDim.y * kBprChunk) {  // CTA-uniform
+    const int cn = min(kBprChunk, n - c0);
+    for (int j = threadIdx.x; j < kBprChunk; j += blockDim.x) {
+      keys[j] = j < cn ? static_cast<unsigned long long>(
+                             __double_as_longlong(gates[static_cast<size_t>(lst[c0 + j] / k) * k]))
+                       : 0ull;                        // padding: key 0 sorts last
+      pos[j] = j < cn ? c0 + j : 0x7fffffff;
     }
-  }
-  const size_t base = static_cast<size_t>(list_base[be]) + c0;
-  for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-    skeys[base + j] = keys[j];
-    spos[base + j] = pos[j];
+    __syncthreads();
+    for (int size = 2; size <= kBprChunk; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const int t = threadIdx.x;  // kBprChunk / 2 == blockDim.x
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long kl = keys[lo], kh = keys[hi];
+        const int pl = pos[lo], ph = pos[hi];
+        if (bpr_before(kh, ph, kl, pl) == up) {
+          keys[lo] = kh; keys[hi] = kl;
+          pos[lo] = ph; pos[hi] = pl;
+        }
+        __syncthreads();
+      }
+    }
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      skeys[lb + c0 + j] = keys[j];
+      spos[lb + c0 + j] = pos[j];
+    }
+    __syncthreads();
   }
 }
 
+// Phase 2 stages the whole sorted list (all chunks, kBprRankMax members max) in shared memory;
+// longer lists search the chunks in global memory.
+constexpr int kBprRankMax = 8192;
+constexpr int kBprRankSmem = kBprRankMax * (8 + 4);
+
 __global__ void __launch_bounds__(256)
-    bpr_chunk_rank_kernel(const double* __restrict__ gates, int k, int E, int nchunk_max,
+    bpr_chunk_rank_kernel(const double* __restrict__ gates, int k, int E,
                           const int32_t* __restrict__ demand, const int32_t* __restrict__ list_base,
                           const int32_t* __restrict__ list, const unsigned long long* __restrict__ skeys,
                           const int32_t* __restrict__ spos, const int32_t* __restrict__ cap_ptr,
                           int32_t* __restrict__ locations, int32_t* __restrict__ slot_token,
                           float* __restrict__ slot_gate, int32_t* __restrict__ drops) {
   pdl_entry();
-  const int be = blockIdx.x / nchunk_max, ch = blockIdx.x % nchunk_max;
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const int be = blockIdx.x;
   const int b = be / E, e = be % E;
   const int n = demand[be];
-  const int c0 = ch * kBprChunk;
-  if (c0 >= n) return;  // CTA-uniform
-  const int cn = min(kBprChunk, n - c0);
+  if (n == 0) return;
   const int nch = (n + kBprChunk - 1) / kBprChunk;
   const size_t lb = static_cast<size_t>(list_base[be]);
+  const bool staged = n <= kBprRankMax;
+  const unsigned long long* K = skeys + lb;
+  const int32_t* P = spos + lb;
+  if (staged) {
+    unsigned long long* ks = reinterpret_cast<unsigned long long*>(rsm);
+    int32_t* ps = reinterpret_cast<int32_t*>(rsm + static_cast<size_t>(kBprRankMax) * 8);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      ks[j] = skeys[lb + j];
+      ps[j] = spos[lb + j];
+    }
+    __syncthreads();
+    K = ks;
+    P = ps;
+  }
   const int cap = *cap_ptr;
   const int32_t* lst = list + lb;
   const int lane = threadIdx.x % 32;
-  for (int j0 = 0; j0 < kBprChunk; j0 += blockDim.x) {  // warp-uniform trip count
-    const int j = j0 + threadIdx.x;
-    const bool active = j < cn;
-    int loc = 0, f = 0;
+  // this CTA ranks members [blockIdx.y * 256 + i * gridDim.y * 256 ...) of the sorted chunks
+  for (int j0 = blockIdx.y * blockDim.x; j0 < n; j0 += gridDim.y * blockDim.x) {  // warp-uniform
+    const int jj = j0 + threadIdx.x;
+    const bool active = jj < n;
+    int loc = 0;
     if (active) {
-      const unsigned long long kj = skeys[lb + c0 + j];
-      const int pj = spos[lb + c0 + j];
+      const int ch = jj / kBprChunk, j = jj % kBprChunk;
+      const unsigned long long kj = K[jj];
+      const int pj = P[jj];
       int rank = j;  // members of its own chunk ordered before it
       for (int oc = 0; oc < nch; ++oc) {
         if (oc == ch) continue;
         const int o0 = oc * kBprChunk, on = min(kBprChunk, n - o0);
-        // first index of chunk oc NOT ordered before (kj, pj)
-        int lo = 0, hi = on;
+        int lo = 0, hi = on;  // first index of chunk oc NOT ordered before (kj, pj)
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (bpr_before(skeys[lb + o0 + mid], spos[lb + o0 + mid], kj, pj)) lo = mid + 1;
+          if (bpr_before(K[o0 + mid], P[o0 + mid], kj, pj)) lo = mid + 1;
           else hi = mid;
         }
         rank += lo;
       }
-      f = lst[pj];
+      const int f = lst[pj];
       loc = rank < cap ? rank : -1;
       locations[f] = loc;
       if (loc >= 0) {
@@ -1264,15 +1284,16 @@ int run_assign_device(const GatingArgs& a, const GatingBuffers& g, int cap_bound
       const char* e = std::getenv("MOE_BPR_PAIRWISE");  // A/B: the O(n^2) pairwise-count kernel
       return e != nullptr && e[0] == '1';
     }();
-    if (!pairwise && g.bpr_keys != nullptr && g.bpr_pos != nullptr) {
-      const int nchunk_max = (a.T * a.k + kBprChunk - 1) / kBprChunk;
-      const dim3 grid(a.blocks * a.E * nchunk_max);
-      launch_k(bpr_chunk_sort_kernel, grid, kBprChunk / 2, 0, st, g.gates, a.k, nchunk_max, g.demand,
-               g.list_base, g.list, g.bpr_keys, g.bpr_pos);
+    if (!pairwise && g.bpr_keys != nullptr && g.bpr_pos != nullptr &&
+        smem_optin(bpr_chunk_rank_kernel, kBprRankSmem)) {
+      // y: CTAs per list; the lists average T*k/E members (C3: 2048 = 4 chunks)
+      const int per = std::max(1, std::min(8, (a.T * a.k / a.E + kBprChunk - 1) / kBprChunk));
+      launch_k(bpr_chunk_sort_kernel, dim3(a.blocks * a.E, per), kBprChunk / 2, 0, st, g.gates, a.k,
+               g.demand, g.list_base, g.list, g.bpr_keys, g.bpr_pos);
       if (launch_status() != 0) return -2;
-      launch_k(bpr_chunk_rank_kernel, grid, 256, 0, st, g.gates, a.k, a.E, nchunk_max, g.demand,
-               g.list_base, g.list, g.bpr_keys, g.bpr_pos, g.cap, g.locations, g.slot_token,
-               g.slot_gate, g.drops);
+      launch_k(bpr_chunk_rank_kernel, dim3(a.blocks * a.E, per * 2), 256, kBprRankSmem, st, g.gates,
+               a.k, a.E, g.demand, g.list_base, g.list, g.bpr_keys, g.bpr_pos, g.cap, g.locations,
+               g.slot_token, g.slot_gate, g.drops);
     } else if (!pairwise && smem_optin(bpr_sort_kernel, kBprSortSmem)) {
       launch_k(bpr_sort_kernel, dim3(a.blocks * a.E), kBprSortThreads, kBprSortSmem, st, g.gates, a.k,
                a.E, g.demand, g.list_base, g.list, g.cap, g.locations, g.slot_token, g.slot_gate,

@@ -368,12 +368,14 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
         }
       }
       unsigned long long mw[kSubs];
+#ifndef MOE_EXP_ACT_MASK
       if constexpr (kEpi == kEpiMaskBf16) {
         // issued before the accumulator wait so their latency hides under the MMAs
 #pragma unroll
         for (uint32_t c = 0; c < kSubs; ++c)
           mw[c] = row_ok ? __ldg(args.relu_mask + mrow + col0 / 64 + c) : 0ull;
       }
+#endif
       TRACE_WAIT(w_tfull, ptx::mbar_wait(&tfull_bar[acc], acc_phase));
       ptx::tc_fence_after();
 #pragma unroll 1
@@ -461,6 +463,23 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
 #pragma unroll
             for (uint32_t j = 0; j < 32; ++j) w[j] = __vmaxs2(w[j], 0u);  // int16 max == bf16 relu
           }
+#ifdef MOE_EXP_ACT_MASK
+          if constexpr (kEpi == kEpiMaskBf16) {
+            // experiment: [h > 0] == [act != 0] from the saved bf16 activation row segment
+            const uint4* ar = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(args.aux) +
+                                                             orow * args.N + cols);
+#pragma unroll
+            for (uint32_t q = 0; q < 8; ++q) {
+              const uint4 av = row_ok ? __ldg(ar + q) : make_uint4(0u, 0u, 0u, 0u);
+              const uint32_t a4[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+              for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t nz = (((a4[u] & 0x7fff7fffu) + 0x7fff7fffu) & 0x80008000u) >> 15;
+                w[4 * q + u] &= nz * 0xffffu;
+              }
+            }
+          }
+#else
           if constexpr (kEpi == kEpiMaskBf16) {
             // dh = (dY . W2^T) * [h > 0]; the up-GEMM's ReLU bitmask carries [h > 0]
             unsigned long long mk = 0ull;
@@ -474,6 +493,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
               w[j] &= (b2 & 1u ? 0x0000ffffu : 0u) | (b2 & 2u ? 0xffff0000u : 0u);
             }
           }
+#endif
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
             ptx::st_shared_v4(stage_row + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1],
