@@ -73,5 +73,20 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     return LIB
 
 
+def build_checks(force: bool = False) -> Path:
+    """The bounds-checked variant (-DMOE_CHECKS: device-side MOE_CHECK traps, csrc/checks.cuh),
+    in-tree beside the product library; tests/test_gpu_checks.py runs the GPU suite against it."""
+    global OBJ, LIB, EXTRA
+    saved = (OBJ, LIB, EXTRA)
+    try:
+        OBJ, LIB, EXTRA = PKG / "build_checks", PKG / "libmoe_b200_checks.so", EXTRA + ["-DMOE_CHECKS"]
+        return build(force=force)
+    finally:
+        OBJ, LIB, EXTRA = saved
+
+
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--checks" in sys.argv:
+        print(build_checks(force="-f" in sys.argv))
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -16,6 +16,7 @@
 
 #include <cstdint>
 
+#include "checks.cuh"
 #include "kernels.h"
 #include "pdl.cuh"
 #include "peer_flags.cuh"
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     const int e = (rem / g.cc) % g.E;
     const int c = i * g.cc + rem % g.cc;
     const int t = c < g.cap ? slot_token[static_cast<size_t>(b * g.E + e) * g.cap + c] : -1;
+    MOE_CHECK(t == -1 || (t >= b * g.T && t < (b + 1) * g.T), "encode: slot token outside its block");
     if constexpr (kVec) {
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
@@ -260,6 +262,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         // top-2: both rows' loads in flight before any math; same j-ascending fma order
         const int2 loc = *reinterpret_cast<const int2*>(locations + static_cast<size_t>(t) * 2);
         const int2 ex = *reinterpret_cast<const int2*>(idxs + static_cast<size_t>(t) * 2);
+        MOE_CHECK(loc.x < g.cap && loc.y < g.cap && (loc.x < 0 || (ex.x >= 0 && ex.x < g.E)) &&
+                      (loc.y < 0 || (ex.y >= 0 && ex.y < g.E)), "decode: location / expert out of range");
         const double2 gt = *reinterpret_cast<const double2*>(gates + static_cast<size_t>(t) * 2);
         const uint4* s0 = loc.x >= 0 ? reinterpret_cast<const uint4*>(z + slot_row(g, b, ex.x, loc.x) * g.M) : nullptr;
         const uint4* s1 = loc.y >= 0 ? reinterpret_cast<const uint4*>(z + slot_row(g, b, ex.y, loc.y) * g.M) : nullptr;
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       t = slot_token[s];
       gv = slot_gate[s];
     }
+    MOE_CHECK(t == -1 || (t >= b * g.T && t < (b + 1) * g.T), "decode_bwd: slot token outside its block");
     if constexpr (kVec) {
       constexpr int VN = Vec<T>::N;
       const int nv = g.M / VN;
@@ -454,6 +459,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         // top-2: both rows' loads in flight before any math; same j-ascending sum order
         const int2 loc = *reinterpret_cast<const int2*>(locations + static_cast<size_t>(t) * 2);
         const int2 ex = *reinterpret_cast<const int2*>(idxs + static_cast<size_t>(t) * 2);
+        MOE_CHECK(loc.x < g.cap && loc.y < g.cap && (loc.x < 0 || (ex.x >= 0 && ex.x < g.E)) &&
+                      (loc.y < 0 || (ex.y >= 0 && ex.y < g.E)), "encode_bwd: location / expert out of range");
         const uint4* s0 = loc.x >= 0 ? reinterpret_cast<const uint4*>(dz + slot_row(g, b, ex.x, loc.x) * g.M) : nullptr;
         const uint4* s1 = loc.y >= 0 ? reinterpret_cast<const uint4*>(dz + slot_row(g, b, ex.y, loc.y) * g.M) : nullptr;
         for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {

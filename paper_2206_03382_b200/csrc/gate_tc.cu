@@ -36,6 +36,7 @@
 #include <cfloat>
 #include <cstdint>
 
+#include "checks.cuh"
 #include "kernels.h"
 #include "pdl.cuh"
 
@@ -305,7 +306,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel
           atomicAdd(&sh_hist[sel[r]], 1);
         }
       } else {
-        a.flag_list[atomicAdd(a.flag_count, 1)] = t;
+        const int slot = atomicAdd(a.flag_count, 1);
+        MOE_CHECK(slot < static_cast<int>(gridDim.x / a.cpb) * a.T, "gate: uncertified-token list overflow");
+        a.flag_list[slot] = t;
       }
     }
   }

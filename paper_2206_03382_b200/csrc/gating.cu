@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "checks.cuh"
 #include "kernels.h"
 #include "pdl.cuh"
 
@@ -761,8 +762,10 @@ __global__ void __launch_bounds__(256)
     if (active && in_warp == 0) wcnt[warp * E + e] = __popc(grp);
     __syncthreads();
     if (active) {
+      MOE_CHECK(e >= 0 && e < E, "assign: expert id out of range");
       int r = cnt[e] + in_warp;
       for (int w = 0; w < warp; ++w) r += wcnt[w * E + e];
+      MOE_CHECK(r >= 0 && r < demand[b * E + e], "assign: FIFO rank outside the expert's demand");
       if (!bpr) {
         const int loc = r < cap ? r : -1;
         locations[f] = loc;
@@ -987,6 +990,7 @@ __global__ void __launch_bounds__(256)
         }
         rank += lo;
       }
+      MOE_CHECK(rank >= 0 && rank < n && pj >= 0 && pj < n, "bpr rank: rank / position out of range");
       const int f = lst[pj];
       loc = rank < cap ? rank : -1;
       locations[f] = loc;

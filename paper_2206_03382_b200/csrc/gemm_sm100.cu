@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "gemm_sm100.h"
+#include "checks.cuh"
 #include "kernels.h"
 #include "pdl.cuh"
 #include "peer_flags.cuh"
@@ -443,6 +444,8 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
                 for (uint32_t i = 0; i < 64; ++i) {
                   if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
                     const unsigned int slot = atomicAdd(args.fix_count, 1u);
+                    MOE_CHECK(seg < (1u << 20) && row_in < (1u << 20) && cols + i < (1u << 24),
+                              "up epilogue: certificate entry does not fit its packing");
                     if (slot < args.fix_cap) args.fix_list[slot] = fix_pack(seg, row_in, cols + i);
                   }
                 }

@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "gemm_sm100.h"
+#include "checks.cuh"
 #include "kernels.h"
 #include "pdl.cuh"
 #include "peer_flags.cuh"
@@ -234,11 +235,52 @@ __global__ void __launch_bounds__(256) relu_fixup_kernel(
       const uint32_t row = static_cast<uint32_t>((e[j] >> 24) & 0xFFFFF);
       col[j] = static_cast<uint32_t>(e[j] & 0xFFFFFF);
       r[j] = static_cast<size_t>(seg) * seg_rows + row;
+      MOE_CHECK(row < static_cast<uint32_t>(seg_rows) && col[j] < static_cast<uint32_t>(V), "relu fixup: entry out of range");
     }
+    const __nv_bfloat16* xr[2];
+    const __nv_bfloat16* wr[2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      s[j] = fixup_dot(x + r[j] * M, w1t + (static_cast<size_t>(static_cast<uint32_t>(e[j] >> 44) % G) * V + col[j]) * M,
-                       M, lane);
+    for (int j = 0; j < 2; ++j) {
+      xr[j] = x + r[j] * M;
+      wr[j] = w1t + (static_cast<size_t>(static_cast<uint32_t>(e[j] >> 44) % G) * V + col[j]) * M;
+    }
+    if ((M & 255) == 0) {
+      // both entries' rows in flight 4 vectors per lane at a time before the fp64 math (the loop
+      // is latency-bound on these gathers)
+      constexpr int kV = 4;
+      const int nv = M / 256;  // 16-byte vectors per lane per row
+      double acc[2] = {0.0, 0.0};
+      for (int v0 = 0; v0 < nv; v0 += kV) {
+        uint4 av[2][kV], bv[2][kV];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int v = 0; v < kV; ++v)
+            if (v0 + v < nv) {
+              av[j][v] = __ldg(reinterpret_cast<const uint4*>(xr[j]) + (v0 + v) * 32 + lane);
+              bv[j][v] = __ldg(reinterpret_cast<const uint4*>(wr[j]) + (v0 + v) * 32 + lane);
+            }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int v = 0; v < kV; ++v)
+            if (v0 + v < nv) {
+              const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&av[j][v]);
+              const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&bv[j][v]);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 af = __bfloat1622float2(ah[q]), wf = __bfloat1622float2(wh[q]);
+                acc[j] = fma(static_cast<double>(af.x), static_cast<double>(wf.x), acc[j]);
+                acc[j] = fma(static_cast<double>(af.y), static_cast<double>(wf.y), acc[j]);
+              }
+            }
+      }
+      s[0] = acc[0];
+      s[1] = acc[1];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) s[j] = fixup_dot(xr[j], wr[j], M, lane);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);

@@ -115,3 +115,20 @@ def test_c4_full_shape_parity_and_strategy_invariance(cuda):
     print(r.stdout[-6000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "FAIL" not in r.stdout and "ALL PASS" in r.stdout
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_c4_parity_under_bounds_checks(cuda):
+    """The full-shape C4 exchange (peer and NCCL transports, fused dispatch) on 2 GPUs against the
+    bounds-checked library (-DMOE_CHECKS device traps; compute-sanitizer is closed on this pool)."""
+    lib = ROOT / "paper_2206_03382_b200" / "libmoe_b200_checks.so"
+    import os
+    env = dict(os.environ, MOE_LIB_PATH=str(lib))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           str(ROOT / "tools" / "mp_parity_c4.py"), "--degrees", "1,4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT, env=env)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "FAIL" not in r.stdout and "ALL PASS" in r.stdout and "MOE_CHECK failed" not in r.stderr
