@@ -47,7 +47,10 @@ namespace {
 constexpr int kTcWarps = 4;              // 4 warps x 16 tokens = the 64-token gate block
 constexpr int kTcTok = kTcWarps * 16;
 constexpr int kTcKC = 64;                // K per stage (one 128-byte row chunk)
-constexpr int kTcStages = 3;  // 48 KiB (E = 32): 4 CTAs per SM, the 512 TGT blocks in one wave
+#ifndef MOE_TC_STAGES
+#define MOE_TC_STAGES 3
+#endif
+constexpr int kTcStages = MOE_TC_STAGES;  // 3: 48 KiB (E = 32), 4 CTAs per SM, the 512 TGT blocks in one wave
 constexpr double kTcEpsScale = 1.0 / 32768.0;  // 2^-15
 constexpr int kTcFold = 2;                      // hi-piece mma steps per fp32 accumulator
 constexpr int kFixWarps = 32;                  // fixup CTA: warps split M
@@ -115,7 +118,10 @@ struct TcArgs {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? 4 : 2) gate_tc_kernel(TcArgs a) {
+#ifndef MOE_GATE_MINB
+#define MOE_GATE_MINB 4
+#endif
+__global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? MOE_GATE_MINB : 2) gate_tc_kernel(TcArgs a) {
   using Cf = TcCfg<NT>;
   constexpr int E = Cf::E;
   constexpr int NTH = kTcWarps * 32;
