@@ -34,11 +34,14 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 
 #include "checks.cuh"
+#include "gemm_sm100.h"
 #include "kernels.h"
 #include "pdl.cuh"
+#include "ptx.cuh"
 
 namespace moe {
 
@@ -323,6 +326,217 @@ __global__ void __launch_bounds__(kTcWarps * 32, NT <= 4 ? MOE_GATE_MINB : 2) ga
   for (int e = threadIdx.x; e < E; e += NTH) a.hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
 }
 
+// ---------------------------------------------------------------- tcgen05 variant
+// Same certificate, on the 5th-gen tensor cores: one CTA = 128 tokens (M = 128, TMEM lane =
+// token), N = 2E columns (hi | lo pieces of Wg), K streamed by TMA in 64-wide k-blocks (SW128).
+// Each k-block's 4 MMAs write a fresh accumulator (double-buffered in TMEM); the 4 epilogue
+// warps drain it with tcgen05.ld and add it into per-thread fp32 running logits -- the same
+// fold schedule as the HMMA kernel (hi piece: 4 mma steps per window, 2^-16.8 of the window's
+// sum|x w|), so the same eps_t. The epilogue warps also read their row of each A stage from
+// shared memory for |x_t|^2 (fp32, exact products), and after the last k-block finish softmax
+// / top-(k+1) / certificate per thread (one token per thread: no shuffles).
+// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM alloc), 2..5 epilogue (TMEM lane quadrant = warp % 4).
+constexpr int kT5Tok = 128;
+constexpr int kT5KB = 64;       // K per stage (one 128-byte swizzle atom of bf16)
+constexpr int kT5Stages = 4;
+constexpr int kT5Threads = 192;
+
+template <int E>
+struct T5Cfg {
+  static_assert(E % 16 == 0, "hi | lo accumulators are drained 32 columns at a time");
+  static constexpr int N = 2 * E;
+  static constexpr uint32_t A_BYTES = kT5Tok * kT5KB * 2;  // 16 KiB
+  static constexpr uint32_t B_BYTES = N * kT5KB * 2;       // 8 KiB at E = 32
+  static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  static constexpr uint32_t BAR_OFF = kT5Stages * STAGE;
+  static constexpr uint32_t SMEM = BAR_OFF + 256 + 1024;   // + barriers + alignment slack
+  static constexpr uint32_t TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
+};
+
+struct T5Args {
+  TcArgs a;
+  int rows_total;  // blocks * T
+};
+
+template <int E>
+__global__ void __launch_bounds__(kT5Threads, 1)
+    gate_tc5_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                    const T5Args args) {
+  using C = T5Cfg<E>;
+  constexpr int N = C::N;
+  const TcArgs& a = args.a;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* empty = full + kT5Stages;
+  uint64_t* accf = empty + kT5Stages;
+  uint64_t* acce = accf + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  __shared__ int32_t sh_hist[2][E];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // this CTA: tokens [t0, t0 + ntok) of block b (tiles never cross a block)
+  const int tiles = (a.T + kT5Tok - 1) / kT5Tok;
+  const int b = blockIdx.x / tiles, c = blockIdx.x % tiles;
+  const int t0 = b * a.T + c * kT5Tok;
+  const int ntok = min(kT5Tok, a.T - c * kT5Tok);
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) (&sh_hist[0][0])[i] = 0;
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(&tmX);
+    ptx::prefetch_tmap(&tmW);
+    for (int i = 0; i < kT5Stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1 + 4);  // the MMA commit + the 4 epilogue warps (A rows read)
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&accf[i], 1);
+      ptx::mbar_init(&acce[i], 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+  const int nkb = a.M / kT5KB;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kT5Stages;
+      ptx::mbar_wait(&empty[s], ((kb / kT5Stages) & 1) ^ 1);
+      uint8_t* st = smem + s * C::STAGE;
+      ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
+      ptx::tma_load_3d(&tmX, &full[s], st, kb * kT5KB, t0, 0);
+      ptx::tma_load_3d(&tmW, &full[s], st + C::A_BYTES, kb * kT5KB, 0, 0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(128, N, false, false);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kT5Stages;
+      const int buf = kb & 1;
+      ptx::mbar_wait(&acce[buf], ((kb >> 1) & 1) ^ 1);  // the epilogue drained this buffer
+      ptx::mbar_wait(&full[s], (kb / kT5Stages) & 1);
+      ptx::tc_fence_after();
+      const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE);
+      const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+      for (int k = 0; k < kT5KB / 16; ++k)
+        ptx::umma_bf16(tmem + buf * N, ptx::make_sw128_desc(sa + k * 32, 16, 1024),
+                       ptx::make_sw128_desc(sb + k * 32, 16, 1024), idesc, k > 0 ? 1u : 0u);
+      ptx::umma_commit(&empty[s]);
+      ptx::umma_commit(&accf[buf]);
+    }
+  } else if (warp >= 2) {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp % 4;            // TMEM lane quadrant
+    const int row = q * 32 + lane;     // token row within the tile
+    const uint32_t taddr = tmem + ((q * 32) << 16);
+    float L[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) L[e] = 0.0f;
+    float ss = 0.0f;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kT5Stages;
+      const int buf = kb & 1;
+      // |x_row|^2 from this stage's A tile (SW128: chunk j of row r at ((j ^ (r % 8)) << 4))
+      ptx::mbar_wait(&full[s], (kb / kT5Stages) & 1);
+      const uint8_t* ar = smem + s * C::STAGE + row * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 v = *reinterpret_cast<const uint4*>(ar + ((j ^ (row & 7)) << 4));
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float lo = __uint_as_float(w4[u] << 16), hi = __uint_as_float(w4[u] & 0xffff0000u);
+          ss = fmaf(lo, lo, ss);
+          ss = fmaf(hi, hi, ss);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      // this k-block's accumulator: hi | lo columns
+      ptx::mbar_wait(&accf[buf], (kb >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < N / 32; ++h) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(taddr + buf * N + h * 32, v);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) L[(h * 32 + i) % E] += __uint_as_float(v[i]);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acce[buf]);
+    }
+    // ---- certificate, softmax, top-(k + 1) of this thread's token
+    const int k = a.k;
+    const bool tok_ok = row < ntok;
+    const int t = t0 + row;
+    const float wn = __ldg(a.wn_max);
+    // fp32 sum of M squares: relative error <= M * 2^-24; (1 + 2^-8) covers M up to 65 K
+    const float eps = static_cast<float>(kTcEpsScale) * sqrtf(ss * (1.0f + 1.0f / 256.0f)) * wn;
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int e = 0; e < E; ++e) mx = fmaxf(mx, L[e]);
+    float sden = 0.0f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) sden += __expf(L[e] - mx);
+    unsigned long long taken = 0ull;
+    bool certified = true;
+    float prev = 0.0f;
+    int sel[kTcMaxK];
+    float selv[kTcMaxK];
+    const int kk = k < E ? k + 1 : k;
+    for (int r = 0; r < kk; ++r) {
+      float bv = -FLT_MAX;
+      int bi = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (!((taken >> e) & 1ull) && L[e] > bv) {  // strict: ties keep the lower expert id
+          bv = L[e];
+          bi = e;
+        }
+      taken |= 1ull << bi;
+      if (r > 0 && !(prev - bv > 2.0f * eps)) certified = false;
+      if (r < k && bv - mx < -690.0f) certified = false;  // see gate_tc_kernel
+      prev = bv;
+      if (r < k) {
+        sel[r] = bi;
+        selv[r] = bv;
+      }
+    }
+    if (tok_ok) {
+      if (certified) {
+        for (int r = 0; r < k; ++r) {
+          a.idxs[static_cast<size_t>(t) * k + r] = sel[r];
+          a.gates[static_cast<size_t>(t) * k + r] =
+              exp(static_cast<double>(selv[r] - mx)) / static_cast<double>(sden);
+          atomicAdd(&sh_hist[row / kTcTok][sel[r]], 1);
+        }
+      } else {
+        const int slot = atomicAdd(a.flag_count, 1);
+        MOE_CHECK(slot < args.rows_total, "gate: uncertified-token list overflow");
+        a.flag_list[slot] = t;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  // histogram rows of the (up to) two 64-token gate blocks this tile covers
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) {
+    const int hb = i / E, e = i % E;
+    const int blk64 = c * 2 + hb;
+    if (blk64 * kTcTok < a.T) a.hist[(static_cast<size_t>(b) * a.cpb + blk64) * E + e] = sh_hist[hb][e];
+  }
+  if (warp == 1) ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 // fp64 re-decision of the tokens gate_tc_kernel could not certify. A CTA takes up to kFixTok
 // listed tokens at once (their x rows staged in shared memory) so each fp64 Wg element it streams
 // from L2 serves all of them; warps split M, lanes own experts (lane, lane + 32). Then warp j
@@ -512,6 +726,36 @@ int gate_tc_device(const void* x, const void* pieces, const double* wg, const fl
   a.fixups = fixups;
   a.flag_list = flag_list;
   a.flag_count = flag_count;
+  static const bool hmma = [] {
+    const char* e = std::getenv("MOE_GATE_HMMA");  // =1: the mma.sync kernel (A/B runs)
+    return e != nullptr && e[0] == '1';
+  }();
+  if (!hmma && E <= 64 && E % 16 == 0) {  // N = 2E columns drained 32 at a time
+    CUtensorMap mx{}, mw{};
+    const int rows = blocks * T;
+    if (tensor_map_3d(&mx, x, false, M, rows, 1, kT5KB, kT5Tok) == 0 &&
+        tensor_map_3d(&mw, pieces, false, M, 2 * E, 1, kT5KB, 2 * E) == 0) {
+      T5Args ta{a, rows};
+      const int tiles = (T + kT5Tok - 1) / kT5Tok;
+      auto go5 = [&](auto e_tag) -> int {
+        constexpr int EE = decltype(e_tag)::value;
+        auto kern = gate_tc5_kernel<EE>;
+        if (!smem_optin(kern, T5Cfg<EE>::SMEM)) return -2;
+        launch_k(kern, dim3(blocks * tiles), dim3(kT5Threads), T5Cfg<EE>::SMEM, st, mx, mw, ta);
+        if (launch_status() != 0) return -2;
+        const int fsmem = kFixTok * M * 2 + kFixTok * kFixWarps * 64 * 8;
+        if (!smem_optin(gate_fixup_kernel, fsmem)) return -2;
+        launch_k(gate_fixup_kernel, dim3(148), dim3(kFixWarps * 32), fsmem, st, a, M);
+        return launch_status();
+      };
+      switch (E / 16) {
+        case 1: return go5(std::integral_constant<int, 16>{});
+        case 2: return go5(std::integral_constant<int, 32>{});
+        case 3: return go5(std::integral_constant<int, 48>{});
+        default: return go5(std::integral_constant<int, 64>{});
+      }
+    }
+  }
   auto go = [&](auto nt_tag) -> int {
     constexpr int NT = decltype(nt_tag)::value;
     auto kern = gate_tc_kernel<NT>;

@@ -654,6 +654,12 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, con
 
 }  // namespace
 
+// Public wrapper (gate_tc.cu): a 3-D bf16 / fp32 tensor map with a {b0, b1, 1} box, 128-byte swizzle.
+int tensor_map_3d(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,
+                  uint32_t b0, uint32_t b1) {
+  return make_map_3d(m, base, f32, d0, d1, d2, b0, b1);
+}
+
 int gemm_validate(const GemmArgs& a, int kind) {
   if (a.G < 1 || a.S < 1 || a.seg_rows < 1 || a.N < 1) return -1;
   if (kind != kGemmWgrad) {

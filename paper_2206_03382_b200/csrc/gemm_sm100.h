@@ -1,6 +1,7 @@
 // Grouped expert GEMM (tcgen05/TMEM/TMA, sm_100a). See gemm_sm100.cu.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -82,5 +83,9 @@ int gemm_validate(const GemmArgs& a, int kind);
 
 int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArgs& args,
              int nseg_total, int num_sms, cudaStream_t stream);
+
+// 3-D tensor map, box {b0, b1, 1}, 128-byte swizzle (0 on success).
+int tensor_map_3d(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_t d1, uint64_t d2,
+                  uint32_t b0, uint32_t b1);
 
 }  // namespace moe
