@@ -16,9 +16,10 @@ from paper_2206_03382_b200 import rng
 pytestmark = pytest.mark.gpu
 
 
-def _route(x, wg, E, k, f, M, T, precision):
+def _route(x, wg, E, k, f, M, T, precision, cap="fixed"):
     cfg = MoELayerConfig(global_experts=E, model_dim=M, hidden_dim=256, tokens_per_step=T,
-                         top_k=k, capacity_factor=f, dtype="bf16", gate_precision=precision)
+                         top_k=k, capacity=cap, capacity_factor=f, dtype="bf16",
+                         gate_precision=precision)
     st = LayerState.init(cfg, 5)
     st.set_router(wg)
     forward(st, torch.as_tensor(x).to(torch.bfloat16).cuda())
@@ -87,3 +88,17 @@ def test_certified_gate_tgt_shape_fixup_rate(cuda):
     _check_gates(gates, r_gates, x, wg)
     print("gate_fixups", m.gate_fixups, "max rel gate err", float(np.abs(gates / r_gates - 1).max()))
     assert 0 < m.gate_fixups < T // 10
+
+
+@pytest.mark.parametrize("cap,kind,f", [("auto", 1, 1.0), ("bounded", 2, 1.25), ("bounded", 2, 0.5)])
+def test_certified_gate_capacity_policies(cuda, cap, kind, f):
+    """Auto / Bounded capacity on the certified path: the fix-up kernel's last CTA runs the
+    capacity scan and resolve_capacity (core.cpp:47-59) itself."""
+    T, M, E, k = 3000, 512, 32, 2
+    x, wg = _inputs(23, T, M, E, "near_ties")
+    idxs, loc, gates, capv, m = _route(x, wg, E, k, f, M, T, "auto", cap)
+    probs = oracle.gate_linear(x, wg)
+    r_idx, r_gates, r_loc, r_cap = oracle.run_gating_blocked(probs, 1, k, kind, f, False)
+    assert capv == r_cap
+    assert np.array_equal(idxs, r_idx) and np.array_equal(loc, r_loc)
+    assert m.drop_count == int((r_loc < 0).sum())
