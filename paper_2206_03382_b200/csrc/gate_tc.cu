@@ -56,7 +56,14 @@ constexpr int kTcKC = 64;                // K per stage (one 128-byte row chunk)
 constexpr int kTcStages = MOE_TC_STAGES;  // 3: 48 KiB (E = 32), 4 CTAs per SM, the 512 TGT blocks in one wave
 constexpr double kTcEpsScale = 1.0 / 32768.0;  // 2^-15
 constexpr int kTcFold = 2;                      // hi-piece mma steps per fp32 accumulator
-constexpr int kFixWarps = 32;                  // fixup CTA: warps split M
+#ifndef MOE_FIX_WARPS
+#define MOE_FIX_WARPS 32
+#endif
+#ifndef MOE_FIX_CTAS
+#define MOE_FIX_CTAS 148
+#endif
+constexpr int kFixWarps = MOE_FIX_WARPS;       // fixup CTA: warps split M
+constexpr int kFixCtas = MOE_FIX_CTAS;
 #ifndef MOE_FIX_TOK
 #define MOE_FIX_TOK 1  // measured: one token per CTA beats sharing Wg reads across 4 (shorter critical path)
 #endif
@@ -118,10 +125,6 @@ struct TcArgs {
   int32_t* fixups;              // += tokens re-decided in fp64 (metrics; may be null)
   int32_t* flag_list;           // [blocks*T] uncertified token indices
   int32_t* flag_count;          // [0] list size, [1] fixup CTAs done (reset by the fixup kernel)
-  // capacity scan + resolve fused into the fix-up's last CTA (the separate scan_cols /
-  // finalize_capacity kernels otherwise): null offs = not fused
-  int blocks, cap_kind, cap_formula;
-  int32_t *offs, *demand, *list_base, *fill, *cap, *drops;
 };
 
 template <int NT>
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
 // runs the fp64 softmax + top-k (prob desc, expert asc; gating.cpp:19-78) of token j and patches
 // idxs / gates / the token's CTA histogram row. The last CTA to finish resets the list and adds
 // its size to the metrics counter.
-__global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a, int max_m) {
+__global__ void __launch_bounds__(kFixWarps * 32, kFixWarps <= 16 ? 2 : 1) gate_fixup_kernel(TcArgs a, int max_m) {
   static_assert(kFixTok <= kFixWarps, "one finalising warp per token");
   extern __shared__ __align__(16) uint8_t fsm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(fsm);                         // [kFixTok][M]
@@ -653,74 +656,12 @@ __global__ void __launch_bounds__(kFixWarps * 32, 1) gate_fixup_kernel(TcArgs a,
     }
     __syncthreads();
   }
-  __shared__ int last_sh;
   if (threadIdx.x == 0) {
     __threadfence();
-    last_sh = atomicAdd(a.flag_count + 1, 1) == static_cast<int>(gridDim.x) - 1;
-    if (last_sh) {
+    if (atomicAdd(a.flag_count + 1, 1) == static_cast<int>(gridDim.x) - 1) {
       if (a.fixups) atomicAdd(a.fixups, n);
       a.flag_count[0] = 0;
       a.flag_count[1] = 0;
-    }
-  }
-  __syncthreads();
-  if (!last_sh || a.offs == nullptr) return;
-  // ---- the last CTA: every histogram is final. Per (block, expert) column: exclusive scan of
-  // the gate CTAs' counts -> offs, total -> demand (scan_cols_kernel), one warp per column;
-  // then resolve_capacity (core.cpp:47-59), fill counts and member-list bases
-  // (finalize_capacity_kernel).
-  __threadfence();
-  const int cpb = a.cpb;
-  const int per = (cpb + 31) / 32;
-  for (int col = warp; col < a.blocks * E; col += blockDim.x / 32) {
-    const int b = col / E, e = col % E;
-    const int c0 = lane * per;
-    int sum = 0;
-    for (int i = 0; i < per; ++i) {
-      const int c = c0 + i;
-      if (c < cpb) sum += __ldcg(a.hist + static_cast<size_t>(b * cpb + c) * E + e);
-    }
-    int inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    int run = inc - sum;
-    for (int i = 0; i < per; ++i) {
-      const int c = c0 + i;
-      if (c < cpb) {
-        const size_t idx = static_cast<size_t>(b * cpb + c) * E + e;
-        a.offs[idx] = run;
-        run += __ldcg(a.hist + idx);
-      }
-    }
-    if (lane == 31) a.demand[col] = run;
-  }
-  __syncthreads();
-  __shared__ int mx_sh, cap_sh;
-  if (threadIdx.x == 0) {
-    *a.drops = 0;  // the assign pass accumulates this step's drops
-    mx_sh = 1;     // max demand floors at 1
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < a.blocks * E; p += blockDim.x) atomicMax(&mx_sh, a.demand[p]);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int cap = a.cap_formula;
-    if (a.cap_kind == 1) cap = mx_sh;                       // Auto
-    if (a.cap_kind == 2) cap = min(mx_sh, a.cap_formula);   // Bounded (formula at max_factor)
-    cap_sh = cap;
-    *a.cap = cap;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < a.blocks; b += blockDim.x) {
-    int run = b * a.T * a.k;
-    for (int e = 0; e < E; ++e) {
-      const int d = a.demand[b * E + e];
-      a.list_base[b * E + e] = run;
-      a.fill[b * E + e] = min(d, cap_sh);
-      run += d;
     }
   }
 }
@@ -774,7 +715,7 @@ int gate_tc_prepare_device(const double* wg, int M, int E, void* pieces, float* 
 int gate_tc_device(const void* x, const void* pieces, const double* wg, const float* wn_max,
                    int blocks, int T, int M, int E, int k, int32_t* idxs, double* gates,
                    int32_t* hist, int32_t* fixups, int32_t* flag_list, int32_t* flag_count,
-                   const GateScan* scan, cudaStream_t st) {
+                   cudaStream_t st) {
   if (!gate_tc_supported(M, E, k) || (reinterpret_cast<uintptr_t>(x) % 16) != 0) return -1;
   TcArgs a{};
   a.x = static_cast<const __nv_bfloat16*>(x);
@@ -792,17 +733,7 @@ int gate_tc_device(const void* x, const void* pieces, const double* wg, const fl
   a.fixups = fixups;
   a.flag_list = flag_list;
   a.flag_count = flag_count;
-  a.blocks = blocks;
-  if (scan) {
-    a.cap_kind = scan->cap_kind;
-    a.cap_formula = scan->cap_formula;
-    a.offs = scan->offs;
-    a.demand = scan->demand;
-    a.list_base = scan->list_base;
-    a.fill = scan->fill;
-    a.cap = scan->cap;
-    a.drops = scan->drops;
-  }
+
   static const bool hmma = [] {
     const char* e = std::getenv("MOE_GATE_HMMA");  // =1: the mma.sync kernel (A/B runs)
     return e != nullptr && e[0] == '1';
@@ -822,7 +753,7 @@ int gate_tc_device(const void* x, const void* pieces, const double* wg, const fl
         if (launch_status() != 0) return -2;
         const int fsmem = kFixTok * M * 2 + kFixTok * kFixWarps * 64 * 8;
         if (!smem_optin(gate_fixup_kernel, fsmem)) return -2;
-        launch_k(gate_fixup_kernel, dim3(148), dim3(kFixWarps * 32), fsmem, st, a, M);
+        launch_k(gate_fixup_kernel, dim3(kFixCtas), dim3(kFixWarps * 32), fsmem, st, a, M);
         return launch_status();
       };
       switch (E / 16) {
@@ -841,7 +772,7 @@ int gate_tc_device(const void* x, const void* pieces, const double* wg, const fl
     if (launch_status() != 0) return -2;
     const int fsmem = kFixTok * M * 2 + kFixTok * kFixWarps * 64 * 8;
     if (!smem_optin(gate_fixup_kernel, fsmem)) return -2;
-    launch_k(gate_fixup_kernel, dim3(148), dim3(kFixWarps * 32), fsmem, st, a, M);
+    launch_k(gate_fixup_kernel, dim3(kFixCtas), dim3(kFixWarps * 32), fsmem, st, a, M);
     return launch_status();
   };
   switch (E / 8) {

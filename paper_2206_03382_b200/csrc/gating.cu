@@ -1256,12 +1256,8 @@ int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t 
     rc = a.x_is_f32 ? launch_cosine_gate<float>(a, g, st) : launch_cosine_gate<__nv_bfloat16>(a, g, st);
   else if (!a.x_is_f32 && a.wg_pieces != nullptr && a.gate_flags != nullptr && g.probs == nullptr &&
            gate_tc_supported(a.M, a.E, a.k) && (reinterpret_cast<uintptr_t>(a.x) % 16) == 0)
-  {
-    const GateScan sc{a.cap_kind, a.cap_formula, g.offs, g.demand, g.list_base, g.fill, g.cap, g.drops};
     rc = gate_tc_device(a.x, a.wg_pieces, a.wg, a.wg_norm_max, a.blocks, a.T, a.M, a.E, a.k, g.idxs,
-                        g.gates, g.hist, a.gate_fixups, a.gate_flags, a.gate_flag_count, &sc, st);
-    if (rc == 0) return 0;  // the fix-up kernel's last CTA ran the capacity scan / resolve
-  }
+                        g.gates, g.hist, a.gate_fixups, a.gate_flags, a.gate_flag_count, st);
   else
     rc = a.x_is_f32 ? launch_gate<float>(a.x, a.wg, a.blocks, a.T, a.M, a.E, a.k, g.idxs, g.gates,
                                          g.hist, g.probs, st)

@@ -57,17 +57,10 @@ struct GatingArgs {
 bool gate_tc_supported(int M, int E, int k);
 int gate_tc_prepare_device(const double* wg, int M, int E, void* pieces, float* wn_max,
                            cudaStream_t st);
-// The capacity scan / resolve outputs (scan_cols + finalize_capacity): when given, the certified
-// gate's fix-up kernel computes them in its last CTA and the caller skips those two kernels.
-struct GateScan {
-  int cap_kind, cap_formula;
-  int32_t *offs, *demand, *list_base, *fill, *cap, *drops;
-};
-// Returns 0 and sets *scanned = 1 when the scan ran inside (the tcgen05 path).
 int gate_tc_device(const void* x, const void* pieces, const double* wg, const float* wn_max,
                    int blocks, int T, int M, int E, int k, int32_t* idxs, double* gates,
                    int32_t* hist, int32_t* fixups, int32_t* flag_list, int32_t* flag_count,
-                   const GateScan* scan, cudaStream_t st);
+                   cudaStream_t st);
 
 // Cosine router weights: ct = C^T, en[e] = |C_e|; err = 2 if an expert row has zero norm.
 int cosine_prep_device(const double* ce, int E, int D, double* ct, double* en, int32_t* err,

@@ -1142,8 +1142,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
   prof_mark(kPhAssign, false, st);
   // gate + column scan + capacity finalize, assign (+ BPR rank), (+ resolve_capacity)
-  // (certified gate: gate + fix-up with the capacity scan inside, then assign)
-  launches_ += (gate_tc_ ? 3 : 4) + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
+  launches_ += 4 + (gate_tc_ ? 1 : 0) + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
   if (stats_dirty_) {

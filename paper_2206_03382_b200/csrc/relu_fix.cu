@@ -212,7 +212,7 @@ __device__ __forceinline__ double fixup_dot(const __nv_bfloat16* xr, const __nv_
   return s;
 }
 
-__global__ void __launch_bounds__(256) relu_fixup_kernel(
+__global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows,
     int M, int V, const unsigned long long* __restrict__ list, const unsigned int* __restrict__ count,
     unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
@@ -372,7 +372,12 @@ int wait_flags_device(const FlagWait& w, cudaStream_t st) {
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
                       void* act, unsigned long long* relu_mask, cudaStream_t st) {
-  launch_k(relu_fixup_kernel, 148 * 8, 256, 0, st, static_cast<const __nv_bfloat16*>(x),
+  // one wave: the CTAs resident at once (2 per SM at this kernel's 128 registers) grid-stride
+  // over the list, instead of 4 waves of mostly latency-bound CTAs
+#ifndef MOE_FIXUP_CTAS_PER_SM
+#define MOE_FIXUP_CTAS_PER_SM 2
+#endif
+  launch_k(relu_fixup_kernel, 148 * MOE_FIXUP_CTAS_PER_SM, 256, 0, st, static_cast<const __nv_bfloat16*>(x),
                                              static_cast<const __nv_bfloat16*>(w1t), G, seg_rows,
                                              M, V, list, count, cap,
                                              static_cast<__nv_bfloat16*>(act), relu_mask);

@@ -92,8 +92,8 @@ def test_certified_gate_tgt_shape_fixup_rate(cuda):
 
 @pytest.mark.parametrize("cap,kind,f", [("auto", 1, 1.0), ("bounded", 2, 1.25), ("bounded", 2, 0.5)])
 def test_certified_gate_capacity_policies(cuda, cap, kind, f):
-    """Auto / Bounded capacity on the certified path: the fix-up kernel's last CTA runs the
-    capacity scan and resolve_capacity (core.cpp:47-59) itself."""
+    """Auto / Bounded capacity (resolve_capacity, core.cpp:47-59) after the certified gate: the
+    histograms the fix-up patched feed the capacity scan."""
     T, M, E, k = 3000, 512, 32, 2
     x, wg = _inputs(23, T, M, E, "near_ties")
     idxs, loc, gates, capv, m = _route(x, wg, E, k, f, M, T, "auto", cap)
