@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
   // programmatic dependent launch: the prologue above overlapped the previous kernel's tail;
   // operands produced by it are read only after this wait
   pdl_entry();
+  if (args.span != nullptr && threadIdx.x == 0) atomicMin(args.span, globaltimer_ns());
   if (args.wait.base != nullptr && (warp == 0 || warp >= 4)) {
     // fused receive wait: the producer warp polls the peers' flags (ld.acquire.sys) before its
     // first TMA load -- the async proxy must then see what the copy engines wrote before the
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
     __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc<kTmemCols, kCG>(tmem_base);
+  if (args.span != nullptr && threadIdx.x == 0) atomicMax(args.span + 1, globaltimer_ns());
 }
 
 // ---------------------------------------------------------------- host side

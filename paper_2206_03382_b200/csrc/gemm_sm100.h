@@ -70,6 +70,9 @@ struct GemmArgs {
   // kIdxPeerD: destination combine buffer of every rank (this rank's own for src == rank)
   uint32_t peer_world, peer_rank, peer_out_segs;  // out_segs = chunks * E
   void* peer_d[kMaxPeers];
+  // Kernel span (measurement): [0] = min over CTAs of %globaltimer once the kernel may start
+  // work (after the programmatic-dependent-launch wait), [1] = max at CTA exit. Null: off.
+  unsigned long long* span = nullptr;
 };
 
 // Pack / unpack of one ReLU-fixup entry.

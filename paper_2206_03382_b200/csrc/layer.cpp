@@ -400,6 +400,7 @@ void Layer::tl_flush() {
 }
 
 void Layer::prof_mark(int phase, bool begin, cudaStream_t st) {
+  cur_phase_ = begin ? phase : -1;
   if (tl_on_) {
     static const char* names[] = {"gate", "encode", "gemm_up", "gemm_down", "decode", "decode_bwd",
                                   "gemm_dgrad_mask", "gemm_dgrad", "gemm_wgrad1", "gemm_wgrad2",
@@ -690,8 +691,17 @@ void Layer::gemm(int kind, const void* A, const void* B, void* D, const GemmArgs
   if (cfg_.dtype == MOE_DTYPE_F32)
     rc = gemm_f32(kind, static_cast<const float*>(A), static_cast<const float*>(B),
                   static_cast<float*>(D), a, st);
-  else if (tc_ok(kind, a))
-    rc = gemm_fwd(static_cast<GemmKind>(kind), A, B, D, a, nseg, num_sms_, st);
+  else if (tc_ok(kind, a)) {
+    constexpr int kMaxSpans = 4096;
+    if (kspan_on_ && static_cast<int>(kspan_phase_.size()) < kMaxSpans) {
+      GemmArgs b = a;
+      b.span = static_cast<unsigned long long*>(kspan_.p) + 2 * kspan_phase_.size();
+      kspan_phase_.push_back(cur_phase_);
+      rc = gemm_fwd(static_cast<GemmKind>(kind), A, B, D, b, nseg, num_sms_, st);
+    } else {
+      rc = gemm_fwd(static_cast<GemmKind>(kind), A, B, D, a, nseg, num_sms_, st);
+    }
+  }
   else
     rc = gemm_bf16_simt(kind, A, B, D, a, st);
   ckr(rc, "expert gemm");
@@ -2021,6 +2031,43 @@ void Layer::get_grads(float* dw1, float* dw2) {
   // the last backward's gradients, wherever they went (internal or caller-supplied buffers)
   if (dw1) ck(cudaMemcpy(dw1, last_dw1_, 4 * n, cudaMemcpyDeviceToHost), "copy");
   if (dw2) ck(cudaMemcpy(dw2, last_dw2_, 4 * n, cudaMemcpyDeviceToHost), "copy");
+}
+
+void Layer::set_kernel_spans(bool on) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  constexpr size_t kMaxSpans = 4096;
+  if (on && kspan_.p == nullptr) kspan_.alloc(sizeof(unsigned long long) * 2 * kMaxSpans);
+  if (on) {
+    ck(cudaDeviceSynchronize(), "sync");
+    std::vector<unsigned long long> init(2 * kMaxSpans);
+    for (size_t i = 0; i < kMaxSpans; ++i) {
+      init[2 * i] = ~0ull;
+      init[2 * i + 1] = 0ull;
+    }
+    ck(cudaMemcpy(kspan_.p, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice),
+       "span init");
+  }
+  kspan_phase_.clear();
+  kspan_on_ = on;
+}
+
+void Layer::take_kernel_spans(double* ms, int64_t* counts, int n) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  for (int i = 0; i < n; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  if (kspan_phase_.empty()) return;
+  ck(cudaDeviceSynchronize(), "sync");
+  std::vector<unsigned long long> h(2 * kspan_phase_.size());
+  ck(cudaMemcpy(h.data(), kspan_.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "copy");
+  for (size_t i = 0; i < kspan_phase_.size(); ++i) {
+    const int ph = kspan_phase_[i];
+    if (ph < 0 || ph >= n || h[2 * i + 1] < h[2 * i]) continue;
+    ms[ph] += static_cast<double>(h[2 * i + 1] - h[2 * i]) * 1e-6;
+    counts[ph] += 1;
+  }
+  set_kernel_spans(kspan_on_);  // re-arm (clears the records)
 }
 
 }  // namespace moe

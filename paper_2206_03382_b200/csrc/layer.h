@@ -85,6 +85,10 @@ class Layer {
   void* w2() { return w2_.p; }
   // resident weights changed in place: rebuild the derived state (W1^T, column norms, W1 slice)
   void weights_updated() { stats_dirty_ = true; }
+  // Kernel spans of the tcgen05 expert GEMMs (device %globaltimer; no events, so programmatic
+  // dependent launch stays intact): per phase, the summed span in ms and the launch count.
+  void set_kernel_spans(bool on);
+  void take_kernel_spans(double* ms, int64_t* counts, int n);
   int64_t launches() const { return launches_; }
   void set_profiling(bool on) { prof_ = on; }
   // Sums (ms) and counts per phase since the last call; synchronizes.
@@ -164,6 +168,10 @@ class Layer {
   // certified tensor-core gate: bf16 hi/lo split of Wg, max column norm, re-decision counter
   DevMem wg_pieces_, wg_nmax_, gate_fix_, gate_flags_;
   DevMem bpr_keys_, bpr_pos_;  // chunked BPR ranking scratch
+  DevMem kspan_;                 // [kMaxSpans][2] u64 kernel spans (set_kernel_spans)
+  std::vector<int> kspan_phase_;
+  bool kspan_on_ = false;
+  int cur_phase_ = -1;
   bool gate_tc_ = false, wg_dirty_ = true;
   // peer transport: dispatch fused into encode / decode-backward (NVLink stores, MOE_DISPATCH=fused)
   bool fused_dispatch_ = false;

@@ -275,6 +275,19 @@ class LayerState:
                                      cnt.ctypes.data_as(C.POINTER(C.c_int64)), n), self._h)
         return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(_lib.PHASES)}
 
+    def set_kernel_spans(self, on: bool) -> None:
+        check(lib().moe_set_kernel_spans(self._h, int(on)), self._h)
+
+    def take_kernel_spans(self) -> dict:
+        """{phase: (summed GEMM kernel span ms, launches)} from the device clock (no events)."""
+        import numpy as np
+        n = len(_lib.PHASES)
+        ms = np.zeros(n, np.float64)
+        cnt = np.zeros(n, np.int64)
+        check(lib().moe_take_kernel_spans(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                          cnt.ctypes.data_as(C.POINTER(C.c_int64)), n), self._h)
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(_lib.PHASES)}
+
     @property
     def handle(self):
         return self._h
