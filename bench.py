@@ -593,6 +593,7 @@ def run_gpu(args):
                          "achieved_event_timed": achieved_ev,
                          "gemm_span_ms_per_step": ({n: spans[n][0] / args.steps for n in gemm_names}
                                                    if gemm_ms_span else None),
+                         "gemm_effective_sm_mhz": (spans["_sm_mhz"][0] if gemm_ms_span else None),
                          "peak_source": gemm_peak_src,
                          "timing": ("device-clock kernel spans (%globaltimer, first CTA past the "
                                     "launch-dependency wait to the last CTA exit) over a third "

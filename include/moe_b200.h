@@ -245,9 +245,10 @@ int moe_set_profiling(moe_handle* h, int32_t on);
 /* Kernel spans of the tcgen05 expert GEMMs, measured with the device clock (%globaltimer: first
  * CTA past its launch-dependency wait to last CTA exit) instead of CUDA events, so programmatic
  * dependent launch keeps overlapping the kernels. moe_take_kernel_spans fills, per phase of the
- * MOE_NUM_PHASES list above, the summed span in ms and the launch count since the last call. */
+ * MOE_NUM_PHASES list above, the summed span in ms and the launch count since the last call;
+ * sm_mhz (optional): the effective SM clock inside those kernels (clock64 / %globaltimer). */
 int moe_set_kernel_spans(moe_handle* h, int32_t on);
-int moe_take_kernel_spans(moe_handle* h, double* ms, int64_t* counts, int32_t n);
+int moe_take_kernel_spans(moe_handle* h, double* ms, int64_t* counts, int32_t n, double* sm_mhz);
 /* Per-phase summed milliseconds and interval counts since the last call (synchronizes). */
 int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n);
 

@@ -87,7 +87,7 @@ SIGNATURES = {
     "moe_get_weights_device": (I32, [P, I32, C.POINTER(P)]),
     "moe_weights_updated": (I32, [P]),
     "moe_set_kernel_spans": (I32, [P, I32]),
-    "moe_take_kernel_spans": (I32, [P, PD, PI64, I32]),
+    "moe_take_kernel_spans": (I32, [P, PD, PI64, I32, PD]),
     "moe_get_expert_grad_slices": (I32, [P, P, P, P]),
     "moe_kernel_launches": (I64, [P]),
     "moe_set_profiling": (I32, [P, I32]),

@@ -343,8 +343,11 @@ int moe_weights_updated(moe_handle* h) { LAYER_CALL(h, h->layer->weights_updated
 int64_t moe_kernel_launches(const moe_handle* h) { return h ? h->layer->launches() : 0; }
 int moe_set_profiling(moe_handle* h, int32_t on) { LAYER_CALL(h, h->layer->set_profiling(on != 0)); }
 int moe_set_kernel_spans(moe_handle* h, int32_t on) { LAYER_CALL(h, h->layer->set_kernel_spans(on != 0)); }
-int moe_take_kernel_spans(moe_handle* h, double* ms, int64_t* counts, int32_t n) {
-  LAYER_CALL(h, h->layer->take_kernel_spans(ms, counts, n));
+int moe_take_kernel_spans(moe_handle* h, double* ms, int64_t* counts, int32_t n, double* sm_mhz) {
+  LAYER_CALL(h, {
+    h->layer->take_kernel_spans(ms, counts, n);
+    if (sm_mhz) *sm_mhz = h->layer->span_mhz();
+  });
 }
 int moe_take_profile(moe_handle* h, double* ms, int64_t* counts, int32_t n) {
   LAYER_CALL(h, h->layer->take_profile(ms, counts, n));

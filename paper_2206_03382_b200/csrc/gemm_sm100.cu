@@ -194,7 +194,13 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
   // programmatic dependent launch: the prologue above overlapped the previous kernel's tail;
   // operands produced by it are read only after this wait
   pdl_entry();
-  if (args.span != nullptr && threadIdx.x == 0) atomicMin(args.span, globaltimer_ns());
+  long long clk0 = 0;
+  uint64_t ns0 = 0;
+  if (args.span != nullptr && threadIdx.x == 0) {
+    ns0 = globaltimer_ns();
+    clk0 = clock64();
+    atomicMin(args.span, ns0);
+  }
   if (args.wait.base != nullptr && (warp == 0 || warp >= 4)) {
     // fused receive wait: the producer warp polls the peers' flags (ld.acquire.sys) before its
     // first TMA load -- the async proxy must then see what the copy engines wrote before the
@@ -552,7 +558,14 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
     __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc<kTmemCols, kCG>(tmem_base);
-  if (args.span != nullptr && threadIdx.x == 0) atomicMax(args.span + 1, globaltimer_ns());
+  if (args.span != nullptr && threadIdx.x == 0) {
+    const uint64_t ns1 = globaltimer_ns();
+    atomicMax(args.span + 1, ns1);
+    if (blockIdx.x == 0) {  // CTA 0's own SM clock over its lifetime: cycles, ns
+      args.span[2] = static_cast<unsigned long long>(clock64() - clk0);
+      args.span[3] = ns1 - ns0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- host side

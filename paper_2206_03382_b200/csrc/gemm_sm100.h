@@ -71,7 +71,8 @@ struct GemmArgs {
   uint32_t peer_world, peer_rank, peer_out_segs;  // out_segs = chunks * E
   void* peer_d[kMaxPeers];
   // Kernel span (measurement): [0] = min over CTAs of %globaltimer once the kernel may start
-  // work (after the programmatic-dependent-launch wait), [1] = max at CTA exit. Null: off.
+  // work (after the programmatic-dependent-launch wait), [1] = max at CTA exit; [2] / [3] = CTA
+  // 0's clock64 cycles / nanoseconds over its lifetime (the effective SM clock). Null: off.
   unsigned long long* span = nullptr;
 };
 

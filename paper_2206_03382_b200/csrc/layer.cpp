@@ -695,7 +695,7 @@ void Layer::gemm(int kind, const void* A, const void* B, void* D, const GemmArgs
     constexpr int kMaxSpans = 4096;
     if (kspan_on_ && static_cast<int>(kspan_phase_.size()) < kMaxSpans) {
       GemmArgs b = a;
-      b.span = static_cast<unsigned long long*>(kspan_.p) + 2 * kspan_phase_.size();
+      b.span = static_cast<unsigned long long*>(kspan_.p) + 4 * kspan_phase_.size();
       kspan_phase_.push_back(cur_phase_);
       rc = gemm_fwd(static_cast<GemmKind>(kind), A, B, D, b, nseg, num_sms_, st);
     } else {
@@ -2036,14 +2036,11 @@ void Layer::get_grads(float* dw1, float* dw2) {
 void Layer::set_kernel_spans(bool on) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   constexpr size_t kMaxSpans = 4096;
-  if (on && kspan_.p == nullptr) kspan_.alloc(sizeof(unsigned long long) * 2 * kMaxSpans);
+  if (on && kspan_.p == nullptr) kspan_.alloc(sizeof(unsigned long long) * 4 * kMaxSpans);
   if (on) {
     ck(cudaDeviceSynchronize(), "sync");
-    std::vector<unsigned long long> init(2 * kMaxSpans);
-    for (size_t i = 0; i < kMaxSpans; ++i) {
-      init[2 * i] = ~0ull;
-      init[2 * i + 1] = 0ull;
-    }
+    std::vector<unsigned long long> init(4 * kMaxSpans, 0ull);
+    for (size_t i = 0; i < kMaxSpans; ++i) init[4 * i] = ~0ull;
     ck(cudaMemcpy(kspan_.p, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice),
        "span init");
   }
@@ -2059,14 +2056,18 @@ void Layer::take_kernel_spans(double* ms, int64_t* counts, int n) {
   }
   if (kspan_phase_.empty()) return;
   ck(cudaDeviceSynchronize(), "sync");
-  std::vector<unsigned long long> h(2 * kspan_phase_.size());
+  std::vector<unsigned long long> h(4 * kspan_phase_.size());
   ck(cudaMemcpy(h.data(), kspan_.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "copy");
+  double cyc = 0.0, nsec = 0.0;
   for (size_t i = 0; i < kspan_phase_.size(); ++i) {
     const int ph = kspan_phase_[i];
-    if (ph < 0 || ph >= n || h[2 * i + 1] < h[2 * i]) continue;
-    ms[ph] += static_cast<double>(h[2 * i + 1] - h[2 * i]) * 1e-6;
+    if (ph < 0 || ph >= n || h[4 * i + 1] < h[4 * i]) continue;
+    ms[ph] += static_cast<double>(h[4 * i + 1] - h[4 * i]) * 1e-6;
     counts[ph] += 1;
+    cyc += static_cast<double>(h[4 * i + 2]);
+    nsec += static_cast<double>(h[4 * i + 3]);
   }
+  span_mhz_ = nsec > 0.0 ? cyc / nsec * 1e3 : 0.0;
   set_kernel_spans(kspan_on_);  // re-arm (clears the records)
 }
 

@@ -89,6 +89,7 @@ class Layer {
   // dependent launch stays intact): per phase, the summed span in ms and the launch count.
   void set_kernel_spans(bool on);
   void take_kernel_spans(double* ms, int64_t* counts, int n);
+  double span_mhz() const { return span_mhz_; }
   int64_t launches() const { return launches_; }
   void set_profiling(bool on) { prof_ = on; }
   // Sums (ms) and counts per phase since the last call; synchronizes.
@@ -168,8 +169,9 @@ class Layer {
   // certified tensor-core gate: bf16 hi/lo split of Wg, max column norm, re-decision counter
   DevMem wg_pieces_, wg_nmax_, gate_fix_, gate_flags_;
   DevMem bpr_keys_, bpr_pos_;  // chunked BPR ranking scratch
-  DevMem kspan_;                 // [kMaxSpans][2] u64 kernel spans (set_kernel_spans)
+  DevMem kspan_;                 // [kMaxSpans][4] u64 kernel spans (set_kernel_spans)
   std::vector<int> kspan_phase_;
+  double span_mhz_ = 0.0;  // effective SM clock inside the spanned GEMMs (last take)
   bool kspan_on_ = false;
   int cur_phase_ = -1;
   bool gate_tc_ = false, wg_dirty_ = true;

@@ -284,9 +284,13 @@ class LayerState:
         n = len(_lib.PHASES)
         ms = np.zeros(n, np.float64)
         cnt = np.zeros(n, np.int64)
+        mhz = C.c_double(0.0)
         check(lib().moe_take_kernel_spans(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
-                                          cnt.ctypes.data_as(C.POINTER(C.c_int64)), n), self._h)
-        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(_lib.PHASES)}
+                                          cnt.ctypes.data_as(C.POINTER(C.c_int64)), n,
+                                          C.byref(mhz)), self._h)
+        out = {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(_lib.PHASES)}
+        out["_sm_mhz"] = (float(mhz.value), 0)
+        return out
 
     @property
     def handle(self):
