@@ -1,6 +1,9 @@
 // Copy-engine all-to-all over NVLink peer memory. See peer_a2a.h.
 #include "peer_a2a.h"
 
+#include <algorithm>
+#include <cstdlib>
+
 #include <cudaTypedefs.h>
 
 #include <cstring>
@@ -102,6 +105,23 @@ PeerExchange::PeerExchange(int rank, int world, ncclComm_t comm, void* const buf
     ck(cudaEventCreateWithFlags(&ev_out_[p], cudaEventDisableTiming), "event");
   }
   ck(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming), "event");
+  {
+    const char* e = std::getenv("MOE_CE_SPLIT");
+    split_ = e ? std::max(1, std::min(8, std::atoi(e))) : 1;
+  }
+  xstreams_.assign(world, {});
+  xevents_.assign(world, {});
+  for (int p = 0; p < world; ++p) {
+    if (p == rank) continue;
+    for (int j = 1; j < split_; ++j) {
+      cudaStream_t xs;
+      cudaEvent_t xe;
+      ck(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreateWithFlags(&xe, cudaEventDisableTiming), "event");
+      xstreams_[p].push_back(xs);
+      xevents_[p].push_back(xe);
+    }
+  }
 
   peer_flags_.assign(world, nullptr);
   peer_norms_.assign(world, nullptr);
@@ -131,6 +151,10 @@ PeerExchange::~PeerExchange() {
   }
   for (auto st : pstreams_)
     if (st) cudaStreamDestroy(st);
+  for (auto& v : xstreams_)
+    for (auto st : v) cudaStreamDestroy(st);
+  for (auto& v : xevents_)
+    for (auto e : v) cudaEventDestroy(e);
   for (auto e : ev_out_)
     if (e) cudaEventDestroy(e);
   if (ev_in_) cudaEventDestroy(ev_in_);
@@ -196,9 +220,27 @@ void PeerExchange::push_chunk(cudaStream_t copy, int ch, int chunk, const void* 
     cudaStream_t ps = pstreams_[p];
     ck(cudaStreamWaitEvent(ps, ev_in_, 0), "wait");
     char* dst = static_cast<char*>(p == rank_ ? local_bufs_[ch] : peer_bufs_[ch][p]) + ro[rank_] * esz;
-    ck(cudaMemcpyAsync(dst, static_cast<const char*>(src) + so[p] * esz, block_bytes,
+    const char* sp = static_cast<const char*>(src) + so[p] * esz;
+    const int pieces = p == rank_ ? 1 : split_;
+    // pieces 1.. on helper streams (more copy engines per destination), joined before the flag
+    const size_t piece = ((block_bytes / pieces) + 255) & ~static_cast<size_t>(255);
+    for (int j = 1; j < pieces; ++j) {
+      const size_t off = piece * j;
+      if (off >= block_bytes) break;
+      cudaStream_t xs = xstreams_[p][j - 1];
+      ck(cudaStreamWaitEvent(xs, ev_in_, 0), "wait");
+      ck(cudaMemcpyAsync(dst + off, sp + off, std::min(piece, block_bytes - off), cudaMemcpyDeviceToDevice,
+                         xs),
+         "peer copy");
+    }
+    ck(cudaMemcpyAsync(dst, sp, pieces > 1 ? std::min(piece, block_bytes) : block_bytes,
                        cudaMemcpyDeviceToDevice, ps),
        "peer copy");
+    for (int j = 1; j < pieces; ++j) {
+      if (piece * j >= block_bytes) break;
+      ck(cudaEventRecord(xevents_[p][j - 1], xstreams_[p][j - 1]), "event");
+      ck(cudaStreamWaitEvent(ps, xevents_[p][j - 1], 0), "wait");
+    }
     if (norm_src) {  // the rows' norms travel with them (before the flag)
       float* nd = static_cast<float*>(p == rank_ ? local_norms_ : peer_norms_[p]) + ro[rank_] / row_len;
       ck(cudaMemcpyAsync(nd, norm_src + so[p] / row_len, block_bytes / esz / row_len * sizeof(float),
@@ -230,8 +272,25 @@ void PeerExchange::push_rows(cudaStream_t copy, int ch, int slot, const void* sr
     // segs expert segments of seg_bytes each; rows [row0, row0 + rows) of every segment
     char* dst = static_cast<char*>(peer_bufs_[ch][p]) + ro[rank_] + row0_bytes;
     const char* s0 = static_cast<const char*>(src) + so[p] + row0_bytes;
-    ck(cudaMemcpy2DAsync(dst, seg_bytes, s0, seg_bytes, rows_bytes, segs, cudaMemcpyDeviceToDevice, ps),
+    // segments split over the helper streams (more copy engines per destination)
+    const size_t per = (segs + split_ - 1) / split_;
+    for (int j = 1; j < split_; ++j) {
+      const size_t s0j = per * j;
+      if (s0j >= segs) break;
+      cudaStream_t xs = xstreams_[p][j - 1];
+      ck(cudaStreamWaitEvent(xs, ev_in_, 0), "wait");
+      ck(cudaMemcpy2DAsync(dst + s0j * seg_bytes, seg_bytes, s0 + s0j * seg_bytes, seg_bytes, rows_bytes,
+                           std::min(per, segs - s0j), cudaMemcpyDeviceToDevice, xs),
+         "peer copy (rows)");
+    }
+    ck(cudaMemcpy2DAsync(dst, seg_bytes, s0, seg_bytes, rows_bytes, split_ > 1 ? std::min(per, segs) : segs,
+                         cudaMemcpyDeviceToDevice, ps),
        "peer copy (rows)");
+    for (int j = 1; j < split_; ++j) {
+      if (per * j >= segs) break;
+      ck(cudaEventRecord(xevents_[p][j - 1], xstreams_[p][j - 1]), "event");
+      ck(cudaStreamWaitEvent(ps, xevents_[p][j - 1], 0), "wait");
+    }
     if (norm_src) {  // the rows' norms travel with them (before the flag)
       const size_t npitch = seg_bytes / row_bytes * sizeof(float);
       float* nd = static_cast<float*>(peer_norms_[p]) + (ro[rank_] + row0_bytes) / row_bytes;

@@ -104,6 +104,11 @@ class PeerExchange {
   std::vector<void*> peer_norms_;  // mapped norm arrays of peers
   size_t nflags_ = 0;
   std::vector<cudaStream_t> pstreams_;  // per-destination copy streams
+  // MOE_CE_SPLIT = s > 1: each destination's block is cut into s pieces on s streams (s copy
+  // engines per destination); helper streams / join events per destination (piece 0 on pstreams_)
+  int split_ = 1;
+  std::vector<std::vector<cudaStream_t>> xstreams_;
+  std::vector<std::vector<cudaEvent_t>> xevents_;
   cudaEvent_t ev_in_ = nullptr;
   std::vector<cudaEvent_t> ev_out_;
 };
