@@ -117,6 +117,9 @@ typedef struct moe_step_metrics {
   int32_t parallel;    /* MOE_PARALLEL_P1 / _P2: the exchange form used (StepMetrics::parallel) */
   int64_t gate_fixups; /* certified gate: tokens re-decided from fp64 logits since the last
                           moe_get_metrics (0 with the fp64 gate) */
+  int64_t simt_gemms;  /* bf16 expert-GEMM launches of the last forward + backward that ran the
+                          SIMT kernel because the shape is not tcgen05-eligible (N % 256, K % 64,
+                          wgrad rows % 128): ~10x slower; 0 on every BASELINE config */
 } moe_step_metrics;
 #define MOE_FUSED_DECODE 1  /* W = 1, k = 1: decode / encode-backward = down / dgrad epilogue scatter */
 #define MOE_FUSED_COMBINE 2 /* W > 1 peer backend: combine = down / dgrad epilogue NVLink stores */

@@ -47,7 +47,7 @@ class StepMetrics(C.Structure):
         ("f", C.c_double), ("capacity", C.c_int64), ("a2a_algo", C.c_int32),
         ("degree", C.c_int32), ("seconds", C.c_double), ("comm_bytes", C.c_double),
         ("drop_count", C.c_int64), ("relu_fixups", C.c_int64), ("fused", C.c_int32),
-        ("parallel", C.c_int32), ("gate_fixups", C.c_int64),
+        ("parallel", C.c_int32), ("gate_fixups", C.c_int64), ("simt_gemms", C.c_int64),
     ]
 
 

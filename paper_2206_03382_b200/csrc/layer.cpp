@@ -702,8 +702,17 @@ void Layer::gemm(int kind, const void* A, const void* B, void* D, const GemmArgs
       rc = gemm_fwd(static_cast<GemmKind>(kind), A, B, D, a, nseg, num_sms_, st);
     }
   }
-  else
+  else {
+    // shape not tcgen05-eligible: ~10x slower SIMT kernel, counted in moe_step_metrics.simt_gemms
+    static bool warned = false;
+    if (!warned) {
+      warned = true;
+      std::fprintf(stderr, "moe_b200: expert GEMM N=%u K=%u Mo=%u is not tcgen05-eligible (N %% 256, "
+                           "K %% 64, wgrad rows %% 128); using the SIMT kernel\n", a.N, a.K, a.Mo);
+    }
+    ++simt_gemms_;
     rc = gemm_bf16_simt(kind, A, B, D, a, st);
+  }
   ckr(rc, "expert gemm");
   ++launches_;
 }
@@ -1108,6 +1117,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ck(cudaSetDevice(device_), "cudaSetDevice");
   if (W_ > 1 && comm_ == nullptr) throw MoeError(MOE_ECOMM, "forward: communicator aborted after an earlier failure");
   check_comm("forward");
+  simt_gemms_ = 0;
   launches_ = 0;
   comm_bytes_ = 0.0;
   ck(cudaEventRecord(ev_fwd_start_, st), "event");
@@ -2006,6 +2016,7 @@ void Layer::get_metrics(moe_step_metrics* m) {
   m->fused = (fused_ ? MOE_FUSED_DECODE : 0) | (peer_ && fused_combine_ ? MOE_FUSED_COMBINE : 0);
   m->parallel = parallel_;
   m->gate_fixups = 0;
+  m->simt_gemms = simt_gemms_;  // since the last forward began: that forward + its backward
   if (gate_tc_) {
     int32_t nf = 0;
     ck(cudaMemcpy(&nf, gate_fix_.p, 4, cudaMemcpyDeviceToHost), "copy");

@@ -173,6 +173,7 @@ class Layer {
   std::vector<int> kspan_phase_;
   double span_mhz_ = 0.0;  // effective SM clock inside the spanned GEMMs (last take)
   bool kspan_on_ = false;
+  int64_t simt_gemms_ = 0;  // SIMT fallback GEMM launches since the last forward began
   int cur_phase_ = -1;
   bool gate_tc_ = false, wg_dirty_ = true;
   // peer transport: dispatch fused into encode / decode-backward (NVLink stores, MOE_DISPATCH=fused)

@@ -88,6 +88,7 @@ class StepMetricsPy:
     fused: int = 0  # MOE_FUSED_DECODE (1) | MOE_FUSED_COMBINE (2)
     parallel: str = "p1"  # StepMetrics::parallel
     gate_fixups: int = 0  # certified gate: tokens re-decided in fp64 since the last read
+    simt_gemms: int = 0   # bf16 GEMM launches that fell back to the SIMT kernel (shape cliff)
 
 
 @dataclass
@@ -243,7 +244,7 @@ class LayerState:
         check(lib().moe_get_metrics(self._h, C.byref(m)), self._h)
         return StepMetricsPy(m.f, m.capacity, "linear" if m.a2a_algo == 0 else "2dh", m.degree,
                              m.seconds, m.comm_bytes, m.drop_count, m.relu_fixups, m.fused,
-                             "p2" if m.parallel == 1 else "p1", m.gate_fixups)
+                             "p2" if m.parallel == 1 else "p1", m.gate_fixups, m.simt_gemms)
 
     def grad_slices(self):
         """reduce_scatter_grads_p1: this rank's slice of every expert's dW1 / dW2 (fp32 device),
