@@ -642,11 +642,22 @@ __global__ void __launch_bounds__(kDmWarps * 32) gate_dmma2_kernel(DmmaArgs a) {
   for (int e = threadIdx.x; e < E; e += NTH) hist[static_cast<size_t>(blockIdx.x) * E + e] = sh_hist[e];
 }
 
+__device__ void finalize_capacity_cta(int blocks, int E, int T, int k, int cap_kind, int cap_formula,
+                                      const int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
+                                      int32_t* __restrict__ fill, int32_t* __restrict__ cap_out,
+                                      int32_t* __restrict__ drops);
+
+struct FinalizeArgs {
+  int32_t* done;  // null: the separate finalize kernel runs
+  int blocks, T, k, cap_kind, cap_formula;
+  int32_t *list_base, *fill, *cap, *drops;
+};
+
 // Per (block, expert) column: exclusive scan of the CTA histograms -> offs, demand.
 // One CTA per column; each thread scans a contiguous run of CTA counts, then a block scan.
 __global__ void __launch_bounds__(256)
     scan_cols_kernel(const int32_t* __restrict__ hist, int cta_per_block, int E,
-                     int32_t* __restrict__ offs, int32_t* __restrict__ demand) {
+                     int32_t* __restrict__ offs, int32_t* __restrict__ demand, FinalizeArgs fa) {
   pdl_entry();
   __shared__ int32_t wsum[8];
   const int p = blockIdx.x, b = p / E, e = p % E;
@@ -679,22 +690,37 @@ __global__ void __launch_bounds__(256)
     run += local[i];
   }
   if (threadIdx.x == blockDim.x - 1) demand[p] = run;
+  if (fa.done == nullptr) return;
+  // the last column CTA to finish resolves the capacity (finalize_capacity_kernel's work)
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(fa.done, 1) == static_cast<int>(gridDim.x) - 1;
+    if (last) *fa.done = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_capacity_cta(fa.blocks, E, fa.T, fa.k, fa.cap_kind, fa.cap_formula, demand, fa.list_base,
+                        fa.fill, fa.cap, fa.drops);
 }
 
 // resolve_capacity (core.cpp:47-59) over the per-block max demand, fill counts and the BPR
 // member-list bases. One small CTA.
-__global__ void finalize_capacity_kernel(int blocks, int E, int T, int k, int cap_kind,
-                                         int cap_formula, const int32_t* __restrict__ demand,
-                                         int32_t* __restrict__ list_base,
-                                         int32_t* __restrict__ fill, int32_t* __restrict__ cap_out,
-                                         int32_t* __restrict__ drops) {
-  pdl_entry();
-  if (threadIdx.x == 0) *drops = 0;  // the assign pass accumulates this step's drops
+// resolve_capacity body (one CTA): shared by the standalone kernel and the scan's last CTA.
+__device__ void finalize_capacity_cta(int blocks, int E, int T, int k, int cap_kind, int cap_formula,
+                                      const int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
+                                      int32_t* __restrict__ fill, int32_t* __restrict__ cap_out,
+                                      int32_t* __restrict__ drops) {
   __shared__ int32_t cap_sh;
   __shared__ int32_t mx_sh;
-  if (threadIdx.x == 0) mx_sh = 1;  // max demand floors at 1
+  if (threadIdx.x == 0) {
+    *drops = 0;  // the assign pass accumulates this step's drops
+    mx_sh = 1;   // max demand floors at 1
+  }
   __syncthreads();
-  for (int p = threadIdx.x; p < blocks * E; p += blockDim.x) atomicMax(&mx_sh, demand[p]);
+  for (int p = threadIdx.x; p < blocks * E; p += blockDim.x) atomicMax(&mx_sh, __ldcg(demand + p));
   __syncthreads();
   if (threadIdx.x == 0) {
     int cap = cap_formula;
@@ -708,12 +734,21 @@ __global__ void finalize_capacity_kernel(int blocks, int E, int T, int k, int ca
   for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
     int run = b * T * k;
     for (int e = 0; e < E; ++e) {
-      const int d = demand[b * E + e];
+      const int d = __ldcg(demand + b * E + e);
       list_base[b * E + e] = run;
       fill[b * E + e] = min(d, cap);
       run += d;
     }
   }
+}
+
+__global__ void finalize_capacity_kernel(int blocks, int E, int T, int k, int cap_kind,
+                                         int cap_formula, const int32_t* __restrict__ demand,
+                                         int32_t* __restrict__ list_base,
+                                         int32_t* __restrict__ fill, int32_t* __restrict__ cap_out,
+                                         int32_t* __restrict__ drops) {
+  pdl_entry();
+  finalize_capacity_cta(blocks, E, T, k, cap_kind, cap_formula, demand, list_base, fill, cap_out, drops);
 }
 
 // FIFO ranks over the flattened (t, j) grid of each gate CTA. bpr==0: write locations + slots.
@@ -1265,8 +1300,11 @@ int run_gating_device(const GatingArgs& a, const GatingBuffers& g, cudaStream_t 
                                                  g.gates, g.hist, g.probs, st);
   if (rc) return rc;
   if (cpb > 16 * 256) return -1;
-  launch_k(scan_cols_kernel, a.blocks * a.E, 256, 0, st, g.hist, cpb, a.E, g.offs, g.demand);
+  FinalizeArgs fa{g.scan_done, a.blocks, a.T, a.k, a.cap_kind, a.cap_formula, g.list_base, g.fill,
+                  g.cap, g.drops};
+  launch_k(scan_cols_kernel, a.blocks * a.E, 256, 0, st, g.hist, cpb, a.E, g.offs, g.demand, fa);
   if (launch_status() != 0) return -2;
+  if (g.scan_done != nullptr) return 0;  // the scan's last CTA resolved the capacity
   launch_k(finalize_capacity_kernel, 1, 256, 0, st, a.blocks, a.E, a.T, a.k, a.cap_kind, a.cap_formula,
                                              g.demand, g.list_base, g.fill, g.cap, g.drops);
   if (launch_status() != 0) return -2;

@@ -81,6 +81,9 @@ struct GatingBuffers {
   int32_t* slot_token;  // [blocks, E, cap]
   float* slot_gate;     // [blocks, E, cap]
   double* probs;        // optional [blocks*T, E]
+  // resolve_capacity in the capacity scan's last CTA: a zeroed counter (reset by that CTA);
+  // null: a separate finalize kernel
+  int32_t* scan_done = nullptr;
   // BPR chunked ranking scratch ([blocks*T*k] each); null: the one-CTA-per-list sort
   unsigned long long* bpr_keys = nullptr;
   int32_t* bpr_pos = nullptr;

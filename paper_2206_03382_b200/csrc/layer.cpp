@@ -297,6 +297,8 @@ Layer::Layer(const moe_config& cfg, int rank, const uint8_t* nccl_id, int device
   list_base_.alloc(4 * E_);
   fill_.alloc(4 * E_);
   list_.alloc(4 * Tk);
+  scan_done_.alloc(sizeof(int32_t));
+  ck(cudaMemset(scan_done_.p, 0, sizeof(int32_t)), "memset");
   if (cfg.bpr) {  // chunked BPR ranking scratch
     bpr_keys_.alloc(8 * Tk);
     bpr_pos_.alloc(4 * Tk);
@@ -766,6 +768,7 @@ GatingBuffers Layer::gating_buffers() {
   b.slot_token = static_cast<int32_t*>(slot_token_.p);
   b.slot_gate = static_cast<float*>(slot_gate_.p);
   b.probs = nullptr;
+  b.scan_done = static_cast<int32_t*>(scan_done_.p);
   if (cfg_.bpr) {
     b.bpr_keys = static_cast<unsigned long long*>(bpr_keys_.p);
     b.bpr_pos = static_cast<int32_t*>(bpr_pos_.p);
@@ -1162,7 +1165,8 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   ckr(run_assign_device(ga, gb, cap_, st), "assign_locations");
   prof_mark(kPhAssign, false, st);
   // gate + column scan + capacity finalize, assign (+ BPR rank), (+ resolve_capacity)
-  launches_ += 4 + (gate_tc_ ? 1 : 0) + (cfg_.bpr ? 1 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
+  // gate (+ certified fix-up), capacity scan (+ resolve in its last CTA), assign (+ BPR rank)
+  launches_ += 3 + (gate_tc_ ? 1 : 0) + (cfg_.bpr ? 2 : 0) + (cfg_.capacity_kind != MOE_CAP_FIXED ? 1 : 0);
 
   const bool cert = cfg_.dtype == MOE_DTYPE_BF16;
   if (stats_dirty_) {

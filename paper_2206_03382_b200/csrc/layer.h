@@ -169,6 +169,7 @@ class Layer {
   // certified tensor-core gate: bf16 hi/lo split of Wg, max column norm, re-decision counter
   DevMem wg_pieces_, wg_nmax_, gate_fix_, gate_flags_;
   DevMem bpr_keys_, bpr_pos_;  // chunked BPR ranking scratch
+  DevMem scan_done_;           // capacity scan: last-CTA counter
   DevMem kspan_;                 // [kMaxSpans][4] u64 kernel spans (set_kernel_spans)
   std::vector<int> kspan_phase_;
   double span_mhz_ = 0.0;  // effective SM clock inside the spanned GEMMs (last take)
