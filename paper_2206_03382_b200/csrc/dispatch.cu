@@ -251,6 +251,62 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   }
   const int lane = threadIdx.x % 32;
   const int ntok = g.blocks * g.T;
+  if constexpr (kVec) {
+    if (g.k == 1 && g.M / Vec<T>::N <= 32 * kUnroll) {
+      // top-1 (W > 1 combine, NCCL transport): two tokens per warp with all their row loads in
+      // flight before any math (the gather is latency-bound); y = g * row, dropped -> 0
+      constexpr int VN = Vec<T>::N;
+      const int nv = g.M / VN;
+      const int S = gridDim.x * kWarpsPerCta;
+      for (int t0 = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t0 < ntok; t0 += 2 * S) {
+        const int tt[2] = {t0, t0 + S};
+        const uint4* src[2];
+        float gv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          src[h] = nullptr;
+          gv[h] = 0.0f;
+          if (tt[h] < ntok) {
+            const int loc = locations[tt[h]];
+            if (loc >= 0) {
+              const int e = idxs[tt[h]];
+              MOE_CHECK(loc < g.cap && e >= 0 && e < g.E, "decode: location / expert out of range");
+              src[h] = reinterpret_cast<const uint4*>(z + slot_row(g, tt[h] / g.T, e, loc) * g.M);
+              gv[h] = static_cast<float>(gates[tt[h]]);
+            }
+          }
+        }
+        uint4 buf[2][kUnroll];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = u * 32 + lane;
+            if (src[h] && v < nv) buf[h][u] = ld_stream(src[h] + v);
+          }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (tt[h] >= ntok) continue;
+          uint4* dst = reinterpret_cast<uint4*>(y + static_cast<size_t>(tt[h]) * g.M);
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = u * 32 + lane;
+            if (v >= nv) continue;
+            float f[VN], acc[VN];
+#pragma unroll
+            for (int q = 0; q < VN; ++q) acc[q] = 0.0f;
+            if (src[h]) {
+              Vec<T>::to_f32(buf[h][u], f);
+#pragma unroll
+              for (int q = 0; q < VN; ++q) acc[q] = fmaf(gv[h], f[q], acc[q]);
+            }
+            dst[v] = Vec<T>::from_f32(acc);
+          }
+        }
+      }
+      return;
+    }
+  }
   for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
        t += gridDim.x * kWarpsPerCta) {
     const int b = t / g.T;
@@ -448,6 +504,48 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   }
   const int lane = threadIdx.x % 32;
   const int ntok = g.blocks * g.T;
+  if constexpr (kVec) {
+    if (g.k == 1 && g.M / Vec<T>::N <= 32 * kUnroll) {
+      // top-1: two tokens per warp, all row loads in flight; dx = row, dropped -> 0
+      const int nv = g.M / Vec<T>::N;
+      const int S = gridDim.x * kWarpsPerCta;
+      for (int t0 = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t0 < ntok; t0 += 2 * S) {
+        const int tt[2] = {t0, t0 + S};
+        const uint4* src[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          src[h] = nullptr;
+          if (tt[h] < ntok) {
+            const int loc = locations[tt[h]];
+            if (loc >= 0) {
+              const int e = idxs[tt[h]];
+              MOE_CHECK(loc < g.cap && e >= 0 && e < g.E, "encode_bwd: location / expert out of range");
+              src[h] = reinterpret_cast<const uint4*>(dz + slot_row(g, tt[h] / g.T, e, loc) * g.M);
+            }
+          }
+        }
+        uint4 buf[2][kUnroll];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = u * 32 + lane;
+            if (src[h] && v < nv) buf[h][u] = ld_stream(src[h] + v);
+          }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (tt[h] >= ntok) continue;
+          uint4* dst = reinterpret_cast<uint4*>(dx + static_cast<size_t>(tt[h]) * g.M);
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int v = u * 32 + lane;
+            if (v < nv) dst[v] = src[h] ? buf[h][u] : make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+      }
+      return;
+    }
+  }
   for (int t = blockIdx.x * kWarpsPerCta + threadIdx.x / 32; t < ntok;
        t += gridDim.x * kWarpsPerCta) {
     const int b = t / g.T;
