@@ -708,13 +708,16 @@ __global__ void __launch_bounds__(256)
 
 // resolve_capacity (core.cpp:47-59) over the per-block max demand, fill counts and the BPR
 // member-list bases. One small CTA.
-// resolve_capacity body (one CTA): shared by the standalone kernel and the scan's last CTA.
+// resolve_capacity body (one CTA of 256 threads): shared by the standalone kernel and the scan's
+// last CTA. Every demand is loaded once, in parallel; member-list bases are a block-wide
+// exclusive scan over the experts of each source block.
 __device__ void finalize_capacity_cta(int blocks, int E, int T, int k, int cap_kind, int cap_formula,
                                       const int32_t* __restrict__ demand, int32_t* __restrict__ list_base,
                                       int32_t* __restrict__ fill, int32_t* __restrict__ cap_out,
                                       int32_t* __restrict__ drops) {
   __shared__ int32_t cap_sh;
   __shared__ int32_t mx_sh;
+  __shared__ int32_t wsum[8];
   if (threadIdx.x == 0) {
     *drops = 0;  // the assign pass accumulates this step's drops
     mx_sh = 1;   // max demand floors at 1
@@ -731,13 +734,30 @@ __device__ void finalize_capacity_cta(int blocks, int E, int T, int k, int cap_k
   }
   __syncthreads();
   const int cap = cap_sh;
-  for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
-    int run = b * T * k;
-    for (int e = 0; e < E; ++e) {
-      const int d = __ldcg(demand + b * E + e);
-      list_base[b * E + e] = run;
-      fill[b * E + e] = min(d, cap);
-      run += d;
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+  for (int b = 0; b < blocks; ++b) {
+    int run = b * T * k;  // running base across chunks of blockDim.x experts
+    for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+      const int e = e0 + threadIdx.x;
+      const int d = e < E ? __ldcg(demand + b * E + e) : 0;
+      int inc = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      int base = run;
+      for (int w = 0; w < warp; ++w) base += wsum[w];
+      if (e < E) {
+        list_base[b * E + e] = base + inc - d;
+        fill[b * E + e] = min(d, cap);
+      }
+      int tot = 0;
+      for (int w = 0; w < nw; ++w) tot += wsum[w];
+      run += tot;
+      __syncthreads();
     }
   }
 }
