@@ -401,6 +401,68 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   }
 }
 
+// ------------------------------------------------------------------ top-1 combine, slot-major
+// k = 1 (W > 1 after the combine, or unfused): walk the combined rows in slot order -- sequential
+// reads -- and store each kept slot's row at its token (y = g * row; encode-backward: dx = row).
+// Every token has at most one slot, so each output row is written exactly once: the same values
+// as the token-major gather, whose random 2 KiB reads it replaces by fire-and-forget row stores.
+// Dropped tokens' rows are zeroed by the same pass.
+template <typename T, bool kScale>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    slot_scatter_kernel(SlotGeom g, const T* __restrict__ src, const int32_t* __restrict__ slot_token,
+                        const float* __restrict__ slot_gate, T* __restrict__ out, FlagWait fw,
+                        DropZero dzero) {
+  pdl_entry();
+  if (fw.base != nullptr) {  // fused receive wait (the peers' combined rows)
+    if (threadIdx.x < 32) wait_flags_warp(fw);
+    __syncthreads();
+  }
+  zero_dropped_rows(dzero);
+  constexpr int VN = Vec<T>::N;
+  const int nv = g.M / VN;
+  const int lane = threadIdx.x % 32;
+  const size_t rows = static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc;
+  const size_t per_block = static_cast<size_t>(g.degree) * g.E * g.cc;
+  for (size_t row = static_cast<size_t>(blockIdx.x) * kWarpsPerCta + threadIdx.x / 32; row < rows;
+       row += static_cast<size_t>(gridDim.x) * kWarpsPerCta) {
+    const int b = static_cast<int>(row / per_block);
+    const int rem = static_cast<int>(row % per_block);
+    const int i = rem / (g.E * g.cc);
+    const int e = (rem / g.cc) % g.E;
+    const int c = i * g.cc + rem % g.cc;
+    if (c >= g.cap) continue;
+    const size_t sl = static_cast<size_t>(b * g.E + e) * g.cap + c;
+    const int t = slot_token[sl];
+    if (t < 0) continue;
+    MOE_CHECK(t >= b * g.T && t < (b + 1) * g.T, "slot scatter: slot token outside its block");
+    const float gv = kScale ? slot_gate[sl] : 1.0f;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + row * g.M);
+    uint4* d4 = reinterpret_cast<uint4*>(out + static_cast<size_t>(t) * g.M);
+    for (int v0 = 0; v0 < nv; v0 += 32 * kUnroll) {
+      uint4 buf[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nv) buf[u] = ld_stream(s4 + v);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v >= nv) continue;
+        if constexpr (kScale) {
+          float f[VN], acc[VN];
+          Vec<T>::to_f32(buf[u], f);
+#pragma unroll
+          for (int q = 0; q < VN; ++q) acc[q] = fmaf(gv, f[q], 0.0f);
+          d4[v] = Vec<T>::from_f32(acc);
+        } else {
+          d4[v] = buf[u];
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ decode backward
 // dZ[row] = g_slot * dy[t_slot] or 0 (slot-major; each kept slot has exactly one (t, j)).
 template <typename T, bool kVec>
@@ -826,6 +888,24 @@ int build_slots_device(int blocks, int T, int k, int E, int cap, const int32_t* 
   const int grid = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
   launch_k(build_slots_kernel, grid > 0 ? grid : 1, 256, 0, st, n, T, k, E, cap, idxs, locations, gates,
                                                          slot_token, slot_gate);
+  return launch_status();
+}
+
+int slot_scatter_device(const SlotGeom& g, int dtype, const void* src, const int32_t* slot_token,
+                        const float* slot_gate, void* out, const DropZero& dzero, cudaStream_t st,
+                        const FlagWait* wait) {
+  if (g.k != 1 || !vec_ok(dtype, g.M)) return -1;
+  const FlagWait fw = wait ? *wait : FlagWait{};
+  const int grid = grid_for(static_cast<size_t>(g.blocks) * g.degree * g.E * g.cc);
+  using B = __nv_bfloat16;
+  const bool scale = slot_gate != nullptr;
+  if (dtype == 1) {
+    if (scale) launch_k(slot_scatter_kernel<float, true>, grid, 256, 0, st, g, static_cast<const float*>(src), slot_token, slot_gate, static_cast<float*>(out), fw, dzero);
+    else launch_k(slot_scatter_kernel<float, false>, grid, 256, 0, st, g, static_cast<const float*>(src), slot_token, slot_gate, static_cast<float*>(out), fw, dzero);
+  } else {
+    if (scale) launch_k(slot_scatter_kernel<B, true>, grid, 256, 0, st, g, static_cast<const B*>(src), slot_token, slot_gate, static_cast<B*>(out), fw, dzero);
+    else launch_k(slot_scatter_kernel<B, false>, grid, 256, 0, st, g, static_cast<const B*>(src), slot_token, slot_gate, static_cast<B*>(out), fw, dzero);
+  }
   return launch_status();
 }
 

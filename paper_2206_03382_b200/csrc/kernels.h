@@ -146,6 +146,11 @@ int decode_backward_device(const SlotGeom& g, int dtype, const void* dy,
                            const int32_t* slot_token, const float* slot_gate, void* dz,
                            cudaStream_t st, const DropZero& dzero = DropZero{},
                            const LocalDest& local = LocalDest{});
+// k = 1 combine, slot-major (layer path): out[token of slot] = (slot_gate ? g : 1) * src[slot row]
+// for every kept slot of the [blocks][degree][E][cc] rows; dropped tokens' rows zeroed (dzero).
+int slot_scatter_device(const SlotGeom& g, int dtype, const void* src, const int32_t* slot_token,
+                        const float* slot_gate, void* out, const DropZero& dzero, cudaStream_t st,
+                        const FlagWait* wait = nullptr);
 // Optional d_gates[t, j] = <Z[e, loc], dy[t]> (dispatch.cpp:143-156); 0 for dropped.
 int decode_backward_gates_device(const SlotGeom& g, int dtype, const void* z, const void* dy,
                                  const int32_t* idxs, const int32_t* locations, double* dgates,

@@ -1465,9 +1465,22 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   if (!fused_) {
     prof_mark(kPhDecode, true, st);
-    ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st,
-                      combine_wait.base ? &combine_wait : nullptr),
-        "decode");
+    if (k_ == 1) {
+      // slot-major: sequential reads of the combined rows, one row store per kept token
+      DropZero dz;
+      dz.locations = gb.locations;
+      dz.T = T_;
+      dz.k = k_;
+      dz.out = y;
+      dz.row_bytes = static_cast<size_t>(M_) * esz_;
+      ckr(slot_scatter_device(g, cfg_.dtype, ycomb, gb.slot_token, gb.slot_gate, y, dz, st,
+                              combine_wait.base ? &combine_wait : nullptr),
+          "decode");
+    } else {
+      ckr(decode_device(g, cfg_.dtype, ycomb, gb.idxs, gb.locations, gb.gates, y, st,
+                        combine_wait.base ? &combine_wait : nullptr),
+          "decode");
+    }
     prof_mark(kPhDecode, false, st);
     ++launches_;
   }
@@ -1806,9 +1819,21 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   }
   if (!fused_) {
     prof_mark(kPhEncodeBwd, true, st);
-    ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st,
-                               combine_wait.base ? &combine_wait : nullptr),
-        "encode_bwd");
+    if (k_ == 1) {
+      DropZero dz;
+      dz.locations = gb.locations;
+      dz.T = T_;
+      dz.k = k_;
+      dz.out = dx;
+      dz.row_bytes = static_cast<size_t>(M_) * esz_;
+      ckr(slot_scatter_device(g, cfg_.dtype, dxcomb, gb.slot_token, nullptr, dx, dz, st,
+                              combine_wait.base ? &combine_wait : nullptr),
+          "encode_bwd");
+    } else {
+      ckr(encode_backward_device(g, cfg_.dtype, dxcomb, gb.idxs, gb.locations, dx, st,
+                                 combine_wait.base ? &combine_wait : nullptr),
+          "encode_bwd");
+    }
     prof_mark(kPhEncodeBwd, false, st);
     ++launches_;
   }
