@@ -1465,7 +1465,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   }
   if (!fused_) {
     prof_mark(kPhDecode, true, st);
-    if (k_ == 1) {
+    if (k_ == 1 && (static_cast<size_t>(M_) * esz_) % 16 == 0) {
       // slot-major: sequential reads of the combined rows, one row store per kept token
       DropZero dz;
       dz.locations = gb.locations;
@@ -1819,7 +1819,7 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
   }
   if (!fused_) {
     prof_mark(kPhEncodeBwd, true, st);
-    if (k_ == 1) {
+    if (k_ == 1 && (static_cast<size_t>(M_) * esz_) % 16 == 0) {
       DropZero dz;
       dz.locations = gb.locations;
       dz.T = T_;
