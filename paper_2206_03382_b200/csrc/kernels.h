@@ -192,12 +192,7 @@ int rownorm_device(const void* x, int M, float* rownorm, const RowSet& rs, cudaS
 int wait_flags_device(const FlagWait& w, cudaStream_t st);
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
-                      void* act, unsigned long long* relu_mask, cudaStream_t st,
-                      uint32_t* defer = nullptr);
-// Second half of a deferred fix-up (defer != null above): apply the values, bits and counters.
-int relu_fixup_apply_device(int seg_rows, int V, const unsigned long long* list, const unsigned int* count,
-                            unsigned int cap, const uint32_t* defer, void* act,
-                            unsigned long long* relu_mask, cudaStream_t st);
+                      void* act, unsigned long long* relu_mask, cudaStream_t st);
 
 // fp32 SIMT GEMM path (the 1e-5 fp32 layer): same kinds/addressing as the bf16 tcgen05 GEMM.
 struct GemmArgs;

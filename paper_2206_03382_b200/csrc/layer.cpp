@@ -349,18 +349,6 @@ void Layer::alloc_capacity(int cap) {
     if (W_ > 1) znorm_.alloc(sizeof(float) * rows_all);
     fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));
     fix_list_.alloc(sizeof(unsigned long long) * fix_cap_);
-    {
-      const char* e = std::getenv("MOE_DEFER_FIXUP");  // =0: the fix-up stays in line (A/B)
-      defer_fix_ = !(e && e[0] == '0') && fused_ && W_ == 1;
-    }
-    if (defer_fix_) {
-      fix_defer_.alloc(sizeof(uint32_t) * fix_cap_);
-      if (!fix_stream_) {
-        ck(cudaStreamCreateWithFlags(&fix_stream_, cudaStreamNonBlocking), "stream");
-        ck(cudaEventCreateWithFlags(&ev_up_done_, cudaEventDisableTiming), "event");
-        ck(cudaEventCreateWithFlags(&ev_fix_done_, cudaEventDisableTiming), "event");
-      }
-    }
   }
   if (W_ > 1) {
     recv_.alloc(rowsM);
@@ -463,12 +451,6 @@ void Layer::take_profile(double* ms, int64_t* counts, int n) {
 Layer::~Layer() {
   cudaSetDevice(device_);
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);
-  if (fix_stream_) {
-    cudaStreamSynchronize(fix_stream_);
-    cudaStreamDestroy(fix_stream_);
-    cudaEventDestroy(ev_up_done_);
-    cudaEventDestroy(ev_fix_done_);
-  }
   if (d2h_) cudaStreamSynchronize(d2h_);
   for (auto& p : pipe_)
     for (int i = 0; i < 2; ++i)
@@ -1139,7 +1121,6 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
   if (W_ > 1 && comm_ == nullptr) throw MoeError(MOE_ECOMM, "forward: communicator aborted after an earlier failure");
   check_comm("forward");
   simt_gemms_ = 0;
-  settle_fixup(st);  // a forward without a backward since the last one
   launches_ = 0;
   comm_bytes_ = 0.0;
   ck(cudaEventRecord(ev_fwd_start_, st), "event");
@@ -1290,24 +1271,7 @@ void Layer::forward(const void* x, void* y, cudaStream_t st) {
     prof_mark(kPhUp, true, st);
     gemm(kGemmUp, recv, w1_.p, act_.p, up, nseg, st);
     prof_mark(kPhUp, false, st);
-    if (cert && defer_fix_) {
-      // the re-decisions run beside the down GEMM; settle_fixup applies them before the backward
-      ck(cudaEventRecord(ev_up_done_, st), "event");
-      ck(cudaStreamWaitEvent(fix_stream_, ev_up_done_, 0), "wait");
-      prof_mark(kPhReluFix, true, fix_stream_);
-      ckr(relu_fixup_device(recv, w1t_.p, dE_, cc_, M_, V_,
-                            static_cast<const unsigned long long*>(fix_list_.p),
-                            static_cast<const unsigned int*>(fix_count_.p), fix_cap_, act_.p,
-                            static_cast<unsigned long long*>(relu_mask_.p), fix_stream_,
-                            static_cast<uint32_t*>(fix_defer_.p)),
-          "relu_fixup");
-      prof_mark(kPhReluFix, false, fix_stream_);
-      ck(cudaEventRecord(ev_fix_done_, fix_stream_), "event");
-      fixup_pending_ = true;
-      ++launches_;
-    } else {
-      fixup(recv);
-    }
+    fixup(recv);
     prof_mark(kPhDown, true, st);
     gemm(kGemmDown, act_.p, w2_.p, y, down, nseg, st);
     prof_mark(kPhDown, false, st);
@@ -1596,18 +1560,6 @@ void Layer::check_comm(const char* what) {
   }
 }
 
-void Layer::settle_fixup(cudaStream_t st) {
-  if (!fixup_pending_) return;
-  ck(cudaStreamWaitEvent(st, ev_fix_done_, 0), "wait");
-  ckr(relu_fixup_apply_device(cc_, V_, static_cast<const unsigned long long*>(fix_list_.p),
-                              static_cast<const unsigned int*>(fix_count_.p), fix_cap_,
-                              static_cast<const uint32_t*>(fix_defer_.p), act_.p,
-                              static_cast<unsigned long long*>(relu_mask_.p), st),
-      "relu_fixup apply");
-  ++launches_;
-  fixup_pending_ = false;
-}
-
 double Layer::allreduce_max_host(double v) {
   DevMem d;
   d.alloc(sizeof(double));
@@ -1638,7 +1590,6 @@ void Layer::backward(const void* dy, void* dx, float* dw1, float* dw2, cudaStrea
     dxzero.out = dx;
     dxzero.row_bytes = static_cast<size_t>(M_) * esz_;
   }
-  settle_fixup(st);  // the deferred ReLU re-decisions land in act / the mask first
   prof_mark(kPhDecodeBwd, true, st);
   LocalDest own;  // peer backend: this rank's experts' dZ rows go straight into drecv
   uint32_t fd_epoch = 0;

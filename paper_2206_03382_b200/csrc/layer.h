@@ -159,14 +159,6 @@ class Layer {
   cudaStream_t comm_stream_ = nullptr;
   ncclComm_t comm_ = nullptr;
   cudaEvent_t ev_fwd_start_{}, ev_fwd_end_{}, ev_sync_{}, ev_comm_done_{};
-  // deferred ReLU fix-up (W = 1 fused path): the fp64 re-decisions run on fix_stream_ beside the
-  // down GEMM (which reads the uncorrected act -- the forward output is continuous in h), and are
-  // applied to act / the ReLU bits before the backward (settle_fixup)
-  cudaStream_t fix_stream_ = nullptr;
-  cudaEvent_t ev_up_done_{}, ev_fix_done_{};
-  DevMem fix_defer_;
-  bool defer_fix_ = false, fixup_pending_ = false;
-  void settle_fixup(cudaStream_t st);
   cudaEvent_t ev_a_[8]{}, ev_b_[8]{}, ev_c_[8]{};
   cudaEvent_t ev_freed_[PeerExchange::kChannels]{};
   std::unique_ptr<PeerExchange> peer_;

@@ -215,12 +215,8 @@ __device__ __forceinline__ double fixup_dot(const __nv_bfloat16* xr, const __nv_
 __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows,
     int M, int V, const unsigned long long* __restrict__ list, const unsigned int* __restrict__ count,
-    unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask,
-    uint32_t* __restrict__ defer) {
+    unsigned int cap, __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
   pdl_entry();
-  // defer != null: the re-decided values go to defer[i] (bf16 bits | positive << 16) for
-  // relu_fixup_apply_kernel, and act / mask / the counters are left alone (the down GEMM may
-  // be reading act concurrently).
   // count[0]: entries listed by the up GEMM; count[1]: CTAs done; count[2]: the last list's size
   // (metrics); count[3]: the largest list since the host last read it (overflow check). The last CTA to finish resets [0] and [1], so the next chunk's up GEMM starts from
   // an empty list without a memset or reset kernel.
@@ -292,12 +288,6 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
     }
     if (lane < (two ? 2 : 1)) {
       const int j = lane;
-      if (defer) {
-        const __nv_bfloat16 v = __double2bfloat16(s[j] > 0.0 ? s[j] : 0.0);
-        defer[i + j * nw] = static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&v)) |
-                            (s[j] > 0.0 ? 0x10000u : 0u);
-        continue;
-      }
       act[r[j] * V + col[j]] = __double2bfloat16(s[j] > 0.0 ? s[j] : 0.0);
       if (relu_mask) {
         unsigned long long* w = relu_mask + r[j] * (V / 64) + col[j] / 64;
@@ -307,7 +297,6 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
       }
     }
   }
-  if (defer) return;  // relu_fixup_apply_kernel finishes the step (values, mask, counters)
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int* c = const_cast<unsigned int*>(count);
@@ -315,44 +304,6 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
     if (atomicAdd(c + 1, 1u) == gridDim.x - 1) {
       c[2] = c[0];
       c[3] = max(c[3], c[0]);  // sticky: the largest list since the last metrics read
-      c[0] = 0u;
-      c[1] = 0u;
-    }
-  }
-}
-
-// The deferred fix-up's second half, stream-ordered after the GEMM that read act: store the
-// re-decided values into act, set / clear the ReLU bits, and reset the list like the in-line
-// kernel's last CTA.
-__global__ void __launch_bounds__(256) relu_fixup_apply_kernel(
-    int seg_rows, int V, const unsigned long long* __restrict__ list,
-    const unsigned int* __restrict__ count, unsigned int cap, const uint32_t* __restrict__ defer,
-    __nv_bfloat16* __restrict__ act, unsigned long long* __restrict__ relu_mask) {
-  pdl_entry();
-  const unsigned int n = min(__ldcg(count), cap);
-  for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned long long e = list[i];
-    const uint32_t seg = static_cast<uint32_t>(e >> 44);
-    const uint32_t row = static_cast<uint32_t>((e >> 24) & 0xFFFFF);
-    const uint32_t col = static_cast<uint32_t>(e & 0xFFFFFF);
-    const size_t r = static_cast<size_t>(seg) * seg_rows + row;
-    MOE_CHECK(row < static_cast<uint32_t>(seg_rows) && col < static_cast<uint32_t>(V), "relu fixup apply: entry out of range");
-    const uint32_t d = defer[i];
-    reinterpret_cast<uint16_t*>(act)[r * V + col] = static_cast<uint16_t>(d & 0xFFFFu);
-    if (relu_mask) {
-      unsigned long long* w = relu_mask + r * (V / 64) + col / 64;
-      const unsigned long long bit = 1ull << (col % 64);
-      if (d & 0x10000u) atomicOr(w, bit);
-      else atomicAnd(w, ~bit);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int* c = const_cast<unsigned int*>(count);
-    __threadfence();
-    if (atomicAdd(c + 1, 1u) == gridDim.x - 1) {
-      c[2] = c[0];
-      c[3] = max(c[3], c[0]);
       c[0] = 0u;
       c[1] = 0u;
     }
@@ -420,23 +371,16 @@ int wait_flags_device(const FlagWait& w, cudaStream_t st) {
 
 int relu_fixup_device(const void* x, const void* w1t, int G, int seg_rows, int M, int V,
                       const unsigned long long* list, const unsigned int* count, unsigned int cap,
-                      void* act, unsigned long long* relu_mask, cudaStream_t st, uint32_t* defer) {
+                      void* act, unsigned long long* relu_mask, cudaStream_t st) {
   // one wave: the CTAs resident at once (2 per SM at this kernel's 128 registers) grid-stride
   // over the list, instead of 4 waves of mostly latency-bound CTAs
 #ifndef MOE_FIXUP_CTAS_PER_SM
 #define MOE_FIXUP_CTAS_PER_SM 2
 #endif
   launch_k(relu_fixup_kernel, 148 * MOE_FIXUP_CTAS_PER_SM, 256, 0, st, static_cast<const __nv_bfloat16*>(x),
-           static_cast<const __nv_bfloat16*>(w1t), G, seg_rows, M, V, list, count, cap,
-           static_cast<__nv_bfloat16*>(act), relu_mask, defer);
-  return launch_status();
-}
-
-int relu_fixup_apply_device(int seg_rows, int V, const unsigned long long* list, const unsigned int* count,
-                            unsigned int cap, const uint32_t* defer, void* act,
-                            unsigned long long* relu_mask, cudaStream_t st) {
-  launch_k(relu_fixup_apply_kernel, 148, 256, 0, st, seg_rows, V, list, count, cap, defer,
-           static_cast<__nv_bfloat16*>(act), relu_mask);
+                                             static_cast<const __nv_bfloat16*>(w1t), G, seg_rows,
+                                             M, V, list, count, cap,
+                                             static_cast<__nv_bfloat16*>(act), relu_mask);
   return launch_status();
 }
 
