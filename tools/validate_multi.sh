@@ -3,7 +3,7 @@
 # small-shape mp_parity, scenarios), bench lines (copy engines, NCCL), the capacity x degree sweep.
 cd $GRAFT_REPO_ROOT
 N=4
-O=gpurun_out/r2m4b
+O=gpurun_out/vmulti
 mkdir -p $O
 ./tools/probe/gtimer > $O/gtimer.txt 2>&1; cat $O/gtimer.txt
 timeout 2400 python -m pytest tests/test_gpu_multi.py -x -q -s > $O/pytest_multi.log 2>&1; echo "multi rc=$?"

@@ -1,7 +1,7 @@
 # Single-GPU round-end evidence: every workload's bench line (device-clock GEMM spans), the
 # reference arm, and the gate fix-up variant A/B.
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r2t
+O=gpurun_out/vsingle
 mkdir -p $O
 for w in TGT C1 C2 C3; do
   timeout 400 python bench.py --workload $w > $O/$w.json 2> $O/$w.err; echo "$w rc=$?"

@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 N=2
-O=gpurun_out/r2x3
+O=gpurun_out/vw2
 mkdir -p $O
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
 timeout 900 python -m pytest tests/test_gpu_layer.py tests/test_gpu_ops.py tests/test_gpu_gate_tc.py -m gpu -x -q > $O/pytest1.log 2>&1; echo "single rc=$?"; tail -1 $O/pytest1.log
