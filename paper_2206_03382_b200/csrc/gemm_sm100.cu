@@ -26,6 +26,7 @@
 #include "pdl.cuh"
 #include "peer_flags.cuh"
 #include "ptx.cuh"
+#include "relu_mask.cuh"
 
 #ifndef MOE_GEMM_STAGES
 #define MOE_GEMM_STAGES 4
@@ -376,14 +377,12 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
         }
       }
       unsigned long long mw[kSubs];
-#ifndef MOE_EXP_ACT_MASK
       if constexpr (kEpi == kEpiMaskBf16) {
         // issued before the accumulator wait so their latency hides under the MMAs
 #pragma unroll
         for (uint32_t c = 0; c < kSubs; ++c)
           mw[c] = row_ok ? __ldg(args.relu_mask + mrow + col0 / 64 + c) : 0ull;
       }
-#endif
       TRACE_WAIT(w_tfull, ptx::mbar_wait(&tfull_bar[acc], acc_phase));
       ptx::tc_fence_after();
 #pragma unroll 1
@@ -432,12 +431,15 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j) w[j] = ptx::pack_bf16x2(f[2 * j], f[2 * j + 1]);
           if constexpr (kEpi == kEpiReluBf16) {
+            // mn = min |bf16(h)| over the 64 columns (magnitude order == unsigned order of the 15
+            // low bits): the certificate prefilter, and mn > 0 (no zero) lets the mask come from
+            // the sign bits alone
+            bool signs = false;
 #ifndef MOE_EXP_NO_CERT  // timing experiments only (tools/gemm_exp.sh): drops the certificate
             if (cert) {
               // ReLU-mask certificate: |h| below the accumulation-error bound -> fp64
-              // re-decision. Prefilter: min |bf16(h)| over the 64 columns (magnitude order ==
-              // unsigned order of the 15 low bits) against the block bound widened by 2^-7 for
-              // the rounding; on a hit, the exact per-element test on the fp32 values.
+              // re-decision. Prefilter: mn against the block bound widened by 2^-7 for the
+              // rounding; on a hit, the exact per-element test on the fp32 values.
               float tmax = 0.0f;
 #pragma unroll
               for (uint32_t c2 = 0; c2 < kSubs; ++c2)
@@ -446,6 +448,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
 #pragma unroll
               for (uint32_t j = 1; j < 32; ++j) m2 = __vminu2(m2, w[j] & 0x7fff7fffu);
               const float mn = __uint_as_float(min(m2 & 0xffffu, m2 >> 16) << 16);
+              signs = mn > 0.0f;
               if (mn < tmax * (1.0f + 1.0f / 128.0f)) {
                 const float* ca = args.colnorm + static_cast<size_t>(tc.g) * args.N + cols;
                 for (uint32_t i = 0; i < 64; ++i) {
@@ -460,12 +463,23 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
             }
 #endif
 #ifndef MOE_EXP_NO_MASK  // timing experiments only: drops the ReLU bitmask
-            // [h > 0] bits from the fp32 values (exact zeros stay 0), relu on the pairs
+            // [h > 0] bits in the relu_mask.cuh order. No zero among the 64 values: [h > 0] is
+            // the inverted sign bit, gathered by one funnel shift per column; else compares.
             uint32_t lo = 0u, hi = 0u;
+            if (signs) {
 #pragma unroll
-            for (uint32_t i = 0; i < 32; ++i) {
-              lo |= static_cast<uint32_t>(f[i] > 0.0f) << i;
-              hi |= static_cast<uint32_t>(f[32 + i] > 0.0f) << i;
+              for (int b = 31; b >= 0; --b) {
+                lo = __funnelshift_l(v[relu_mask_col(b)], lo, 1);
+                hi = __funnelshift_l(v[32 + relu_mask_col(b)], hi, 1);
+              }
+              lo = ~lo;
+              hi = ~hi;
+            } else {
+#pragma unroll
+              for (uint32_t b = 0; b < 32; ++b) {
+                lo |= static_cast<uint32_t>(f[relu_mask_col(b)] > 0.0f) << b;
+                hi |= static_cast<uint32_t>(f[32 + relu_mask_col(b)] > 0.0f) << b;
+              }
             }
             if (args.relu_mask != nullptr && row_ok)
               args.relu_mask[mrow + cols / 64] = (static_cast<unsigned long long>(hi) << 32) | lo;
@@ -473,37 +487,17 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
 #pragma unroll
             for (uint32_t j = 0; j < 32; ++j) w[j] = __vmaxs2(w[j], 0u);  // int16 max == bf16 relu
           }
-#ifdef MOE_EXP_ACT_MASK
-          if constexpr (kEpi == kEpiMaskBf16) {
-            // experiment: [h > 0] == [act != 0] from the saved bf16 activation row segment
-            const uint4* ar = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(args.aux) +
-                                                             orow * args.N + cols);
-#pragma unroll
-            for (uint32_t q = 0; q < 8; ++q) {
-              const uint4 av = row_ok ? __ldg(ar + q) : make_uint4(0u, 0u, 0u, 0u);
-              const uint32_t a4[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-              for (uint32_t u = 0; u < 4; ++u) {
-                const uint32_t nz = (((a4[u] & 0x7fff7fffu) + 0x7fff7fffu) & 0x80008000u) >> 15;
-                w[4 * q + u] &= nz * 0xffffu;
-              }
-            }
-          }
-#else
           if constexpr (kEpi == kEpiMaskBf16) {
             // dh = (dY . W2^T) * [h > 0]; the up-GEMM's ReLU bitmask carries [h > 0]
             unsigned long long mk = 0ull;
 #pragma unroll
             for (uint32_t c2 = 0; c2 < kSubs; ++c2)
               if (c2 == c) mk = mw[c2];
-            const uint32_t mlo = static_cast<uint32_t>(mk), mhi = static_cast<uint32_t>(mk >> 32);
+            uint32_t pm[32];
+            relu_mask_pairs(mk, pm);
 #pragma unroll
-            for (uint32_t j = 0; j < 32; ++j) {
-              const uint32_t b2 = ((j < 16 ? mlo : mhi) >> (2 * (j % 16))) & 3u;
-              w[j] &= (b2 & 1u ? 0x0000ffffu : 0u) | (b2 & 2u ? 0xffff0000u : 0u);
-            }
+            for (uint32_t j = 0; j < 32; ++j) w[j] &= pm[j];
           }
-#endif
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
             ptx::st_shared_v4(stage_row + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1],

@@ -17,6 +17,7 @@
 #include "kernels.h"
 #include "pdl.cuh"
 #include "peer_flags.cuh"
+#include "relu_mask.cuh"
 
 namespace moe {
 
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
       act[r[j] * V + col[j]] = __double2bfloat16(s[j] > 0.0 ? s[j] : 0.0);
       if (relu_mask) {
         unsigned long long* w = relu_mask + r[j] * (V / 64) + col[j] / 64;
-        const unsigned long long bit = 1ull << (col[j] % 64);
+        const unsigned long long bit = 1ull << relu_mask_bit(col[j] % 64);
         if (s[j] > 0.0) atomicOr(w, bit);
         else atomicAnd(w, ~bit);
       }
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
   }
 }
 
-// mask[r][w] bit i = act[r][64 w + i] > 0 (one thread per 64-column word)
+// mask[r][w] bit relu_mask_bit(i) = act[r][64 w + i] > 0 (one thread per 64-column word)
 __global__ void mask_from_act_kernel(const __nv_bfloat16* __restrict__ act, int64_t rows, int V,
                                      unsigned long long* __restrict__ mask) {
   pdl_entry();
@@ -320,7 +321,8 @@ __global__ void mask_from_act_kernel(const __nv_bfloat16* __restrict__ act, int6
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const __nv_bfloat16* a = act + (i / nw) * V + (i % nw) * 64;
     unsigned long long b = 0ull;
-    for (int j = 0; j < 64; ++j) b |= static_cast<unsigned long long>(__bfloat162float(a[j]) > 0.0f) << j;
+    for (int j = 0; j < 64; ++j)
+      b |= static_cast<unsigned long long>(__bfloat162float(a[j]) > 0.0f) << relu_mask_bit(j);
     mask[i] = b;
   }
 }

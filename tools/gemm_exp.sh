@@ -2,7 +2,7 @@
 # TGT bench phase breakdown with each (MOE_LIB_PATH). Timing only: NO_MASK / NO_CERT variants
 # compute wrong gradients. Build here (CPU): bash tools/gemm_exp.sh build; on the box: ... run
 cd ${GRAFT_REPO_ROOT:-/root/repo}
-VARS=${GEXP_VARS:-"base: actmask:-DMOE_EXP_NO_MASK+-DMOE_EXP_ACT_MASK"}
+VARS=${GEXP_VARS:-"base: nomask:-DMOE_EXP_NO_MASK"}
 if [ "$1" = build ]; then
   for v in $VARS; do
     tag=${v%%:*}; flags=$(echo ${v#*:} | tr '+' ' ')
