@@ -15,4 +15,6 @@ TR2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr
 timeout 600 $TR2 --master-port 29584 bench.py --gpus 2 --no-cpu-baseline > $O/bench_n2.json 2> $O/bench_n2.err; echo "bench n2 rc=$?"
 timeout 600 $TR --master-port 29585 bench.py --gpus $N --impl reference > $O/ref_n4.json 2> $O/ref_n4.err; echo "ref n4 rc=$?"
 for f in bench bench_nccl bench_n2; do python -c "import json;d=json.loads(open('$O/$f.json').read().strip().splitlines()[-1]);print('$f', d['value'], d['ms_per_step'], d['clocks'], d.get('a2a',{}).get('dispatch_gbs'), d['e2e']['value'])"; done
-[ "$SWEEP" = 0 ] || timeout 1500 $TR --master-port 29583 tools/sweep.py --out $O/sweep_n4.json > $O/sweep.log 2>&1; echo "sweep rc=$?"; tail -5 $O/sweep.log
+if [ "$SWEEP" != 0 ]; then
+  timeout 1500 $TR --master-port 29583 tools/sweep.py --out $O/sweep_n4.json > $O/sweep.log 2>&1; echo "sweep rc=$?"; tail -5 $O/sweep.log
+fi
