@@ -133,7 +133,7 @@ unsigned long long* certified_up(int dtype, const void* x, const void* w1, void*
   }
   float* colnorm = sc.get<float>(static_cast<size_t>(n) * V);
   float* colnorm_blk = sc.get<float>(static_cast<size_t>(n) * (V / 64 + 1));
-  auto* mask = sc.get<unsigned long long>(static_cast<size_t>(n) * rows * (V / 64 + 1));
+  auto* mask = sc.get<unsigned long long>(moe::relu_mask_words(static_cast<size_t>(n) * rows, V / 64));
   void* w1t = sc.get<char>(static_cast<size_t>(n) * M * V * 2);
   float* rownorm = sc.get<float>(static_cast<size_t>(n) * rows);
   const unsigned int cap =
@@ -631,7 +631,7 @@ int moe_op_gemm(int32_t kind, int32_t dtype, int32_t use_tc, const void* A, cons
     if (kind == moe::kGemmDgradMask && dtype == MOE_DTYPE_BF16 && use_tc != 0 && tc_shape_ok(kind, a)) {
       if (!aux) throw moe::MoeError(MOE_EINVAL, "dgrad-mask needs the activation (aux)");
       const int64_t rows = nseg_total * seg_rows;
-      a.relu_mask = sc.get<unsigned long long>(static_cast<size_t>(rows) * (N / 64));
+      a.relu_mask = sc.get<unsigned long long>(moe::relu_mask_words(rows, N / 64));
       ckr(moe::relu_mask_from_act_device(aux, rows, static_cast<int>(N), a.relu_mask, S(stream)),
           "relu mask");
     }

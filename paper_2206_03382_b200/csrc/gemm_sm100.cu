@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
           kRowK || row_in < (args.nrows ? min(args.seg_rows, args.row0 + args.nrows) : args.seg_rows);
       const uint32_t col0 = tc.n0 + half * kEpiCols;
       const size_t orow = static_cast<size_t>(seg) * args.seg_rows + row_in;  // row-M kinds
-      const size_t mrow = orow * (args.N / 64);
+      const size_t mrow = relu_mask_word(orow, col0 / 64, args.N / 64);  // + 32 per 64 columns
       // token-indexed epilogue: the row's token (scatter) and gate scale
       int tok = -1;
       float scale = 1.0f;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
         // issued before the accumulator wait so their latency hides under the MMAs
 #pragma unroll
         for (uint32_t c = 0; c < kSubs; ++c)
-          mw[c] = row_ok ? __ldg(args.relu_mask + mrow + col0 / 64 + c) : 0ull;
+          mw[c] = row_ok ? __ldg(args.relu_mask + mrow + 32 * c) : 0ull;
       }
       TRACE_WAIT(w_tfull, ptx::mbar_wait(&tfull_bar[acc], acc_phase));
       ptx::tc_fence_after();
@@ -406,6 +406,15 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
               ptx::mbar_arrive(&tempty_bar[acc]);
           }
         }
+#ifdef MOE_EXP_DRAIN_ONLY  // timing experiments only: the up epilogue drains TMEM, nothing else
+        if constexpr (kEpi == kEpiReluBf16) {
+          uint32_t acc_or = 0u;
+#pragma unroll
+          for (uint32_t i = 0; i < kSub; ++i) acc_or |= v[i];
+          if (acc_or == 0x7fc00001u) args.fix_count[1] = acc_or;  // keeps the loads live
+          continue;
+        }
+#endif
         const uint32_t cols = col0 + c * kSub;
         uint8_t* stage = stage_base + ebuf * EPI_WARP_BYTES;
         const uint32_t stage_row = ptx::smem_u32(stage) + lane * 128;
@@ -444,19 +453,34 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
 #pragma unroll
               for (uint32_t c2 = 0; c2 < kSubs; ++c2)
                 if (c2 == c) tmax = tblk[c2];
-              uint32_t m2 = w[0] & 0x7fff7fffu;
+              // (a reduction tree: the epilogue is latency-bound, a 32-deep chain is not free)
+              uint32_t m16[16];
 #pragma unroll
-              for (uint32_t j = 1; j < 32; ++j) m2 = __vminu2(m2, w[j] & 0x7fff7fffu);
-              const float mn = __uint_as_float(min(m2 & 0xffffu, m2 >> 16) << 16);
+              for (uint32_t j = 0; j < 16; ++j)
+                m16[j] = __vminu2(w[2 * j] & 0x7fff7fffu, w[2 * j + 1] & 0x7fff7fffu);
+#pragma unroll
+              for (uint32_t h = 8; h > 0; h /= 2)
+#pragma unroll
+                for (uint32_t j = 0; j < h; ++j) m16[j] = __vminu2(m16[j], m16[j + h]);
+              const float mn = __uint_as_float(min(m16[0] & 0xffffu, m16[0] >> 16) << 16);
               signs = mn > 0.0f;
               if (mn < tmax * (1.0f + 1.0f / 128.0f)) {
+                // exact test of all 64 columns first (loads free to run ahead), then one
+                // atomic reservation for this row's entries
                 const float* ca = args.colnorm + static_cast<size_t>(tc.g) * args.N + cols;
-                for (uint32_t i = 0; i < 64; ++i) {
-                  if (fabsf(f[i]) < rmax * __ldg(ca + i)) {
-                    const unsigned int slot = atomicAdd(args.fix_count, 1u);
+                unsigned long long hits = 0ull;
+#pragma unroll
+                for (uint32_t i = 0; i < 64; ++i)
+                  hits |= static_cast<unsigned long long>(fabsf(f[i]) < rmax * __ldg(ca + i)) << i;
+                if (hits != 0ull) {
+                  unsigned int slot = atomicAdd(args.fix_count, static_cast<unsigned int>(__popcll(hits)));
+                  while (hits != 0ull) {
+                    const uint32_t i = static_cast<uint32_t>(__ffsll(static_cast<long long>(hits)) - 1);
+                    hits &= hits - 1;
                     MOE_CHECK(seg < (1u << 20) && row_in < (1u << 20) && cols + i < (1u << 24),
                               "up epilogue: certificate entry does not fit its packing");
                     if (slot < args.fix_cap) args.fix_list[slot] = fix_pack(seg, row_in, cols + i);
+                    ++slot;
                   }
                 }
               }
@@ -467,13 +491,17 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
             // the inverted sign bit, gathered by one funnel shift per column; else compares.
             uint32_t lo = 0u, hi = 0u;
             if (signs) {
+              // four independent 8-deep chains per half instead of one 32-deep chain
+              uint32_t g[8];
 #pragma unroll
-              for (int b = 31; b >= 0; --b) {
-                lo = __funnelshift_l(v[relu_mask_col(b)], lo, 1);
-                hi = __funnelshift_l(v[32 + relu_mask_col(b)], hi, 1);
+              for (uint32_t q = 0; q < 8; ++q) {
+                g[q] = 0u;  // bits 8 (q % 4) .. + 7 of half q / 4
+#pragma unroll
+                for (int b = 7; b >= 0; --b)
+                  g[q] = __funnelshift_l(v[32 * (q / 4) + relu_mask_col(8 * (q % 4) + b)], g[q], 1);
               }
-              lo = ~lo;
-              hi = ~hi;
+              lo = ~(g[0] | (g[1] << 8) | (g[2] << 16) | (g[3] << 24));
+              hi = ~(g[4] | (g[5] << 8) | (g[6] << 16) | (g[7] << 24));
             } else {
 #pragma unroll
               for (uint32_t b = 0; b < 32; ++b) {
@@ -482,7 +510,7 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
               }
             }
             if (args.relu_mask != nullptr && row_ok)
-              args.relu_mask[mrow + cols / 64] = (static_cast<unsigned long long>(hi) << 32) | lo;
+              args.relu_mask[mrow + 32 * c] = (static_cast<unsigned long long>(hi) << 32) | lo;
 #endif
 #pragma unroll
             for (uint32_t j = 0; j < 32; ++j) w[j] = __vmaxs2(w[j], 0u);  // int16 max == bf16 relu

@@ -83,6 +83,10 @@ __host__ __device__ inline unsigned long long fix_pack(uint32_t seg, uint32_t ro
 }
 constexpr float kReluTauScale = 1.0f / 262144.0f;  // 2^-18
 
+// 64-bit words of a ReLU mask over `rows` capacity rows with nblk 64-column blocks per row
+// (32-row interleaved layout, relu_mask.cuh)
+inline size_t relu_mask_words(size_t rows, size_t nblk) { return (rows + 31) / 32 * 32 * nblk; }
+
 int gemm_validate(const GemmArgs& a, int kind);
 
 int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArgs& args,

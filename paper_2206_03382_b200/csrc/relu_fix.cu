@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
       const int j = lane;
       act[r[j] * V + col[j]] = __double2bfloat16(s[j] > 0.0 ? s[j] : 0.0);
       if (relu_mask) {
-        unsigned long long* w = relu_mask + r[j] * (V / 64) + col[j] / 64;
+        unsigned long long* w = relu_mask + relu_mask_word(r[j], col[j] / 64, V / 64);
         const unsigned long long bit = 1ull << relu_mask_bit(col[j] % 64);
         if (s[j] > 0.0) atomicOr(w, bit);
         else atomicAnd(w, ~bit);
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
   }
 }
 
-// mask[r][w] bit relu_mask_bit(i) = act[r][64 w + i] > 0 (one thread per 64-column word)
+// word (r, w) bit relu_mask_bit(i) = act[r][64 w + i] > 0 (one thread per 64-column word)
 __global__ void mask_from_act_kernel(const __nv_bfloat16* __restrict__ act, int64_t rows, int V,
                                      unsigned long long* __restrict__ mask) {
   pdl_entry();
@@ -323,7 +323,7 @@ __global__ void mask_from_act_kernel(const __nv_bfloat16* __restrict__ act, int6
     unsigned long long b = 0ull;
     for (int j = 0; j < 64; ++j)
       b |= static_cast<unsigned long long>(__bfloat162float(a[j]) > 0.0f) << relu_mask_bit(j);
-    mask[i] = b;
+    mask[relu_mask_word(i / nw, static_cast<uint32_t>(i % nw), nw)] = b;
   }
 }
 

@@ -1,5 +1,9 @@
-// Bit layout of the ReLU mask [h > 0]: one 64-bit word per (capacity row, 64-column block),
+// Layout of the ReLU mask [h > 0]: one 64-bit word per (capacity row, 64-column block),
 // written by the up-GEMM epilogue, patched by the fp64 fix-up, read by the dgrad x mask epilogue.
+//
+// Words are interleaved by 32-row groups, [rows / 32][V / 64][32]: the epilogues map one row to
+// each lane, so a warp's 32 words of one column block are 256 contiguous bytes (one coalesced
+// store / load instead of 32 scattered sectors). Allocation: relu_mask_words(rows, V / 64).
 //
 // The order inside each 32-column half is chosen for the two epilogues' instruction counts, not
 // for readability: column pair p (columns 2p, 2p + 1 of the half) has its even column at bit
@@ -12,6 +16,11 @@
 #include <cstdint>
 
 namespace moe {
+
+// word of (global capacity row, 64-column block) with nblk blocks per row
+__host__ __device__ __forceinline__ size_t relu_mask_word(size_t row, uint32_t blk, uint32_t nblk) {
+  return ((row >> 5) * nblk + blk) * 32 + (row & 31);
+}
 
 // bit index (0..63) of column c (0..63) of a 64-column block
 __host__ __device__ constexpr uint32_t relu_mask_bit(uint32_t c) {

@@ -10,6 +10,17 @@ if [ "$1" = build ]; then
       python -m paper_2206_03382_b200.build > /dev/null || echo "build $tag failed"
     echo "built $tag ($flags)"
   done
+elif [ "$1" = ncu ]; then
+  # per-cycle view, each variant's GEMM launches of one step replayed alone
+  mkdir -p gpurun_out/gexp
+  for v in $VARS; do
+    tag=${v%%:*}
+    MOE_LIB_PATH=$PWD/paper_2206_03382_b200/var_$tag.so timeout 600 ncu --clock-control none -k regex:gemm_bf16 -s 60 -c 6 \
+      --metrics gpu__time_duration.sum,sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second,smsp__issue_active.avg.pct_of_peak_sustained_active \
+      --csv python bench.py --steps 12 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/gexp/ncu_$tag.csv 2>/dev/null
+    echo "ncu $tag rc=$?"
+    python tools/ncu_gemm_table.py gpurun_out/gexp/ncu_$tag.csv $tag
+  done
 else
   mkdir -p gpurun_out/gexp
   for rep in 1 2; do
