@@ -281,9 +281,19 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
+  } else if (warp == 1 && leader) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
+    // The whole warp walks the loop so descriptors stay warp-uniform (uniform datapath, no
+    // per-MMA register-to-uniform broadcast); one elected lane issues. The issue path shares its
+    // SM sub-partition with two epilogue warps, so its instruction count is on the critical path
+    // of the K = 1024 GEMMs.
     constexpr uint32_t idesc = ptx::make_idesc_bf16(C::TM, BN, kAMN, kBMN);
+    // descriptor of stage 0, k-step 0; stage s / k-step k add (s * bytes + k * step) >> 4
+    constexpr uint32_t kAStep = kAMN ? 2048 : 32, kBStep = kBMN ? 2048 : 32;
+    const uint64_t adesc0 = kAMN ? ptx::make_sw128_desc(ptx::smem_u32(smem + C::SMEM_A_OFF), BK * 128, 1024)
+                                 : ptx::make_sw128_desc(ptx::smem_u32(smem + C::SMEM_A_OFF), 16, 1024);
+    const uint64_t bdesc0 = kBMN ? ptx::make_sw128_desc(ptx::smem_u32(smem + C::SMEM_B_OFF), BK * 128, 1024)
+                                 : ptx::make_sw128_desc(ptx::smem_u32(smem + C::SMEM_B_OFF), 16, 1024);
     uint32_t stage = 0, phase = 0;
     uint32_t iter = 0;
     for (uint32_t tile = unit0; tile < ntiles; tile += unit_step, ++iter) {
@@ -295,27 +305,27 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
       for (uint32_t kb = 0; kb < nkb; ++kb) {
         TRACE_WAIT(w_full, ptx::mbar_wait(&full_bar[stage], phase));
         ptx::tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + C::SMEM_A_OFF + stage * C::A_BYTES);
-        const uint32_t sb = ptx::smem_u32(smem + C::SMEM_B_OFF + stage * C::B_BYTES);
+        const uint64_t ad = adesc0 + ((stage * C::A_BYTES) >> 4);
+        const uint64_t bd = bdesc0 + ((stage * C::B_BYTES) >> 4);
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (uint32_t k = 0; k < BK / UK; ++k) {
-          // K-major: advance 32 B inside the swizzle atom. MN-major: advance 16 K-rows (2 KiB).
-          const uint64_t adesc = kAMN ? ptx::make_sw128_desc(sa + k * 2048, BK * 128, 1024)
-                                      : ptx::make_sw128_desc(sa + k * 32, 16, 1024);
-          const uint64_t bdesc = kBMN ? ptx::make_sw128_desc(sb + k * 2048, BK * 128, 1024)
-                                      : ptx::make_sw128_desc(sb + k * 32, 16, 1024);
-          if constexpr (kCG == 2)
-            ptx::umma_bf16_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
-          else
-            ptx::umma_bf16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          for (uint32_t k = 0; k < BK / UK; ++k) {
+            const uint64_t adesc = ad + ((k * kAStep) >> 4);
+            const uint64_t bdesc = bd + ((k * kBStep) >> 4);
+            if constexpr (kCG == 2)
+              ptx::umma_bf16_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            else
+              ptx::umma_bf16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          if constexpr (kCG == 2) {
+            ptx::umma_commit_pair(&empty_bar[stage]);
+            if (kb == nkb - 1) ptx::umma_commit_pair(&tfull_bar[acc]);
+          } else {
+            ptx::umma_commit(&empty_bar[stage]);
+            if (kb == nkb - 1) ptx::umma_commit(&tfull_bar[acc]);
+          }
         }
-        if constexpr (kCG == 2) {
-          ptx::umma_commit_pair(&empty_bar[stage]);
-          if (kb == nkb - 1) ptx::umma_commit_pair(&tfull_bar[acc]);
-        } else {
-          ptx::umma_commit(&empty_bar[stage]);
-          if (kb == nkb - 1) ptx::umma_commit(&tfull_bar[acc]);
-        }
+        __syncwarp();
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
