@@ -219,8 +219,10 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
   const long long t_start = clock64();
 #endif
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
+    // Like the MMA issuer: the whole warp walks the loop (warp-uniform coordinates), one elected
+    // lane issues the loads and the barrier arrival.
     uint32_t stage = 0, phase = 0;
     const uint32_t kb_per_seg = (args.seg_rows + BK - 1) / BK;
     auto load = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2) {
@@ -230,7 +232,9 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
         ptx::tma_load_3d(m, bar, dst, c0, c1, c2);
     };
     // the (A, B) boxes of k-block kb of a tile into one smem stage
-    auto issue = [&](const TileCoord& tc, uint32_t kb, uint8_t* sa, uint8_t* sb, uint64_t* bar) {
+    // row-K: k-block kb is block kr of segment ks (kept as counters, no division)
+    auto issue = [&](const TileCoord& tc, uint32_t kb, uint32_t ks, uint32_t kr, uint8_t* sa,
+                     uint8_t* sb, uint64_t* bar) {
       const uint32_t m0 = tc.m0 + rank * BM;       // this CTA's A rows
       const uint32_t nb = tc.n0 + rank * C::BNL;   // this CTA's B columns
       auto go = [&](const CUtensorMap* m, void* dst, int c0, int c1, int c2) {
@@ -251,9 +255,8 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
             go(&tmB, sb + a * (BK * 128), static_cast<int>(nb + a * 64), k0, static_cast<int>(tc.g));
         }
       } else {
-        const uint32_t s = kb / kb_per_seg;
-        const int r0 = static_cast<int>((kb % kb_per_seg) * BK);
-        const int seg = static_cast<int>((args.seg_base + s) * args.G + tc.g);
+        const int r0 = static_cast<int>(kr * BK);
+        const int seg = static_cast<int>((args.seg_base + ks) * args.G + tc.g);
         // A^T: rows are K, MN-major [seg][seg_rows][Mo]
 #pragma unroll
         for (uint32_t a = 0; a < BM / 64; ++a)
@@ -266,15 +269,23 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
     };
     for (uint32_t tile = unit0; tile < ntiles; tile += unit_step) {
       const TileCoord tc = tile_coord<kRowK, C::TM>(args, tile);
+      uint32_t ks = 0, kr = 0;
       for (uint32_t kb = 0; kb < nkb; ++kb) {
         ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + C::SMEM_A_OFF + stage * C::A_BYTES;
         uint8_t* sb = smem + C::SMEM_B_OFF + stage * C::B_BYTES;
-        issue(tc, kb, sa, sb, &full_bar[stage]);
-        if (leader)
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], (C::A_BYTES + C::B_BYTES) * kCG);
-        else
-          ptx::mbar_arrive_cluster(&full_bar[stage], 0);
+        if (ptx::elect_one()) {
+          issue(tc, kb, ks, kr, sa, sb, &full_bar[stage]);
+          if (leader)
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], (C::A_BYTES + C::B_BYTES) * kCG);
+          else
+            ptx::mbar_arrive_cluster(&full_bar[stage], 0);
+        }
+        __syncwarp();
+        if (++kr == kb_per_seg) {
+          kr = 0;
+          ++ks;
+        }
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
