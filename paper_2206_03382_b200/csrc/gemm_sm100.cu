@@ -37,6 +37,9 @@
 #ifndef MOE_GEMM_EPI_BUFS
 #define MOE_GEMM_EPI_BUFS 1
 #endif
+#ifndef MOE_GEMM_EPI_BUFS4  // staging buffers per warp with 4 epilogue warps (fits 6 stages at 2)
+#define MOE_GEMM_EPI_BUFS4 MOE_GEMM_EPI_BUFS
+#endif
 
 // MOE_GEMM_TRACE (debug builds only): per-role barrier wait cycles, printed by CTAs 0 and 1.
 #ifdef MOE_GEMM_TRACE
@@ -82,7 +85,8 @@ struct EpiCfg {
 template <int kCG, bool kPeer = false, int kEW = 8>
 struct Cfg : EpiCfg<kEW> {
   using EpiCfg<kEW>::kEpiWarps;
-  static constexpr uint32_t kEpiBufs = kPeer ? 2 : MOE_GEMM_EPI_BUFS;  // staging buffers per warp
+  static constexpr uint32_t kEpiBufs =  // staging buffers per warp
+      kPeer ? 2 : (kEW == 4 ? MOE_GEMM_EPI_BUFS4 : MOE_GEMM_EPI_BUFS);
   // peer stores double the staging: with 8 epilogue warps that costs one pipeline stage
   static constexpr uint32_t kStages =
       (kCG == 1 ? MOE_GEMM_STAGES : MOE_GEMM_STAGES_PAIR) -
@@ -701,10 +705,15 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, con
 #ifndef MOE_UP_EPI_WARPS
 #define MOE_UP_EPI_WARPS 8
 #endif
+#ifndef MOE_WGRAD_EPI_WARPS
+#define MOE_WGRAD_EPI_WARPS 4
+#endif
 #ifndef MOE_EPI_WARPS
 #define MOE_EPI_WARPS 4
 #endif
-  constexpr int kEW = kEpi == kEpiReluBf16 ? MOE_UP_EPI_WARPS : MOE_EPI_WARPS;  // see EpiCfg
+  constexpr int kEW = kEpi == kEpiReluBf16 ? MOE_UP_EPI_WARPS
+                      : kEpi == kEpiF32    ? MOE_WGRAD_EPI_WARPS
+                                           : MOE_EPI_WARPS;  // see EpiCfg
   if (gemm_cta_group() == 2)
     return launch_cg<kAMN, kBMN, kEpi, kRowK, 2, kIdx, kEW>(a, b, d, args, p, num_sms, stream);
   return launch_cg<kAMN, kBMN, kEpi, kRowK, 1, kIdx, kEW>(a, b, d, args, p, num_sms, stream);
