@@ -535,20 +535,27 @@ def run_gpu(args):
             L.forward_host_async(state, xh, yh)
             L.backward_host_async(state, dyh, dxh)
         L.host_sync(state)
-        barrier()
-        t0 = time.perf_counter()
+        # three timed windows, the median reported (a single window is exposed to one-off host
+        # hiccups: page-cache / scheduler noise on the box's shared host cores)
         n_e2e = max(3, args.steps // 2)
-        for _ in range(n_e2e):
-            L.forward_host_async(state, xh, yh)
-            L.backward_host_async(state, dyh, dxh)
-        L.host_sync(state)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        windows = []
+        for _ in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                L.forward_host_async(state, xh, yh)
+                L.backward_host_async(state, dyh, dxh)
+            L.host_sync(state)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t.item())
+            windows.append(el)
+        el = sorted(windows)[1]
         e2e = {"value": world * T * n_e2e / el, "unit": "tokens/s",
+               "windows_tokens_per_s": [round(world * T * n_e2e / w) for w in windows],
                "h2d_bytes_per_step": 2 * T * M * esz, "d2h_bytes_per_step": 2 * T * M * esz,
                "steps": n_e2e,
                "api": "moe_forward_host_async + moe_backward_host_async + moe_host_sync (C ABI, "
