@@ -387,7 +387,7 @@ def run_gpu(args):
     # Alg. 1 explores its strategy space (2 forward steps per strategy: the first, cold one is not
     # recorded) before exploiting; let that finish
     # in the untimed warm-up so the timed steps run the chosen pipelining degree.
-    for _ in range(args.warmup + (12 if adaptive else 0)):
+    for _ in range(args.warmup + (20 if adaptive else 0)):  # Alg. 1: 4 candidates x (1 + 3) forwards
         step()
     barrier()
     state.take_profile()  # drop warm-up records

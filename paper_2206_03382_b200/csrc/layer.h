@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
+#include <map>
 #include <set>
 #include <string>
 #include <vector>
@@ -149,7 +150,8 @@ class Layer {
   double f_ = 1.0;
   Strategy strategy_;
   StrategySearch search_;
-  std::set<std::pair<double, int>> warm_;  // (f, strategy) pairs executed once (not recorded)
+  // (f, strategy) -> executions so far and the fastest timed one (the first is not timed)
+  std::map<std::pair<double, int>, std::pair<int, double>> trials_;
   bool fwd_done_ = false, metrics_valid_ = false;
   int64_t launches_ = 0, bwd_launches_ = 0;
   double comm_bytes_ = 0.0;

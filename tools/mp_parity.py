@@ -37,7 +37,7 @@ def run(rank, W, dev, E_per, k, f, M, V, T, bpr, dt, degree, adaptive, backend, 
     tdt = cfg.torch_dtype
     xs = torch.as_tensor(inp["x"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
     dys = torch.as_tensor(inp["dy"][rank * T:(rank + 1) * T]).to(tdt).to(dev)
-    steps = 10 if adaptive else 2
+    steps = 18 if adaptive else 2
     for it in range(steps):
         res = forward(st, xs)
         if it == 0 and not adaptive:

@@ -111,7 +111,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         st = LayerState.init(cfg, SEED, rank=rank, device=local, nccl_id=obj[0])
         os.environ.pop("MOE_DISPATCH", None)
-        steps = 12 if adaptive else 2
+        steps = 20 if adaptive else 2
         for _ in range(steps):
             res = forward(st, x)
             g = backward(st, res.saved, dy)
