@@ -855,13 +855,35 @@ void Layer::exchange_2dh(const char* send, char* recv, size_t B, ncclDataType_t 
 // Copy-engine version of exchange(): push chunk `chunk` of `src` into every peer's channel
 // buffer (same plan), then publish the chunk's ready flag.
 // Row parts of the first chunk (pipelined in pieces so its first rows land while the own
-// segment is computed): 1/4, 1/4, 1/2 when the quarters are whole 256-row tiles, else halves,
-// else one part. Parts except the last publish kPartSlot0 + i, the last the chunk's slot 0.
+// segment is computed): the chunk's 256-row tiles in three near-equal parts, larger first
+// (MOE_PARTS: an explicit comma list of tile counts). With the peers' transfer about as long as
+// their GEMM (C4 at N = 4), equal parts let every part's GEMM start as its rows land; the
+// earlier 1/4, 1/4, 1/2 split left the last half's transfer exposed. Parts except the last
+// publish kPartSlot0 + i, the last the chunk's slot 0.
 static std::vector<uint32_t> first_chunk_parts(int64_t cc, bool enable) {
-  if (enable && cc % 1024 == 0) return {static_cast<uint32_t>(cc / 4), static_cast<uint32_t>(cc / 4),
-                                        static_cast<uint32_t>(cc / 2)};
-  if (enable && cc % 512 == 0) return {static_cast<uint32_t>(cc / 2), static_cast<uint32_t>(cc / 2)};
-  return {static_cast<uint32_t>(cc)};
+  if (!enable || cc % 256 != 0 || cc < 512) return {static_cast<uint32_t>(cc)};
+  const int64_t tiles = cc / 256;
+  std::vector<uint32_t> parts;
+  if (const char* e = std::getenv("MOE_PARTS")) {
+    int64_t sum = 0;
+    for (const char* q = e; *q;) {
+      const long v = std::strtol(q, const_cast<char**>(&q), 10);
+      if (v > 0) {
+        parts.push_back(static_cast<uint32_t>(v * 256));
+        sum += v;
+      }
+      while (*q == ',' || *q == ' ') ++q;
+      if (v <= 0 && *q && (*q < '0' || *q > '9')) ++q;
+    }
+    if (sum == tiles && !parts.empty() &&
+        parts.size() <= static_cast<size_t>(PeerExchange::kPartSlots) + 1)
+      return parts;
+    parts.clear();  // malformed or not covering the chunk: the default
+  }
+  const int64_t k = std::min<int64_t>(3, tiles);
+  for (int64_t i = 0; i < k; ++i)
+    parts.push_back(static_cast<uint32_t>((tiles / k + (i < tiles % k ? 1 : 0)) * 256));
+  return parts;
 }
 
 // Rows [row0, row0 + nrows) of every segment of chunk `chunk` to every peer (slot: ready flag).

@@ -32,7 +32,7 @@ class PeerExchange {
   static constexpr int kMaxChunks = 8;
   // ready-flag slots per (channel, source): one per chunk + kPartSlots for the leading row
   // parts of chunk 0 (its last part publishes the chunk's own slot 0)
-  static constexpr int kPartSlots = 2;
+  static constexpr int kPartSlots = 7;  // up to 8 row parts
   static constexpr int kPartSlot0 = kMaxChunks;
   static constexpr int kFlagSlots = kMaxChunks + kPartSlots;
   // optional profiling hook: called on the copy stream at the start (begin) and end of each
