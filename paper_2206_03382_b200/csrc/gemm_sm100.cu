@@ -37,6 +37,9 @@
 #ifndef MOE_GEMM_EPI_BUFS
 #define MOE_GEMM_EPI_BUFS 1
 #endif
+#ifndef MOE_TMA_4D  // MN-major operands loaded as one 4-D box per stage instead of one per atom
+#define MOE_TMA_4D 1
+#endif
 #ifndef MOE_GEMM_EPI_BUFS4  // staging buffers per warp with 4 epilogue warps (fits 6 stages at 2)
 #define MOE_GEMM_EPI_BUFS4 MOE_GEMM_EPI_BUFS
 #endif
@@ -235,6 +238,15 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
       else
         ptx::tma_load_3d(m, bar, dst, c0, c1, c2);
     };
+#if MOE_TMA_4D
+    // MN-major operand: all 64-column atoms of the box in one 4-D load ([seg][atom][row][64])
+    auto load4 = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int row, int atom, int seg) {
+      if constexpr (kCG == 2)
+        ptx::tma_load_4d_pair(m, bar, dst, 0, row, atom, seg);
+      else
+        ptx::tma_load_4d(m, bar, dst, 0, row, atom, seg);
+    };
+#endif
     // the (A, B) boxes of k-block kb of a tile into one smem stage
     // row-K: k-block kb is block kr of segment ks (kept as counters, no division)
     auto issue = [&](const TileCoord& tc, uint32_t kb, uint32_t ks, uint32_t kr, uint8_t* sa,
@@ -254,21 +266,29 @@ __global__ void __launch_bounds__(EpiCfg<kEW>::kThreads, 1)
           go(&tmB, sb, k0, static_cast<int>(nb), static_cast<int>(tc.g));
         } else {
           // B: N-major [G][K][N], 64-column atoms
+#if MOE_TMA_4D
+          load4(&tmB, bar, sb, k0, static_cast<int>(nb / 64), static_cast<int>(tc.g));
+#else
 #pragma unroll
           for (uint32_t a = 0; a < C::BNL / 64; ++a)
             go(&tmB, sb + a * (BK * 128), static_cast<int>(nb + a * 64), k0, static_cast<int>(tc.g));
+#endif
         }
       } else {
         const int r0 = static_cast<int>(kr * BK);
         const int seg = static_cast<int>((args.seg_base + ks) * args.G + tc.g);
-        // A^T: rows are K, MN-major [seg][seg_rows][Mo]
+        // A^T: rows are K, MN-major [seg][seg_rows][Mo]; B: N-major [seg][seg_rows][N]
+#if MOE_TMA_4D
+        load4(&tmA, bar, sa, r0, static_cast<int>(m0 / 64), seg);
+        load4(&tmB, bar, sb, r0, static_cast<int>(nb / 64), seg);
+#else
 #pragma unroll
         for (uint32_t a = 0; a < BM / 64; ++a)
           go(&tmA, sa + a * (BK * 128), static_cast<int>(m0 + a * 64), r0, seg);
-        // B: N-major [seg][seg_rows][N]
 #pragma unroll
         for (uint32_t a = 0; a < C::BNL / 64; ++a)
           go(&tmB, sb + a * (BK * 128), static_cast<int>(nb + a * 64), r0, seg);
+#endif
       }
     };
     for (uint32_t tile = unit0; tile < ntiles; tile += unit_step) {
@@ -645,6 +665,23 @@ int make_map_3d(CUtensorMap* m, const void* base, bool f32, uint64_t d0, uint64_
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// 4-D view [d2][d0 / 64][d1][64] of a 3-D bf16 [d2][d1][d0] tensor: box {64, b1, atoms, 1}
+// lands `atoms` 64-column swizzle atoms of b1 rows back to back (one TMA op per MN-major stage).
+int make_map_mn4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b1,
+                 uint32_t atoms) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  if (d0 % 64 != 0) return -3;
+  cuuint64_t dims[4] = {64, d1, d0 / 64, d2};
+  cuuint64_t strides[3] = {d0 * 2, 128, d0 * d1 * 2};
+  cuuint32_t box[4] = {64, b1, atoms, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 // 2-D [rows][cols] bf16 map with a one-row box: the row-scatter (tile::scatter4) target.
 int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows) {
   auto fn = encode_fn();
@@ -776,7 +813,11 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
     case kGemmUp:      // act = relu(X . W1)      A K-major, W1 [G][K=M][N=V] N-major
     case kGemmDown: {  // Y   = act . W2          A K-major, W2 [G][K=V][N=M] N-major
       rc |= make_map_3d(&ma, A, false, args.K, args.seg_rows, nseg, 64, BM);
+#if MOE_TMA_4D
+      rc |= make_map_mn4(&mb, B, args.N, args.K, args.G, 64, BN / gemm_cta_group() / 64);
+#else
       rc |= make_map_3d(&mb, B, false, args.N, args.K, args.G, 64, 64);
+#endif
       rc |= map_d(&md);
       if (rc) return -2;
       if (kind == kGemmUp)
@@ -808,8 +849,13 @@ int gemm_fwd(GemmKind kind, const void* A, const void* B, void* D, const GemmArg
     }
     case kGemmWgrad: {  // dW[g] = A[g]^T . B[g] over all (segment, row); fp32 out [G][Mo][N]
       if (im != 0) return -1;
+#if MOE_TMA_4D
+      rc |= make_map_mn4(&ma, A, args.Mo, args.seg_rows, nseg, 64, BM / 64);
+      rc |= make_map_mn4(&mb, B, args.N, args.seg_rows, nseg, 64, BN / gemm_cta_group() / 64);
+#else
       rc |= make_map_3d(&ma, A, false, args.Mo, args.seg_rows, nseg, 64, 64);
       rc |= make_map_3d(&mb, B, false, args.N, args.seg_rows, nseg, 64, 64);
+#endif
       rc |= make_map_3d(&md, D, true, args.N, args.Mo, args.G, 32, 32);
       if (rc) return -2;
       return launch<true, true, kEpiF32, true>(ma, mb, md, args, num_sms, stream);
