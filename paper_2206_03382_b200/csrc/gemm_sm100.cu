@@ -74,9 +74,10 @@ constexpr uint32_t EPI_WARP_BYTES = 32 * 128;    // 32 rows x 128 B staging per 
 // kPeer: the fused-combine kernels store over NVLink, where a bulk store holds its staging
 // buffer longer -- two staging buffers per epilogue warp.
 // Epilogue warps per CTA: 4 (one per TMEM lane quadrant, draining all 256 columns) or 8 (two
-// column halves). Measured at TGT: the up GEMM's certificate epilogue needs 8 to keep pace with
-// its K = 1024 mainloop; every other kind is faster with 4 (wgrad -8 %: fewer warps contending
-// with the MMA / TMA issuers).
+// column halves). Measured at TGT before the issuers ran on whole warps: the up GEMM's
+// certificate epilogue needed 8 to keep pace with its K = 1024 mainloop; every other kind is
+// faster with 4 (wgrad -8 %: fewer warps contending with the MMA / TMA issuers). Since then the
+// up GEMM measures the same with 4 or 8 (179 / 180 us isolated); it stays at 8.
 template <int kGemmEpiWarps>
 struct EpiCfg {
   static constexpr uint32_t kEpiWarps = kGemmEpiWarps;
