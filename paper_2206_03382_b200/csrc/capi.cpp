@@ -133,7 +133,7 @@ unsigned long long* certified_up(int dtype, const void* x, const void* w1, void*
   }
   float* colnorm = sc.get<float>(static_cast<size_t>(n) * V);
   float* colnorm_blk = sc.get<float>(static_cast<size_t>(n) * (V / 64 + 1));
-  auto* mask = sc.get<unsigned long long>(moe::relu_mask_words(static_cast<size_t>(n) * rows, V / 64));
+  auto* mask = sc.get<unsigned long long>(moe::relu_mask_words(static_cast<size_t>(n) * rows, (V + 63) / 64));
   void* w1t = sc.get<char>(static_cast<size_t>(n) * M * V * 2);
   float* rownorm = sc.get<float>(static_cast<size_t>(n) * rows);
   const unsigned int cap =

@@ -83,8 +83,9 @@ __host__ __device__ inline unsigned long long fix_pack(uint32_t seg, uint32_t ro
 }
 constexpr float kReluTauScale = 1.0f / 262144.0f;  // 2^-18
 
-// 64-bit words of a ReLU mask over `rows` capacity rows with nblk 64-column blocks per row
-// (32-row interleaved layout, relu_mask.cuh)
+// 64-bit words of a ReLU mask over `rows` capacity rows with nblk = ceil(V / 64) column blocks
+// per row (32-row interleaved layout, relu_mask.cuh; the fix-up indexes with the same nblk, so a
+// partial last block -- SIMT shapes, whose dgrad reads the activation instead -- stays in bounds)
 inline size_t relu_mask_words(size_t rows, size_t nblk) { return (rows + 31) / 32 * 32 * nblk; }
 
 int gemm_validate(const GemmArgs& a, int kind);

@@ -345,7 +345,7 @@ void Layer::alloc_capacity(int cap) {
     dxe_.alloc(rowsM);
   }
   if (cfg_.dtype == MOE_DTYPE_BF16) {
-    relu_mask_.alloc(sizeof(unsigned long long) * relu_mask_words(rows_all, V_ / 64));
+    relu_mask_.alloc(sizeof(unsigned long long) * relu_mask_words(rows_all, (V_ + 63) / 64));
     rownorm_.alloc(sizeof(float) * rows_all);
     if (W_ > 1) znorm_.alloc(sizeof(float) * rows_all);
     fix_cap_ = static_cast<unsigned int>(std::max<size_t>(1 << 16, rows_all * V_ / 256));

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
       const int j = lane;
       act[r[j] * V + col[j]] = __double2bfloat16(s[j] > 0.0 ? s[j] : 0.0);
       if (relu_mask) {
-        unsigned long long* w = relu_mask + relu_mask_word(r[j], col[j] / 64, V / 64);
+        unsigned long long* w = relu_mask + relu_mask_word(r[j], col[j] / 64, (V + 63) / 64);
         const unsigned long long bit = 1ull << relu_mask_bit(col[j] % 64);
         if (s[j] > 0.0) atomicOr(w, bit);
         else atomicAnd(w, ~bit);
