@@ -213,6 +213,10 @@ __device__ __forceinline__ double fixup_dot(const __nv_bfloat16* xr, const __nv_
   return s;
 }
 
+#ifndef MOE_FIXUP_F32_PRODUCTS
+#define MOE_FIXUP_F32_PRODUCTS 1
+#endif
+
 __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w1t, int G, int seg_rows,
     int M, int V, const unsigned long long* __restrict__ list, const unsigned int* __restrict__ count,
@@ -271,8 +275,16 @@ __global__ void __launch_bounds__(256, 2) relu_fixup_kernel(
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float2 af = __bfloat1622float2(ah[q]), wf = __bfloat1622float2(wh[q]);
+#if MOE_FIXUP_F32_PRODUCTS
+                // bf16 x bf16 products are exact in fp32 (8 + 8 significand bits; down to
+                // |product| ~ 2^-134, where a whole 1024-term row stays below 1e-37): one fp64
+                // conversion per term instead of two, the sum still in fp64 (ncu: 17.8 -> 15.7 us)
+                acc[j] += static_cast<double>(__fmul_rn(af.x, wf.x));
+                acc[j] += static_cast<double>(__fmul_rn(af.y, wf.y));
+#else
                 acc[j] = fma(static_cast<double>(af.x), static_cast<double>(wf.x), acc[j]);
                 acc[j] = fma(static_cast<double>(af.y), static_cast<double>(wf.y), acc[j]);
+#endif
               }
             }
       }
