@@ -867,13 +867,19 @@ static std::vector<uint32_t> first_chunk_parts(int64_t cc, bool enable) {
   if (const char* e = std::getenv("MOE_PARTS")) {
     int64_t sum = 0;
     for (const char* q = e; *q;) {
-      const long v = std::strtol(q, const_cast<char**>(&q), 10);
-      if (v > 0) {
-        parts.push_back(static_cast<uint32_t>(v * 256));
-        sum += v;
+      char* end = nullptr;
+      const long v = std::strtol(q, &end, 10);
+      if (end == q) {  // not a number: skip one separator character
+        ++q;
+        continue;
       }
-      while (*q == ',' || *q == ' ') ++q;
-      if (v <= 0 && *q && (*q < '0' || *q > '9')) ++q;
+      q = end;
+      if (v <= 0) {  // a zero or negative part: malformed
+        sum = -1;
+        break;
+      }
+      parts.push_back(static_cast<uint32_t>(v * 256));
+      sum += v;
     }
     if (sum == tiles && !parts.empty() &&
         parts.size() <= static_cast<size_t>(PeerExchange::kPartSlots) + 1)
