@@ -10,6 +10,14 @@ run() {  # tag, env, args
   env $2 timeout 600 $TR --master-port $((29600+i)) bench.py --gpus $N --no-cpu-baseline --no-e2e $3 > $O/$1.json 2> $O/$1.err
   python -c "import json;d=json.loads(open('$O/$1.json').read().strip().splitlines()[-1]);p=d['phases_ms'];print('$1', round(d['value']/1e6,2), round(d['ms_per_step'],3), d['config'].get('degree'), p['gemm_up'], p['gemm_dgrad_mask'], p['encode'], p['decode_bwd'], (d.get('a2a') or {}).get('dispatch_gbs'), d['clocks']['reasons'])"
 }
+if [ "$SET" = final ]; then
+  run copy "X=1" ""
+  run fused "MOE_DISPATCH=fused" ""
+  run nccl "X=1" "--a2a nccl"
+  run copy_b "X=1" ""
+  run fused_b "MOE_DISPATCH=fused" ""
+  exit 0
+fi
 if [ "$SET" = parts ]; then
   run p332 "X=1" "--degree 1"
   run p224 "MOE_PARTS=2,2,4" "--degree 1"
