@@ -90,6 +90,7 @@ def main():
     runs = [("peer", d, False) for d in map(int, a.degrees.split(","))]
     runs += [("nccl", d, False) for d in (1, max(map(int, a.degrees.split(","))))]
     runs += [("peer-fd", d, False) for d in (1, 4)]  # dispatch fused into encode (NVLink stores)
+    runs += [("peer-parts", 1, False)]  # chunk 0 in 2-tile row parts (MOE_PARTS) instead of thirds
     runs += [("peer", 1, True)]
     base = None
     all_ok = True
@@ -103,10 +104,12 @@ def main():
         fd = backend == "peer-fd"
         if fd:
             os.environ["MOE_DISPATCH"] = "fused"
+        if backend == "peer-parts":  # capacity 8192 / W rows = 32 / W tiles of 256
+            os.environ["MOE_PARTS"] = ",".join(["2"] * (16 // W))
         cfg = MoELayerConfig(world_size=W, gpus_per_node=W, global_experts=E, model_dim=M,
                              hidden_dim=V, tokens_per_step=T, top_k=k, capacity_factor=f,
                              dtype="bf16", degree=degree, adaptive=adaptive,
-                             a2a_backend="peer" if fd else backend)
+                             a2a_backend="peer" if backend.startswith("peer") else backend)
         obj = [LayerState.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         st = LayerState.init(cfg, SEED, rank=rank, device=local, nccl_id=obj[0])
@@ -116,6 +119,7 @@ def main():
             res = forward(st, x)
             g = backward(st, res.saved, dy)
         torch.cuda.synchronize()
+        os.environ.pop("MOE_PARTS", None)
         idxs, loc, gates, cap = st.routing()
         m = st.metrics()
         out = dict(y=res.y.clone(), dx=g.dx.clone(), dw1=g.dw1.clone(), dw2=g.dw2.clone(),
